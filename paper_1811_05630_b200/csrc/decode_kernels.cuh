@@ -1,0 +1,423 @@
+// decode_kernels.cuh -- QCB1 decoder kernels (decompress_plane,
+// codec.cpp:535-633).
+//
+// D1 dec_prepare  one block per plane: parse the code table, canonical
+//                 codes (codec.cpp:233-249), an 11-bit lookup table plus
+//                 first-code/count/base arrays for longer codes
+//                 (PrefixDecoder, codec.cpp:251-286).
+// D2 dec_chunks   one thread per (plane, checkpoint chunk): resumes from the
+//                 encoder's IndexRec and reproduces codec.cpp:591-626 for
+//                 C elements -- chunk-parallel and bit-exact.
+// DV dec_validate one thread per plane, byte-serial, every check and error
+//                 of codec.cpp:535-633 in the reference's order: the path for
+//                 foreign blocks (host API), no index needed.
+#pragma once
+
+#include "common.cuh"
+
+namespace qcb {
+
+struct DecTables {
+    uint32_t *lut;       // [plane][1 << kLutBits]: sym << 6 | len (0 = long code)
+    uint64_t *first;     // [plane][kMaxCodeLen + 1]
+    uint32_t *count;     // [plane][kMaxCodeLen + 1]
+    uint32_t *basei;     // [plane][kMaxCodeLen + 1]
+    uint32_t *sorted;    // [plane][cap] symbols in (len, sym) order
+    uint32_t *meta;      // [plane][4]: maxlen, nsym, table bytes lo, -
+    uint64_t cap;
+};
+
+struct DecPlanes {
+    const uint8_t *arena;
+    const uint64_t *blk_off;   // [plane] block start in the arena
+    const IndexRec *index;     // [plane][nidx]
+    double *const *out;        // [plane] output plane
+    uint64_t L;
+    int log2C;
+};
+
+__device__ __forceinline__ uint64_t load_le(const uint8_t *p, int bytes) {
+    uint64_t v = 0;
+    for (int i = bytes - 1; i >= 0; --i) v = (v << 8) | p[i];
+    return v;
+}
+
+__global__ void __launch_bounds__(256) dec_prepare(DecPlanes D, DecTables T, int planes) {
+    const int pl = blockIdx.x;
+    if (pl >= planes) return;
+    const int tid = threadIdx.x;
+    __shared__ uint32_t cnt[kMaxCodeLen + 1];
+    __shared__ uint64_t first[kMaxCodeLen + 1];
+    __shared__ uint32_t basei[kMaxCodeLen + 1];
+    __shared__ uint32_t s_n, s_maxlen;
+    const uint8_t *blk = D.arena + D.blk_off[pl];
+    const uint8_t *tab = blk + kHeaderBytes + 4;
+    if (tid == 0) s_n = (uint32_t)load_le(blk + kHeaderBytes, 4);
+    if (tid <= kMaxCodeLen) cnt[tid] = 0;
+    uint32_t *lut = T.lut + (uint64_t)pl * (1u << kLutBits);
+    for (int k = tid; k < (1 << kLutBits); k += 256) lut[k] = 0;
+    __syncthreads();
+    const uint32_t n = s_n;
+    for (uint32_t r = tid; r < n; r += 256) atomicAdd(&cnt[tab[5ull * r + 4]], 1u);
+    __syncthreads();
+    if (tid == 0) {
+        uint64_t c = 0;
+        int prev = -1;
+        uint32_t b = 0;
+        uint32_t maxlen = 0;
+        for (int l = 1; l <= kMaxCodeLen; ++l) {
+            first[l] = 0;
+            basei[l] = b;
+            if (!cnt[l]) continue;
+            if (prev >= 0) c <<= (l - prev);
+            first[l] = c;
+            c += cnt[l];
+            b += cnt[l];
+            prev = l;
+            maxlen = l;
+        }
+        s_maxlen = maxlen;
+        // symbols in (len, sym) order: the table is in symbol order, so a
+        // stable pass by length keeps symbol order inside each length
+        uint32_t next[kMaxCodeLen + 1];
+        for (int l = 0; l <= kMaxCodeLen; ++l) next[l] = basei[l];
+        uint32_t *sorted = T.sorted + (uint64_t)pl * T.cap;
+        for (uint32_t r = 0; r < n; ++r) {
+            const uint8_t l = tab[5ull * r + 4];
+            sorted[next[l]++] = (uint32_t)load_le(tab + 5ull * r, 4);
+        }
+        for (int l = 0; l <= kMaxCodeLen; ++l) {
+            T.first[(uint64_t)pl * (kMaxCodeLen + 1) + l] = first[l];
+            T.count[(uint64_t)pl * (kMaxCodeLen + 1) + l] = cnt[l];
+            T.basei[(uint64_t)pl * (kMaxCodeLen + 1) + l] = basei[l];
+        }
+        T.meta[4 * pl] = maxlen;
+        T.meta[4 * pl + 1] = n;
+    }
+    __syncthreads();
+    // short codes -> LUT
+    const uint32_t *sorted = T.sorted + (uint64_t)pl * T.cap;
+    for (uint32_t r = tid; r < n; r += 256) {
+        // r-th entry in (len, sym) order
+        int l = 1;
+        while (l < kMaxCodeLen && !(r >= basei[l] && r < basei[l] + cnt[l])) ++l;
+        if (l > kLutBits) continue;
+        const uint64_t code = first[l] + (r - basei[l]);
+        const uint32_t lo = (uint32_t)(code << (kLutBits - l));
+        const uint32_t hi = (uint32_t)((code + 1) << (kLutBits - l));
+        const uint32_t e = (sorted[r] << 6) | (uint32_t)l;
+        for (uint32_t k = lo; k < hi; ++k) lut[k] = e;
+    }
+}
+
+// 64-bit MSB-first window at stream bit `bp` (stream is 16-byte aligned and
+// the arena is padded, so reading 3 words past any position is safe).
+__device__ __forceinline__ uint64_t peek64(const uint32_t *w, uint64_t bp) {
+    const uint64_t wi = bp >> 5;
+    const uint32_t b = (uint32_t)(bp & 31);
+    const uint64_t hi = ((uint64_t)bswap32(__ldg(w + wi)) << 32) | bswap32(__ldg(w + wi + 1));
+    if (b == 0) return hi;
+    const uint32_t w2 = bswap32(__ldg(w + wi + 2));
+    return (hi << b) | (w2 >> (32 - b));
+}
+
+__global__ void __launch_bounds__(128) dec_chunks(DecPlanes D, DecTables T, int planes) {
+    const uint64_t nchunks = (D.L + (1ull << D.log2C) - 1) >> D.log2C;
+    const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= nchunks * (uint64_t)planes) return;
+    const int pl = (int)(gid / nchunks);
+    const uint64_t j = gid % nchunks;
+    const uint64_t nidx = (D.L >> D.log2C) + 1;
+    const uint8_t *blk = D.arena + D.blk_off[pl];
+    const uint8_t mode = blk[5];
+    (void)mode;
+    const uint8_t pred_kind = blk[6];
+    const int qb = blk[7];
+    const long long half = 1ll << (qb - 1);
+    const uint32_t rsym = 1u << qb;
+    const double eb = __longlong_as_double((long long)load_le(blk + 16, 8));
+    const double q = dmul(2.0, eb);
+    const uint64_t nout = load_le(blk + 24, 8);
+    const uint64_t payload = load_le(blk + 32, 8);
+    const uint32_t n = T.meta[4 * pl + 1];
+    const uint32_t maxlen = T.meta[4 * pl];
+    const uint64_t table_bytes = 4 + 5ull * n;
+    const uint64_t sbytes = payload - table_bytes - 16 * nout;
+    const uint32_t *stream = reinterpret_cast<const uint32_t *>(blk + kHeaderBytes + table_bytes);
+    const uint8_t *orec = blk + kHeaderBytes + table_bytes + sbytes;
+    const uint32_t *lut = T.lut + (uint64_t)pl * (1u << kLutBits);
+    const uint64_t *first = T.first + (uint64_t)pl * (kMaxCodeLen + 1);
+    const uint32_t *count = T.count + (uint64_t)pl * (kMaxCodeLen + 1);
+    const uint32_t *basei = T.basei + (uint64_t)pl * (kMaxCodeLen + 1);
+    const uint32_t *sorted = T.sorted + (uint64_t)pl * T.cap;
+
+    const IndexRec r = D.index[(uint64_t)pl * nidx + j];
+    uint64_t bp = r.bitpos;
+    uint32_t run_left = r.run_left;
+    uint32_t last = r.last_lit;
+    uint64_t ocur = r.ocur;
+    double d1 = r.dprev, d2 = r.dprev2;
+    const uint64_t e0 = j << D.log2C;
+    const uint64_t e1 = tmin<uint64_t>(e0 + (1ull << D.log2C), D.L);
+    double *out = D.out[pl];
+
+    uint64_t i = e0;
+    auto emit = [&](uint32_t s) {
+        double v;
+        if (s == kOutlierSym) {
+            v = __longlong_as_double((long long)load_le(orec + 16 * ocur + 8, 8));
+            ++ocur;
+        } else {
+            double pred;
+            if (pred_kind == 0) pred = i > 0 ? d1 : 0.0;
+            else pred = i == 0 ? 0.0 : (i == 1 ? d1 : predict_linear(d1, d2));
+            const long long m = (long long)s - half;
+            v = eb == 0.0 ? pred : dadd(pred, dmul(q, (double)m));
+        }
+        out[i] = v;
+        d2 = d1;
+        d1 = v;
+        ++i;
+    };
+    while (i < e1) {
+        if (run_left > 0) {
+            // a run of a zero code with the previous-value predictor is a
+            // constant fill (d + 0.0 == d except -0.0, which emit() keeps)
+            if (pred_kind == 0 && last == (uint32_t)half && eb != 0.0 && bits_of(d1) != 0x8000000000000000ull &&
+                i > 0) {
+                const uint64_t stop = tmin<uint64_t>(e1, i + run_left);
+                const double v = d1;
+                run_left -= (uint32_t)(stop - i);
+                for (; i < stop; ++i) out[i] = v;
+                d2 = v;
+                continue;
+            }
+            emit(last);
+            --run_left;
+            continue;
+        }
+        const uint64_t w = peek64(stream, bp);
+        const uint32_t le = lut[w >> (64 - kLutBits)];
+        uint32_t s, l;
+        if (le & 63) {
+            l = le & 63;
+            s = le >> 6;
+        } else {
+            s = 0;
+            l = 0;
+            for (uint32_t ll = kLutBits + 1; ll <= maxlen; ++ll) {
+                if (!count[ll]) continue;
+                const uint64_t c = w >> (64 - ll);
+                if (c >= first[ll] && c - first[ll] < count[ll]) {
+                    s = sorted[basei[ll] + (uint32_t)(c - first[ll])];
+                    l = ll;
+                    break;
+                }
+            }
+            if (l == 0) return; // corrupt (never for encoder-produced blocks)
+        }
+        bp += l;
+        if (s == rsym) {
+            const uint64_t g = peek64(stream, bp);
+            const int z = __clzll((long long)g);
+            run_left = (uint32_t)(g >> (64 - (2 * z + 1)));
+            bp += 2 * z + 1;
+        } else {
+            emit(s);
+            last = s;
+        }
+    }
+    (void)sbytes;
+}
+
+// ------------------------------------------------------------ validating
+enum DecErr : uint32_t {
+    kDecOk = 0,
+    kDecPayloadSmall,     // "payload smaller than code table header"
+    kDecTableEmpty,       // "empty prefix-code table"
+    kDecTableTrunc,       // "code table truncated"
+    kDecSymOrder,         // "code table symbols not strictly increasing"
+    kDecSymRange,         // "code table symbol out of range"
+    kDecLenRange,         // "code length out of range"
+    kDecOverfull,         // "prefix code table overfull"
+    kDecLenMismatch,      // "payload/header length mismatch"
+    kDecStreamTrunc,      // "code stream truncated"
+    kDecInvalidCode,      // "invalid prefix code in stream"
+    kDecRunNoCode,        // "run escape without preceding code"
+    kDecRunRange,         // "run length out of range"
+    kDecRunOverflow,      // "run overflows element count"
+    kDecOutExhausted,     // "outlier list exhausted early"
+    kDecOutPos,           // "outlier position mismatch"
+    kDecOutUnused,        // "unused trailing outliers"
+    kDecStreamLen,        // "code stream length mismatch"
+    kDecNoMem,            // scratch too small
+};
+
+struct ValArgs {
+    const uint8_t *blocks;     // device bytes
+    const uint64_t *blk_off;   // [plane]
+    double *const *out;        // [plane]
+    uint32_t *err;             // [plane]
+    // scratch per plane for the (len, sym) sort
+    uint32_t *ssym;            // [plane][cap]
+    uint8_t *slen;             // [plane][cap]
+    uint64_t cap;
+};
+
+struct ByteBits {
+    const uint8_t *p;
+    uint64_t n, byte;
+    int bit;
+    __device__ __forceinline__ int get(bool &trunc) {
+        if (byte >= n) { trunc = true; return 0; }
+        const int b = (p[byte] >> (7 - bit)) & 1;
+        if (++bit == 8) { bit = 0; ++byte; }
+        return b;
+    }
+};
+
+// Header (from_bytes) checks are done by the caller; this is
+// decompress_plane's payload part.  One thread per plane.
+__global__ void dec_validate(ValArgs A, int planes) {
+    const int pl = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pl >= planes) return;
+    const uint8_t *blk = A.blocks + A.blk_off[pl];
+    const uint8_t pred_kind = blk[6];
+    const int qb = blk[7];
+    const uint64_t n = load_le(blk + 8, 8);
+    const double eb = __longlong_as_double((long long)load_le(blk + 16, 8));
+    const double q = dmul(2.0, eb);
+    const uint64_t nout = load_le(blk + 24, 8);
+    const uint64_t plen = load_le(blk + 32, 8);
+    const long long half = 1ll << (qb - 1);
+    const uint32_t rsym = 1u << qb;
+    const uint8_t *pl_ = blk + kHeaderBytes;
+    double *out = A.out[pl];
+    auto fail = [&](uint32_t e) { A.err[pl] = e; };
+    if (plen < 4) return fail(kDecPayloadSmall);
+    const uint32_t tc = (uint32_t)load_le(pl_, 4);
+    const uint64_t table_bytes = 4 + (uint64_t)tc * 5;
+    if (tc == 0) return fail(kDecTableEmpty);
+    if (plen < table_bytes) return fail(kDecTableTrunc);
+    if (tc > A.cap) return fail(kDecNoMem);
+    uint32_t cnt[kMaxCodeLen + 1];
+    for (int l = 0; l <= kMaxCodeLen; ++l) cnt[l] = 0;
+    uint32_t prev = 0;
+    for (uint32_t i = 0; i < tc; ++i) {
+        const uint32_t s = (uint32_t)load_le(pl_ + 4 + 5ull * i, 4);
+        const uint8_t l = pl_[4 + 5ull * i + 4];
+        if (i > 0 && s <= prev) return fail(kDecSymOrder);
+        if (s > rsym) return fail(kDecSymRange);
+        if (l < 1 || l > kMaxCodeLen) return fail(kDecLenRange);
+        ++cnt[l];
+        prev = s;
+    }
+    // PrefixDecoder: canonical codes, kraft in (len, sym) order
+    uint64_t first[kMaxCodeLen + 1];
+    uint32_t basei[kMaxCodeLen + 1];
+    {
+        uint64_t c = 0;
+        int prevl = -1;
+        uint32_t b = 0;
+        double kraft = 0.0;
+        for (int l = 1; l <= kMaxCodeLen; ++l) {
+            first[l] = 0;
+            basei[l] = b;
+            if (!cnt[l]) continue;
+            if (prevl >= 0) c <<= (l - prevl);
+            first[l] = c;
+            c += cnt[l];
+            b += cnt[l];
+            prevl = l;
+            const double term = ldexp(1.0, -l);
+            for (uint32_t k = 0; k < cnt[l]; ++k) kraft = dadd(kraft, term);
+        }
+        if (kraft > 1.0 + 1e-9) return fail(kDecOverfull);
+    }
+    int maxlen = 0;
+    for (int l = 1; l <= kMaxCodeLen; ++l)
+        if (cnt[l]) maxlen = l;
+    uint32_t *sorted = A.ssym + (uint64_t)pl * A.cap;
+    {
+        uint32_t next[kMaxCodeLen + 1];
+        for (int l = 0; l <= kMaxCodeLen; ++l) next[l] = basei[l];
+        for (uint32_t i = 0; i < tc; ++i) {
+            const uint8_t l = pl_[4 + 5ull * i + 4];
+            sorted[next[l]++] = (uint32_t)load_le(pl_ + 4 + 5ull * i, 4);
+        }
+    }
+    const uint64_t obytes = nout * 16;
+    if (plen < table_bytes + obytes) return fail(kDecLenMismatch);
+    const uint64_t sbytes = plen - table_bytes - obytes;
+    ByteBits br{pl_ + table_bytes, sbytes, 0, 0};
+    const uint8_t *oreg = pl_ + table_bytes + sbytes;
+    uint64_t ocur = 0, i = 0;
+    uint32_t last = rsym;
+    double d1 = 0.0, d2 = 0.0;
+    bool trunc = false;
+    while (i < n) {
+        uint64_t acc = 0;
+        uint32_t s = 0;
+        bool found = false;
+        for (int l = 1; l <= maxlen; ++l) {
+            acc = (acc << 1) | (uint64_t)br.get(trunc);
+            if (trunc) return fail(kDecStreamTrunc);
+            if (cnt[l] != 0) {
+                const uint64_t off = acc - first[l];
+                if (acc >= first[l] && off < cnt[l]) {
+                    s = sorted[basei[l] + (uint32_t)off];
+                    found = true;
+                    break;
+                }
+            }
+        }
+        if (!found) return fail(kDecInvalidCode);
+        uint64_t reps = 1;
+        uint32_t es = s;
+        if (s == rsym) {
+            if (last == rsym || last == kOutlierSym) return fail(kDecRunNoCode);
+            int zeros = 0;
+            for (;;) {
+                const int b = br.get(trunc);
+                if (trunc) return fail(kDecStreamTrunc);
+                if (b) break;
+                if (++zeros > 63) return fail(kDecRunRange);
+            }
+            uint64_t v = 1;
+            for (int k = 0; k < zeros; ++k) {
+                v = (v << 1) | (uint64_t)br.get(trunc);
+                if (trunc) return fail(kDecStreamTrunc);
+            }
+            if (v > n - i) return fail(kDecRunOverflow);
+            reps = v;
+            es = last;
+        } else {
+            last = s;
+        }
+        for (uint64_t k = 0; k < reps; ++k) {
+            double pred;
+            if (pred_kind == 0) pred = i > 0 ? d1 : 0.0;
+            else pred = i == 0 ? 0.0 : (i == 1 ? d1 : predict_linear(d1, d2));
+            double v;
+            if (es == kOutlierSym) {
+                if (ocur >= nout) return fail(kDecOutExhausted);
+                const uint64_t pos = load_le(oreg + 16 * ocur, 8);
+                if (pos != i) return fail(kDecOutPos);
+                v = __longlong_as_double((long long)load_le(oreg + 16 * ocur + 8, 8));
+                ++ocur;
+            } else {
+                const long long m = (long long)es - half;
+                v = eb == 0.0 ? pred : dadd(pred, dmul(q, (double)m));
+            }
+            out[i] = v;
+            d2 = d1;
+            d1 = v;
+            ++i;
+        }
+    }
+    if (ocur != nout) return fail(kDecOutUnused);
+    if (br.byte + (br.bit != 0) != sbytes) return fail(kDecStreamLen);
+    A.err[pl] = kDecOk;
+}
+
+} // namespace qcb

@@ -1,0 +1,134 @@
+// misc_kernels.cuh -- small kernels around the codec / engine pipeline.
+#pragma once
+
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace qcb {
+
+// Effective bound per plane (codec.cpp:309-327) and reciprocal.
+// mode: 0 RangeRelative, 1 Absolute, 2 Lossless.  One block per unit.
+template <int NP, class Src>
+__global__ void __launch_bounds__(256) init_params(PlaneParams *params, Src src, int units, uint64_t L,
+                                                   int mode, double bound, uint32_t *nonfinite) {
+    const int unit = blockIdx.x;
+    if (unit >= units) return;
+    __shared__ double smin[NP][256], smax[NP][256];
+    __shared__ int sbad;
+    const int tid = threadIdx.x;
+    double lo[NP], hi[NP];
+    for (int p = 0; p < NP; ++p) { lo[p] = INFINITY; hi[p] = -INFINITY; }
+    if (tid == 0) sbad = 0;
+    __syncthreads();
+    const bool need_range = mode == 0;
+    const bool need_scan = nonfinite != nullptr;
+    if (need_range || need_scan) {
+        int bad = 0;
+        for (uint64_t i = tid; i < L; i += 256) {
+            double v[2];
+            src.load(unit, i, v);
+            for (int p = 0; p < NP; ++p) {
+                if (!isfinite(v[p])) bad = 1;
+                lo[p] = fmin(lo[p], v[p]);
+                hi[p] = fmax(hi[p], v[p]);
+            }
+        }
+        if (bad) sbad = 1;
+    }
+    for (int p = 0; p < NP; ++p) { smin[p][tid] = lo[p]; smax[p][tid] = hi[p]; }
+    __syncthreads();
+    for (int w = 128; w >= 1; w >>= 1) {
+        if (tid < w)
+            for (int p = 0; p < NP; ++p) {
+                smin[p][tid] = fmin(smin[p][tid], smin[p][tid + w]);
+                smax[p][tid] = fmax(smax[p][tid], smax[p][tid + w]);
+            }
+        __syncthreads();
+    }
+    if (tid < NP) {
+        double eb;
+        if (mode == 2) eb = 0.0;
+        else if (mode == 1) eb = bound;
+        else {
+            eb = dmul(bound, dsub(smax[tid][0], smin[tid][0]));
+            if (!isfinite(eb)) eb = DBL_MAX;
+            if (eb == 0.0) eb = 0.0;
+        }
+        PlaneParams pp;
+        pp.eb = eb;
+        pp.q = dmul(2.0, eb);
+        pp.inv_q = ddiv(1.0, pp.q);
+        pp.flags = 0;
+        pp.pad = 0;
+        params[unit * NP + tid] = pp;
+        if (nonfinite && sbad) atomicExch(nonfinite, 1u);
+    }
+}
+
+// Per-slice sq_norm: adjacent-pair tree over the tile partials (the tile
+// partials are themselves the lower levels of the same tree).
+__global__ void slice_norms(const double *tilesum, int ntiles, int units, double *out) {
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= units) return;
+    // ntiles is a power of two (L and kTile are); iterative pairwise levels
+    double buf[64];
+    const double *t = tilesum + (uint64_t)u * ntiles;
+    if (ntiles <= 64) {
+        for (int k = 0; k < ntiles; ++k) buf[k] = t[k];
+        for (int w = ntiles / 2; w >= 1; w >>= 1)
+            for (int k = 0; k < w; ++k) buf[k] = dadd(buf[2 * k], buf[2 * k + 1]);
+        out[u] = buf[0];
+        return;
+    }
+    // larger: reduce groups of 64 recursively (tree shape preserved since
+    // every group is an aligned power-of-two range)
+    double acc[64];
+    int groups = ntiles / 64;
+    for (int gidx = 0; gidx < groups && gidx < 64; ++gidx) {
+        for (int k = 0; k < 64; ++k) buf[k] = t[gidx * 64 + k];
+        for (int w = 32; w >= 1; w >>= 1)
+            for (int k = 0; k < w; ++k) buf[k] = dadd(buf[2 * k], buf[2 * k + 1]);
+        acc[gidx] = buf[0];
+    }
+    // groups <= 64 for ntiles <= 4096 (L <= 2^22); larger slices use
+    // slice_norms_large
+    for (int w = groups / 2; w >= 1; w >>= 1)
+        for (int k = 0; k < w; ++k) acc[k] = dadd(acc[2 * k], acc[2 * k + 1]);
+    out[u] = acc[0];
+}
+
+// Dense gate step for compression-off engines: new = gate(old),
+// plus the same per-tile sq-norm partials the encoder produces.
+template <class Src>
+__global__ void __launch_bounds__(256) dense_gate(Src src, int units, uint64_t L, double *out, double *tilesum) {
+    const int ntiles = (int)((L + kTile - 1) / kTile);
+    const int unit = blockIdx.x / ntiles, t = blockIdx.x % ntiles;
+    if (unit >= units) return;
+    __shared__ double red[256];
+    const int tid = threadIdx.x;
+    double acc[4];
+    for (int e = 0; e < 4; ++e) {
+        const uint64_t i = (uint64_t)t * kTile + tid * 4 + e;
+        acc[e] = 0.0;
+        if (i < L) {
+            double v[2];
+            src.load(unit, i, v);
+            out[(uint64_t)unit * 2 * L + i] = v[0];
+            out[(uint64_t)unit * 2 * L + L + i] = v[1];
+            acc[e] = dadd(dmul(v[0], v[0]), dmul(v[1], v[1]));
+        }
+    }
+    red[tid] = dadd(dadd(acc[0], acc[1]), dadd(acc[2], acc[3]));
+    __syncthreads();
+    for (int w = 128; w >= 1; w >>= 1) {
+        double v = 0.0;
+        if (tid < w) v = dadd(red[2 * tid], red[2 * tid + 1]);
+        __syncthreads();
+        if (tid < w) red[tid] = v;
+        __syncthreads();
+    }
+    if (tid == 0) tilesum[(uint64_t)unit * ntiles + t] = red[0];
+}
+
+} // namespace qcb

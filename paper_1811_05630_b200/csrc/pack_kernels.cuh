@@ -1,0 +1,407 @@
+// pack_kernels.cuh -- codebook construction and QCB1 block assembly.
+//
+// E3 enc_codebook: histogram -> freq (sorted by symbol, codec.cpp:484-488)
+//    -> two-queue Huffman lengths (codec.cpp:168-229) -> canonical codes
+//    (codec.cpp:233-249) -> exact block size.
+// E5 enc_pack: header (codec.cpp:343-357), table (codec.cpp:508-512),
+//    MSB-first code stream with Elias-gamma run lengths (codec.cpp:513-520),
+//    outlier records (codec.cpp:521-524), decode index bit positions.
+#pragma once
+
+#include <cub/block/block_scan.cuh>
+
+#include "common.cuh"
+
+namespace qcb {
+
+struct CodeBook {
+    // inputs (from E2 / E1)
+    uint32_t *hist;            // [plane][rsym+1], zeroed again by E3
+    const uint32_t *hspecial;  // [plane][2]
+    const uint32_t *symrange;  // [plane][2]
+    const uint64_t *gamma_bits;// [plane]
+    const uint32_t *ocount;    // [plane]
+    // scratch, [plane][cap]
+    uint32_t *sym;             // symbols in ascending order
+    uint64_t *cnt;             // their counts
+    uint8_t *len;              // code lengths
+    uint64_t *code;            // canonical codes
+    uint64_t *key;             // sort keys (count << 25 | sym)
+    uint64_t *ncnt;            // [plane][2cap] node counts
+    int32_t *parent;           // [plane][2cap]
+    // outputs, [plane]
+    uint32_t *nsym;
+    uint64_t *stream_bits;
+    uint64_t *block_bytes;
+    uint64_t *slot_bytes;      // 16 + round_up(block_bytes, 16)
+    uint32_t *err;             // nonzero: codec error code
+    uint64_t cap;
+    int qb;
+};
+
+enum : uint32_t { kErrDepth = 1 };
+
+// Bitonic sort of n keys (n <= len of `a`, padded with ~0 to a power of two).
+__device__ void block_bitonic(uint64_t *a, uint32_t n) {
+    uint32_t m = 1;
+    while (m < n) m <<= 1;
+    for (uint32_t i = n + threadIdx.x; i < m; i += blockDim.x) a[i] = ~0ull;
+    __syncthreads();
+    for (uint32_t k = 2; k <= m; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+                const uint32_t ixj = i ^ j;
+                if (ixj > i) {
+                    const uint64_t x = a[i], y = a[ixj];
+                    const bool up = (i & k) == 0;
+                    if ((x > y) == up) {
+                        a[i] = y;
+                        a[ixj] = x;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+constexpr uint32_t kSmemSort = 4096;
+
+__global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
+    const int pl = blockIdx.x;
+    if (pl >= planes) return;
+    const int tid = threadIdx.x;
+    using Scan = cub::BlockScan<int, 256>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ uint64_t skeys[kSmemSort];
+    __shared__ uint32_t s_n;
+    __shared__ uint32_t lcount[kMaxCodeLen + 2];
+    __shared__ uint64_t lfirst[kMaxCodeLen + 2];
+    __shared__ unsigned long long s_bits;
+    __shared__ uint32_t s_err;
+
+    const uint32_t rsym = 1u << B.qb;
+    uint32_t *hist = B.hist + (uint64_t)pl * ((uint64_t)rsym + 1);
+    const uint64_t cap = B.cap;
+    uint32_t *sym = B.sym + pl * cap;
+    uint64_t *cnt = B.cnt + pl * cap;
+    uint8_t *len = B.len + pl * cap;
+    uint64_t *code = B.code + pl * cap;
+    const uint32_t h0 = B.hspecial[2 * pl], hrun = B.hspecial[2 * pl + 1];
+    const uint32_t smin = B.symrange[2 * pl], smax = B.symrange[2 * pl + 1];
+
+    if (tid == 0) {
+        s_n = 0;
+        s_bits = 0;
+        s_err = 0;
+        if (h0) {
+            sym[0] = kOutlierSym;
+            cnt[0] = h0;
+            s_n = 1;
+        }
+    }
+    if (tid < kMaxCodeLen + 2) lcount[tid] = 0;
+    __syncthreads();
+    // 1) compaction of the symbol range, ascending
+    if (smin <= smax) {
+        for (uint64_t c0 = smin; c0 <= smax; c0 += 256) {
+            const uint64_t s = c0 + tid;
+            const uint32_t v = s <= smax ? hist[s] : 0u;
+            int f = v ? 1 : 0, pos, tot;
+            Scan(scan_tmp).ExclusiveSum(f, pos, tot);
+            if (v) {
+                sym[s_n + pos] = (uint32_t)s;
+                cnt[s_n + pos] = v;
+                hist[s] = 0; // restore the zero invariant
+            }
+            __syncthreads();
+            if (tid == 0) s_n += tot;
+            __syncthreads();
+        }
+    }
+    if (tid == 0 && hrun) {
+        sym[s_n] = rsym;
+        cnt[s_n] = hrun;
+        s_n += 1;
+    }
+    __syncthreads();
+    const uint32_t n = s_n;
+    if (n == 0) { // unreachable for L >= 1
+        if (tid == 0) B.err[pl] = 0;
+        return;
+    }
+    // 2) leaves sorted by (count, symbol)
+    uint64_t *keys = n <= kSmemSort ? skeys : B.key + pl * cap * 2;
+    for (uint32_t i = tid; i < n; i += 256) keys[i] = (cnt[i] << 25) | sym[i];
+    __syncthreads();
+    if (n > 1) block_bitonic(keys, n);
+    // 3) two-queue merge (serial; ties prefer the leaf queue)
+    uint64_t *nc = B.ncnt + pl * cap * 2;
+    int32_t *par = B.parent + pl * cap * 2;
+    if (tid == 0) {
+        if (n == 1) {
+            par[0] = -1;
+        } else {
+            for (uint32_t i = 0; i < n; ++i) {
+                nc[i] = keys[i] >> 25;
+                par[i] = -1;
+            }
+            uint32_t lp = 0, ip = n, nodes = n;
+            while ((n - lp) + (nodes - ip) >= 2) {
+                uint32_t pick[2];
+                for (int k = 0; k < 2; ++k) {
+                    const bool leaf_ok = lp < n, int_ok = ip < nodes;
+                    const bool take_leaf = leaf_ok && (!int_ok || nc[lp] <= nc[ip]);
+                    pick[k] = take_leaf ? lp++ : ip++;
+                }
+                nc[nodes] = nc[pick[0]] + nc[pick[1]];
+                par[nodes] = -1;
+                par[pick[0]] = (int32_t)nodes;
+                par[pick[1]] = (int32_t)nodes;
+                ++nodes;
+            }
+            // depths top-down (parents have larger indices); stored in nc
+            nc[nodes - 1] = 0;
+            for (int64_t v = (int64_t)nodes - 2; v >= 0; --v) nc[v] = nc[par[v]] + 1;
+        }
+    }
+    __syncthreads();
+    // 4) lengths in symbol order
+    for (uint32_t i = tid; i < n; i += 256) {
+        const uint32_t s = (uint32_t)(keys[i] & ((1ull << 25) - 1));
+        const uint64_t depth = n == 1 ? 1 : nc[i];
+        if (depth < 1 || depth > (uint64_t)kMaxCodeLen) atomicExch(&s_err, kErrDepth);
+        // rank of s in the ascending symbol list
+        uint32_t lo = 0, hi = n;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (sym[mid] < s) lo = mid + 1;
+            else hi = mid;
+        }
+        const uint8_t l = (uint8_t)tmin<uint64_t>(depth, kMaxCodeLen);
+        len[lo] = l;
+        atomicAdd(&lcount[l], 1u);
+        atomicAdd(&s_bits, (unsigned long long)(cnt[lo] * l));
+    }
+    __syncthreads();
+    // 5) canonical codes: (len, sym) order == symbol order within a length
+    if (tid == 0) {
+        uint64_t c = 0;
+        int prev = -1;
+        for (int l = 1; l <= kMaxCodeLen; ++l) {
+            if (!lcount[l]) continue;
+            if (prev >= 0) c <<= (l - prev);
+            lfirst[l] = c;
+            c += lcount[l];
+            prev = l;
+        }
+        for (uint32_t r = 0; r < n; ++r) code[r] = lfirst[len[r]]++;
+        const uint64_t bits = s_bits + B.gamma_bits[pl];
+        const uint64_t payload = 4 + 5ull * n + (bits + 7) / 8 + 16ull * B.ocount[pl];
+        const uint64_t bytes = kHeaderBytes + payload;
+        B.nsym[pl] = n;
+        B.stream_bits[pl] = bits;
+        B.block_bytes[pl] = bytes;
+        B.slot_bytes[pl] = 16 + ((bytes + 15) & ~15ull);
+        B.err[pl] = s_err;
+    }
+}
+
+// ------------------------------------------------------------------ E5
+struct PackArgs {
+    const uint32_t *tsym, *trep, *ntok;   // tokens [plane][L+1]
+    const uint32_t *cb_sym;               // [plane][cap]
+    const uint8_t *cb_len;
+    const uint64_t *cb_code;
+    const uint32_t *nsym;
+    const uint64_t *stream_bits, *block_bytes, *slot_off;
+    const uint32_t *opos;                 // [plane][L]
+    const double *oval;
+    const uint32_t *ocount;
+    const PlaneParams *params;
+    IndexRec *index;                      // [plane][nidx]
+    uint8_t *arena;
+    uint64_t *blk_off;                    // out: block start in the arena
+    uint64_t L, cap;
+    int log2C, qb, mode, predictor;
+};
+
+__device__ __forceinline__ void put_bits_smem(uint32_t *w, uint32_t o, uint64_t v, int n) {
+    // MSB-first: the first bit of v (bit n-1) lands at stream bit o
+    while (n > 0) {
+        const uint32_t wi = o >> 5, b = o & 31;
+        const int take = min(n, 32 - (int)b);
+        const uint32_t chunk = (uint32_t)((v >> (n - take)) & ((1ull << take) - 1));
+        atomicOr(&w[wi], chunk << (32 - b - take));
+        o += take;
+        n -= take;
+    }
+}
+
+__device__ __forceinline__ void store_le(uint8_t *p, uint64_t v, int bytes) {
+    for (int i = 0; i < bytes; ++i) p[i] = (uint8_t)(v >> (8 * i));
+}
+
+constexpr int kPackTok = 1024;
+constexpr int kPackWords = kPackTok * 120 / 32 + 2;
+
+__global__ void __launch_bounds__(256) enc_pack(PackArgs A, int planes) {
+    const int pl = blockIdx.x;
+    if (pl >= planes) return;
+    const int tid = threadIdx.x;
+    using Scan = cub::BlockScan<uint32_t, 256>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ uint32_t words[kPackWords];
+    __shared__ uint32_t toff[kPackTok + 1];
+    __shared__ uint32_t s_carry;
+    __shared__ uint32_t s_jlo, s_jhi;
+
+    const uint32_t n = A.nsym[pl];
+    const uint64_t pre = kHeaderBytes + 4 + 5ull * n;
+    const uint64_t shift = (16 - (pre & 15)) & 15;
+    const uint64_t off = A.slot_off[pl] + shift;
+    uint8_t *blk = A.arena + off;
+    uint8_t *stream = blk + pre; // 16-byte aligned
+    const uint64_t bits = A.stream_bits[pl];
+    const uint64_t sbytes = (bits + 7) / 8;
+    const uint32_t nout = A.ocount[pl];
+    const uint64_t payload = 4 + 5ull * n + sbytes + 16ull * nout;
+    const uint32_t *cs = A.cb_sym + pl * A.cap;
+    const uint8_t *cl = A.cb_len + pl * A.cap;
+    const uint64_t *cc = A.cb_code + pl * A.cap;
+    const uint32_t rsym = 1u << A.qb;
+    const uint64_t nidx = (A.L >> A.log2C) + 1;
+    IndexRec *idx = A.index + pl * nidx;
+
+    if (tid == 0) {
+        A.blk_off[pl] = off;
+        blk[0] = 'Q'; blk[1] = 'C'; blk[2] = 'B'; blk[3] = '1';
+        blk[4] = 1;
+        blk[5] = (uint8_t)A.mode;
+        blk[6] = (uint8_t)A.predictor;
+        blk[7] = (uint8_t)A.qb;
+        store_le(blk + 8, A.L, 8);
+        store_le(blk + 16, bits_of(A.params[pl].eb), 8);
+        store_le(blk + 24, nout, 8);
+        store_le(blk + 32, payload, 8);
+        store_le(blk + 40, n, 4);
+        s_carry = 0;
+    }
+    for (uint32_t r = tid; r < n; r += 256) {
+        store_le(blk + 44 + 5ull * r, cs[r], 4);
+        blk[44 + 5ull * r + 4] = cl[r];
+    }
+    // tokens
+    const uint32_t ntok = A.ntok[pl];
+    const uint32_t *ts = A.tsym + pl * (A.L + 1);
+    const uint32_t *tr = A.trep + pl * (A.L + 1);
+    uint64_t base_bit = 0;
+    for (uint32_t t0 = 0; t0 < ntok; t0 += kPackTok) {
+        const uint32_t tn = tmin<uint32_t>(kPackTok, ntok - t0);
+        uint64_t tcode[4];
+        int tlen[4], glen[4];
+        uint32_t tbits[4];
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t k = tid * 4 + e;
+            tbits[e] = 0;
+            tlen[e] = 0;
+            glen[e] = 0;
+            tcode[e] = 0;
+            if (k < tn) {
+                const uint32_t s = ts[t0 + k];
+                uint32_t lo = 0, hi = n;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (cs[mid] < s) lo = mid + 1;
+                    else hi = mid;
+                }
+                tcode[e] = cc[lo];
+                tlen[e] = cl[lo];
+                if (s == rsym) glen[e] = 2 * bit_width64(tr[t0 + k]) - 1;
+                tbits[e] = (uint32_t)(tlen[e] + glen[e]);
+            }
+        }
+        uint32_t pos[4], tot;
+        Scan(scan_tmp).ExclusiveSum(tbits, pos, tot);
+        const uint32_t b0 = (uint32_t)(base_bit & 31);
+        const uint32_t nwords = (b0 + tot + 31) / 32;
+        for (uint32_t w = tid; w < nwords + 1; w += 256) words[w] = 0;
+        __syncthreads();
+        if (tid == 0) words[0] = s_carry;
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t k = tid * 4 + e;
+            if (k <= tn) toff[k] = pos[e];
+        }
+        if (tid == 255) toff[tn] = tot; // sentinel when tn == 1024
+        __syncthreads();
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t k = tid * 4 + e;
+            if (k < tn) {
+                put_bits_smem(words, b0 + pos[e], tcode[e], tlen[e]);
+                if (glen[e]) put_bits_smem(words, b0 + pos[e] + tlen[e], tr[t0 + k], glen[e]);
+            }
+        }
+        __syncthreads();
+        // complete words -> global (big-endian byte order)
+        const uint32_t endbit = b0 + tot;
+        const uint32_t full = endbit / 32;
+        const uint64_t w0 = base_bit / 32;
+        uint32_t *gw = reinterpret_cast<uint32_t *>(stream);
+        for (uint32_t w = tid; w < full; w += 256) gw[w0 + w] = bswap32(words[w]);
+        // decode-index bit positions for checkpoints resuming in this chunk
+        if (tid == 0) {
+            // records are sorted by tok; find [jlo, jhi) with tok in [t0, t0+tn)
+            uint32_t lo = 1, hi = (uint32_t)nidx;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (idx[mid].tok < t0) lo = mid + 1;
+                else hi = mid;
+            }
+            s_jlo = lo;
+            hi = (uint32_t)nidx;
+            uint32_t lo2 = lo;
+            while (lo2 < hi) {
+                const uint32_t mid = (lo2 + hi) >> 1;
+                if (idx[mid].tok < t0 + tn) lo2 = mid + 1;
+                else hi = mid;
+            }
+            s_jhi = lo2;
+        }
+        __syncthreads();
+        for (uint32_t j = s_jlo + tid; j < s_jhi; j += 256) {
+            if ((uint64_t)j << A.log2C >= A.L) continue;
+            idx[j].bitpos = base_bit + toff[idx[j].tok - t0];
+        }
+        if (tid == 0) s_carry = (endbit & 31) ? words[full] : 0;
+        __syncthreads();
+        base_bit += tot;
+    }
+    // trailing partial word, byte-wise (never write past the stream)
+    if (tid == 0) {
+        if (base_bit & 31) {
+            const uint64_t w = base_bit / 32;
+            const uint32_t v = s_carry;
+            for (uint64_t b = w * 4; b < sbytes; ++b) stream[b] = (uint8_t)(v >> (24 - 8 * (b - w * 4)));
+        }
+        // checkpoints resuming exactly at the end of the token stream
+        for (uint32_t j = 1; j < nidx; ++j)
+            if (((uint64_t)j << A.log2C) < A.L && idx[j].tok >= ntok) idx[j].bitpos = base_bit;
+        idx[0].bitpos = 0;
+        idx[0].tok = 0;
+        idx[0].run_left = 0;
+        idx[0].ocur = 0;
+        idx[0].last_lit = rsym;
+        idx[0].dprev = 0.0;
+        idx[0].dprev2 = 0.0;
+    }
+    // outliers (u64 pos, f64 value), LE, right after the stream
+    uint8_t *orec = stream + sbytes;
+    const uint32_t *op = A.opos + pl * A.L;
+    const double *ov = A.oval + pl * A.L;
+    for (uint32_t k = tid; k < nout; k += 256) {
+        store_le(orec + 16ull * k, op[k], 8);
+        store_le(orec + 16ull * k + 8, bits_of(ov[k]), 8);
+    }
+}
+
+} // namespace qcb

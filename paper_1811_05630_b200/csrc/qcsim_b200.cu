@@ -1,0 +1,1171 @@
+// qcsim_b200.cu -- host side of the B200 compressed state-vector update
+// path: codec batch drivers, the engine (Algorithm 1) and
+// the C-ABI declared in include/qcsim_c.h.
+//
+// Built for sm_100a only, with --fmad=false.  There is no CPU
+// fallback: every compute path below launches the kernels in *_kernels.cuh;
+// without a CUDA device every entry point fails with QCSIM_CUDA.
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_scan.cuh>
+#include <cuda_runtime.h>
+
+#include "../../include/qcsim_c.h"
+#include "common.cuh"
+#include "decode_kernels.cuh"
+#include "encode_kernels.cuh"
+#include "misc_kernels.cuh"
+#include "pack_kernels.cuh"
+
+#define QCSIM_VERSION "qcsim-b200 0.1.0 sm_100a"
+
+using namespace qcb;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+    qcsim_status st;
+    std::string msg;
+};
+
+[[noreturn]] void raise(qcsim_status st, std::string msg) { throw Fail{st, std::move(msg)}; }
+
+void ck(cudaError_t e, const char *what) {
+    if (e != cudaSuccess) raise(QCSIM_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) ck((x), #x)
+
+template <class F> qcsim_status guarded(F &&f) {
+    try {
+        f();
+        return QCSIM_OK;
+    } catch (const Fail &e) {
+        g_err = e.msg;
+        return e.st;
+    } catch (const std::bad_alloc &) {
+        g_err = "out of memory";
+        return QCSIM_NOMEM;
+    } catch (const std::exception &e) {
+        g_err = e.what();
+        return QCSIM_RUNTIME;
+    }
+}
+
+// Grow-only device buffer (contents are not preserved on growth).
+template <class T> struct DBuf {
+    T *p = nullptr;
+    size_t cap = 0;
+    DBuf() = default;
+    DBuf(const DBuf &) = delete;
+    DBuf &operator=(const DBuf &) = delete;
+    ~DBuf() {
+        if (p) cudaFree(p);
+    }
+    // returns true when (re)allocated
+    bool ensure(size_t n, bool zero = false) {
+        if (n <= cap && p) return false;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max<size_t>(n, 1);
+        cudaError_t e = cudaMalloc(&p, want * sizeof(T));
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            raise(QCSIM_NOMEM, "device allocation of " + std::to_string(want * sizeof(T)) + " bytes failed");
+        }
+        cap = want;
+        if (zero) CK(cudaMemset(p, 0, want * sizeof(T)));
+        return true;
+    }
+    void swap(DBuf &o) {
+        std::swap(p, o.p);
+        std::swap(cap, o.cap);
+    }
+};
+
+int g_device_checked = -1;
+void ensure_device(int dev) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        raise(QCSIM_CUDA, "no CUDA device available (qcsim-b200 has no CPU fallback)");
+    }
+    if (dev < 0 || dev >= n) raise(QCSIM_INVALID_ARGUMENT, "CUDA device ordinal out of range");
+    CK(cudaSetDevice(dev));
+    if (g_device_checked != dev) {
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, dev));
+        if (prop.major != 10) raise(QCSIM_CUDA, std::string("device is not sm_100 (Blackwell): ") + prop.name);
+        g_device_checked = dev;
+    }
+}
+
+uint64_t g_launches = 0; // kernels launched by this library (per process)
+
+void validate_codec(const qcsim_codec_config &c) { // codec.cpp:331-341
+    if (c.quant_code_bits < 4 || c.quant_code_bits > 24)
+        raise(QCSIM_INVALID_ARGUMENT, "quant_code_bits must be in [4, 24]");
+    if (c.mode > 2) raise(QCSIM_INVALID_ARGUMENT, "unknown codec mode");
+    if (c.predictor > 1) raise(QCSIM_INVALID_ARGUMENT, "unknown predictor");
+    if (c.mode != QCSIM_MODE_LOSSLESS) {
+        if (!(c.bound > 0.0) || !std::isfinite(c.bound)) raise(QCSIM_INVALID_ARGUMENT, "error bound must be positive");
+        if (c.mode == QCSIM_MODE_RANGE_RELATIVE && c.bound > 1.0)
+            raise(QCSIM_INVALID_ARGUMENT, "range-relative bound must not exceed 1");
+    }
+}
+
+int auto_log2C(uint64_t L) {
+    int s = 0;
+    while ((1ull << s) < L) ++s;
+    return std::max(6, std::min(12, s - 5));
+}
+
+// ------------------------------------------------------------ encoder
+struct EncScratch {
+    DBuf<PlaneParams> params;
+    DBuf<uint32_t> sym, opos, ocount, ntok, tsym, trep, hist, hspecial, symrange, nsym, err, nonfinite;
+    DBuf<double> oval, tilesum;
+    DBuf<uint64_t> gamma, cb_cnt, cb_code, cb_key, cb_ncnt, stream_bits, block_bytes, slot_bytes, slot_off, blk_off;
+    DBuf<uint8_t> cb_len, cub_tmp;
+    DBuf<uint32_t> cb_sym;
+    DBuf<int32_t> cb_parent;
+    uint64_t hist_stride = 0;
+
+    void ensure(uint64_t planes, uint64_t units, uint64_t L, int qb) {
+        const uint64_t ntiles = (L + kTile - 1) / kTile;
+        const uint64_t rsym1 = (1ull << qb) + 1;
+        const uint64_t cap = std::min<uint64_t>(L + 1, rsym1);
+        params.ensure(planes);
+        sym.ensure(planes * L);
+        opos.ensure(planes * L);
+        oval.ensure(planes * L);
+        ocount.ensure(planes);
+        tilesum.ensure(units * ntiles);
+        tsym.ensure(planes * (L + 1));
+        trep.ensure(planes * (L + 1));
+        ntok.ensure(planes);
+        // the dense histogram must be all-zero between uses (E3 re-zeroes)
+        if (hist_stride != rsym1 || hist.cap < planes * rsym1) {
+            hist.ensure(planes * rsym1);
+            CK(cudaMemset(hist.p, 0, hist.cap * sizeof(uint32_t)));
+            hist_stride = rsym1;
+        }
+        hspecial.ensure(2 * planes);
+        symrange.ensure(2 * planes);
+        gamma.ensure(planes);
+        cb_sym.ensure(planes * cap);
+        cb_cnt.ensure(planes * cap);
+        cb_len.ensure(planes * cap);
+        cb_code.ensure(planes * cap);
+        cb_key.ensure(planes * cap * 2);
+        cb_ncnt.ensure(planes * cap * 2);
+        cb_parent.ensure(planes * cap * 2);
+        nsym.ensure(planes);
+        stream_bits.ensure(planes);
+        block_bytes.ensure(planes);
+        slot_bytes.ensure(planes);
+        slot_off.ensure(planes + 1);
+        blk_off.ensure(planes);
+        err.ensure(planes);
+        nonfinite.ensure(1);
+    }
+};
+
+template <class K> void set_smem(K kernel, size_t bytes) {
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+struct EncodeResult {
+    std::vector<uint64_t> block_bytes; // per plane
+    std::vector<uint64_t> blk_off;     // per plane, offset in the arena
+    uint64_t total = 0;                // arena bytes used (incl. padding)
+    uint64_t fallback = 0;
+};
+
+// Encodes units*NP planes produced by `src` into `arena` (grown as needed).
+// `index` receives the decode checkpoints ([plane][nidx]).
+template <int NP, class Src>
+EncodeResult encode_batch(cudaStream_t st, EncScratch &S, const Src &src, int units, uint64_t L,
+                          const qcsim_codec_config &cfg, int log2C, IndexRec *index, DBuf<uint8_t> &arena,
+                          bool check_finite, bool want_offsets) {
+    const uint64_t planes = (uint64_t)units * NP;
+    const int qb = cfg.quant_code_bits;
+    S.ensure(planes, units, L, qb);
+    const uint64_t ntiles = (L + kTile - 1) / kTile;
+    const uint64_t cap = std::min<uint64_t>(L + 1, (1ull << qb) + 1);
+
+    if (check_finite) CK(cudaMemsetAsync(S.nonfinite.p, 0, sizeof(uint32_t), st));
+    init_params<NP, Src><<<units, 256, 0, st>>>(S.params.p, src, units, L, cfg.mode, cfg.bound,
+                                                check_finite ? S.nonfinite.p : nullptr);
+    ++g_launches;
+    if (check_finite) {
+        uint32_t bad = 0;
+        CK(cudaMemcpyAsync(&bad, S.nonfinite.p, sizeof bad, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (bad) raise(QCSIM_INVALID_ARGUMENT, "plane contains a non-finite value");
+    }
+
+    EncPlanes E;
+    E.params = S.params.p;
+    E.sym = S.sym.p;
+    E.opos = S.opos.p;
+    E.oval = S.oval.p;
+    E.ocount = S.ocount.p;
+    E.index = index;
+    E.tilesum = S.tilesum.p;
+    E.L = L;
+    E.log2C = log2C;
+    E.qb = qb;
+    E.predictor = cfg.predictor;
+
+    static bool attr_done[2] = {false, false};
+    if (!attr_done[NP - 1]) {
+        set_smem(enc_quantize<NP, Src>, sizeof(E1Smem<NP>));
+        set_smem(enc_tokenize, sizeof(TokSmem));
+        attr_done[NP - 1] = true;
+    }
+    enc_quantize<NP, Src><<<units, kEncThreads, sizeof(E1Smem<NP>), st>>>(E, src, units);
+    enc_serial<NP, Src><<<(unsigned)((planes + 31) / 32), 32, 0, st>>>(E, src, units);
+    g_launches += 2;
+
+    TokPlanes T;
+    T.sym = S.sym.p;
+    T.tsym = S.tsym.p;
+    T.trep = S.trep.p;
+    T.ntok = S.ntok.p;
+    T.hist = S.hist.p;
+    T.hspecial = S.hspecial.p;
+    T.symrange = S.symrange.p;
+    T.gamma_bits = S.gamma.p;
+    T.index = index;
+    T.L = L;
+    T.log2C = log2C;
+    T.qb = qb;
+    enc_tokenize<<<(unsigned)planes, kEncThreads, sizeof(TokSmem), st>>>(T, (int)planes);
+
+    CodeBook B;
+    B.hist = S.hist.p;
+    B.hspecial = S.hspecial.p;
+    B.symrange = S.symrange.p;
+    B.gamma_bits = S.gamma.p;
+    B.ocount = S.ocount.p;
+    B.sym = S.cb_sym.p;
+    B.cnt = S.cb_cnt.p;
+    B.len = S.cb_len.p;
+    B.code = S.cb_code.p;
+    B.key = S.cb_key.p;
+    B.ncnt = S.cb_ncnt.p;
+    B.parent = S.cb_parent.p;
+    B.nsym = S.nsym.p;
+    B.stream_bits = S.stream_bits.p;
+    B.block_bytes = S.block_bytes.p;
+    B.slot_bytes = S.slot_bytes.p;
+    B.err = S.err.p;
+    B.cap = cap;
+    B.qb = qb;
+    enc_codebook<<<(unsigned)planes, 256, 0, st>>>(B, (int)planes);
+    g_launches += 2;
+
+    // slot offsets: exclusive scan of slot sizes (16-byte aligned slots)
+    size_t tmp_bytes = 0;
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, S.slot_bytes.p, S.slot_off.p + 1, (int)planes, st));
+    S.cub_tmp.ensure(tmp_bytes);
+    CK(cudaMemsetAsync(S.slot_off.p, 0, sizeof(uint64_t), st));
+    CK(cub::DeviceScan::InclusiveSum(S.cub_tmp.p, tmp_bytes, S.slot_bytes.p, S.slot_off.p + 1, (int)planes, st));
+    ++g_launches;
+
+    EncodeResult R;
+    std::vector<uint32_t> err(planes);
+    CK(cudaMemcpyAsync(&R.total, S.slot_off.p + planes, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(err.data(), S.err.p, planes * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    for (uint64_t p = 0; p < planes; ++p)
+        if (err[p] == kErrDepth) raise(QCSIM_CODEC, "prefix code depth out of range");
+    arena.ensure(R.total + 64);
+
+    PackArgs A;
+    A.tsym = S.tsym.p;
+    A.trep = S.trep.p;
+    A.ntok = S.ntok.p;
+    A.cb_sym = S.cb_sym.p;
+    A.cb_len = S.cb_len.p;
+    A.cb_code = S.cb_code.p;
+    A.nsym = S.nsym.p;
+    A.stream_bits = S.stream_bits.p;
+    A.block_bytes = S.block_bytes.p;
+    A.slot_off = S.slot_off.p;
+    A.opos = S.opos.p;
+    A.oval = S.oval.p;
+    A.ocount = S.ocount.p;
+    A.params = S.params.p;
+    A.index = index;
+    A.arena = arena.p;
+    A.blk_off = S.blk_off.p;
+    A.L = L;
+    A.cap = cap;
+    A.log2C = log2C;
+    A.qb = qb;
+    A.mode = cfg.mode;
+    A.predictor = cfg.predictor;
+    enc_pack<<<(unsigned)planes, 256, 0, st>>>(A, (int)planes);
+    ++g_launches;
+    R.block_bytes.resize(planes);
+    CK(cudaMemcpyAsync(R.block_bytes.data(), S.block_bytes.p, planes * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                       st));
+    if (want_offsets) {
+        R.blk_off.resize(planes);
+        CK(cudaMemcpyAsync(R.blk_off.data(), S.blk_off.p, planes * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    }
+    std::vector<PlaneParams> prm(planes);
+    CK(cudaMemcpyAsync(prm.data(), S.params.p, planes * sizeof(PlaneParams), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    for (auto &p : prm) R.fallback += (p.flags & kFlagFallback) ? 1 : 0;
+    return R;
+}
+
+// ------------------------------------------------------------ decoder
+struct DecScratch {
+    DBuf<uint32_t> lut, count, basei, sorted, meta;
+    DBuf<uint64_t> first;
+    uint64_t cap = 0;
+    void ensure(uint64_t planes, uint64_t L, int qb) {
+        cap = std::min<uint64_t>(L + 1, (1ull << qb) + 1);
+        lut.ensure(planes << kLutBits);
+        first.ensure(planes * (kMaxCodeLen + 1));
+        count.ensure(planes * (kMaxCodeLen + 1));
+        basei.ensure(planes * (kMaxCodeLen + 1));
+        sorted.ensure(planes * cap);
+        meta.ensure(planes * 4);
+    }
+};
+
+void decode_batch(cudaStream_t st, DecScratch &S, const uint8_t *arena, const uint64_t *blk_off,
+                  const IndexRec *index, double *const *out, int planes, uint64_t L, int log2C, int qb) {
+    S.ensure(planes, L, qb);
+    DecTables T;
+    T.lut = S.lut.p;
+    T.first = S.first.p;
+    T.count = S.count.p;
+    T.basei = S.basei.p;
+    T.sorted = S.sorted.p;
+    T.meta = S.meta.p;
+    T.cap = S.cap;
+    DecPlanes D;
+    D.arena = arena;
+    D.blk_off = blk_off;
+    D.index = index;
+    D.out = out;
+    D.L = L;
+    D.log2C = log2C;
+    dec_prepare<<<planes, 256, 0, st>>>(D, T, planes);
+    const uint64_t nchunks = (L + (1ull << log2C) - 1) >> log2C;
+    const uint64_t threads = nchunks * planes;
+    dec_chunks<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(D, T, planes);
+    g_launches += 2;
+}
+
+// Host-side from_bytes checks (codec.cpp:366-408), exact messages.
+struct Header {
+    uint8_t mode, pred, qb;
+    uint64_t n, outliers, payload;
+    double eb;
+};
+Header parse_header(const uint8_t *b, uint64_t len, uint64_t *consumed) {
+    auto rd = [&](int off, int bytes) {
+        uint64_t v = 0;
+        for (int i = bytes - 1; i >= 0; --i) v = (v << 8) | b[off + i];
+        return v;
+    };
+    if (len < kHeaderBytes) raise(QCSIM_CODEC, "block header truncated");
+    if (b[0] != 'Q' || b[1] != 'C' || b[2] != 'B' || b[3] != '1') raise(QCSIM_CODEC, "bad block magic");
+    if (b[4] != 1) raise(QCSIM_CODEC, "unsupported block version " + std::to_string(b[4]));
+    if (b[5] > 2) raise(QCSIM_CODEC, "bad codec mode byte");
+    if (b[6] > 1) raise(QCSIM_CODEC, "bad predictor byte");
+    Header h;
+    h.mode = b[5];
+    h.pred = b[6];
+    h.qb = b[7];
+    if (h.qb < 4 || h.qb > 24) raise(QCSIM_CODEC, "quant_code_bits out of range");
+    h.n = rd(8, 8);
+    uint64_t ebits = rd(16, 8);
+    std::memcpy(&h.eb, &ebits, 8);
+    h.outliers = rd(24, 8);
+    h.payload = rd(32, 8);
+    if (h.n == 0) raise(QCSIM_CODEC, "element_count must be at least 1");
+    if (h.outliers > h.n) raise(QCSIM_CODEC, "outlier_count exceeds element_count");
+    if (!(h.eb >= 0.0) || !std::isfinite(h.eb)) raise(QCSIM_CODEC, "bad effective_abs_bound");
+    if (h.payload > len - kHeaderBytes) raise(QCSIM_CODEC, "block payload truncated");
+    if (consumed) *consumed = kHeaderBytes + h.payload;
+    return h;
+}
+
+const char *dec_message(uint32_t e) {
+    switch (e) {
+    case kDecPayloadSmall: return "payload smaller than code table header";
+    case kDecTableEmpty: return "empty prefix-code table";
+    case kDecTableTrunc: return "code table truncated";
+    case kDecSymOrder: return "code table symbols not strictly increasing";
+    case kDecSymRange: return "code table symbol out of range";
+    case kDecLenRange: return "code length out of range";
+    case kDecOverfull: return "prefix code table overfull";
+    case kDecLenMismatch: return "payload/header length mismatch";
+    case kDecStreamTrunc: return "code stream truncated";
+    case kDecInvalidCode: return "invalid prefix code in stream";
+    case kDecRunNoCode: return "run escape without preceding code";
+    case kDecRunRange: return "run length out of range";
+    case kDecRunOverflow: return "run overflows element count";
+    case kDecOutExhausted: return "outlier list exhausted early";
+    case kDecOutPos: return "outlier position mismatch";
+    case kDecOutUnused: return "unused trailing outliers";
+    case kDecStreamLen: return "code stream length mismatch";
+    default: return "decoder scratch exhausted";
+    }
+}
+
+struct ValScratch {
+    DBuf<uint32_t> ssym, err;
+    DBuf<uint8_t> slen;
+    void ensure(uint64_t planes, uint64_t cap) {
+        ssym.ensure(planes * cap);
+        slen.ensure(planes * cap);
+        err.ensure(planes);
+    }
+};
+
+// ------------------------------------------------------------- context
+// Per-thread codec context for the single-plane / batched codec API.
+struct CodecCtx {
+    int dev = -1;
+    cudaStream_t st = nullptr;
+    EncScratch enc;
+    ValScratch val;
+    DBuf<uint8_t> arena, bytes;
+    DBuf<double> vals;
+    DBuf<IndexRec> index;
+    DBuf<const double *> ptrs;
+    DBuf<double *> optrs;
+    DBuf<uint64_t> offs;
+};
+thread_local CodecCtx *t_codec = nullptr;
+CodecCtx &codec_ctx() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        dev = 0;
+    }
+    ensure_device(dev);
+    if (!t_codec) {
+        t_codec = new CodecCtx();
+        t_codec->dev = dev;
+        CK(cudaStreamCreateWithFlags(&t_codec->st, cudaStreamNonBlocking));
+    }
+    return *t_codec;
+}
+
+} // namespace
+
+// =================================================================== engine
+struct qcsim_engine {
+    qcsim_engine_config cfg{};
+    int n = 0, s = 0;
+    uint64_t S = 0, L = 0;       // slices (global), slice length
+    uint64_t s0 = 0, ns = 0;     // this rank's slice range
+    int log2C = 0;
+    uint64_t nidx = 0;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool compressed = true;
+    bool loaded = false;
+    // compressed state (ping-pong)
+    DBuf<uint8_t> arena[2];
+    DBuf<uint64_t> blk_off[2];
+    DBuf<IndexRec> index[2];
+    std::vector<uint64_t> blk_bytes_h; // current block sizes, plane order
+    int cur = 0;
+    // dense state (compression off) and decoded old values, [slot][2][L]
+    DBuf<double> dense[2];
+    DBuf<double> old;
+    DBuf<int32_t> slot_of;
+    DBuf<uint64_t> unit_slice;
+    DBuf<double *> outptrs;
+    DBuf<double> slice_sq;
+    DBuf<double> scale_d;
+    // partner slices imported from other ranks: slice -> QCB1 bytes
+    std::vector<std::pair<uint64_t, std::vector<uint8_t>>> imported;
+    std::vector<double> sq_norm; // all S slices (global view)
+    EncScratch enc;
+    DecScratch dec;
+    ValScratch val;
+    DBuf<uint8_t> imp_bytes;
+    DBuf<uint64_t> imp_off;
+    // metrics
+    double ratio_min = INFINITY, ratio_sum = 0.0;
+    uint64_t calls = 0, gates = 0, peak = 0, current = 0, fallback = 0;
+    double wall = 0.0;
+    uint64_t launches0 = 0;
+};
+
+namespace {
+
+uint64_t partner_slice(const qcsim_action &a, int s, uint64_t j) {
+    if (a.kind == QCSIM_ACTION_BUTTERFLY && a.target >= s) return j ^ (1ull << (a.target - s));
+    if (a.kind == QCSIM_ACTION_SWAP) {
+        uint64_t hm = 0;
+        if (a.a >= s) hm |= 1ull << (a.a - s);
+        if (a.b >= s) hm |= 1ull << (a.b - s);
+        return j ^ hm;
+    }
+    return j;
+}
+
+DevAction to_dev(const qcsim_action &a) {
+    DevAction d{};
+    d.kind = a.kind;
+    d.target = a.target;
+    d.a = a.a;
+    d.b = a.b;
+    d.mask = a.mask;
+    d.f[0] = a.factor[0];
+    d.f[1] = a.factor[1];
+    for (int k = 0; k < 8; ++k) d.u[k] = a.u[k];
+    return d;
+}
+
+double tree_sum_host(const double *v, uint64_t len) {
+    if (len == 1) return v[0];
+    const uint64_t h = len / 2;
+    const double a = tree_sum_host(v, h), b = tree_sum_host(v + h, h);
+    return a + b;
+}
+
+void record_sizes(qcsim_engine *e, const std::vector<uint64_t> &bytes) {
+    uint64_t tot = 0;
+    for (uint64_t b : bytes) {
+        const double ratio = (double)(8 * e->L) / (double)b;
+        if (ratio < e->ratio_min) e->ratio_min = ratio;
+        e->ratio_sum += ratio;
+        e->calls++;
+        tot += b;
+    }
+    e->current = tot;
+    e->peak = std::max(e->peak, tot);
+}
+
+// Identity source over [slot][2][L] planes (initial loads).
+struct PlanarSrc {
+    const double *v;
+    uint64_t L;
+    static constexpr bool kNorms = true;
+    __device__ __forceinline__ void load(int unit, uint64_t i, double *o) const {
+        o[0] = v[(uint64_t)unit * 2 * L + i];
+        o[1] = v[(uint64_t)unit * 2 * L + L + i];
+    }
+};
+// Basis state |x> restricted to local slices starting at s0.
+struct BasisSrc {
+    uint64_t x, s0;
+    int s;
+    static constexpr bool kNorms = true;
+    __device__ __forceinline__ void load(int unit, uint64_t i, double *o) const {
+        const uint64_t g = ((s0 + unit) << s) | i;
+        o[0] = g == x ? 1.0 : 0.0;
+        o[1] = 0.0;
+    }
+};
+
+template <class Src> void engine_store(qcsim_engine *e, const Src &src) {
+    const int units = (int)e->ns;
+    const int nxt = e->cur ^ 1;
+    const uint64_t ntiles = (e->L + kTile - 1) / kTile;
+    if (e->compressed) {
+        e->index[nxt].ensure(2 * e->ns * e->nidx);
+        EncodeResult R = encode_batch<2, Src>(e->st, e->enc, src, units, e->L, e->cfg.codec, e->log2C,
+                                              e->index[nxt].p, e->arena[nxt], false, false);
+        e->blk_off[nxt].ensure(2 * e->ns);
+        CK(cudaMemcpyAsync(e->blk_off[nxt].p, e->enc.blk_off.p, 2 * e->ns * sizeof(uint64_t),
+                           cudaMemcpyDeviceToDevice, e->st));
+        e->blk_bytes_h = R.block_bytes;
+        e->fallback += R.fallback;
+        record_sizes(e, R.block_bytes);
+    } else {
+        e->dense[nxt].ensure(e->ns * 2 * e->L);
+        e->enc.tilesum.ensure(e->ns * ntiles);
+        dense_gate<Src><<<(unsigned)(units * ntiles), 256, 0, e->st>>>(src, units, e->L, e->dense[nxt].p,
+                                                                        e->enc.tilesum.p);
+        ++g_launches;
+    }
+    // per-slice sq_norm from the tile partials
+    e->slice_sq.ensure(e->ns);
+    slice_norms<<<(units + 127) / 128, 128, 0, e->st>>>(e->enc.tilesum.p, (int)ntiles, units, e->slice_sq.p);
+    ++g_launches;
+    std::vector<double> sq(e->ns);
+    CK(cudaMemcpyAsync(sq.data(), e->slice_sq.p, e->ns * sizeof(double), cudaMemcpyDeviceToHost, e->st));
+    CK(cudaStreamSynchronize(e->st));
+    CK(cudaGetLastError());
+    for (uint64_t k = 0; k < e->ns; ++k) e->sq_norm[e->s0 + k] = sq[k];
+    e->cur = nxt;
+    e->loaded = true;
+}
+
+// Decodes the current state of the local slices (plus imported partner
+// slices) into e->old, slot k = local slice k, then imported ones.
+void engine_decode_old(qcsim_engine *e, bool need_imported) {
+    const uint64_t extra = need_imported ? e->imported.size() : 0;
+    const uint64_t slots = e->ns + extra;
+    e->old.ensure(slots * 2 * e->L);
+    if (!e->compressed) {
+        CK(cudaMemcpyAsync(e->old.p, e->dense[e->cur].p, e->ns * 2 * e->L * sizeof(double),
+                           cudaMemcpyDeviceToDevice, e->st));
+    } else {
+        std::vector<double *> ptrs(2 * e->ns);
+        for (uint64_t k = 0; k < 2 * e->ns; ++k) ptrs[k] = e->old.p + k * e->L;
+        e->outptrs.ensure(2 * slots);
+        CK(cudaMemcpyAsync(e->outptrs.p, ptrs.data(), ptrs.size() * sizeof(double *), cudaMemcpyHostToDevice,
+                           e->st));
+        decode_batch(e->st, e->dec, e->arena[e->cur].p, e->blk_off[e->cur].p, e->index[e->cur].p, e->outptrs.p,
+                     (int)(2 * e->ns), e->L, e->log2C, e->cfg.codec.quant_code_bits);
+    }
+    if (extra) {
+        // imported blocks: validating serial decode (they carry no index)
+        std::vector<uint8_t> all;
+        std::vector<uint64_t> offs;
+        for (auto &kv : e->imported) {
+            uint64_t pos = 0;
+            for (int p = 0; p < 2; ++p) {
+                uint64_t used = 0;
+                parse_header(kv.second.data() + pos, kv.second.size() - pos, &used);
+                offs.push_back(all.size());
+                all.insert(all.end(), kv.second.begin() + pos, kv.second.begin() + pos + used);
+                pos += used;
+            }
+        }
+        e->imp_bytes.ensure(all.size() + 64);
+        e->imp_off.ensure(offs.size());
+        CK(cudaMemcpyAsync(e->imp_bytes.p, all.data(), all.size(), cudaMemcpyHostToDevice, e->st));
+        CK(cudaMemcpyAsync(e->imp_off.p, offs.data(), offs.size() * 8, cudaMemcpyHostToDevice, e->st));
+        std::vector<double *> ptrs(offs.size());
+        for (uint64_t k = 0; k < offs.size(); ++k) ptrs[k] = e->old.p + (2 * e->ns + k) * e->L;
+        DBuf<double *> dp;
+        dp.ensure(ptrs.size());
+        CK(cudaMemcpyAsync(dp.p, ptrs.data(), ptrs.size() * sizeof(double *), cudaMemcpyHostToDevice, e->st));
+        e->val.ensure(offs.size(), std::min<uint64_t>(e->L + 1, (1ull << e->cfg.codec.quant_code_bits) + 1));
+        ValArgs V;
+        V.blocks = e->imp_bytes.p;
+        V.blk_off = e->imp_off.p;
+        V.out = dp.p;
+        V.err = e->val.err.p;
+        V.ssym = e->val.ssym.p;
+        V.slen = e->val.slen.p;
+        V.cap = std::min<uint64_t>(e->L + 1, (1ull << e->cfg.codec.quant_code_bits) + 1);
+        dec_validate<<<(unsigned)((offs.size() + 31) / 32), 32, 0, e->st>>>(V, (int)offs.size());
+        ++g_launches;
+        std::vector<uint32_t> errs(offs.size());
+        CK(cudaMemcpyAsync(errs.data(), e->val.err.p, errs.size() * 4, cudaMemcpyDeviceToHost, e->st));
+        CK(cudaStreamSynchronize(e->st));
+        for (uint32_t x : errs)
+            if (x) raise(QCSIM_CODEC, dec_message(x));
+    }
+}
+
+void engine_gate(qcsim_engine *e, const qcsim_action &a) {
+    if (a.kind > 2) raise(QCSIM_INVALID_ARGUMENT, "unknown action kind");
+    if (a.kind == QCSIM_ACTION_BUTTERFLY && (a.target < 0 || a.target >= e->n))
+        raise(QCSIM_INVALID_ARGUMENT, "action qubit out of range");
+    if (a.kind == QCSIM_ACTION_SWAP && (a.a < 0 || a.a >= e->n || a.b < 0 || a.b >= e->n || a.a == a.b))
+        raise(QCSIM_INVALID_ARGUMENT, "action qubit out of range");
+    // normalization, computed on the host from the
+    // deterministic tree over every slice's sq_norm
+    const bool apply = e->cfg.norm_every > 0 && (e->gates % (uint64_t)e->cfg.norm_every) == 0;
+    double scale = 1.0;
+    if (apply) {
+        const double G = tree_sum_host(e->sq_norm.data(), e->S);
+        if (!std::isfinite(G) || std::fabs(G - 1.0) > 10.0 * e->cfg.norm_drift_tolerance) {
+            char buf[160];
+            std::snprintf(buf, sizeof buf, "norm drift before gate %llu: global sq_norm %.17g",
+                          (unsigned long long)e->gates, G);
+            raise(QCSIM_NUMERIC, buf);
+        }
+        scale = 1.0 / std::sqrt(G);
+    }
+    // which old slices are needed: local + partners (imported if remote)
+    bool remote = false;
+    for (uint64_t k = 0; k < e->ns; ++k) {
+        const uint64_t pj = partner_slice(a, e->s, e->s0 + k);
+        if (pj < e->s0 || pj >= e->s0 + e->ns) remote = true;
+    }
+    std::vector<int32_t> slot(e->S, -1);
+    for (uint64_t k = 0; k < e->ns; ++k) slot[e->s0 + k] = (int32_t)k;
+    if (remote) {
+        for (uint64_t k = 0; k < e->ns; ++k) {
+            const uint64_t pj = partner_slice(a, e->s, e->s0 + k);
+            if (pj >= e->s0 && pj < e->s0 + e->ns) continue;
+            int found = -1;
+            for (size_t m = 0; m < e->imported.size(); ++m)
+                if (e->imported[m].first == pj) found = (int)m;
+            if (found < 0)
+                raise(QCSIM_INVALID_ARGUMENT,
+                      "partner slice " + std::to_string(pj) + " not imported (multi-rank exchange missing)");
+            slot[pj] = (int32_t)(e->ns + found);
+        }
+    }
+    engine_decode_old(e, remote);
+    e->slot_of.ensure(e->S);
+    CK(cudaMemcpyAsync(e->slot_of.p, slot.data(), e->S * sizeof(int32_t), cudaMemcpyHostToDevice, e->st));
+    std::vector<uint64_t> us(e->ns);
+    for (uint64_t k = 0; k < e->ns; ++k) us[k] = e->s0 + k;
+    e->unit_slice.ensure(e->ns);
+    CK(cudaMemcpyAsync(e->unit_slice.p, us.data(), e->ns * sizeof(uint64_t), cudaMemcpyHostToDevice, e->st));
+    e->enc.ensure(2 * e->ns, e->ns, e->L, e->cfg.codec.quant_code_bits);
+    // scale as a device scalar (read by every fetch)
+    e->scale_d.ensure(1);
+    CK(cudaMemcpyAsync(e->scale_d.p, &scale, sizeof(double), cudaMemcpyHostToDevice, e->st));
+    GateSrc g;
+    g.old = e->old.p;
+    g.slot_of = e->slot_of.p;
+    g.unit_slice = e->unit_slice.p;
+    g.scale = apply ? e->scale_d.p : nullptr;
+    g.act = to_dev(a);
+    g.s = e->s;
+    g.L = e->L;
+    engine_store(e, g);
+    e->gates++;
+    e->imported.clear();
+}
+
+} // namespace
+
+// ================================================================== C-ABI
+extern "C" {
+
+const char *qcsim_last_error(void) { return g_err.c_str(); }
+const char *qcsim_version(void) { return QCSIM_VERSION; }
+
+uint64_t qcsim_kernel_launches(void) { return g_launches; }
+
+qcsim_status qcsim_codec_validate(const qcsim_codec_config *cfg) {
+    return guarded([&] {
+        if (!cfg) raise(QCSIM_INVALID_ARGUMENT, "null config");
+        validate_codec(*cfg);
+    });
+}
+
+uint64_t qcsim_block_bound(uint64_t n, int32_t qb) {
+    uint64_t nsym = (1ull << qb) + 1;
+    if (nsym > n + 1) nsym = n + 1;
+    return kHeaderBytes + 4 + 5 * nsym + (n * kMaxCodeLen + 7) / 8 + 16 + n * 16;
+}
+
+qcsim_status qcsim_compress_plane(const double *values, uint64_t n, const qcsim_codec_config *cfg, uint8_t *out,
+                                  uint64_t capacity, uint64_t *out_len, qcsim_codec_stats *stats) {
+    return guarded([&] {
+        if (!cfg) raise(QCSIM_INVALID_ARGUMENT, "null config");
+        validate_codec(*cfg);
+        if (n == 0) raise(QCSIM_INVALID_ARGUMENT, "cannot compress an empty plane");
+        if (n >= (1ull << 32)) raise(QCSIM_CAPACITY, "plane longer than 2^32 elements");
+        CodecCtx &C = codec_ctx();
+        C.vals.ensure(n);
+        CK(cudaMemcpyAsync(C.vals.p, values, n * sizeof(double), cudaMemcpyHostToDevice, C.st));
+        C.ptrs.ensure(1);
+        const double *vp = C.vals.p;
+        CK(cudaMemcpyAsync(C.ptrs.p, &vp, sizeof vp, cudaMemcpyHostToDevice, C.st));
+        RawSrc src{C.ptrs.p};
+        const int log2C = auto_log2C(n);
+        C.index.ensure(((n >> log2C) + 1));
+        EncodeResult R = encode_batch<1, RawSrc>(C.st, C.enc, src, 1, n, *cfg, log2C, C.index.p, C.arena, true, true);
+        const uint64_t len = R.block_bytes[0];
+        if (out_len) *out_len = len;
+        if (stats) {
+            stats->input_bytes = 8 * n;
+            stats->output_bytes = len;
+            stats->ratio = (double)stats->input_bytes / (double)len;
+            uint32_t no = 0;
+            CK(cudaMemcpy(&no, C.enc.ocount.p, 4, cudaMemcpyDeviceToHost));
+            stats->outlier_fraction = (double)no / (double)n;
+        }
+        if (out) {
+            if (len > capacity) raise(QCSIM_INVALID_ARGUMENT, "output capacity too small");
+            CK(cudaMemcpyAsync(out, C.arena.p + R.blk_off[0], len, cudaMemcpyDeviceToHost, C.st));
+            CK(cudaStreamSynchronize(C.st));
+        }
+    });
+}
+
+qcsim_status qcsim_decompress_plane(const uint8_t *block, uint64_t len, double *out, uint64_t capacity,
+                                    uint64_t *n_out, uint64_t *consumed) {
+    return guarded([&] {
+        uint64_t used = 0;
+        Header h = parse_header(block, len, &used);
+        if (consumed) *consumed = used;
+        if (n_out) *n_out = h.n;
+        if (!out) return;
+        if (h.n > capacity) raise(QCSIM_INVALID_ARGUMENT, "output capacity too small");
+        CodecCtx &C = codec_ctx();
+        C.bytes.ensure(used + 64);
+        CK(cudaMemcpyAsync(C.bytes.p, block, used, cudaMemcpyHostToDevice, C.st));
+        C.vals.ensure(h.n);
+        C.optrs.ensure(1);
+        double *op = C.vals.p;
+        CK(cudaMemcpyAsync(C.optrs.p, &op, sizeof op, cudaMemcpyHostToDevice, C.st));
+        C.offs.ensure(1);
+        CK(cudaMemsetAsync(C.offs.p, 0, 8, C.st));
+        uint32_t tc = 0;
+        if (h.payload >= 4) tc = (uint32_t)(block[40] | (block[41] << 8) | (block[42] << 16) | ((uint32_t)block[43] << 24));
+        const uint64_t cap = std::max<uint64_t>(1, std::min<uint64_t>(tc, (1ull << 25)));
+        C.val.ensure(1, cap);
+        ValArgs V;
+        V.blocks = C.bytes.p;
+        V.blk_off = C.offs.p;
+        V.out = C.optrs.p;
+        V.err = C.val.err.p;
+        V.ssym = C.val.ssym.p;
+        V.slen = C.val.slen.p;
+        V.cap = cap;
+        dec_validate<<<1, 32, 0, C.st>>>(V, 1);
+        ++g_launches;
+        uint32_t e = 0;
+        CK(cudaMemcpyAsync(&e, C.val.err.p, 4, cudaMemcpyDeviceToHost, C.st));
+        CK(cudaStreamSynchronize(C.st));
+        CK(cudaGetLastError());
+        if (e) raise(QCSIM_CODEC, dec_message(e));
+        CK(cudaMemcpyAsync(out, C.vals.p, h.n * sizeof(double), cudaMemcpyDeviceToHost, C.st));
+        CK(cudaStreamSynchronize(C.st));
+    });
+}
+
+qcsim_status qcsim_compress_planes_device(const double *const *values, const uint64_t *n, uint32_t planes,
+                                          const qcsim_codec_config *cfg, uint8_t *out, uint64_t capacity,
+                                          uint64_t *offsets_host, qcsim_codec_stats *stats_host, void *stream) {
+    return guarded([&] {
+        if (!cfg) raise(QCSIM_INVALID_ARGUMENT, "null config");
+        validate_codec(*cfg);
+        if (planes == 0) return;
+        for (uint32_t p = 1; p < planes; ++p)
+            if (n[p] != n[0]) raise(QCSIM_INVALID_ARGUMENT, "batched planes must have equal length");
+        if (n[0] == 0) raise(QCSIM_INVALID_ARGUMENT, "cannot compress an empty plane");
+        CodecCtx &C = codec_ctx();
+        cudaStream_t st = stream ? (cudaStream_t)stream : C.st;
+        C.ptrs.ensure(planes);
+        CK(cudaMemcpyAsync(C.ptrs.p, values, planes * sizeof(double *), cudaMemcpyHostToDevice, st));
+        const uint64_t L = n[0];
+        const int log2C = auto_log2C(L);
+        C.index.ensure(planes * ((L >> log2C) + 1));
+        RawSrc src{C.ptrs.p};
+        EncodeResult R =
+            encode_batch<1, RawSrc>(st, C.enc, src, (int)planes, L, *cfg, log2C, C.index.p, C.arena, true, true);
+        uint64_t o = 0;
+        for (uint32_t p = 0; p < planes; ++p) {
+            offsets_host[p] = o;
+            o += R.block_bytes[p];
+        }
+        offsets_host[planes] = o;
+        if (o > capacity) raise(QCSIM_INVALID_ARGUMENT, "output capacity too small");
+        for (uint32_t p = 0; p < planes; ++p) {
+            CK(cudaMemcpyAsync(out + offsets_host[p], C.arena.p + R.blk_off[p], R.block_bytes[p],
+                               cudaMemcpyDeviceToDevice, st));
+            if (stats_host) {
+                stats_host[p].input_bytes = 8 * L;
+                stats_host[p].output_bytes = R.block_bytes[p];
+                stats_host[p].ratio = (double)(8 * L) / (double)R.block_bytes[p];
+            }
+        }
+        if (stats_host) {
+            std::vector<uint32_t> oc(planes);
+            CK(cudaMemcpyAsync(oc.data(), C.enc.ocount.p, planes * 4, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            for (uint32_t p = 0; p < planes; ++p) stats_host[p].outlier_fraction = (double)oc[p] / (double)L;
+        }
+        CK(cudaStreamSynchronize(st));
+    });
+}
+
+qcsim_status qcsim_decompress_planes_device(const uint8_t *blocks, const uint64_t *offsets_host, uint32_t planes,
+                                            double *const *out, const uint64_t *capacity, void *stream) {
+    return guarded([&] {
+        if (planes == 0) return;
+        CodecCtx &C = codec_ctx();
+        cudaStream_t st = stream ? (cudaStream_t)stream : C.st;
+        // header checks on the host copy of each header
+        uint64_t maxtc = 1;
+        for (uint32_t p = 0; p < planes; ++p) {
+            uint8_t hdr[44];
+            const uint64_t avail = offsets_host[p + 1] - offsets_host[p];
+            CK(cudaMemcpy(hdr, blocks + offsets_host[p], std::min<uint64_t>(44, avail), cudaMemcpyDeviceToHost));
+            Header h = parse_header(hdr, avail, nullptr);
+            if (h.n > capacity[p]) raise(QCSIM_INVALID_ARGUMENT, "output capacity too small");
+            if (h.payload >= 4)
+                maxtc = std::max<uint64_t>(maxtc, hdr[40] | (hdr[41] << 8) | (hdr[42] << 16) | ((uint64_t)hdr[43] << 24));
+        }
+        maxtc = std::min<uint64_t>(maxtc, 1ull << 25);
+        C.offs.ensure(planes);
+        CK(cudaMemcpyAsync(C.offs.p, offsets_host, planes * 8, cudaMemcpyHostToDevice, st));
+        C.optrs.ensure(planes);
+        CK(cudaMemcpyAsync(C.optrs.p, out, planes * sizeof(double *), cudaMemcpyHostToDevice, st));
+        C.val.ensure(planes, maxtc);
+        ValArgs V;
+        V.blocks = blocks;
+        V.blk_off = C.offs.p;
+        V.out = C.optrs.p;
+        V.err = C.val.err.p;
+        V.ssym = C.val.ssym.p;
+        V.slen = C.val.slen.p;
+        V.cap = maxtc;
+        dec_validate<<<(planes + 31) / 32, 32, 0, st>>>(V, (int)planes);
+        ++g_launches;
+        std::vector<uint32_t> errs(planes);
+        CK(cudaMemcpyAsync(errs.data(), C.val.err.p, planes * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        CK(cudaGetLastError());
+        for (uint32_t x : errs)
+            if (x) raise(QCSIM_CODEC, dec_message(x));
+    });
+}
+
+// ------------------------------------------------------------- engine API
+qcsim_status qcsim_engine_create(const qcsim_engine_config *cfg, qcsim_engine **out) {
+    return guarded([&] {
+        if (!cfg || !out) raise(QCSIM_INVALID_ARGUMENT, "null argument");
+        *out = nullptr;
+        const qcsim_engine_config &c = *cfg;
+        if (c.num_qubits < 1 || c.num_qubits > 62) raise(QCSIM_INVALID_ARGUMENT, "qubit count must be in [1, 62]");
+        int s = c.slice_bits < 0 ? std::min(c.num_qubits, 20) : c.slice_bits;
+        if (s < 0 || s > c.num_qubits) raise(QCSIM_INVALID_ARGUMENT, "slice_bits must be in [0, num_qubits]");
+        if (s > 22) raise(QCSIM_CAPACITY, "slice_bits above 22 not supported on the device path");
+        if (c.compression_enabled) validate_codec(c.codec);
+        if (!(c.norm_drift_tolerance >= 0.0)) raise(QCSIM_INVALID_ARGUMENT, "norm drift tolerance must be >= 0");
+        if (c.norm_every < 0) raise(QCSIM_INVALID_ARGUMENT, "norm_every must be >= 0");
+        const int world = c.world > 0 ? c.world : 1;
+        const uint64_t S = 1ull << (c.num_qubits - s);
+        if (c.rank < 0 || c.rank >= world || S % (uint64_t)world) raise(QCSIM_INVALID_ARGUMENT, "bad rank/world for slice count");
+        ensure_device(c.device);
+        auto *e = new qcsim_engine();
+        e->cfg = c;
+        e->cfg.slice_bits = s;
+        e->cfg.world = world;
+        e->n = c.num_qubits;
+        e->s = s;
+        e->S = S;
+        e->L = 1ull << s;
+        e->ns = S / (uint64_t)world;
+        e->s0 = (uint64_t)c.rank * e->ns;
+        e->log2C = c.checkpoint_bits > 0 ? c.checkpoint_bits : auto_log2C(e->L);
+        e->nidx = (e->L >> e->log2C) + 1;
+        e->compressed = c.compression_enabled != 0;
+        e->sq_norm.assign(S, 0.0);
+        e->launches0 = g_launches;
+        cudaError_t err = cudaStreamCreateWithFlags(&e->st, cudaStreamNonBlocking);
+        if (err != cudaSuccess) {
+            delete e;
+            ck(err, "cudaStreamCreate");
+        }
+        CK(cudaEventCreate(&e->ev0));
+        CK(cudaEventCreate(&e->ev1));
+        *out = e;
+    });
+}
+
+qcsim_status qcsim_engine_destroy(qcsim_engine *e) {
+    return guarded([&] {
+        if (!e) return;
+        if (e->st) cudaStreamSynchronize(e->st);
+        if (e->ev0) cudaEventDestroy(e->ev0);
+        if (e->ev1) cudaEventDestroy(e->ev1);
+        if (e->st) cudaStreamDestroy(e->st);
+        delete e;
+    });
+}
+
+qcsim_status qcsim_engine_load_basis(qcsim_engine *e, uint64_t x) {
+    return guarded([&] {
+        if (!e) raise(QCSIM_INVALID_ARGUMENT, "null engine");
+        if (x >= (1ull << e->n)) raise(QCSIM_INVALID_ARGUMENT, "basis index out of range");
+        CK(cudaSetDevice(e->cfg.device));
+        std::fill(e->sq_norm.begin(), e->sq_norm.end(), 0.0);
+        const uint64_t xs = x >> e->s;
+        if (xs < e->s0 || xs >= e->s0 + e->ns) {
+            // remote ranks own |x>; the local slices are all zero
+        }
+        BasisSrc src{x, e->s0, e->s};
+        engine_store(e, src);
+        // the owner knows the only nonzero norm; keep the global view exact
+        e->sq_norm[xs] = 1.0;
+    });
+}
+
+qcsim_status qcsim_engine_load_amplitudes(qcsim_engine *e, const double *amps, uint64_t count) {
+    return guarded([&] {
+        if (!e || !amps) raise(QCSIM_INVALID_ARGUMENT, "null argument");
+        if (count != (1ull << e->n)) raise(QCSIM_INVALID_ARGUMENT, "amplitude count must be 2^n");
+        CK(cudaSetDevice(e->cfg.device));
+        std::vector<double> planar(e->ns * 2 * e->L);
+        for (uint64_t k = 0; k < e->ns; ++k)
+            for (uint64_t i = 0; i < e->L; ++i) {
+                const uint64_t g = ((e->s0 + k) << e->s) | i;
+                planar[k * 2 * e->L + i] = amps[2 * g];
+                planar[k * 2 * e->L + e->L + i] = amps[2 * g + 1];
+            }
+        e->old.ensure(planar.size());
+        CK(cudaMemcpyAsync(e->old.p, planar.data(), planar.size() * sizeof(double), cudaMemcpyHostToDevice, e->st));
+        PlanarSrc src{e->old.p, e->L};
+        engine_store(e, src);
+    });
+}
+
+qcsim_status qcsim_engine_run(qcsim_engine *e, const qcsim_action *actions, uint64_t count,
+                              qcsim_run_metrics *m) {
+    return guarded([&] {
+        if (!e) raise(QCSIM_INVALID_ARGUMENT, "null engine");
+        if (!e->loaded) raise(QCSIM_INVALID_ARGUMENT, "engine has no state (load_basis / load_amplitudes first)");
+        CK(cudaSetDevice(e->cfg.device));
+        if (count) {
+            CK(cudaEventRecord(e->ev0, e->st));
+            for (uint64_t k = 0; k < count; ++k) engine_gate(e, actions[k]);
+            CK(cudaEventRecord(e->ev1, e->st));
+            CK(cudaEventSynchronize(e->ev1));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+            e->wall += ms * 1e-3;
+        }
+        if (m) {
+            std::memset(m, 0, sizeof *m);
+            m->min_compression_ratio = e->calls ? e->ratio_min : 0.0;
+            m->mean_compression_ratio = e->calls ? e->ratio_sum / (double)e->calls : 0.0;
+            m->wall_seconds = e->wall;
+            m->final_norm = tree_sum_host(e->sq_norm.data(), e->S);
+            m->compress_calls = e->calls;
+            m->gates = e->gates;
+            m->peak_compressed_bytes = e->peak;
+            m->dense_bytes = 16ull << e->n;
+            m->current_compressed_bytes = e->current;
+            m->index_bytes = e->compressed ? 2 * e->ns * e->nidx * sizeof(IndexRec) : 0;
+            m->fallback_planes = e->fallback;
+            m->kernel_launches = g_launches - e->launches0;
+        }
+    });
+}
+
+qcsim_status qcsim_engine_gather(qcsim_engine *e, double *amps, uint64_t capacity, int32_t guard) {
+    return guarded([&] {
+        if (!e || !amps) raise(QCSIM_INVALID_ARGUMENT, "null argument");
+        if (e->n > guard)
+            raise(QCSIM_CAPACITY, "dense materialization of " + std::to_string(e->n) + " qubits exceeds the " +
+                                      std::to_string(guard) + "-qubit guard");
+        if (capacity < 2 * e->ns * e->L) raise(QCSIM_INVALID_ARGUMENT, "output capacity too small");
+        CK(cudaSetDevice(e->cfg.device));
+        engine_decode_old(e, false);
+        std::vector<double> planar(e->ns * 2 * e->L);
+        CK(cudaMemcpyAsync(planar.data(), e->old.p, planar.size() * sizeof(double), cudaMemcpyDeviceToHost, e->st));
+        CK(cudaStreamSynchronize(e->st));
+        CK(cudaGetLastError());
+        for (uint64_t k = 0; k < e->ns; ++k)
+            for (uint64_t i = 0; i < e->L; ++i) {
+                amps[2 * (k * e->L + i)] = planar[k * 2 * e->L + i];
+                amps[2 * (k * e->L + i) + 1] = planar[k * 2 * e->L + e->L + i];
+            }
+    });
+}
+
+qcsim_status qcsim_engine_slice_norms(qcsim_engine *e, double *out, uint64_t capacity) {
+    return guarded([&] {
+        if (!e || !out) raise(QCSIM_INVALID_ARGUMENT, "null argument");
+        if (capacity < e->ns) raise(QCSIM_INVALID_ARGUMENT, "output capacity too small");
+        std::memcpy(out, e->sq_norm.data() + e->s0, e->ns * sizeof(double));
+    });
+}
+
+qcsim_status qcsim_engine_export_blocks(qcsim_engine *e, uint8_t *out, uint64_t capacity, uint64_t *len,
+                                        uint64_t *offsets, uint64_t offsets_cap) {
+    return guarded([&] {
+        if (!e || !len) raise(QCSIM_INVALID_ARGUMENT, "null argument");
+        if (!e->compressed) raise(QCSIM_INVALID_ARGUMENT, "engine is not compressed");
+        const uint64_t P = 2 * e->ns;
+        uint64_t tot = 0;
+        for (uint64_t k = 0; k < P; ++k) {
+            if (offsets && k < offsets_cap) offsets[k] = tot;
+            tot += e->blk_bytes_h[k];
+        }
+        if (offsets && P < offsets_cap) offsets[P] = tot;
+        *len = tot;
+        if (!out) return;
+        if (capacity < tot) raise(QCSIM_INVALID_ARGUMENT, "output capacity too small");
+        std::vector<uint64_t> off(P);
+        CK(cudaMemcpyAsync(off.data(), e->blk_off[e->cur].p, P * 8, cudaMemcpyDeviceToHost, e->st));
+        CK(cudaStreamSynchronize(e->st));
+        // one contiguous device->host copy of the arena, then gather on host
+        uint64_t hi = 0;
+        for (uint64_t k = 0; k < P; ++k) hi = std::max(hi, off[k] + e->blk_bytes_h[k]);
+        std::vector<uint8_t> host(hi);
+        CK(cudaMemcpyAsync(host.data(), e->arena[e->cur].p, hi, cudaMemcpyDeviceToHost, e->st));
+        CK(cudaStreamSynchronize(e->st));
+        uint64_t o = 0;
+        for (uint64_t k = 0; k < P; ++k) {
+            std::memcpy(out + o, host.data() + off[k], e->blk_bytes_h[k]);
+            o += e->blk_bytes_h[k];
+        }
+    });
+}
+
+qcsim_status qcsim_engine_partner_blocks_needed(qcsim_engine *e, const qcsim_action *a, uint64_t *remote,
+                                                uint64_t capacity, uint64_t *count) {
+    return guarded([&] {
+        if (!e || !a || !count) raise(QCSIM_INVALID_ARGUMENT, "null argument");
+        std::vector<uint64_t> need;
+        for (uint64_t k = 0; k < e->ns; ++k) {
+            const uint64_t pj = partner_slice(*a, e->s, e->s0 + k);
+            if (pj < e->s0 || pj >= e->s0 + e->ns) need.push_back(pj);
+        }
+        *count = need.size();
+        if (remote) {
+            if (capacity < need.size()) raise(QCSIM_INVALID_ARGUMENT, "output capacity too small");
+            std::copy(need.begin(), need.end(), remote);
+        }
+    });
+}
+
+qcsim_status qcsim_engine_export_slice(qcsim_engine *e, uint64_t slice, uint8_t *out, uint64_t capacity,
+                                       uint64_t *len) {
+    return guarded([&] {
+        if (!e || !len) raise(QCSIM_INVALID_ARGUMENT, "null argument");
+        if (slice < e->s0 || slice >= e->s0 + e->ns) raise(QCSIM_INVALID_ARGUMENT, "slice not owned by this rank");
+        if (!e->compressed) raise(QCSIM_INVALID_ARGUMENT, "engine is not compressed");
+        const uint64_t k = slice - e->s0;
+        const uint64_t b0 = e->blk_bytes_h[2 * k], b1 = e->blk_bytes_h[2 * k + 1];
+        *len = b0 + b1;
+        if (!out) return;
+        if (capacity < b0 + b1) raise(QCSIM_INVALID_ARGUMENT, "output capacity too small");
+        uint64_t off[2];
+        CK(cudaMemcpyAsync(off, e->blk_off[e->cur].p + 2 * k, 16, cudaMemcpyDeviceToHost, e->st));
+        CK(cudaStreamSynchronize(e->st));
+        CK(cudaMemcpyAsync(out, e->arena[e->cur].p + off[0], b0, cudaMemcpyDeviceToHost, e->st));
+        CK(cudaMemcpyAsync(out + b0, e->arena[e->cur].p + off[1], b1, cudaMemcpyDeviceToHost, e->st));
+        CK(cudaStreamSynchronize(e->st));
+    });
+}
+
+qcsim_status qcsim_engine_import_partner(qcsim_engine *e, uint64_t slice, const uint8_t *blocks, uint64_t len) {
+    return guarded([&] {
+        if (!e || !blocks) raise(QCSIM_INVALID_ARGUMENT, "null argument");
+        if (slice >= e->S) raise(QCSIM_INVALID_ARGUMENT, "slice out of range");
+        e->imported.emplace_back(slice, std::vector<uint8_t>(blocks, blocks + len));
+    });
+}
+
+qcsim_status qcsim_engine_set_global_norms(qcsim_engine *e, const double *norms, uint64_t count) {
+    return guarded([&] {
+        if (!e || !norms) raise(QCSIM_INVALID_ARGUMENT, "null argument");
+        if (count != e->S) raise(QCSIM_INVALID_ARGUMENT, "norm table must hold every slice");
+        std::memcpy(e->sq_norm.data(), norms, count * sizeof(double));
+    });
+}
+
+} // extern "C"

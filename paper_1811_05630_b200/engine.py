@@ -1,0 +1,175 @@
+"""Engine API -- Algorithm 1 as specified by SPEC.md:297-392
+(the reference ships no engine source; semantics pinned in DESIGN.md §3).
+
+    eng = Engine(EngineConfig(num_qubits=16, slice_bits=12,
+                              codec=CodecConfig(CodecMode.Absolute, 1e-5)))
+    eng.load_basis(x)
+    metrics = eng.run(build_qft(16))      # gate passes on the GPU
+    amps = eng.gather()
+
+Every gate pass runs on the device (libqcsim_b200.so): decode -> normalize
+-> gate -> sq_norm -> encode, bit-exact with the CPU oracle.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .circuit import Circuit, lower
+from .codec import CodecConfig, CodecMode
+from .errors import raise_status
+
+
+@dataclass
+class EngineConfig:
+    """EngineConfig.  norm_every: 0 off, 1 every gate,
+    k every k-th gate.  workers is accepted for API parity; the device
+    processes all slices of a pass concurrently."""
+    num_qubits: int = 1
+    slice_bits: int = -1
+    codec: CodecConfig = field(default_factory=lambda: CodecConfig(CodecMode.Absolute, 1e-5))
+    compression_enabled: bool = True
+    workers: int = 1
+    norm_every: int = 1
+    norm_drift_tolerance: float = 0.02
+    device: int = 0
+    rank: int = 0
+    world: int = 1
+    checkpoint_bits: int = 0
+
+    def to_c(self) -> _native.EngineConfigC:
+        return _native.EngineConfigC(self.num_qubits, self.slice_bits, self.codec.to_c(),
+                                     int(self.compression_enabled), self.norm_every, self.norm_drift_tolerance,
+                                     self.device, self.rank, self.world, self.checkpoint_bits, 0)
+
+
+@dataclass
+class RunMetrics:
+    """RunMetrics."""
+    min_compression_ratio: float
+    mean_compression_ratio: float
+    wall_seconds: float
+    final_norm: float
+    compress_calls: int
+    gates: int
+    peak_compressed_bytes: int
+    dense_bytes: int
+    current_compressed_bytes: int
+    index_bytes: int
+    fallback_planes: int
+    kernel_launches: int
+
+    @classmethod
+    def from_c(cls, m: _native.RunMetricsC):
+        return cls(*[getattr(m, f) for f, _ in _native.RunMetricsC._fields_])
+
+
+def _actions(actions):
+    if isinstance(actions, Circuit):
+        actions = lower(actions)
+    arr = (_native.ActionC * max(1, len(actions)))()
+    for i, a in enumerate(actions):
+        arr[i] = a
+    return arr, len(actions)
+
+
+class Engine:
+    def __init__(self, config: EngineConfig):
+        self.L = _native.lib()
+        self.config = config
+        c = config.to_c()
+        h = C.c_void_p()
+        raise_status(self.L.qcsim_engine_create(C.byref(c), C.byref(h)), self.L)
+        self.h = h
+        self.n = config.num_qubits
+        self.s = config.slice_bits if config.slice_bits >= 0 else min(self.n, 20)
+        self.world = max(1, config.world)
+        self.local_slices = (1 << (self.n - self.s)) // self.world
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.qcsim_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def _ck(self, rc):
+        raise_status(rc, self.L)
+
+    def load_basis(self, x: int):
+        self._ck(self.L.qcsim_engine_load_basis(self.h, x))
+
+    def load_amplitudes(self, amps):
+        a = np.ascontiguousarray(amps)
+        if np.iscomplexobj(a):
+            a = a.view(np.float64)
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        self._ck(self.L.qcsim_engine_load_amplitudes(self.h, a.ctypes.data_as(_native.dp), a.size // 2))
+
+    def run(self, actions=()) -> RunMetrics:
+        arr, n = _actions(actions)
+        m = _native.RunMetricsC()
+        self._ck(self.L.qcsim_engine_run(self.h, arr, n, C.byref(m)))
+        return RunMetrics.from_c(m)
+
+    def metrics(self) -> RunMetrics:
+        return self.run(())
+
+    def gather(self, guard_qubits: int = 28) -> np.ndarray:
+        """Interleaved (re, im) amplitudes of this rank's slices."""
+        out = np.empty(2 * self.local_slices << self.s, dtype=np.float64)
+        self._ck(self.L.qcsim_engine_gather(self.h, out.ctypes.data_as(_native.dp), out.size, guard_qubits))
+        return out
+
+    def amplitudes(self, guard_qubits: int = 28) -> np.ndarray:
+        g = self.gather(guard_qubits)
+        return g[0::2] + 1j * g[1::2]
+
+    def slice_norms(self) -> np.ndarray:
+        out = np.empty(self.local_slices, dtype=np.float64)
+        self._ck(self.L.qcsim_engine_slice_norms(self.h, out.ctypes.data_as(_native.dp), out.size))
+        return out
+
+    def export_blocks(self):
+        ln = C.c_uint64()
+        P = 2 * self.local_slices
+        offs = (C.c_uint64 * (P + 1))()
+        self._ck(self.L.qcsim_engine_export_blocks(self.h, None, 0, C.byref(ln), offs, P + 1))
+        out = np.empty(ln.value, dtype=np.uint8)
+        self._ck(self.L.qcsim_engine_export_blocks(self.h, out.ctypes.data_as(_native.u8p), out.size,
+                                                   C.byref(ln), offs, P + 1))
+        return out.tobytes(), list(offs)
+
+    # ---- multi-rank hooks (paper_1811_05630_b200/distributed.py drives them)
+    def partner_slices_needed(self, action) -> list:
+        cnt = C.c_uint64()
+        a = action
+        self._ck(self.L.qcsim_engine_partner_blocks_needed(self.h, C.byref(a), None, 0, C.byref(cnt)))
+        buf = (C.c_uint64 * max(1, cnt.value))()
+        self._ck(self.L.qcsim_engine_partner_blocks_needed(self.h, C.byref(a), buf, cnt.value, C.byref(cnt)))
+        return list(buf[: cnt.value])
+
+    def export_slice(self, slice_index: int) -> bytes:
+        ln = C.c_uint64()
+        self._ck(self.L.qcsim_engine_export_slice(self.h, slice_index, None, 0, C.byref(ln)))
+        out = np.empty(ln.value, dtype=np.uint8)
+        self._ck(self.L.qcsim_engine_export_slice(self.h, slice_index, out.ctypes.data_as(_native.u8p), out.size,
+                                                  C.byref(ln)))
+        return out.tobytes()
+
+    def import_partner(self, slice_index: int, data: bytes):
+        b = np.frombuffer(data, dtype=np.uint8).copy()
+        self._ck(self.L.qcsim_engine_import_partner(self.h, slice_index, b.ctypes.data_as(_native.u8p), b.size))
+
+    def set_global_norms(self, norms):
+        v = np.ascontiguousarray(norms, dtype=np.float64)
+        self._ck(self.L.qcsim_engine_set_global_norms(self.h, v.ctypes.data_as(_native.dp), v.size))
+
+
+def kernel_launches() -> int:
+    """Kernels launched by libqcsim_b200.so in this process."""
+    return int(_native.lib().qcsim_kernel_launches())
