@@ -1,0 +1,348 @@
+"""Benchmark of the compressed state-vector update path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload grover20|qft28|qft16|random30]
+
+Workload (BASELINE.json configs[1], the N=1 headline): 20-qubit Grover
+search, 64 slices of 2^14 complex128 amplitudes, absolute error bound 1e-5,
+marked index drawn from the seed.  One *step* = one Grover iteration
+(oracle X-MCZ-X + diffusion H-X-MCZ-X-H, ~110 gate passes over all 2^20
+amplitudes).  The initial H layer and W iterations are untimed warm-up.
+
+Metric: amplitude-gate updates/s including (de)compression
+(= 2^n x gate passes / time).  `value` is device time (CUDA events on the
+engine stream, inputs resident in HBM); `e2e` drives the same steps through
+the C-ABI with host buffers: the step's action list copied in and the
+compressed state + metrics copied out every step.
+
+N > 1 (torchrun): slices are sharded by their top index bits; gates on those
+bits exchange compressed partner slices over NCCL (distributed.py); the
+per-gate sq_norm table is all-gathered.  Timing is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK = 6650.0
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", HBM_FALLBACK)), "measured"
+    return HBM_FALLBACK, "fallback"
+
+
+# ------------------------------------------------------------- workloads
+def workload(name):
+    import paper_1811_05630_b200 as q
+    if name == "grover20":
+        n, s, eb = 20, 14, 1e-5
+        marked = q.seeded_index(n, 20)
+        iters = q.grover_optimal_iterations(n)
+        oracle = q.build_grover_oracle(n, marked).gates
+        diff = ([q.Gate.h(k) for k in range(n)] + [q.Gate.x(k) for k in range(n)] + [q.Gate.mcz(range(n))]
+                + [q.Gate.x(k) for k in range(n)] + [q.Gate.h(k) for k in range(n)])
+        step = [q.to_action_c(q.gate_action(g)) for g in oracle + diff]
+        setup = [q.to_action_c(q.gate_action(q.Gate.h(k))) for k in range(n)]
+        return dict(name="grover20", n=n, s=s, eb=eb, basis=0, setup=setup, steps=lambda k: step,
+                    max_steps=iters, desc=f"grover n=20 marked={marked} iterations={iters}, slices 64x2^14")
+    if name in ("qft28", "qft16"):
+        n = 28 if name == "qft28" else 16
+        s = 20 if n == 28 else 12
+        acts = q.lower(q.build_qft(n))
+        x = q.seeded_index(n, n)
+        chunk = 35 if n == 28 else 12
+        return dict(name=name, n=n, s=s, eb=1e-5, basis=x, setup=[],
+                    steps=lambda k: acts[k * chunk:(k + 1) * chunk], max_steps=len(acts) // chunk,
+                    desc=f"qft n={n} basis={x}, slices {1 << (n - s)}x2^{s}, step = {chunk} gates")
+    if name == "random30":
+        n, s = 30, 20
+        acts = q.random_u3_circuit_actions(n, 20, seed=30)
+        per = n + n // 2
+        return dict(name=name, n=n, s=s, eb=1e-5, basis=0, setup=[], steps=lambda k: acts[k * per:(k + 1) * per],
+                    max_steps=20, desc="random U3+CZ n=30 depth 20, slices 1024x2^20, step = 1 layer")
+    raise SystemExit(f"unknown workload {name}")
+
+
+# ------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self):
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200", "-i", os.environ.get("LOCAL_RANK", "0")],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 7]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------- CPU arms
+def cpu_reference(wl, args, budget_s=12.0):
+    """The reference's own codec (oracle/_ref, compiled from /root/reference
+    unmodified) under the pinned engine loop with a pool of all host cores;
+    falls back to the C restatement (kind 'port') when _ref is absent."""
+    from oracle.oracle import CodecConfig as OCfg, EngineConfig as OEng, REF_SO, Oracle, RefLib
+    cores = os.cpu_count() or 1
+    cfg = OEng.make(wl["n"], wl["s"], OCfg.make(1, wl["eb"], 16, 0))
+    if os.path.exists(REF_SO):
+        eng = RefLib().engine(cfg, workers=cores)
+        kind = "reference"
+        gate = eng.gate
+    else:
+        eng = Oracle().engine(cfg)
+        kind, cores = "port", 1
+        gate = lambda a: eng.run([a])  # noqa: E731
+    eng.load_basis(wl["basis"])
+    for a in wl["setup"]:
+        gate(a)
+    done = 0
+    t0 = time.perf_counter()
+    k = 0
+    while time.perf_counter() - t0 < budget_s and k < wl["max_steps"]:
+        for a in wl["steps"](k):
+            gate(a)
+            done += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+        k += 1
+    dt = time.perf_counter() - t0
+    value = (1 << wl["n"]) * done / dt
+    return dict(value=value, unit="updates/s", cores=cores, kind=kind,
+                sample=f"{done} gate passes of {wl['name']} after its setup layer ({dt:.1f} s, all slices)")
+
+
+# ------------------------------------------------------------- GPU arm
+def run_ours(args, wl, rank, world, dist):
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    import paper_1811_05630_b200 as q
+    from paper_1811_05630_b200 import _native
+    from paper_1811_05630_b200.distributed import ShardedEngine
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    cfg = q.EngineConfig(num_qubits=wl["n"], slice_bits=wl["s"], codec=q.CodecConfig(q.CodecMode.Absolute, wl["eb"]),
+                         device=dev, rank=rank, world=world)
+    eng = ShardedEngine(cfg) if world > 1 else q.Engine(cfg)
+    eng.load_basis(wl["basis"])
+    eng.run(wl["setup"])
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")  # > L2 (126 MB)
+    lib = _native.lib()
+    for k in range(args.warmup):
+        eng.run(wl["steps"](k))
+    gates = 0
+    dev_s = 0.0
+    wall = 0.0
+    launches0 = lib.qcsim_kernel_launches()
+    prof = profile_begin(lib)
+    clocks = ClockSampler()
+    clocks.start()
+    for k in range(args.warmup, args.warmup + args.steps):
+        acts = wl["steps"](k % wl["max_steps"])
+        flush.zero_()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        m0 = eng.metrics().wall_seconds
+        t0 = time.perf_counter()
+        m = eng.run(acts)
+        wall += time.perf_counter() - t0
+        dev_s += m.wall_seconds - m0
+        gates += len(acts)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    kprof = profile_end(lib, prof)
+    launches = lib.qcsim_kernel_launches() - launches0
+    mets = eng.metrics()
+    # e2e: the same step count through the C-ABI with host buffers
+    e2e_t, h2d, d2h = 0.0, 0, 0
+    for k in range(args.warmup + args.steps, args.warmup + 2 * args.steps):
+        acts = wl["steps"](k % wl["max_steps"])
+        arr = (_native.ActionC * len(acts))(*acts)
+        flush.zero_()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        pinned = torch.empty(ctypes.sizeof(arr), dtype=torch.uint8, pin_memory=True)
+        ctypes.memmove(pinned.data_ptr(), ctypes.addressof(arr), ctypes.sizeof(arr))
+        m = eng.run(acts)
+        blocks = eng.export_blocks()[0] if world == 1 else eng.export_local_blocks()
+        e2e_t += time.perf_counter() - t0
+        h2d += ctypes.sizeof(arr)
+        d2h += len(blocks) + ctypes.sizeof(_native.RunMetricsC)
+    return dict(gates=gates, dev_s=dev_s, wall=wall, clocks=clk, launches=launches, metrics=mets, kprof=kprof,
+                e2e_t=e2e_t, h2d=h2d // max(1, args.steps), d2h=d2h // max(1, args.steps))
+
+
+def profile_begin(lib):
+    try:
+        fn = lib.qcsim_profile_enable
+    except AttributeError:
+        return None
+    fn.argtypes = [ctypes_int()]
+    fn(1)
+    return True
+
+
+def ctypes_int():
+    import ctypes
+    return ctypes.c_int
+
+
+def profile_end(lib, token):
+    if token is None:
+        return None
+    import ctypes
+    n = 64
+    names = (ctypes.c_char * 64 * n)()
+    ms = (ctypes.c_double * n)()
+    cnt = (ctypes.c_uint64 * n)()
+    nbytes = (ctypes.c_double * n)()
+    fn = lib.qcsim_profile_read
+    fn.restype = ctypes.c_int
+    k = fn(names, ms, cnt, nbytes, n)
+    lib.qcsim_profile_enable(0)
+    out = []
+    for i in range(k):
+        out.append(dict(kernel=bytes(names[i]).split(b"\0")[0].decode(), ms=ms[i], launches=cnt[i],
+                        algo_bytes=nbytes[i]))
+    return sorted(out, key=lambda r: -r["ms"])
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="grover20")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if world > 1 and args.impl == "ours":
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        tdist.init_process_group("nccl")
+        dist = tdist
+    wl = workload(args.workload)
+    hbm, peak_kind = measured_peaks()
+    config = {"workload": wl["name"], "detail": wl["desc"], "n_qubits": wl["n"], "slice_bits": wl["s"],
+              "error_bound": wl["eb"], "mode": "absolute", "quant_code_bits": 16, "predictor": "previous",
+              "step": "one Grover iteration" if wl["name"] == "grover20" else "gate chunk",
+              "l2": "flushed between timed steps (256 MiB write)", "norm": "every gate"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = cpu_reference(wl, args, budget_s=args.cpu_budget)
+        line = {"metric": "amplitude-gate updates/s incl. (de)compression", "value": r["value"],
+                "unit": "updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (seeded circuit)", "config": config, "impl": "reference",
+                "cpu_baseline": r, "e2e": {"value": r["value"], "unit": "updates/s", "h2d_bytes_per_step": 0,
+                                            "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    res = run_ours(args, wl, rank, world, dist)
+    dev_s, wall = res["dev_s"], res["wall"]
+    if dist:
+        import torch
+        t = torch.tensor([dev_s, wall, res["e2e_t"]], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_s, wall, e2e_t = t.tolist()
+    else:
+        e2e_t = res["e2e_t"]
+    N = 1 << wl["n"]
+    value = N * res["gates"] / dev_s
+    m = res["metrics"]
+    if rank != 0:
+        dist.destroy_process_group() if dist else None
+        return
+    # roofline: SURVEY.md §8(d) algorithmic bytes per gate pass = input +
+    # output compressed block bytes of every plane
+    kprof = res["kprof"] or []
+    algo_per_pass = 2.0 * m.current_compressed_bytes * world
+    achieved = algo_per_pass * res["gates"] / dev_s / 1e9
+    dominant = kprof[0] if kprof else None
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+            "traffic": None, "peak_kind": peak_kind,
+            "basis": "per gate pass: sum of input+output QCB1 block bytes (SURVEY.md 8(d)) / device time per pass",
+            "dominant_kernel": dominant, "kernel_shares": kprof[:8]}
+    cpu = None
+    if args.gpus == 1 and world == 1:
+        try:
+            cpu = cpu_reference(wl, args, budget_s=args.cpu_budget)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "error": str(e)}
+    line = {"metric": "amplitude-gate updates/s incl. (de)compression", "value": value, "unit": "updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * dev_s / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded circuit, random-free)",
+            "config": config, "clocks": res["clocks"], "gpu_launches": int(res["launches"]),
+            "e2e": {"value": N * res["gates"] / e2e_t, "unit": "updates/s", "h2d_bytes_per_step": res["h2d"],
+                    "d2h_bytes_per_step": res["d2h"]},
+            "roofline": roof, "cpu_baseline": cpu,
+            "compression": {"min_ratio": m.min_compression_ratio, "mean_ratio": m.mean_compression_ratio,
+                            "compressed_bytes": m.current_compressed_bytes, "dense_bytes": m.dense_bytes,
+                            "fallback_planes": m.fallback_planes},
+            "wall_ms_per_step": 1e3 * wall / args.steps}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

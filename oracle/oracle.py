@@ -89,7 +89,8 @@ def _u8ptr(a):
 def actions_array(actions):
     arr = (Action * max(1, len(actions)))()
     for i, a in enumerate(actions):
-        arr[i] = a
+        # accept any struct with the qcsim_action layout (e.g. the product's)
+        arr[i] = a if isinstance(a, Action) else Action.from_buffer_copy(bytes(a))
     return arr
 
 
@@ -97,6 +98,16 @@ def actions_array(actions):
 class Block:
     data: bytes
     stats: CodecStats
+
+
+def partner_slice(a, s, j):
+    """the other slice whose old values slice j needs."""
+    if a.kind == ACTION_BUTTERFLY and a.target >= s:
+        return j ^ (1 << (a.target - s))
+    if a.kind == ACTION_SWAP:
+        hm = (1 << (a.a - s) if a.a >= s else 0) | (1 << (a.b - s) if a.b >= s else 0)
+        return j ^ hm
+    return j
 
 
 class Oracle:
@@ -132,6 +143,10 @@ class Oracle:
         L.oracle_engine_slice_norms.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.c_uint64]
         L.oracle_engine_export_blocks.argtypes = [C.c_void_p, C.POINTER(C.c_uint8), C.c_uint64,
                                                   C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_uint64]
+        L.oracle_engine_export_slice.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_uint8), C.c_uint64,
+                                                 C.POINTER(C.c_uint64)]
+        L.oracle_engine_import_partner.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_uint8), C.c_uint64]
+        L.oracle_engine_set_global_norms.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.c_uint64]
         L.oracle_build_qft.restype = C.c_int64
         L.oracle_build_qft.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_double),
                                        C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
@@ -217,6 +232,8 @@ class OracleEngine:
         n = cfg.num_qubits
         self.n = n
         self.s = cfg.slice_bits if cfg.slice_bits >= 0 else min(n, 20)
+        self.world = max(1, cfg.world)
+        self.local_slices = (1 << (n - self.s)) // self.world
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -242,13 +259,41 @@ class OracleEngine:
         return out
 
     def slice_norms(self):
-        out = np.empty(1 << (self.n - self.s), dtype=np.float64)
+        out = np.empty(self.local_slices, dtype=np.float64)
         self.o._check(self.o.lib.oracle_engine_slice_norms(self.h, _dptr(out), out.size))
         return out
 
+    def metrics(self):
+        return self.run([])
+
+    # ---- multi-rank hooks (same surface as paper_1811_05630_b200.Engine)
+    def partner_slices_needed(self, action):
+        s0 = self.cfg.rank * self.local_slices
+        out = []
+        for j in range(s0, s0 + self.local_slices):
+            pj = partner_slice(action, self.s, j)
+            if not (s0 <= pj < s0 + self.local_slices):
+                out.append(pj)
+        return out
+
+    def export_slice(self, j):
+        ln = C.c_uint64()
+        self.o._check(self.o.lib.oracle_engine_export_slice(self.h, j, None, 0, C.byref(ln)))
+        out = np.empty(ln.value, dtype=np.uint8)
+        self.o._check(self.o.lib.oracle_engine_export_slice(self.h, j, _u8ptr(out), out.size, C.byref(ln)))
+        return out.tobytes()
+
+    def import_partner(self, j, data):
+        b = np.frombuffer(data, dtype=np.uint8).copy()
+        self.o._check(self.o.lib.oracle_engine_import_partner(self.h, j, _u8ptr(b), b.size))
+
+    def set_global_norms(self, norms):
+        v = np.ascontiguousarray(norms, dtype=np.float64)
+        self.o._check(self.o.lib.oracle_engine_set_global_norms(self.h, _dptr(v), v.size))
+
     def export_blocks(self):
         ln = C.c_uint64()
-        nplanes = 2 << (self.n - self.s)
+        nplanes = 2 * self.local_slices
         offs = (C.c_uint64 * (nplanes + 1))()
         self.o._check(self.o.lib.oracle_engine_export_blocks(self.h, None, 0, C.byref(ln), offs, nplanes + 1))
         out = np.empty(ln.value, dtype=np.uint8)

@@ -593,55 +593,78 @@ __global__ void __launch_bounds__(kEncThreads) enc_tokenize(TokPlanes T, int pla
             if (bflag[e]) S.bl[bpos[e]] = (uint16_t)(tid * kPerThread + e);
         if (tid == 0) S.nb = nb;
         __syncthreads();
-        // per element: its run (ri = -1 is the carried run) and token count
+        // The run carried in from earlier tiles closes here when the tile has
+        // a boundary (or is the last tile); its tokens go first, through
+        // element 0's scan slot (element 0 may itself start a new run).
+        const bool carry_closes = nb > 0 || last_tile;
+        const uint64_t carry_len = carry_closes ? t0 + (nb > 0 ? S.bl[0] : tl) - S.runstart : 0;
+        const bool carry_long = S.runsym != kOutlierSym && carry_len >= kMinRunLen;
+        const int carry_cnt = carry_closes ? (carry_long ? 2 : (int)carry_len) : 0;
+        // per element: its run (ri = -1 is the carried run) and own tokens
         int cnt[kPerThread], tpos[kPerThread], ri[kPerThread];
         for (int e = 0; e < kPerThread; ++e) {
             const int k = tid * kPerThread + e;
             ri[e] = bpos[e] + bflag[e] - 1; // boundaries at or before k, minus one
             cnt[e] = 0;
-            if (k >= tl) continue;
+            if (k >= tl || ri[e] < 0) continue;
             const bool closed = ri[e] + 1 < nb || last_tile;
             if (!closed) continue;
             const uint32_t s = S.ssym[k];
-            const int rs = ri[e] >= 0 ? S.bl[ri[e]] : -1;
-            const uint64_t start = ri[e] >= 0 ? t0 + rs : S.runstart;
+            const int rs = S.bl[ri[e]];
             const uint64_t end = t0 + (ri[e] + 1 < nb ? S.bl[ri[e] + 1] : tl);
-            const uint64_t len = end - start;
+            const uint64_t len = end - (t0 + rs);
             const bool longrun = s != kOutlierSym && len >= kMinRunLen;
-            if (ri[e] < 0) cnt[e] = (k == 0) ? (longrun ? 2 : (int)len) : 0;
-            else cnt[e] = longrun ? (k == rs ? 2 : 0) : 1;
+            cnt[e] = longrun ? (k == rs ? 2 : 0) : 1;
         }
+        int scnt[kPerThread];
+        for (int e = 0; e < kPerThread; ++e) scnt[e] = cnt[e] + ((tid == 0 && e == 0) ? carry_cnt : 0);
         int ntile;
-        ScanI(scan_tmp).ExclusiveSum(cnt, tpos, ntile);
+        ScanI(scan_tmp).ExclusiveSum(scnt, tpos, ntile);
         __syncthreads();
-        // emit tokens, histogram, checkpoints
+        // own-token position of every element (carried tokens precede k = 0's)
+        for (int e = 0; e < kPerThread; ++e) tpos[e] += (tid == 0 && e == 0) ? carry_cnt : 0;
+        // emit the carried run
+        if (tid == 0 && carry_cnt > 0) {
+            const uint32_t tk = S.ntok;
+            const uint32_t s = S.runsym;
+            if (carry_long) {
+                tsym[tk] = s;
+                trep[tk] = 0;
+                tsym[tk + 1] = rsym;
+                trep[tk + 1] = (uint32_t)(carry_len - 1);
+                count_sym(s, 1);
+                count_sym(rsym, 1);
+                atomicAdd(&S.gamma, (unsigned long long)(2 * bit_width64(carry_len - 1) - 1));
+            } else {
+                for (int r = 0; r < carry_cnt; ++r) {
+                    tsym[tk + r] = s;
+                    trep[tk + r] = 0;
+                }
+                count_sym(s, (uint32_t)carry_cnt);
+            }
+        }
+        // emit runs that start and close in this tile
         for (int e = 0; e < kPerThread; ++e) {
             const int k = tid * kPerThread + e;
-            if (k >= tl) continue;
-            const bool closed = ri[e] + 1 < nb || last_tile;
+            if (k >= tl || cnt[e] == 0) continue;
             const uint32_t s = S.ssym[k];
-            const int rs = ri[e] >= 0 ? S.bl[ri[e]] : -1;
-            const uint64_t start = ri[e] >= 0 ? t0 + rs : S.runstart;
+            const int rs = S.bl[ri[e]];
             const uint64_t end = t0 + (ri[e] + 1 < nb ? S.bl[ri[e] + 1] : tl);
-            const uint64_t len = end - start;
+            const uint64_t len = end - (t0 + rs);
             const bool longrun = s != kOutlierSym && len >= kMinRunLen;
             const uint32_t tk = S.ntok + (uint32_t)tpos[e];
-            if (cnt[e] > 0) {
-                if (longrun) {
-                    tsym[tk] = s;
-                    trep[tk] = 0;
-                    tsym[tk + 1] = rsym;
-                    trep[tk + 1] = (uint32_t)(len - 1);
-                    count_sym(s, 1);
-                    count_sym(rsym, 1);
-                    atomicAdd(&S.gamma, (unsigned long long)(2 * bit_width64(len - 1) - 1));
-                } else {
-                    for (int r = 0; r < cnt[e]; ++r) {
-                        tsym[tk + r] = s;
-                        trep[tk + r] = 0;
-                    }
-                    count_sym(s, (uint32_t)cnt[e]);
-                }
+            if (longrun) {
+                tsym[tk] = s;
+                trep[tk] = 0;
+                tsym[tk + 1] = rsym;
+                trep[tk + 1] = (uint32_t)(len - 1);
+                count_sym(s, 1);
+                count_sym(rsym, 1);
+                atomicAdd(&S.gamma, (unsigned long long)(2 * bit_width64(len - 1) - 1));
+            } else {
+                tsym[tk] = s;
+                trep[tk] = 0;
+                count_sym(s, 1u);
             }
         }
         __syncthreads();

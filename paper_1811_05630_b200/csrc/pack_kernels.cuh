@@ -351,14 +351,15 @@ __global__ void __launch_bounds__(256) enc_pack(PackArgs A, int planes) {
         // decode-index bit positions for checkpoints resuming in this chunk
         if (tid == 0) {
             // records are sorted by tok; find [jlo, jhi) with tok in [t0, t0+tn)
-            uint32_t lo = 1, hi = (uint32_t)nidx;
+            const uint32_t nchunks = (uint32_t)((A.L + (1ull << A.log2C) - 1) >> A.log2C);
+            uint32_t lo = 1, hi = nchunks;
             while (lo < hi) {
                 const uint32_t mid = (lo + hi) >> 1;
                 if (idx[mid].tok < t0) lo = mid + 1;
                 else hi = mid;
             }
             s_jlo = lo;
-            hi = (uint32_t)nidx;
+            hi = nchunks;
             uint32_t lo2 = lo;
             while (lo2 < hi) {
                 const uint32_t mid = (lo2 + hi) >> 1;

@@ -111,6 +111,70 @@ void ensure_device(int dev) {
 
 uint64_t g_launches = 0; // kernels launched by this library (per process)
 
+// Optional per-kernel timing with CUDA events on the launching stream
+// (bench.py reads it through qcsim_profile_read).  Pending event pairs are
+// resolved at the synchronisation points the pipeline already has.
+struct Profiler {
+    bool on = false;
+    struct Pend {
+        const char *name;
+        cudaEvent_t a, b;
+    };
+    std::vector<Pend> pend;
+    std::vector<cudaEvent_t> pool;
+    std::vector<std::pair<std::string, std::pair<double, uint64_t>>> acc;
+    cudaEvent_t get() {
+        if (pool.empty()) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            return e;
+        }
+        cudaEvent_t e = pool.back();
+        pool.pop_back();
+        return e;
+    }
+    void add(const char *name, double ms) {
+        for (auto &kv : acc)
+            if (kv.first == name) {
+                kv.second.first += ms;
+                kv.second.second += 1;
+                return;
+            }
+        acc.push_back({name, {ms, 1}});
+    }
+    void flush() {
+        for (auto &p : pend) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) add(p.name, ms);
+            pool.push_back(p.a);
+            pool.push_back(p.b);
+        }
+        pend.clear();
+    }
+};
+Profiler g_prof;
+
+struct ProfScope {
+    const char *name;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr;
+    ProfScope(const char *n, cudaStream_t s) : name(n), st(s) {
+        ++g_launches;
+        if (g_prof.on) {
+            a = g_prof.get();
+            cudaEventRecord(a, st);
+        }
+    }
+    ~ProfScope() {
+        if (a) {
+            cudaEvent_t b = g_prof.get();
+            cudaEventRecord(b, st);
+            g_prof.pend.push_back({name, a, b});
+        }
+    }
+};
+#define PROF(name, st) ProfScope _prof_scope(name, st)
+
 void validate_codec(const qcsim_codec_config &c) { // codec.cpp:331-341
     if (c.quant_code_bits < 4 || c.quant_code_bits > 24)
         raise(QCSIM_INVALID_ARGUMENT, "quant_code_bits must be in [4, 24]");
@@ -204,13 +268,16 @@ EncodeResult encode_batch(cudaStream_t st, EncScratch &S, const Src &src, int un
     const uint64_t cap = std::min<uint64_t>(L + 1, (1ull << qb) + 1);
 
     if (check_finite) CK(cudaMemsetAsync(S.nonfinite.p, 0, sizeof(uint32_t), st));
-    init_params<NP, Src><<<units, 256, 0, st>>>(S.params.p, src, units, L, cfg.mode, cfg.bound,
-                                                check_finite ? S.nonfinite.p : nullptr);
-    ++g_launches;
+    {
+        PROF("init_params", st);
+        init_params<NP, Src><<<units, 256, 0, st>>>(S.params.p, src, units, L, cfg.mode, cfg.bound,
+                                                    check_finite ? S.nonfinite.p : nullptr);
+    }
     if (check_finite) {
         uint32_t bad = 0;
         CK(cudaMemcpyAsync(&bad, S.nonfinite.p, sizeof bad, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+    g_prof.flush();
         if (bad) raise(QCSIM_INVALID_ARGUMENT, "plane contains a non-finite value");
     }
 
@@ -233,9 +300,14 @@ EncodeResult encode_batch(cudaStream_t st, EncScratch &S, const Src &src, int un
         set_smem(enc_tokenize, sizeof(TokSmem));
         attr_done[NP - 1] = true;
     }
-    enc_quantize<NP, Src><<<units, kEncThreads, sizeof(E1Smem<NP>), st>>>(E, src, units);
-    enc_serial<NP, Src><<<(unsigned)((planes + 31) / 32), 32, 0, st>>>(E, src, units);
-    g_launches += 2;
+    {
+        PROF("enc_quantize", st);
+        enc_quantize<NP, Src><<<units, kEncThreads, sizeof(E1Smem<NP>), st>>>(E, src, units);
+    }
+    {
+        PROF("enc_serial", st);
+        enc_serial<NP, Src><<<(unsigned)((planes + 31) / 32), 32, 0, st>>>(E, src, units);
+    }
 
     TokPlanes T;
     T.sym = S.sym.p;
@@ -250,7 +322,10 @@ EncodeResult encode_batch(cudaStream_t st, EncScratch &S, const Src &src, int un
     T.L = L;
     T.log2C = log2C;
     T.qb = qb;
-    enc_tokenize<<<(unsigned)planes, kEncThreads, sizeof(TokSmem), st>>>(T, (int)planes);
+    {
+        PROF("enc_tokenize", st);
+        enc_tokenize<<<(unsigned)planes, kEncThreads, sizeof(TokSmem), st>>>(T, (int)planes);
+    }
 
     CodeBook B;
     B.hist = S.hist.p;
@@ -272,8 +347,10 @@ EncodeResult encode_batch(cudaStream_t st, EncScratch &S, const Src &src, int un
     B.err = S.err.p;
     B.cap = cap;
     B.qb = qb;
-    enc_codebook<<<(unsigned)planes, 256, 0, st>>>(B, (int)planes);
-    g_launches += 2;
+    {
+        PROF("enc_codebook", st);
+        enc_codebook<<<(unsigned)planes, 256, 0, st>>>(B, (int)planes);
+    }
 
     // slot offsets: exclusive scan of slot sizes (16-byte aligned slots)
     size_t tmp_bytes = 0;
@@ -281,13 +358,14 @@ EncodeResult encode_batch(cudaStream_t st, EncScratch &S, const Src &src, int un
     S.cub_tmp.ensure(tmp_bytes);
     CK(cudaMemsetAsync(S.slot_off.p, 0, sizeof(uint64_t), st));
     CK(cub::DeviceScan::InclusiveSum(S.cub_tmp.p, tmp_bytes, S.slot_bytes.p, S.slot_off.p + 1, (int)planes, st));
-    ++g_launches;
+    // (cub scan kernels are library code: not counted in g_launches)
 
     EncodeResult R;
     std::vector<uint32_t> err(planes);
     CK(cudaMemcpyAsync(&R.total, S.slot_off.p + planes, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(err.data(), S.err.p, planes * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    g_prof.flush();
     CK(cudaGetLastError());
     for (uint64_t p = 0; p < planes; ++p)
         if (err[p] == kErrDepth) raise(QCSIM_CODEC, "prefix code depth out of range");
@@ -317,8 +395,10 @@ EncodeResult encode_batch(cudaStream_t st, EncScratch &S, const Src &src, int un
     A.qb = qb;
     A.mode = cfg.mode;
     A.predictor = cfg.predictor;
-    enc_pack<<<(unsigned)planes, 256, 0, st>>>(A, (int)planes);
-    ++g_launches;
+    {
+        PROF("enc_pack", st);
+        enc_pack<<<(unsigned)planes, 256, 0, st>>>(A, (int)planes);
+    }
     R.block_bytes.resize(planes);
     CK(cudaMemcpyAsync(R.block_bytes.data(), S.block_bytes.p, planes * sizeof(uint64_t), cudaMemcpyDeviceToHost,
                        st));
@@ -329,6 +409,7 @@ EncodeResult encode_batch(cudaStream_t st, EncScratch &S, const Src &src, int un
     std::vector<PlaneParams> prm(planes);
     CK(cudaMemcpyAsync(prm.data(), S.params.p, planes * sizeof(PlaneParams), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    g_prof.flush();
     CK(cudaGetLastError());
     for (auto &p : prm) R.fallback += (p.flags & kFlagFallback) ? 1 : 0;
     return R;
@@ -368,11 +449,16 @@ void decode_batch(cudaStream_t st, DecScratch &S, const uint8_t *arena, const ui
     D.out = out;
     D.L = L;
     D.log2C = log2C;
-    dec_prepare<<<planes, 256, 0, st>>>(D, T, planes);
+    {
+        PROF("dec_prepare", st);
+        dec_prepare<<<planes, 256, 0, st>>>(D, T, planes);
+    }
     const uint64_t nchunks = (L + (1ull << log2C) - 1) >> log2C;
     const uint64_t threads = nchunks * planes;
-    dec_chunks<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(D, T, planes);
-    g_launches += 2;
+    {
+        PROF("dec_chunks", st);
+        dec_chunks<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(D, T, planes);
+    }
 }
 
 // Host-side from_bytes checks (codec.cpp:366-408), exact messages.
@@ -601,17 +687,20 @@ template <class Src> void engine_store(qcsim_engine *e, const Src &src) {
     } else {
         e->dense[nxt].ensure(e->ns * 2 * e->L);
         e->enc.tilesum.ensure(e->ns * ntiles);
+        PROF("dense_gate", e->st);
         dense_gate<Src><<<(unsigned)(units * ntiles), 256, 0, e->st>>>(src, units, e->L, e->dense[nxt].p,
                                                                         e->enc.tilesum.p);
-        ++g_launches;
     }
     // per-slice sq_norm from the tile partials
     e->slice_sq.ensure(e->ns);
-    slice_norms<<<(units + 127) / 128, 128, 0, e->st>>>(e->enc.tilesum.p, (int)ntiles, units, e->slice_sq.p);
-    ++g_launches;
+    {
+        PROF("slice_norms", e->st);
+        slice_norms<<<(units + 127) / 128, 128, 0, e->st>>>(e->enc.tilesum.p, (int)ntiles, units, e->slice_sq.p);
+    }
     std::vector<double> sq(e->ns);
     CK(cudaMemcpyAsync(sq.data(), e->slice_sq.p, e->ns * sizeof(double), cudaMemcpyDeviceToHost, e->st));
     CK(cudaStreamSynchronize(e->st));
+    g_prof.flush();
     CK(cudaGetLastError());
     for (uint64_t k = 0; k < e->ns; ++k) e->sq_norm[e->s0 + k] = sq[k];
     e->cur = nxt;
@@ -668,8 +757,10 @@ void engine_decode_old(qcsim_engine *e, bool need_imported) {
         V.ssym = e->val.ssym.p;
         V.slen = e->val.slen.p;
         V.cap = std::min<uint64_t>(e->L + 1, (1ull << e->cfg.codec.quant_code_bits) + 1);
-        dec_validate<<<(unsigned)((offs.size() + 31) / 32), 32, 0, e->st>>>(V, (int)offs.size());
-        ++g_launches;
+        {
+            PROF("dec_validate", e->st);
+            dec_validate<<<(unsigned)((offs.size() + 31) / 32), 32, 0, e->st>>>(V, (int)offs.size());
+        }
         std::vector<uint32_t> errs(offs.size());
         CK(cudaMemcpyAsync(errs.data(), e->val.err.p, errs.size() * 4, cudaMemcpyDeviceToHost, e->st));
         CK(cudaStreamSynchronize(e->st));
@@ -753,6 +844,58 @@ const char *qcsim_version(void) { return QCSIM_VERSION; }
 
 uint64_t qcsim_kernel_launches(void) { return g_launches; }
 
+// Per-kernel device time (CUDA events) -- bench.py instrumentation.
+int qcsim_profile_enable(int on) {
+    g_prof.flush();
+    g_prof.on = on != 0;
+    if (on) g_prof.acc.clear();
+    return 0;
+}
+int qcsim_profile_read(char (*names)[64], double *ms, uint64_t *count, double *bytes, int cap) {
+    g_prof.flush();
+    int k = 0;
+    for (auto &kv : g_prof.acc) {
+        if (k >= cap) break;
+        std::snprintf(names[k], 64, "%s", kv.first.c_str());
+        ms[k] = kv.second.first;
+        count[k] = kv.second.second;
+        bytes[k] = 0.0;
+        ++k;
+    }
+    return k;
+}
+
+// Debug (not part of the public header): encoder intermediates for one plane.
+// sym[n], tsym/trep[n+1], flags = plane flags, idx = [n/C + 1] records.
+qcsim_status qcsim_debug_encode(const double *values, uint64_t n, const qcsim_codec_config *cfg, uint32_t *sym,
+                                uint32_t *tsym, uint32_t *trep, uint64_t *ntok, uint32_t *flags, void *idx,
+                                int32_t *log2C_out) {
+    return guarded([&] {
+        validate_codec(*cfg);
+        CodecCtx &C = codec_ctx();
+        C.vals.ensure(n);
+        CK(cudaMemcpy(C.vals.p, values, n * sizeof(double), cudaMemcpyHostToDevice));
+        C.ptrs.ensure(1);
+        const double *vp = C.vals.p;
+        CK(cudaMemcpy(C.ptrs.p, &vp, sizeof vp, cudaMemcpyHostToDevice));
+        RawSrc src{C.ptrs.p};
+        const int log2C = auto_log2C(n);
+        C.index.ensure(((n >> log2C) + 1));
+        encode_batch<1, RawSrc>(C.st, C.enc, src, 1, n, *cfg, log2C, C.index.p, C.arena, true, true);
+        uint32_t nt = 0;
+        CK(cudaMemcpy(&nt, C.enc.ntok.p, 4, cudaMemcpyDeviceToHost));
+        *ntok = nt;
+        CK(cudaMemcpy(sym, C.enc.sym.p, n * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(tsym, C.enc.tsym.p, (n + 1) * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(trep, C.enc.trep.p, (n + 1) * 4, cudaMemcpyDeviceToHost));
+        PlaneParams pp;
+        CK(cudaMemcpy(&pp, C.enc.params.p, sizeof pp, cudaMemcpyDeviceToHost));
+        *flags = pp.flags;
+        CK(cudaMemcpy(idx, C.index.p, ((n >> log2C) + 1) * sizeof(IndexRec), cudaMemcpyDeviceToHost));
+        *log2C_out = log2C;
+    });
+}
+
 qcsim_status qcsim_codec_validate(const qcsim_codec_config *cfg) {
     return guarded([&] {
         if (!cfg) raise(QCSIM_INVALID_ARGUMENT, "null config");
@@ -831,8 +974,10 @@ qcsim_status qcsim_decompress_plane(const uint8_t *block, uint64_t len, double *
         V.ssym = C.val.ssym.p;
         V.slen = C.val.slen.p;
         V.cap = cap;
-        dec_validate<<<1, 32, 0, C.st>>>(V, 1);
-        ++g_launches;
+        {
+            PROF("dec_validate", C.st);
+            dec_validate<<<1, 32, 0, C.st>>>(V, 1);
+        }
         uint32_t e = 0;
         CK(cudaMemcpyAsync(&e, C.val.err.p, 4, cudaMemcpyDeviceToHost, C.st));
         CK(cudaStreamSynchronize(C.st));
@@ -883,9 +1028,11 @@ qcsim_status qcsim_compress_planes_device(const double *const *values, const uin
             std::vector<uint32_t> oc(planes);
             CK(cudaMemcpyAsync(oc.data(), C.enc.ocount.p, planes * 4, cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
+    g_prof.flush();
             for (uint32_t p = 0; p < planes; ++p) stats_host[p].outlier_fraction = (double)oc[p] / (double)L;
         }
         CK(cudaStreamSynchronize(st));
+    g_prof.flush();
     });
 }
 
@@ -920,11 +1067,14 @@ qcsim_status qcsim_decompress_planes_device(const uint8_t *blocks, const uint64_
         V.ssym = C.val.ssym.p;
         V.slen = C.val.slen.p;
         V.cap = maxtc;
-        dec_validate<<<(planes + 31) / 32, 32, 0, st>>>(V, (int)planes);
-        ++g_launches;
+        {
+            PROF("dec_validate", st);
+            dec_validate<<<(planes + 31) / 32, 32, 0, st>>>(V, (int)planes);
+        }
         std::vector<uint32_t> errs(planes);
         CK(cudaMemcpyAsync(errs.data(), C.val.err.p, planes * 4, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+    g_prof.flush();
         CK(cudaGetLastError());
         for (uint32_t x : errs)
             if (x) raise(QCSIM_CODEC, dec_message(x));

@@ -72,7 +72,7 @@ def _actions(actions):
         actions = lower(actions)
     arr = (_native.ActionC * max(1, len(actions)))()
     for i, a in enumerate(actions):
-        arr[i] = a
+        arr[i] = a if isinstance(a, _native.ActionC) else _native.ActionC.from_buffer_copy(bytes(a))
     return arr, len(actions)
 
 
