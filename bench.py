@@ -128,9 +128,10 @@ def cpu_reference(wl, args, budget_s=12.0):
     cores = os.cpu_count() or 1
     cfg = OEng.make(wl["n"], wl["s"], OCfg.make(1, wl["eb"], 16, 0))
     if os.path.exists(REF_SO):
+        from oracle.oracle import Action
         eng = RefLib().engine(cfg, workers=cores)
         kind = "reference"
-        gate = eng.gate
+        gate = lambda a: eng.gate(Action.from_buffer_copy(bytes(a)))  # noqa: E731
     else:
         eng = Oracle().engine(cfg)
         kind, cores = "port", 1
