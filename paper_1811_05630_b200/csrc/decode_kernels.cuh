@@ -110,27 +110,47 @@ __global__ void __launch_bounds__(256) dec_prepare(DecPlanes D, DecTables T, int
     }
 }
 
-// 64-bit MSB-first window at stream bit `bp` (stream is 16-byte aligned and
-// the arena is padded, so reading 3 words past any position is safe).
+// 64-bit MSB-first window at stream bit `bp` of big-endian-ordered words
+// (the block's stream starts 16-byte aligned in the arena; the arena and
+// the shared staging buffer are padded, so reading 3 words ahead is safe).
+template <bool kShared>
 __device__ __forceinline__ uint64_t peek64(const uint32_t *w, uint64_t bp) {
     const uint64_t wi = bp >> 5;
     const uint32_t b = (uint32_t)(bp & 31);
-    const uint64_t hi = ((uint64_t)bswap32(__ldg(w + wi)) << 32) | bswap32(__ldg(w + wi + 1));
+    uint32_t w0, w1, w2;
+    if (kShared) {
+        w0 = w[wi];
+        w1 = w[wi + 1];
+        w2 = w[wi + 2];
+    } else {
+        w0 = __ldg(w + wi);
+        w1 = __ldg(w + wi + 1);
+        w2 = __ldg(w + wi + 2);
+    }
+    const uint64_t hi = ((uint64_t)bswap32(w0) << 32) | bswap32(w1);
     if (b == 0) return hi;
-    const uint32_t w2 = bswap32(__ldg(w + wi + 2));
-    return (hi << b) | (w2 >> (32 - b));
+    return (hi << b) | (bswap32(w2) >> (32 - b));
 }
 
-__global__ void __launch_bounds__(128) dec_chunks(DecPlanes D, DecTables T, int planes) {
+constexpr int kDecThreads = 128;             // chunks per block
+constexpr int kDecStageWords = 8192;         // 32 KB of stream staged per block
+
+// One block per (plane, group of kDecThreads checkpoint chunks).  The
+// plane's 11-bit LUT and the group's stream bytes are staged in shared
+// memory; each thread then resumes from its IndexRec and reproduces
+// codec.cpp:591-626 for its chunk.
+__global__ void __launch_bounds__(kDecThreads) dec_chunks(DecPlanes D, DecTables T, int planes) {
     const uint64_t nchunks = (D.L + (1ull << D.log2C) - 1) >> D.log2C;
-    const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= nchunks * (uint64_t)planes) return;
-    const int pl = (int)(gid / nchunks);
-    const uint64_t j = gid % nchunks;
+    const uint32_t groups = (uint32_t)((nchunks + kDecThreads - 1) / kDecThreads);
+    const int pl = (int)(blockIdx.x / groups);
+    if (pl >= planes) return;
+    const uint64_t j0 = (uint64_t)(blockIdx.x % groups) * kDecThreads;
+    const uint64_t j = j0 + threadIdx.x;
+    const uint64_t jend = tmin<uint64_t>(j0 + kDecThreads, nchunks);
     const uint64_t nidx = (D.L >> D.log2C) + 1;
+    __shared__ uint32_t slut[1 << kLutBits];
+    __shared__ uint32_t sw[kDecStageWords + 4];
     const uint8_t *blk = D.arena + D.blk_off[pl];
-    const uint8_t mode = blk[5];
-    (void)mode;
     const uint8_t pred_kind = blk[6];
     const int qb = blk[7];
     const long long half = 1ll << (qb - 1);
@@ -145,13 +165,25 @@ __global__ void __launch_bounds__(128) dec_chunks(DecPlanes D, DecTables T, int 
     const uint64_t sbytes = payload - table_bytes - 16 * nout;
     const uint32_t *stream = reinterpret_cast<const uint32_t *>(blk + kHeaderBytes + table_bytes);
     const uint8_t *orec = blk + kHeaderBytes + table_bytes + sbytes;
-    const uint32_t *lut = T.lut + (uint64_t)pl * (1u << kLutBits);
+    const uint32_t *glut = T.lut + (uint64_t)pl * (1u << kLutBits);
     const uint64_t *first = T.first + (uint64_t)pl * (kMaxCodeLen + 1);
     const uint32_t *count = T.count + (uint64_t)pl * (kMaxCodeLen + 1);
     const uint32_t *basei = T.basei + (uint64_t)pl * (kMaxCodeLen + 1);
     const uint32_t *sorted = T.sorted + (uint64_t)pl * T.cap;
+    const IndexRec *idx = D.index + (uint64_t)pl * nidx;
 
-    const IndexRec r = D.index[(uint64_t)pl * nidx + j];
+    for (int k = threadIdx.x; k < (1 << kLutBits); k += kDecThreads) slut[k] = glut[k];
+    // stream words this group reads: [bitpos(j0), bitpos(jend)) + lookahead
+    const uint64_t w_lo = idx[j0].bitpos >> 5;
+    const uint64_t bit_hi = jend < nchunks ? idx[jend].bitpos : sbytes * 8;
+    const uint64_t w_hi = (bit_hi >> 5) + 3;
+    const bool staged = w_hi - w_lo <= (uint64_t)kDecStageWords;
+    if (staged)
+        for (uint64_t w = w_lo + threadIdx.x; w < w_hi; w += kDecThreads) sw[w - w_lo] = __ldg(stream + w);
+    __syncthreads();
+    if (j >= jend) return;
+
+    const IndexRec r = idx[j];
     uint64_t bp = r.bitpos;
     uint32_t run_left = r.run_left;
     uint32_t last = r.last_lit;
@@ -160,6 +192,7 @@ __global__ void __launch_bounds__(128) dec_chunks(DecPlanes D, DecTables T, int 
     const uint64_t e0 = j << D.log2C;
     const uint64_t e1 = tmin<uint64_t>(e0 + (1ull << D.log2C), D.L);
     double *out = D.out[pl];
+    const uint64_t sbase = staged ? w_lo * 32 : 0;
 
     uint64_t i = e0;
     auto emit = [&](uint32_t s) {
@@ -196,8 +229,8 @@ __global__ void __launch_bounds__(128) dec_chunks(DecPlanes D, DecTables T, int 
             --run_left;
             continue;
         }
-        const uint64_t w = peek64(stream, bp);
-        const uint32_t le = lut[w >> (64 - kLutBits)];
+        const uint64_t w = staged ? peek64<true>(sw, bp - sbase) : peek64<false>(stream, bp);
+        const uint32_t le = slut[w >> (64 - kLutBits)];
         uint32_t s, l;
         if (le & 63) {
             l = le & 63;
@@ -218,7 +251,7 @@ __global__ void __launch_bounds__(128) dec_chunks(DecPlanes D, DecTables T, int 
         }
         bp += l;
         if (s == rsym) {
-            const uint64_t g = peek64(stream, bp);
+            const uint64_t g = staged ? peek64<true>(sw, bp - sbase) : peek64<false>(stream, bp);
             const int z = __clzll((long long)g);
             run_left = (uint32_t)(g >> (64 - (2 * z + 1)));
             bp += 2 * z + 1;
@@ -227,7 +260,6 @@ __global__ void __launch_bounds__(128) dec_chunks(DecPlanes D, DecTables T, int 
             last = s;
         }
     }
-    (void)sbytes;
 }
 
 // ------------------------------------------------------------ validating

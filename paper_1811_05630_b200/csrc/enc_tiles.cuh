@@ -1,0 +1,798 @@
+// enc_tiles.cuh -- tile-parallel QCB1 encoder (compress_plane,
+// codec.cpp:410-533), v2.
+//
+// Every stage is a grid over (plane, 1024-element tile) of all planes in the
+// batch; cross-tile state travels through small plane-level scans
+// (plane_scans).  The only serial work is the exact FP64 chain over the
+// nonzero codes (enc_chain), one plane per lane.
+//
+//   T1 enc_x         x = gate(old) (or raw plane), sq-norm tile partials,
+//                    speculative outliers from the jump |x_i - x_{i-1}|
+//   S  scan          base (last outlier) before every tile
+//   T2 enc_lattice   lattice codes m^ = K_i - K_{i-1}, K relative to the
+//                    segment base, event flags
+//   S  scan          event offsets
+//   T3 enc_compact   event list in index order
+//   C  enc_chain     exact d += RN(q*m^) over events (codec.cpp:445)
+//   T4 enc_verify    every decision re-evaluated with the exact prediction
+//                    (codec.cpp:440-451); refuted planes -> enc_serial_x
+//   TA tok_stats     run boundaries / outliers per tile (codec.cpp:468-482)
+//   S  scans         run start/end across tiles, outlier offsets
+//   TB tok_count     tokens per element, histogram (codec.cpp:484-488)
+//   S  scan          token offsets
+//   TC tok_emit      tokens, outlier records, decode-index token state
+#pragma once
+
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include "common.cuh"
+
+namespace qcb {
+
+struct TileArgs {
+    // per plane
+    PlaneParams *params;   // flags |= kFlagFallback on refutation
+    double *x;             // [plane][L] values to encode
+    uint32_t *sym;         // [plane][L] speculated, then exact symbols
+    uint8_t *fl;           // [plane][L] bit0 event, bit1 outlier (speculative)
+    uint32_t *evlist;      // [plane][L] event element indices (bit 31: outlier)
+    double *evc;           // [plane][L] event addend q*m^ (outlier: its value)
+    double *dval;          // [plane][L] chain value per event ordinal
+    IndexRec *index;       // [plane][nidx]
+    // per plane-tile, stride ntiles (+1 for scanned arrays)
+    int32_t *t_lastout;    // last speculative outlier in the tile (-1)
+    int32_t *t_base;       // scanned: last outlier strictly before the tile
+    uint32_t *t_nev;       // events per tile
+    uint32_t *t_evoff;     // scanned (ntiles + 1)
+    double *tilesum;       // [unit][ntiles]
+    uint64_t L;
+    int ntiles;
+    int log2C;
+    int qb;
+    int predictor;
+};
+
+__device__ __forceinline__ bool is_negzero(double v) { return bits_of(v) == 0x8000000000000000ull; }
+
+// ------------------------------------------------------------------ T1
+template <int NP, class Src>
+__global__ void __launch_bounds__(kEncThreads) enc_x(TileArgs A, Src src, int units) {
+    const int unit = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
+    if (unit >= units) return;
+    const int tid = threadIdx.x;
+    const uint64_t L = A.L;
+    const uint64_t t0 = (uint64_t)t * kTile;
+    const int tl = (int)tmin<uint64_t>(kTile, L - t0);
+    __shared__ double xs[NP][kTile + 1];
+    __shared__ double red[kEncThreads];
+    using RedI = cub::BlockReduce<int, kEncThreads>;
+    __shared__ typename RedI::TempStorage red_tmp;
+    // striped load/compute (coalesced), element t0-1 as xs[.][0]
+    for (int k = tid; k <= kTile; k += kEncThreads) {
+        double v[2] = {0.0, 0.0};
+        const int64_t i = (int64_t)t0 + k - 1;
+        if (k == 0 ? t0 > 0 : k - 1 < tl) src.load(unit, (uint64_t)i, v);
+        for (int p = 0; p < NP; ++p) xs[p][k] = v[p];
+    }
+    __syncthreads();
+    for (int p = 0; p < NP; ++p) {
+        double *xrow = A.x + ((uint64_t)unit * NP + p) * L;
+        for (int k = tid; k < tl; k += kEncThreads) xrow[t0 + k] = xs[p][k + 1];
+    }
+    if (Src::kNorms) {
+        double acc[kPerThread];
+        for (int e = 0; e < kPerThread; ++e) {
+            const int k = tid * kPerThread + e + 1;
+            const double a = dmul(xs[0][k], xs[0][k]);
+            const double b = dmul(xs[NP - 1][k], xs[NP - 1][k]);
+            acc[e] = dadd(a, b);
+        }
+        red[tid] = dadd(dadd(acc[0], acc[1]), dadd(acc[2], acc[3]));
+        __syncthreads();
+        for (int w = kEncThreads / 2; w >= 1; w >>= 1) {
+            double v = 0.0;
+            if (tid < w) v = dadd(red[2 * tid], red[2 * tid + 1]);
+            __syncthreads();
+            if (tid < w) red[tid] = v;
+            __syncthreads();
+        }
+        if (tid == 0) A.tilesum[(uint64_t)unit * A.ntiles + t] = red[0];
+    }
+    // speculative outliers
+    const double hh = (double)(1ll << (A.qb - 1));
+    for (int p = 0; p < NP; ++p) {
+        const uint64_t pl = (uint64_t)unit * NP + p;
+        const PlaneParams pp = A.params[pl];
+        int last = -1;
+        uint8_t *flrow = A.fl + pl * L;
+        for (int e = 0; e < kPerThread; ++e) {
+            const int k = tid * kPerThread + e;
+            bool out = false;
+            if (k < tl && pp.eb != 0.0) {
+                const double xp = xs[p][k]; // x[i-1], 0.0 at i = 0
+                const double rr = dmul(dsub(xs[p][k + 1], xp), pp.inv_q);
+                out = !(fabs(rr) < hh - 0.5);
+            }
+            if (k < tl) flrow[t0 + k] = out ? 2 : 0;
+            if (out) last = k;
+        }
+        const int tl_last = RedI(red_tmp).Reduce(last, cub::Max());
+        if (tid == 0) A.t_lastout[pl * A.ntiles + t] = tl_last >= 0 ? (int32_t)(t0 + tl_last) : -1;
+        __syncthreads();
+    }
+}
+
+// ----------------------------------------------------------- plane scans
+// One block per plane over `ntiles` entries (ntiles <= 4096).
+enum ScanKind { kScanMaxExcl = 0, kScanSumExcl = 1, kScanMinExclRev = 2 };
+
+template <int ITEMS>
+__global__ void __launch_bounds__(256) plane_scan(const int32_t *in, int32_t *out, int ntiles, int planes, int kind,
+                                                  int in_stride, int out_stride) {
+    const int pl = blockIdx.x;
+    if (pl >= planes) return;
+    using Scan = cub::BlockScan<int32_t, 256>;
+    __shared__ typename Scan::TempStorage tmp;
+    const int32_t *a = in + (uint64_t)pl * in_stride;
+    int32_t *o = out + (uint64_t)pl * out_stride;
+    int32_t v[ITEMS], r[ITEMS];
+    const int tid = threadIdx.x;
+    for (int e = 0; e < ITEMS; ++e) {
+        const int k = tid * ITEMS + e;
+        const int src = kind == kScanMinExclRev ? ntiles - 1 - k : k;
+        if (k < ntiles) v[e] = a[src];
+        else v[e] = kind == kScanMaxExcl ? -1 : (kind == kScanSumExcl ? 0 : 0x7FFFFFFF);
+    }
+    int32_t total;
+    if (kind == kScanMaxExcl) Scan(tmp).ExclusiveScan(v, r, -1, cub::Max(), total);
+    else if (kind == kScanSumExcl) Scan(tmp).ExclusiveSum(v, r, total);
+    else Scan(tmp).ExclusiveScan(v, r, 0x7FFFFFFF, cub::Min(), total);
+    for (int e = 0; e < ITEMS; ++e) {
+        const int k = tid * ITEMS + e;
+        if (k < ntiles) o[kind == kScanMinExclRev ? ntiles - 1 - k : k] = r[e];
+    }
+    if (tid == 0 && kind == kScanSumExcl) o[ntiles] = total;
+}
+
+// ------------------------------------------------------------------ T2
+__global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int planes) {
+    const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
+    if (pl >= planes) return;
+    const int tid = threadIdx.x;
+    const uint64_t L = A.L;
+    const uint64_t t0 = (uint64_t)t * kTile;
+    const int tl = (int)tmin<uint64_t>(kTile, L - t0);
+    using ScanI = cub::BlockScan<int, kEncThreads>;
+    __shared__ typename ScanI::TempStorage scan_tmp;
+    __shared__ long long kb[kEncThreads];
+    const PlaneParams pp = A.params[pl];
+    const long long half = 1ll << (A.qb - 1);
+    const double *x = A.x + (uint64_t)pl * L;
+    uint8_t *fl = A.fl + (uint64_t)pl * L;
+    uint32_t *sym = A.sym + (uint64_t)pl * L;
+    if (pp.flags & kFlagFallback) {
+        if (tid == 0) A.t_nev[(uint64_t)pl * A.ntiles + t] = 0;
+        return;
+    }
+    if (pp.eb == 0.0) {
+        // lossless / zero range: d == x, symbols final, no events
+        for (int e = 0; e < kPerThread; ++e) {
+            const int k = tid * kPerThread + e;
+            if (k >= tl) continue;
+            const uint64_t i = t0 + k;
+            const double x1 = i > 0 ? x[i - 1] : 0.0;
+            double pred;
+            if (A.predictor == 0) pred = x1;
+            else pred = i == 0 ? 0.0 : (i == 1 ? x1 : predict_linear(x1, x[i - 2]));
+            sym[i] = bits_of(x[i]) == bits_of(pred) ? (uint32_t)half : 0u;
+            fl[i] = 0;
+        }
+        if (tid == 0) A.t_nev[(uint64_t)pl * A.ntiles + t] = 0;
+        return;
+    }
+    // speculative outliers of this tile and the element before it
+    int opos[kPerThread];
+    double xv[kPerThread];
+    for (int e = 0; e < kPerThread; ++e) {
+        const int k = tid * kPerThread + e;
+        opos[e] = (k < tl && (fl[t0 + k] & 2)) ? k : -1;
+        xv[e] = k < tl ? x[t0 + k] : 0.0;
+    }
+    int lo[kPerThread];
+    ScanI(scan_tmp).ExclusiveScan(opos, lo, -1, cub::Max());
+    const int32_t tbase = A.t_base[(uint64_t)pl * A.ntiles + t]; // global position or -1
+    long long K[kPerThread];
+    for (int e = 0; e < kPerThread; ++e) {
+        const int k = tid * kPerThread + e;
+        if (opos[e] >= 0) {
+            K[e] = 0;
+        } else {
+            double base;
+            if (lo[e] >= 0) base = x[t0 + lo[e]];
+            else base = tbase >= 0 ? x[tbase] : 0.0;
+            K[e] = k < tl ? llround_exact(dmul(dsub(xv[e], base), pp.inv_q)) : 0;
+        }
+    }
+    kb[tid] = K[kPerThread - 1];
+    // K and outlier status of element t0-1 (for the first element)
+    long long kprev0 = 0;
+    bool prevout0 = false;
+    double xprev0 = 0.0;
+    if (tid == 0 && t0 > 0) {
+        const uint64_t i = t0 - 1;
+        xprev0 = x[i];
+        prevout0 = (fl[i] & 2) != 0;
+        if (!prevout0) {
+            const double base = tbase >= 0 ? x[tbase] : 0.0;
+            kprev0 = llround_exact(dmul(dsub(xprev0, base), pp.inv_q));
+        }
+    }
+    __syncthreads();
+    int evflag[kPerThread];
+    int bad = 0;
+    for (int e = 0; e < kPerThread; ++e) {
+        const int k = tid * kPerThread + e;
+        evflag[e] = 0;
+        if (k >= tl) continue;
+        long long kprev;
+        bool prev_out;
+        double xp;
+        if (e > 0) { kprev = K[e - 1]; prev_out = opos[e - 1] >= 0; xp = xv[e - 1]; }
+        else if (tid > 0) { kprev = kb[tid - 1]; prev_out = lo[0] == k - 1; xp = x[t0 + k - 1]; }
+        else { kprev = kprev0; prev_out = prevout0; xp = xprev0; }
+        if (prev_out) kprev = 0;
+        uint8_t f;
+        uint32_t sy;
+        if (opos[e] >= 0) {
+            f = 3;
+            sy = kOutlierSym;
+        } else {
+            const long long m = K[e] - kprev;
+            if (m <= -half || m >= half) bad = 1;
+            sy = (uint32_t)(m + half);
+            f = (m != 0 || (prev_out && is_negzero(xp))) ? 1 : 0;
+        }
+        fl[t0 + k] = f;
+        sym[t0 + k] = sy;
+        evflag[e] = f & 1;
+    }
+    if (bad) atomicOr(&A.params[pl].flags, kFlagFallback);
+    using RedI = cub::BlockReduce<int, kEncThreads>;
+    __shared__ typename RedI::TempStorage red_tmp;
+    const int tot = RedI(red_tmp).Sum(evflag[0] + evflag[1] + evflag[2] + evflag[3]);
+    if (tid == 0) A.t_nev[(uint64_t)pl * A.ntiles + t] = (uint32_t)tot;
+}
+
+// ------------------------------------------------------------------ T3
+__global__ void __launch_bounds__(kEncThreads) enc_compact(TileArgs A, int planes) {
+    const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
+    if (pl >= planes) return;
+    if (A.params[pl].flags & kFlagFallback) return;
+    const int tid = threadIdx.x;
+    const uint64_t L = A.L;
+    const uint64_t t0 = (uint64_t)t * kTile;
+    const int tl = (int)tmin<uint64_t>(kTile, L - t0);
+    using ScanI = cub::BlockScan<int, kEncThreads>;
+    __shared__ typename ScanI::TempStorage scan_tmp;
+    const uint8_t *fl = A.fl + (uint64_t)pl * L;
+    int f[kPerThread], pos[kPerThread];
+    for (int e = 0; e < kPerThread; ++e) {
+        const int k = tid * kPerThread + e;
+        f[e] = (k < tl && (fl[t0 + k] & 1)) ? 1 : 0;
+    }
+    ScanI(scan_tmp).ExclusiveSum(f, pos);
+    const uint32_t base = A.t_evoff[(uint64_t)pl * (A.ntiles + 1) + t];
+    uint32_t *ev = A.evlist + (uint64_t)pl * L;
+    double *evc = A.evc + (uint64_t)pl * L;
+    const uint32_t *sym = A.sym + (uint64_t)pl * L;
+    const double *x = A.x + (uint64_t)pl * L;
+    const double q = A.params[pl].q;
+    const long long half = 1ll << (A.qb - 1);
+    for (int e = 0; e < kPerThread; ++e) {
+        if (!f[e]) continue;
+        const uint64_t i = t0 + tid * kPerThread + e;
+        const bool out = (fl[i] & 2) != 0;
+        // the event record the chain consumes: its addend (or outlier value)
+        // and the element index with bit 31 = outlier
+        ev[base + pos[e]] = (uint32_t)i | (out ? 0x80000000u : 0u);
+        evc[base + pos[e]] = out ? x[i] : dmul(q, (double)((long long)sym[i] - half));
+    }
+}
+
+// ------------------------------------------------------------------ chain
+// One warp per plane.  Event records (addend, outlier bit) stream into a
+// shared-memory ring with TMA bulk copies (cp.async.bulk + mbarrier, issued
+// kChainBufs chunks ahead by lane 0); the dependent chain d = RN(d + c)
+// (codec.cpp:445 / :607 in index order) reads warp-broadcast addends, so
+// only the DADD latency is serial.
+constexpr int kChainChunk = 256;  // events per bulk copy
+constexpr int kChainBufs = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(32) enc_chain(TileArgs A, int planes) {
+    const int pl = blockIdx.x;
+    if (pl >= planes) return;
+    const int lane = threadIdx.x;
+    const PlaneParams pp = A.params[pl];
+    if ((pp.flags & kFlagFallback) || pp.eb == 0.0) return;
+    __shared__ alignas(128) double cbuf[kChainBufs][kChainChunk];
+    __shared__ alignas(128) uint32_t obuf[kChainBufs][kChainChunk];
+    __shared__ alignas(8) uint64_t bar[kChainBufs];
+    const uint64_t L = A.L;
+    const uint32_t nev = A.t_evoff[(uint64_t)pl * (A.ntiles + 1) + A.ntiles];
+    if (nev == 0) return;
+    const uint32_t *ev = A.evlist + (uint64_t)pl * L;
+    const double *evc = A.evc + (uint64_t)pl * L;
+    double *dv = A.dval + (uint64_t)pl * L;
+    const uint32_t nchunks = (nev + kChainChunk - 1) / kChainChunk;
+    auto issue = [&](uint32_t ch) {
+        const int b = ch % kChainBufs;
+        const uint32_t n = tmin<uint32_t>(kChainChunk, nev - ch * kChainChunk);
+        const uint32_t cb = (n * 8 + 15) & ~15u, ob = (n * 4 + 15) & ~15u; // buffers are padded
+        mbar_expect_tx(&bar[b], cb + ob);
+        tma_load_1d(cbuf[b], evc + (uint64_t)ch * kChainChunk, cb, &bar[b]);
+        tma_load_1d(obuf[b], ev + (uint64_t)ch * kChainChunk, ob, &bar[b]);
+    };
+    if (lane == 0) {
+        for (int b = 0; b < kChainBufs; ++b) mbar_init(&bar[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (uint32_t ch = 0; ch < nchunks && ch < (uint32_t)kChainBufs; ++ch) issue(ch);
+    }
+    __syncwarp();
+    double d = 0.0;
+    for (uint32_t ch = 0; ch < nchunks; ++ch) {
+        const int b = ch % kChainBufs;
+        mbar_wait(&bar[b], (ch / kChainBufs) & 1);
+        const uint32_t n = tmin<uint32_t>(kChainChunk, nev - ch * kChainChunk);
+        for (uint32_t base = 0; base < n; base += 32) {
+            const uint32_t cnt = tmin<uint32_t>(32, n - base);
+            const uint32_t o = lane < (int)cnt ? obuf[b][base + lane] >> 31 : 0u;
+            const uint32_t outmask = __ballot_sync(0xffffffffu, o != 0);
+            double mine = 0.0;
+            if (outmask == 0 && cnt == 32) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    d = dadd(d, cbuf[b][base + j]);
+                    if (lane == j) mine = d;
+                }
+            } else {
+                for (uint32_t j = 0; j < cnt; ++j) {
+                    const double cj = cbuf[b][base + j];
+                    if ((outmask >> j) & 1) d = cj;
+                    else d = dadd(d, cj);
+                    if (lane == (int)j) mine = d;
+                }
+            }
+            if (lane < (int)cnt) dv[(uint64_t)ch * kChainChunk + base + lane] = mine;
+        }
+        __syncwarp();
+        if (lane == 0 && ch + kChainBufs < nchunks) issue(ch + kChainBufs);
+    }
+}
+
+// ------------------------------------------------------------------ T4
+__global__ void __launch_bounds__(kEncThreads) enc_verify(TileArgs A, int planes) {
+    const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
+    if (pl >= planes) return;
+    const PlaneParams pp = A.params[pl];
+    if (pp.flags & kFlagFallback) return;
+    const int tid = threadIdx.x;
+    const uint64_t L = A.L;
+    const uint64_t t0 = (uint64_t)t * kTile;
+    const int tl = (int)tmin<uint64_t>(kTile, L - t0);
+    const uint64_t C = 1ull << A.log2C;
+    const uint64_t nidx = (L >> A.log2C) + 1;
+    const double *x = A.x + (uint64_t)pl * L;
+    IndexRec *idx = A.index + (uint64_t)pl * nidx;
+    if (pp.eb == 0.0) {
+        // lossless: d == x; only the decode index needs d[e-1], d[e-2]
+        for (int k = tid; k < tl; k += kEncThreads) {
+            const uint64_t i = t0 + k;
+            if ((i & (C - 1)) == 0) {
+                idx[i >> A.log2C].dprev = i > 0 ? x[i - 1] : 0.0;
+                idx[i >> A.log2C].dprev2 = i > 1 ? x[i - 2] : 0.0;
+            }
+        }
+        return;
+    }
+    using ScanI = cub::BlockScan<int, kEncThreads>;
+    __shared__ typename ScanI::TempStorage scan_tmp;
+    __shared__ int s_bad;
+    if (tid == 0) s_bad = 0;
+    const long long half = 1ll << (A.qb - 1);
+    const uint8_t *fl = A.fl + (uint64_t)pl * L;
+    uint32_t *sym = A.sym + (uint64_t)pl * L;
+    const double *dv = A.dval + (uint64_t)pl * L;
+    const uint32_t evbase = A.t_evoff[(uint64_t)pl * (A.ntiles + 1) + t];
+    int f[kPerThread], rank[kPerThread];
+    for (int e = 0; e < kPerThread; ++e) {
+        const int k = tid * kPerThread + e;
+        f[e] = (k < tl && (fl[t0 + k] & 1)) ? 1 : 0;
+    }
+    ScanI(scan_tmp).ExclusiveSum(f, rank);
+    __syncthreads();
+    // prediction = d at the last event strictly before i (ordinal evbase +
+    // rank - 1), else the value carried into the tile, else 0.0
+    const double dcarry = evbase > 0 ? dv[evbase - 1] : 0.0;
+    int bad = 0;
+    for (int e = 0; e < kPerThread; ++e) {
+        const int k = tid * kPerThread + e;
+        if (k >= tl) continue;
+        const uint64_t i = t0 + k;
+        const uint32_t ord = evbase + (uint32_t)rank[e]; // events before i
+        const double pred = ord > 0 ? dv[ord - 1] : 0.0;
+        const double dspec = f[e] ? dv[ord] : pred;
+        double rec = 0.0;
+        const uint32_t sy = quantize(x[i], pred, pp.q, pp.inv_q, pp.eb, half, &rec);
+        if (sy == kOutlierSym) rec = x[i];
+        if (sy != sym[i] || bits_of(rec) != bits_of(dspec)) bad = 1;
+        if ((i & (C - 1)) == 0) {
+            idx[i >> A.log2C].dprev = pred;
+            idx[i >> A.log2C].dprev2 = 0.0; // unused by the previous-value predictor
+        }
+    }
+    (void)dcarry;
+    if (bad) s_bad = 1;
+    __syncthreads();
+    if (tid == 0 && s_bad) atomicOr(&A.params[pl].flags, kFlagFallback);
+}
+
+// E1f: exact serial closed loop for refuted / linear planes (x from A.x).
+__global__ void enc_serial_x(TileArgs A, int planes) {
+    const int pl = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pl >= planes) return;
+    const PlaneParams pp = A.params[pl];
+    if (!(pp.flags & kFlagFallback)) return;
+    const uint64_t L = A.L;
+    const long long half = 1ll << (A.qb - 1);
+    const uint64_t C = 1ull << A.log2C;
+    const uint64_t nidx = (L >> A.log2C) + 1;
+    const double eb = pp.eb, q = pp.q;
+    const double *x = A.x + (uint64_t)pl * L;
+    uint32_t *sym = A.sym + (uint64_t)pl * L;
+    IndexRec *idx = A.index + (uint64_t)pl * nidx;
+    double d1 = 0.0, d2 = 0.0;
+    for (uint64_t i = 0; i < L; ++i) {
+        if ((i & (C - 1)) == 0) {
+            idx[i >> A.log2C].dprev = d1;
+            idx[i >> A.log2C].dprev2 = d2;
+        }
+        const double xi = x[i];
+        double pred;
+        if (A.predictor == 0) pred = i > 0 ? d1 : 0.0;
+        else pred = i == 0 ? 0.0 : (i == 1 ? d1 : predict_linear(d1, d2));
+        double rec = 0.0;
+        uint32_t sy = kOutlierSym;
+        if (eb == 0.0) {
+            if (bits_of(xi) == bits_of(pred)) { sy = (uint32_t)half; rec = pred; }
+        } else {
+            const double r = ddiv(dsub(xi, pred), q);
+            if (isfinite(r) && fabs(r) < (double)half) {
+                const long long m = llround_exact(r);
+                if (m > -half && m < half) {
+                    const double rr = dadd(pred, dmul(q, (double)m));
+                    if (isfinite(rr) && fabs(dsub(xi, rr)) <= eb) { sy = (uint32_t)(m + half); rec = rr; }
+                }
+            }
+        }
+        if (sy == kOutlierSym) rec = xi;
+        sym[i] = sy;
+        d2 = d1;
+        d1 = rec;
+    }
+}
+
+// ------------------------------------------------------------ tokenizer
+struct TokArgs {
+    const uint32_t *sym;   // [plane][L] exact
+    const double *x;       // [plane][L]
+    uint32_t *tsym, *trep; // [plane][L+1]
+    uint32_t *opos;        // [plane][L]
+    double *oval;          // [plane][L]
+    uint32_t *ocount;      // [plane]
+    uint32_t *ntok;        // [plane]
+    uint32_t *hist;        // [plane][rsym+1] (zero between uses)
+    uint32_t *hspecial;    // [plane][2]
+    uint32_t *symrange;    // [plane][2]
+    unsigned long long *gamma_bits; // [plane]
+    IndexRec *index;
+    // per plane-tile
+    int32_t *t_firstb, *t_lastb; // first / last run start in the tile (-1 / INT_MAX none)
+    int32_t *t_nout, *t_ooff;    // outliers per tile, scanned (+1)
+    int32_t *t_prevb;            // scanned: last run start strictly before the tile
+    int32_t *t_nextb;            // scanned: first run start strictly after the tile
+    int32_t *t_ntok, *t_tokoff;  // tokens per tile, scanned (+1)
+    uint64_t L;
+    int ntiles, log2C, qb;
+};
+
+// A run starts at i when i == 0 or sym[i] != sym[i-1].
+__global__ void __launch_bounds__(kEncThreads) tok_stats(TokArgs A, int planes) {
+    const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
+    if (pl >= planes) return;
+    const int tid = threadIdx.x;
+    const uint64_t L = A.L;
+    const uint64_t t0 = (uint64_t)t * kTile;
+    const int tl = (int)tmin<uint64_t>(kTile, L - t0);
+    const uint32_t *sym = A.sym + (uint64_t)pl * L;
+    using RedI = cub::BlockReduce<int, kEncThreads>;
+    __shared__ typename RedI::TempStorage r1, r2, r3;
+    int fb = 0x7FFFFFFF, lb = -1, no = 0;
+    for (int e = 0; e < kPerThread; ++e) {
+        const int k = tid * kPerThread + e;
+        if (k >= tl) continue;
+        const uint64_t i = t0 + k;
+        const uint32_t s = sym[i];
+        if (i == 0 || s != sym[i - 1]) {
+            fb = min(fb, (int)i);
+            lb = max(lb, (int)i);
+        }
+        no += s == kOutlierSym;
+    }
+    const int FB = RedI(r1).Reduce(fb, cub::Min());
+    const int LB = RedI(r2).Reduce(lb, cub::Max());
+    const int NO = RedI(r3).Sum(no);
+    if (tid == 0) {
+        A.t_firstb[(uint64_t)pl * A.ntiles + t] = FB;
+        A.t_lastb[(uint64_t)pl * A.ntiles + t] = LB;
+        A.t_nout[(uint64_t)pl * A.ntiles + t] = NO;
+    }
+}
+
+struct RunInfo {
+    uint64_t start, end;
+};
+
+// Per element: run [start, end) from in-tile scans + the scanned carries.
+template <class ScanI>
+__device__ __forceinline__ void element_runs(const TokArgs &A, const uint32_t *sym, int pl, int t, uint64_t t0,
+                                             int tl, typename ScanI::TempStorage &tmp, int *s_next,
+                                             uint64_t *start, uint64_t *end) {
+    const int tid = threadIdx.x;
+    int isb[kPerThread], st[kPerThread];
+    for (int e = 0; e < kPerThread; ++e) {
+        const int k = tid * kPerThread + e;
+        const uint64_t i = t0 + k;
+        isb[e] = (k < tl && (i == 0 || sym[i] != sym[i - 1])) ? (int)k : -1;
+    }
+    ScanI(tmp).InclusiveScan(isb, st, cub::Max());
+    const int32_t prevb = A.t_prevb[(uint64_t)pl * A.ntiles + t];
+    // first run start after each element: next boundary in the tile, else
+    // the scanned carry from later tiles, else L
+    for (int e = 0; e < kPerThread; ++e) {
+        const int k = tid * kPerThread + e;
+        s_next[k] = isb[e];
+    }
+    __syncthreads();
+    // suffix min over boundaries: s_next[k] = first boundary > k
+    // (small serial-free pass: each thread scans forward within its items,
+    // then a block-wide reverse scan over thread minima)
+    __shared__ int tmin_s[kEncThreads];
+    int m = 0x7FFFFFFF;
+    for (int e = 0; e < kPerThread; ++e) {
+        const int k = tid * kPerThread + e;
+        if (k < tl && isb[e] >= 0) m = min(m, k);
+    }
+    tmin_s[tid] = m;
+    __syncthreads();
+    // reverse inclusive min-scan over threads (Hillis-Steele)
+    for (int off = 1; off < kEncThreads; off <<= 1) {
+        const int v = tid + off < kEncThreads ? tmin_s[tid + off] : 0x7FFFFFFF;
+        __syncthreads();
+        tmin_s[tid] = min(tmin_s[tid], v);
+        __syncthreads();
+    }
+    const int32_t nextb_carry = A.t_nextb[(uint64_t)pl * A.ntiles + t];
+    const uint64_t after = nextb_carry == 0x7FFFFFFF ? A.L : (uint64_t)nextb_carry;
+    for (int e = 0; e < kPerThread; ++e) {
+        const int k = tid * kPerThread + e;
+        // start
+        start[e] = st[e] >= 0 ? t0 + st[e] : (uint64_t)prevb;
+        // end: first boundary > k
+        int nb = 0x7FFFFFFF;
+        for (int e2 = e + 1; e2 < kPerThread; ++e2)
+            if (tid * kPerThread + e2 < tl && isb[e2] >= 0) { nb = tid * kPerThread + e2; break; }
+        if (nb == 0x7FFFFFFF && tid + 1 < kEncThreads) nb = tmin_s[tid + 1];
+        end[e] = (nb != 0x7FFFFFFF && nb < tl) ? t0 + nb : after;
+        (void)k;
+    }
+}
+
+__global__ void __launch_bounds__(kEncThreads) tok_count(TokArgs A, int planes) {
+    const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
+    if (pl >= planes) return;
+    const int tid = threadIdx.x;
+    const uint64_t L = A.L;
+    const uint64_t t0 = (uint64_t)t * kTile;
+    const int tl = (int)tmin<uint64_t>(kTile, L - t0);
+    const uint32_t *sym = A.sym + (uint64_t)pl * L;
+    using ScanI = cub::BlockScan<int, kEncThreads>;
+    using RedI = cub::BlockReduce<int, kEncThreads>;
+    __shared__ typename ScanI::TempStorage tmp;
+    __shared__ typename RedI::TempStorage rtmp;
+    __shared__ int s_next[kTile];
+    __shared__ uint32_t hist[kWin];
+    __shared__ uint32_t h0, hrun, smin, smax;
+    __shared__ unsigned long long gbits;
+    const long long half = 1ll << (A.qb - 1);
+    const uint32_t rsym = 1u << A.qb;
+    const uint32_t wlo = (uint32_t)(half - kWin / 2);
+    uint32_t *ghist = A.hist + (uint64_t)pl * ((uint64_t)rsym + 1);
+    for (int k = tid; k < kWin; k += kEncThreads) hist[k] = 0;
+    if (tid == 0) { h0 = 0; hrun = 0; smin = 0xFFFFFFFFu; smax = 0; gbits = 0; }
+    uint64_t start[kPerThread], end[kPerThread];
+    element_runs<ScanI>(A, sym, pl, t, t0, tl, tmp, s_next, start, end);
+    auto count = [&](uint32_t s, uint32_t n) {
+        if (s == kOutlierSym) atomicAdd(&h0, n);
+        else if (s == rsym) atomicAdd(&hrun, n);
+        else if (s - wlo < (uint32_t)kWin) atomicAdd(&hist[s - wlo], n);
+        else {
+            atomicAdd(&ghist[s], n);
+            atomicMin(&smin, s);
+            atomicMax(&smax, s);
+        }
+    };
+    int cnt = 0;
+    for (int e = 0; e < kPerThread; ++e) {
+        const int k = tid * kPerThread + e;
+        if (k >= tl) continue;
+        const uint64_t i = t0 + k;
+        const uint32_t s = sym[i];
+        const uint64_t len = end[e] - start[e];
+        const bool longrun = s != kOutlierSym && len >= kMinRunLen;
+        if (longrun) {
+            if (i == start[e]) {
+                cnt += 2;
+                count(s, 1);
+                count(rsym, 1);
+                atomicAdd(&gbits, (unsigned long long)(2 * bit_width64(len - 1) - 1));
+            }
+        } else {
+            cnt += 1;
+            count(s, 1);
+        }
+    }
+    const int tot = RedI(rtmp).Sum(cnt);
+    __syncthreads();
+    if (tid == 0) {
+        A.t_ntok[(uint64_t)pl * A.ntiles + t] = tot;
+        if (h0) atomicAdd(&A.hspecial[2 * pl], h0);
+        if (hrun) atomicAdd(&A.hspecial[2 * pl + 1], hrun);
+        if (gbits) atomicAdd(&A.gamma_bits[pl], gbits);
+    }
+    for (int k = tid; k < kWin; k += kEncThreads) {
+        const uint32_t v = hist[k];
+        const uint32_t sy = wlo + k;
+        if (v && sy != kOutlierSym && sy < rsym) {
+            atomicAdd(&ghist[sy], v);
+            atomicMin(&smin, sy);
+            atomicMax(&smax, sy);
+        }
+    }
+    __syncthreads();
+    if (tid == 0 && smin <= smax) {
+        atomicMin(&A.symrange[2 * pl], smin);
+        atomicMax(&A.symrange[2 * pl + 1], smax);
+    }
+}
+
+__global__ void __launch_bounds__(kEncThreads) tok_emit(TokArgs A, int planes) {
+    const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
+    if (pl >= planes) return;
+    const int tid = threadIdx.x;
+    const uint64_t L = A.L;
+    const uint64_t t0 = (uint64_t)t * kTile;
+    const int tl = (int)tmin<uint64_t>(kTile, L - t0);
+    const uint32_t *sym = A.sym + (uint64_t)pl * L;
+    const double *x = A.x + (uint64_t)pl * L;
+    using ScanI = cub::BlockScan<int, kEncThreads>;
+    __shared__ typename ScanI::TempStorage tmp;
+    __shared__ int s_next[kTile];
+    const uint32_t rsym = 1u << A.qb;
+    const uint64_t C = 1ull << A.log2C;
+    const uint64_t nidx = (L >> A.log2C) + 1;
+    uint32_t *tsym = A.tsym + (uint64_t)pl * (L + 1);
+    uint32_t *trep = A.trep + (uint64_t)pl * (L + 1);
+    IndexRec *idx = A.index + (uint64_t)pl * nidx;
+    uint64_t start[kPerThread], end[kPerThread];
+    element_runs<ScanI>(A, sym, pl, t, t0, tl, tmp, s_next, start, end);
+    int cnt[kPerThread], tpos[kPerThread], isout[kPerThread], opos[kPerThread];
+    for (int e = 0; e < kPerThread; ++e) {
+        const int k = tid * kPerThread + e;
+        cnt[e] = 0;
+        isout[e] = 0;
+        if (k >= tl) continue;
+        const uint64_t i = t0 + k;
+        const uint32_t s = sym[i];
+        const uint64_t len = end[e] - start[e];
+        const bool longrun = s != kOutlierSym && len >= kMinRunLen;
+        cnt[e] = longrun ? (i == start[e] ? 2 : 0) : 1;
+        isout[e] = s == kOutlierSym;
+    }
+    __syncthreads();
+    ScanI(tmp).ExclusiveSum(cnt, tpos);
+    __syncthreads();
+    ScanI(tmp).ExclusiveSum(isout, opos);
+    const uint32_t tokbase = (uint32_t)A.t_tokoff[(uint64_t)pl * (A.ntiles + 1) + t];
+    const uint32_t obase = (uint32_t)A.t_ooff[(uint64_t)pl * (A.ntiles + 1) + t];
+    for (int e = 0; e < kPerThread; ++e) {
+        const int k = tid * kPerThread + e;
+        if (k >= tl) continue;
+        const uint64_t i = t0 + k;
+        const uint32_t s = sym[i];
+        const uint32_t tk = tokbase + (uint32_t)tpos[e];
+        const uint64_t len = end[e] - start[e];
+        const bool longrun = s != kOutlierSym && len >= kMinRunLen;
+        if (cnt[e] == 2) {
+            tsym[tk] = s;
+            trep[tk] = 0;
+            tsym[tk + 1] = rsym;
+            trep[tk + 1] = (uint32_t)(len - 1);
+        } else if (cnt[e] == 1) {
+            tsym[tk] = s;
+            trep[tk] = 0;
+        }
+        if (isout[e]) {
+            A.opos[(uint64_t)pl * L + obase + opos[e]] = (uint32_t)i;
+            A.oval[(uint64_t)pl * L + obase + opos[e]] = x[i];
+        }
+        if ((i & (C - 1)) == 0) {
+            // decoder state at element i (codec.cpp:612-626)
+            IndexRec *r = idx + (i >> A.log2C);
+            const uint32_t ocur = obase + (uint32_t)opos[e];
+            if (i == start[e]) {
+                r->tok = tk;
+                r->run_left = 0;
+                r->last_lit = i == 0 ? rsym : sym[i - 1];
+                r->ocur = ocur;
+            } else {
+                r->last_lit = s;
+                r->ocur = ocur;
+                if (longrun) {
+                    // the run's literal + RUN tokens precede: resume after them
+                    // (token index of the run start = tk since non-start
+                    // elements of a long run emit nothing)
+                    r->tok = tk;
+                    r->run_left = (uint32_t)(end[e] - i);
+                } else {
+                    r->tok = tk;
+                    r->run_left = 0;
+                }
+            }
+        }
+    }
+    if (tid == 0 && t == A.ntiles - 1) {
+        A.ntok[pl] = (uint32_t)A.t_tokoff[(uint64_t)pl * (A.ntiles + 1) + A.ntiles];
+        A.ocount[pl] = (uint32_t)A.t_ooff[(uint64_t)pl * (A.ntiles + 1) + A.ntiles];
+    }
+}
+
+} // namespace qcb

@@ -11,7 +11,9 @@ namespace qcb {
 // mode: 0 RangeRelative, 1 Absolute, 2 Lossless.  One block per unit.
 template <int NP, class Src>
 __global__ void __launch_bounds__(256) init_params(PlaneParams *params, Src src, int units, uint64_t L,
-                                                   int mode, double bound, uint32_t *nonfinite) {
+                                                   int mode, double bound, int predictor, uint32_t *nonfinite,
+                                                   uint32_t *symrange, uint32_t *hspecial,
+                                                   unsigned long long *gamma_bits) {
     const int unit = blockIdx.x;
     if (unit >= units) return;
     __shared__ double smin[NP][256], smax[NP][256];
@@ -59,9 +61,16 @@ __global__ void __launch_bounds__(256) init_params(PlaneParams *params, Src src,
         pp.eb = eb;
         pp.q = dmul(2.0, eb);
         pp.inv_q = ddiv(1.0, pp.q);
-        pp.flags = 0;
+        // the linear predictor with eb > 0 has no lattice model: serial path
+        pp.flags = (predictor == 1 && eb != 0.0) ? kFlagFallback : 0u;
         pp.pad = 0;
         params[unit * NP + tid] = pp;
+        const int pl = unit * NP + tid;
+        symrange[2 * pl] = 0xFFFFFFFFu;
+        symrange[2 * pl + 1] = 0;
+        hspecial[2 * pl] = 0;
+        hspecial[2 * pl + 1] = 0;
+        gamma_bits[pl] = 0;
         if (nonfinite && sbad) atomicExch(nonfinite, 1u);
     }
 }

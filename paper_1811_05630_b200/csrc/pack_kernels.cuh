@@ -221,9 +221,12 @@ struct PackArgs {
     const PlaneParams *params;
     IndexRec *index;                      // [plane][nidx]
     uint8_t *arena;
+    uint64_t arena_cap;                   // bytes usable in `arena`
+    uint32_t *overflow;                   // set when the batch does not fit
     uint64_t *blk_off;                    // out: block start in the arena
     uint64_t L, cap;
     int log2C, qb, mode, predictor;
+    int planes_total;                     // slot_off[planes_total] = bytes needed
 };
 
 __device__ __forceinline__ void put_bits_smem(uint32_t *w, uint32_t o, uint64_t v, int n) {
@@ -242,19 +245,136 @@ __device__ __forceinline__ void store_le(uint8_t *p, uint64_t v, int bytes) {
     for (int i = 0; i < bytes; ++i) p[i] = (uint8_t)(v >> (8 * i));
 }
 
-constexpr int kPackTok = 1024;
+constexpr int kPackTok = 1024;                 // tokens per pack block
 constexpr int kPackWords = kPackTok * 120 / 32 + 2;
+constexpr int kCodeWin = 2048;                 // dense shared codebook window
 
-__global__ void __launch_bounds__(256) enc_pack(PackArgs A, int planes) {
-    const int pl = blockIdx.x;
+// Per-block view of a plane's codebook (codec.cpp:493-496 code_of): a dense
+// shared-memory window over the symbol range when it is narrow, else a
+// binary search over the sorted symbol list.
+struct SCodebook {
+    uint64_t code[kCodeWin];
+    uint8_t len[kCodeWin];
+    uint64_t code0, coderun;
+    uint8_t len0, lenrun;
+    uint32_t lo, span, n;
+    bool dense;
+};
+
+__device__ void load_codebook(SCodebook &C, const PackArgs &A, int pl) {
+    const uint32_t n = A.nsym[pl];
+    const uint32_t *cs = A.cb_sym + pl * A.cap;
+    const uint8_t *cl = A.cb_len + pl * A.cap;
+    const uint64_t *cc = A.cb_code + pl * A.cap;
+    const uint32_t rsym = 1u << A.qb;
+    // literal symbols occupy ranks [r0, r1): 0 first, RUN last when present
+    const uint32_t r0 = (n && cs[0] == kOutlierSym) ? 1 : 0;
+    const uint32_t r1 = (n && cs[n - 1] == rsym) ? n - 1 : n;
+    if (threadIdx.x == 0) {
+        C.n = n;
+        C.len0 = 0;
+        C.lenrun = 0;
+        if (r0) { C.code0 = cc[0]; C.len0 = cl[0]; }
+        if (r1 < n) { C.coderun = cc[n - 1]; C.lenrun = cl[n - 1]; }
+        C.lo = r1 > r0 ? cs[r0] : 0;
+        C.span = r1 > r0 ? cs[r1 - 1] - cs[r0] + 1 : 0;
+        C.dense = C.span <= (uint32_t)kCodeWin;
+    }
+    __syncthreads();
+    if (C.dense) {
+        for (uint32_t k = threadIdx.x; k < C.span; k += blockDim.x) C.len[k] = 0;
+        __syncthreads();
+        for (uint32_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+            C.code[cs[r] - C.lo] = cc[r];
+            C.len[cs[r] - C.lo] = cl[r];
+        }
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void lookup_code(const SCodebook &C, const PackArgs &A, int pl, uint32_t s,
+                                            uint64_t &code, int &len) {
+    const uint32_t rsym = 1u << A.qb;
+    if (s == kOutlierSym) { code = C.code0; len = C.len0; return; }
+    if (s == rsym) { code = C.coderun; len = C.lenrun; return; }
+    if (C.dense) { code = C.code[s - C.lo]; len = C.len[s - C.lo]; return; }
+    const uint32_t *cs = A.cb_sym + pl * A.cap;
+    uint32_t lo = 0, hi = C.n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (cs[mid] < s) lo = mid + 1;
+        else hi = mid;
+    }
+    code = A.cb_code[pl * A.cap + lo];
+    len = A.cb_len[pl * A.cap + lo];
+}
+
+// token -> (code, code length, gamma length): codec.cpp:513-520
+__device__ __forceinline__ uint32_t token_bits(const SCodebook &C, const PackArgs &A, int pl, uint32_t s,
+                                               uint32_t rep, uint64_t &code, int &len, int &glen) {
+    lookup_code(C, A, pl, s, code, len);
+    glen = s == (1u << A.qb) ? 2 * bit_width64(rep) - 1 : 0;
+    return (uint32_t)(len + glen);
+}
+
+// P1: bits of every 1024-token chunk (grid: planes x chunks).
+__global__ void __launch_bounds__(256) pack_count(PackArgs A, int planes, int nck, int32_t *cbits) {
+    const int pl = blockIdx.x / nck, c = blockIdx.x % nck;
+    if (pl >= planes) return;
+    const uint32_t ntok = A.ntok[pl];
+    const uint32_t t0 = (uint32_t)c * kPackTok;
+    if (t0 >= ntok) {
+        if (threadIdx.x == 0) cbits[(uint64_t)pl * nck + c] = 0;
+        return;
+    }
+    __shared__ SCodebook C;
+    load_codebook(C, A, pl);
+    const uint32_t tn = tmin<uint32_t>(kPackTok, ntok - t0);
+    const uint32_t *ts = A.tsym + (uint64_t)pl * (A.L + 1);
+    const uint32_t *tr = A.trep + (uint64_t)pl * (A.L + 1);
+    uint32_t bits = 0;
+    for (uint32_t k = threadIdx.x; k < tn; k += blockDim.x) {
+        uint64_t code;
+        int len, glen;
+        bits += token_bits(C, A, pl, ts[t0 + k], tr[t0 + k], code, len, glen);
+    }
+    using Red = cub::BlockReduce<uint32_t, 256>;
+    __shared__ typename Red::TempStorage rt;
+    const uint32_t tot = Red(rt).Sum(bits);
+    if (threadIdx.x == 0) cbits[(uint64_t)pl * nck + c] = (int32_t)tot;
+}
+
+// Zero the batch's arena range (stream words are OR-combined at chunk seams).
+__global__ void arena_zero(uint8_t *arena, uint64_t cap, const uint64_t *total_ptr) {
+    const uint64_t total = *total_ptr + 64;
+    if (total > cap) return;
+    uint4 *w = reinterpret_cast<uint4 *>(arena);
+    const uint64_t nw = (total + 15) / 16;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nw; k += (uint64_t)gridDim.x * blockDim.x)
+        w[k] = make_uint4(0, 0, 0, 0);
+}
+
+
+// P2: header + table (chunk 0), stream bits of every chunk, outlier records,
+// decode-index bit positions (grid: planes x chunks).
+__global__ void __launch_bounds__(256) pack_write(PackArgs A, int planes, int nck, const int32_t *coff) {
+    const int pl = blockIdx.x / nck, c = blockIdx.x % nck;
     if (pl >= planes) return;
     const int tid = threadIdx.x;
-    using Scan = cub::BlockScan<uint32_t, 256>;
-    __shared__ typename Scan::TempStorage scan_tmp;
+    if (A.slot_off[A.planes_total] + 64 > A.arena_cap) {
+        if (tid == 0) atomicExch(A.overflow, 1u);
+        return;
+    }
+    const uint32_t ntok = A.ntok[pl];
+    const uint32_t t0 = (uint32_t)c * kPackTok;
+    const uint32_t nchk = (ntok + kPackTok - 1) / kPackTok;
+    if (c >= (int)nchk) return;
+    __shared__ SCodebook C;
     __shared__ uint32_t words[kPackWords];
     __shared__ uint32_t toff[kPackTok + 1];
-    __shared__ uint32_t s_carry;
     __shared__ uint32_t s_jlo, s_jhi;
+    using Scan = cub::BlockScan<uint32_t, 256>;
+    __shared__ typename Scan::TempStorage scan_tmp;
 
     const uint32_t n = A.nsym[pl];
     const uint64_t pre = kHeaderBytes + 4 + 5ull * n;
@@ -265,143 +385,112 @@ __global__ void __launch_bounds__(256) enc_pack(PackArgs A, int planes) {
     const uint64_t bits = A.stream_bits[pl];
     const uint64_t sbytes = (bits + 7) / 8;
     const uint32_t nout = A.ocount[pl];
-    const uint64_t payload = 4 + 5ull * n + sbytes + 16ull * nout;
-    const uint32_t *cs = A.cb_sym + pl * A.cap;
-    const uint8_t *cl = A.cb_len + pl * A.cap;
-    const uint64_t *cc = A.cb_code + pl * A.cap;
     const uint32_t rsym = 1u << A.qb;
     const uint64_t nidx = (A.L >> A.log2C) + 1;
+    const uint32_t nchunks_idx = (uint32_t)((A.L + (1ull << A.log2C) - 1) >> A.log2C);
     IndexRec *idx = A.index + pl * nidx;
 
-    if (tid == 0) {
-        A.blk_off[pl] = off;
-        blk[0] = 'Q'; blk[1] = 'C'; blk[2] = 'B'; blk[3] = '1';
-        blk[4] = 1;
-        blk[5] = (uint8_t)A.mode;
-        blk[6] = (uint8_t)A.predictor;
-        blk[7] = (uint8_t)A.qb;
-        store_le(blk + 8, A.L, 8);
-        store_le(blk + 16, bits_of(A.params[pl].eb), 8);
-        store_le(blk + 24, nout, 8);
-        store_le(blk + 32, payload, 8);
-        store_le(blk + 40, n, 4);
-        s_carry = 0;
-    }
-    for (uint32_t r = tid; r < n; r += 256) {
-        store_le(blk + 44 + 5ull * r, cs[r], 4);
-        blk[44 + 5ull * r + 4] = cl[r];
-    }
-    // tokens
-    const uint32_t ntok = A.ntok[pl];
-    const uint32_t *ts = A.tsym + pl * (A.L + 1);
-    const uint32_t *tr = A.trep + pl * (A.L + 1);
-    uint64_t base_bit = 0;
-    for (uint32_t t0 = 0; t0 < ntok; t0 += kPackTok) {
-        const uint32_t tn = tmin<uint32_t>(kPackTok, ntok - t0);
-        uint64_t tcode[4];
-        int tlen[4], glen[4];
-        uint32_t tbits[4];
-        for (int e = 0; e < 4; ++e) {
-            const uint32_t k = tid * 4 + e;
-            tbits[e] = 0;
-            tlen[e] = 0;
-            glen[e] = 0;
-            tcode[e] = 0;
-            if (k < tn) {
-                const uint32_t s = ts[t0 + k];
-                uint32_t lo = 0, hi = n;
-                while (lo < hi) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (cs[mid] < s) lo = mid + 1;
-                    else hi = mid;
-                }
-                tcode[e] = cc[lo];
-                tlen[e] = cl[lo];
-                if (s == rsym) glen[e] = 2 * bit_width64(tr[t0 + k]) - 1;
-                tbits[e] = (uint32_t)(tlen[e] + glen[e]);
-            }
-        }
-        uint32_t pos[4], tot;
-        Scan(scan_tmp).ExclusiveSum(tbits, pos, tot);
-        const uint32_t b0 = (uint32_t)(base_bit & 31);
-        const uint32_t nwords = (b0 + tot + 31) / 32;
-        for (uint32_t w = tid; w < nwords + 1; w += 256) words[w] = 0;
-        __syncthreads();
-        if (tid == 0) words[0] = s_carry;
-        for (int e = 0; e < 4; ++e) {
-            const uint32_t k = tid * 4 + e;
-            if (k <= tn) toff[k] = pos[e];
-        }
-        if (tid == 255) toff[tn] = tot; // sentinel when tn == 1024
-        __syncthreads();
-        for (int e = 0; e < 4; ++e) {
-            const uint32_t k = tid * 4 + e;
-            if (k < tn) {
-                put_bits_smem(words, b0 + pos[e], tcode[e], tlen[e]);
-                if (glen[e]) put_bits_smem(words, b0 + pos[e] + tlen[e], tr[t0 + k], glen[e]);
-            }
-        }
-        __syncthreads();
-        // complete words -> global (big-endian byte order)
-        const uint32_t endbit = b0 + tot;
-        const uint32_t full = endbit / 32;
-        const uint64_t w0 = base_bit / 32;
-        uint32_t *gw = reinterpret_cast<uint32_t *>(stream);
-        for (uint32_t w = tid; w < full; w += 256) gw[w0 + w] = bswap32(words[w]);
-        // decode-index bit positions for checkpoints resuming in this chunk
+    if (c == 0) {
+        const uint64_t payload = 4 + 5ull * n + sbytes + 16ull * nout;
+        const uint32_t *cs = A.cb_sym + pl * A.cap;
+        const uint8_t *cl = A.cb_len + pl * A.cap;
         if (tid == 0) {
-            // records are sorted by tok; find [jlo, jhi) with tok in [t0, t0+tn)
-            const uint32_t nchunks = (uint32_t)((A.L + (1ull << A.log2C) - 1) >> A.log2C);
-            uint32_t lo = 1, hi = nchunks;
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (idx[mid].tok < t0) lo = mid + 1;
-                else hi = mid;
-            }
-            s_jlo = lo;
-            hi = nchunks;
-            uint32_t lo2 = lo;
-            while (lo2 < hi) {
-                const uint32_t mid = (lo2 + hi) >> 1;
-                if (idx[mid].tok < t0 + tn) lo2 = mid + 1;
-                else hi = mid;
-            }
-            s_jhi = lo2;
+            A.blk_off[pl] = off;
+            blk[0] = 'Q'; blk[1] = 'C'; blk[2] = 'B'; blk[3] = '1';
+            blk[4] = 1;
+            blk[5] = (uint8_t)A.mode;
+            blk[6] = (uint8_t)A.predictor;
+            blk[7] = (uint8_t)A.qb;
+            store_le(blk + 8, A.L, 8);
+            store_le(blk + 16, bits_of(A.params[pl].eb), 8);
+            store_le(blk + 24, nout, 8);
+            store_le(blk + 32, payload, 8);
+            store_le(blk + 40, n, 4);
+            idx[0].bitpos = 0;
+            idx[0].tok = 0;
+            idx[0].run_left = 0;
+            idx[0].ocur = 0;
+            idx[0].last_lit = rsym;
         }
-        __syncthreads();
-        for (uint32_t j = s_jlo + tid; j < s_jhi; j += 256) {
-            if ((uint64_t)j << A.log2C >= A.L) continue;
-            idx[j].bitpos = base_bit + toff[idx[j].tok - t0];
+        for (uint32_t r = tid; r < n; r += 256) {
+            store_le(blk + 44 + 5ull * r, cs[r], 4);
+            blk[44 + 5ull * r + 4] = cl[r];
         }
-        if (tid == 0) s_carry = (endbit & 31) ? words[full] : 0;
-        __syncthreads();
-        base_bit += tot;
+        // outlier records (u64 pos, f64 value), LE, after the stream
+        uint8_t *orec = stream + sbytes;
+        const uint32_t *op = A.opos + pl * A.L;
+        const double *ov = A.oval + pl * A.L;
+        for (uint32_t k = tid; k < nout; k += 256) {
+            store_le(orec + 16ull * k, op[k], 8);
+            store_le(orec + 16ull * k + 8, bits_of(ov[k]), 8);
+        }
     }
-    // trailing partial word, byte-wise (never write past the stream)
+    load_codebook(C, A, pl);
+    const uint32_t tn = tmin<uint32_t>(kPackTok, ntok - t0);
+    const uint32_t *ts = A.tsym + (uint64_t)pl * (A.L + 1);
+    const uint32_t *tr = A.trep + (uint64_t)pl * (A.L + 1);
+    uint64_t tcode[4];
+    int tlen[4], glen[4];
+    uint32_t tbits[4];
+    for (int e = 0; e < 4; ++e) {
+        const uint32_t k = tid * 4 + e;
+        tbits[e] = 0;
+        tlen[e] = glen[e] = 0;
+        tcode[e] = 0;
+        if (k < tn) tbits[e] = token_bits(C, A, pl, ts[t0 + k], tr[t0 + k], tcode[e], tlen[e], glen[e]);
+    }
+    uint32_t pos[4], tot;
+    Scan(scan_tmp).ExclusiveSum(tbits, pos, tot);
+    const uint64_t base_bit = (uint64_t)(uint32_t)coff[(uint64_t)pl * (nck + 1) + c];
+    const uint32_t b0 = (uint32_t)(base_bit & 31);
+    const uint32_t nwords = (b0 + tot + 31) / 32;
+    for (uint32_t w = tid; w < nwords; w += 256) words[w] = 0;
+    for (int e = 0; e < 4; ++e) {
+        const uint32_t k = tid * 4 + e;
+        if (k <= tn) toff[k] = pos[e];
+    }
+    if (tid == 255) toff[tn] = tot;
+    __syncthreads();
+    for (int e = 0; e < 4; ++e) {
+        const uint32_t k = tid * 4 + e;
+        if (k < tn) {
+            put_bits_smem(words, b0 + pos[e], tcode[e], tlen[e]);
+            if (glen[e]) put_bits_smem(words, b0 + pos[e] + tlen[e], tr[t0 + k], glen[e]);
+        }
+    }
+    __syncthreads();
+    // words -> global (big-endian byte order); the first and last words may
+    // be shared with the neighbouring chunks (or outlier bytes): OR them
+    uint32_t *gw = reinterpret_cast<uint32_t *>(stream);
+    const uint64_t w0 = base_bit / 32;
+    for (uint32_t w = tid; w < nwords; w += 256) {
+        const uint32_t v = bswap32(words[w]);
+        if (w == 0 || w == nwords - 1) atomicOr(&gw[w0 + w], v);
+        else gw[w0 + w] = v;
+    }
+    // decode-index bit positions for checkpoints resuming in this chunk
     if (tid == 0) {
-        if (base_bit & 31) {
-            const uint64_t w = base_bit / 32;
-            const uint32_t v = s_carry;
-            for (uint64_t b = w * 4; b < sbytes; ++b) stream[b] = (uint8_t)(v >> (24 - 8 * (b - w * 4)));
+        uint32_t lo = 1, hi = nchunks_idx;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (idx[mid].tok < t0) lo = mid + 1;
+            else hi = mid;
         }
-        // checkpoints resuming exactly at the end of the token stream
-        for (uint32_t j = 1; j < nidx; ++j)
-            if (((uint64_t)j << A.log2C) < A.L && idx[j].tok >= ntok) idx[j].bitpos = base_bit;
-        idx[0].bitpos = 0;
-        idx[0].tok = 0;
-        idx[0].run_left = 0;
-        idx[0].ocur = 0;
-        idx[0].last_lit = rsym;
-        idx[0].dprev = 0.0;
-        idx[0].dprev2 = 0.0;
+        s_jlo = lo;
+        const bool last_chunk = c == (int)nchk - 1;
+        hi = nchunks_idx;
+        uint32_t lo2 = lo;
+        while (lo2 < hi) {
+            const uint32_t mid = (lo2 + hi) >> 1;
+            if (last_chunk || idx[mid].tok < t0 + tn) lo2 = mid + 1;
+            else hi = mid;
+        }
+        s_jhi = last_chunk ? nchunks_idx : lo2;
     }
-    // outliers (u64 pos, f64 value), LE, right after the stream
-    uint8_t *orec = stream + sbytes;
-    const uint32_t *op = A.opos + pl * A.L;
-    const double *ov = A.oval + pl * A.L;
-    for (uint32_t k = tid; k < nout; k += 256) {
-        store_le(orec + 16ull * k, op[k], 8);
-        store_le(orec + 16ull * k + 8, bits_of(ov[k]), 8);
+    __syncthreads();
+    for (uint32_t j = s_jlo + tid; j < s_jhi; j += 256) {
+        const uint32_t tk = idx[j].tok;
+        idx[j].bitpos = tk >= t0 + tn ? base_bit + tot : base_bit + toff[tk - t0];
     }
 }
 

@@ -9,6 +9,7 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -20,7 +21,8 @@
 #include "../../include/qcsim_c.h"
 #include "common.cuh"
 #include "decode_kernels.cuh"
-#include "encode_kernels.cuh"
+#include "enc_tiles.cuh"
+#include "sources.cuh"
 #include "misc_kernels.cuh"
 #include "pack_kernels.cuh"
 
@@ -165,11 +167,22 @@ struct ProfScope {
             cudaEventRecord(a, st);
         }
     }
-    ~ProfScope() {
+    ~ProfScope() noexcept(false) {
         if (a) {
             cudaEvent_t b = g_prof.get();
             cudaEventRecord(b, st);
             g_prof.pend.push_back({name, a, b});
+        }
+        // QCSIM_DEBUG_SYNC=1: synchronise after every kernel and name the
+        // one that failed (fault localisation without compute-sanitizer)
+        static const bool dbg = [] {
+            const char *v = std::getenv("QCSIM_DEBUG_SYNC");
+            return v && v[0] == '1';
+        }();
+        if (dbg) {
+            cudaError_t e = cudaStreamSynchronize(st);
+            if (e == cudaSuccess) e = cudaGetLastError();
+            if (e != cudaSuccess) raise(QCSIM_CUDA, std::string("kernel ") + name + ": " + cudaGetErrorString(e));
         }
     }
 };
@@ -190,18 +203,50 @@ void validate_codec(const qcsim_codec_config &c) { // codec.cpp:331-341
 int auto_log2C(uint64_t L) {
     int s = 0;
     while ((1ull << s) < L) ++s;
-    return std::max(6, std::min(12, s - 5));
+    return std::max(6, std::min(10, s - 7));
 }
+
+// Grow-only pinned host buffer.
+template <class T> struct HBuf {
+    T *p = nullptr;
+    size_t cap = 0;
+    HBuf() = default;
+    HBuf(const HBuf &) = delete;
+    HBuf &operator=(const HBuf &) = delete;
+    ~HBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    void ensure(size_t n) {
+        if (n <= cap && p) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        if (cudaHostAlloc((void **)&p, std::max<size_t>(n, 1) * sizeof(T), cudaHostAllocDefault) != cudaSuccess) {
+            cudaGetLastError();
+            raise(QCSIM_NOMEM, "pinned host allocation failed");
+        }
+        cap = std::max<size_t>(n, 1);
+    }
+};
 
 // ------------------------------------------------------------ encoder
 struct EncScratch {
     DBuf<PlaneParams> params;
-    DBuf<uint32_t> sym, opos, ocount, ntok, tsym, trep, hist, hspecial, symrange, nsym, err, nonfinite;
-    DBuf<double> oval, tilesum;
-    DBuf<uint64_t> gamma, cb_cnt, cb_code, cb_key, cb_ncnt, stream_bits, block_bytes, slot_bytes, slot_off, blk_off;
-    DBuf<uint8_t> cb_len, cub_tmp;
+    DBuf<double> x, dval, evc, oval, tilesum;
+    DBuf<uint32_t> sym, evlist, opos, ocount, ntok, tsym, trep, hist, hspecial, symrange, nsym, err, nonfinite;
+    DBuf<uint8_t> fl, cb_len, cub_tmp;
+    DBuf<int32_t> t_lastout, t_base, t_nev, t_evoff, t_firstb, t_lastb, t_nout, t_ooff, t_prevb, t_nextb, t_ntok,
+        t_tokoff, t_cbits, t_coff;
+    DBuf<unsigned long long> gamma;
+    DBuf<uint64_t> cb_cnt, cb_code, cb_key, cb_ncnt, stream_bits, block_bytes, slot_bytes, slot_off, blk_off;
     DBuf<uint32_t> cb_sym;
     DBuf<int32_t> cb_parent;
+    DBuf<uint32_t> overflow;
+    HBuf<uint64_t> h_bytes, h_off, h_misc;
+    HBuf<PlaneParams> h_params;
+    HBuf<uint32_t> h_err;
+    PackArgs pack{};
+    uint64_t planes = 0;
     uint64_t hist_stride = 0;
 
     void ensure(uint64_t planes, uint64_t units, uint64_t L, int qb) {
@@ -209,7 +254,12 @@ struct EncScratch {
         const uint64_t rsym1 = (1ull << qb) + 1;
         const uint64_t cap = std::min<uint64_t>(L + 1, rsym1);
         params.ensure(planes);
+        x.ensure(planes * L);
+        dval.ensure(planes * L);
+        evc.ensure(planes * L + 8);       // TMA chunks round up to 16 bytes
+        evlist.ensure(planes * L + 8);
         sym.ensure(planes * L);
+        fl.ensure(planes * L);
         opos.ensure(planes * L);
         oval.ensure(planes * L);
         ocount.ensure(planes);
@@ -217,6 +267,9 @@ struct EncScratch {
         tsym.ensure(planes * (L + 1));
         trep.ensure(planes * (L + 1));
         ntok.ensure(planes);
+        for (DBuf<int32_t> *b : {&t_lastout, &t_base, &t_nev, &t_evoff, &t_firstb, &t_lastb, &t_nout, &t_ooff,
+                                 &t_prevb, &t_nextb, &t_ntok, &t_tokoff, &t_cbits, &t_coff})
+            b->ensure(planes * (ntiles + 2));
         // the dense histogram must be all-zero between uses (E3 re-zeroes)
         if (hist_stride != rsym1 || hist.cap < planes * rsym1) {
             hist.ensure(planes * rsym1);
@@ -241,6 +294,7 @@ struct EncScratch {
         blk_off.ensure(planes);
         err.ensure(planes);
         nonfinite.ensure(1);
+        overflow.ensure(1);
     }
 };
 
@@ -255,83 +309,181 @@ struct EncodeResult {
     uint64_t fallback = 0;
 };
 
-// Encodes units*NP planes produced by `src` into `arena` (grown as needed).
-// `index` receives the decode checkpoints ([plane][nidx]).
+void launch_plane_scan(cudaStream_t st, const int32_t *in, int32_t *out, int ntiles, int planes, ScanKind kind);
+
+// Block assembly: chunk bit counts + plane scan (once per batch), then the
+// arena range is zeroed and every (plane, token chunk) writes its bits.
+// Re-entrant after an arena overflow (count = false reuses the offsets).
+void launch_pack(cudaStream_t st, EncScratch &S, DBuf<uint8_t> &arena, bool count = true) {
+    if (!arena.p) arena.ensure(1 << 20);
+    PackArgs P = S.pack;
+    P.arena = arena.p;
+    P.arena_cap = arena.cap;
+    const int nck = (int)((P.L + 1 + kPackTok - 1) / kPackTok);
+    const unsigned grid = (unsigned)(S.planes * nck);
+    if (count) {
+        {
+            PROF("pack_count", st);
+            pack_count<<<grid, 256, 0, st>>>(P, (int)S.planes, nck, S.t_cbits.p);
+        }
+        launch_plane_scan(st, S.t_cbits.p, S.t_coff.p, nck, (int)S.planes, kScanSumExcl);
+    }
+    {
+        PROF("arena_zero", st);
+        arena_zero<<<296, 256, 0, st>>>(arena.p, arena.cap, S.slot_off.p + S.planes);
+    }
+    {
+        PROF("pack_write", st);
+        pack_write<<<grid, 256, 0, st>>>(P, (int)S.planes, nck, S.t_coff.p);
+    }
+}
+
+// Synchronous convenience wrapper (codec API).
+template <int NP, class Src>
+void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, uint64_t L,
+                   const qcsim_codec_config &cfg, int log2C, IndexRec *index, DBuf<uint8_t> &arena,
+                   bool check_finite, bool sync_now);
+EncodeResult encode_finish(cudaStream_t st, EncScratch &S, DBuf<uint8_t> &arena);
 template <int NP, class Src>
 EncodeResult encode_batch(cudaStream_t st, EncScratch &S, const Src &src, int units, uint64_t L,
                           const qcsim_codec_config &cfg, int log2C, IndexRec *index, DBuf<uint8_t> &arena,
-                          bool check_finite, bool want_offsets) {
+                          bool check_finite, bool /*want_offsets*/) {
+    encode_launch<NP, Src>(st, S, src, units, L, cfg, log2C, index, arena, check_finite, true);
+    return encode_finish(st, S, arena);
+}
+
+void launch_plane_scan(cudaStream_t st, const int32_t *in, int32_t *out, int ntiles, int planes, ScanKind kind) {
+    const int out_stride = kind == kScanSumExcl ? ntiles + 1 : ntiles;
+    PROF("plane_scan", st);
+    if (ntiles <= 256) plane_scan<1><<<planes, 256, 0, st>>>(in, out, ntiles, planes, kind, ntiles, out_stride);
+    else if (ntiles <= 1024) plane_scan<4><<<planes, 256, 0, st>>>(in, out, ntiles, planes, kind, ntiles, out_stride);
+    else if (ntiles <= 4096) plane_scan<16><<<planes, 256, 0, st>>>(in, out, ntiles, planes, kind, ntiles, out_stride);
+    else if (ntiles <= 8192) plane_scan<32><<<planes, 256, 0, st>>>(in, out, ntiles, planes, kind, ntiles, out_stride);
+    else raise(QCSIM_CAPACITY, "planes longer than 2^22 elements are not supported on the device path");
+}
+
+// Encodes units*NP planes produced by `src` into `arena` (grown as needed).
+// `index` receives the decode checkpoints ([plane][nidx]).
+template <int NP, class Src>
+void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, uint64_t L,
+                   const qcsim_codec_config &cfg, int log2C, IndexRec *index, DBuf<uint8_t> &arena,
+                   bool check_finite, bool sync_now) {
     const uint64_t planes = (uint64_t)units * NP;
     const int qb = cfg.quant_code_bits;
     S.ensure(planes, units, L, qb);
-    const uint64_t ntiles = (L + kTile - 1) / kTile;
+    const int ntiles = (int)((L + kTile - 1) / kTile);
     const uint64_t cap = std::min<uint64_t>(L + 1, (1ull << qb) + 1);
+    const unsigned tgrid_u = (unsigned)(units * ntiles), tgrid_p = (unsigned)(planes * ntiles);
 
     if (check_finite) CK(cudaMemsetAsync(S.nonfinite.p, 0, sizeof(uint32_t), st));
     {
         PROF("init_params", st);
-        init_params<NP, Src><<<units, 256, 0, st>>>(S.params.p, src, units, L, cfg.mode, cfg.bound,
-                                                    check_finite ? S.nonfinite.p : nullptr);
+        init_params<NP, Src><<<units, 256, 0, st>>>(S.params.p, src, units, L, cfg.mode, cfg.bound, cfg.predictor,
+                                                    check_finite ? S.nonfinite.p : nullptr, S.symrange.p,
+                                                    S.hspecial.p, S.gamma.p);
     }
     if (check_finite) {
         uint32_t bad = 0;
         CK(cudaMemcpyAsync(&bad, S.nonfinite.p, sizeof bad, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-    g_prof.flush();
+        g_prof.flush();
         if (bad) raise(QCSIM_INVALID_ARGUMENT, "plane contains a non-finite value");
     }
 
-    EncPlanes E;
-    E.params = S.params.p;
-    E.sym = S.sym.p;
-    E.opos = S.opos.p;
-    E.oval = S.oval.p;
-    E.ocount = S.ocount.p;
-    E.index = index;
-    E.tilesum = S.tilesum.p;
-    E.L = L;
-    E.log2C = log2C;
-    E.qb = qb;
-    E.predictor = cfg.predictor;
-
-    static bool attr_done[2] = {false, false};
-    if (!attr_done[NP - 1]) {
-        set_smem(enc_quantize<NP, Src>, sizeof(E1Smem<NP>));
-        set_smem(enc_tokenize, sizeof(TokSmem));
-        attr_done[NP - 1] = true;
+    TileArgs A;
+    A.params = S.params.p;
+    A.x = S.x.p;
+    A.sym = S.sym.p;
+    A.fl = S.fl.p;
+    A.evlist = S.evlist.p;
+    A.evc = S.evc.p;
+    A.dval = S.dval.p;
+    A.index = index;
+    A.t_lastout = S.t_lastout.p;
+    A.t_base = S.t_base.p;
+    A.t_evoff = reinterpret_cast<uint32_t *>(S.t_evoff.p);
+    A.tilesum = S.tilesum.p;
+    A.L = L;
+    A.ntiles = ntiles;
+    A.log2C = log2C;
+    A.qb = qb;
+    A.predictor = cfg.predictor;
+    A.t_nev = reinterpret_cast<uint32_t *>(S.t_nev.p);
+    {
+        PROF("enc_x", st);
+        enc_x<NP, Src><<<tgrid_u, kEncThreads, 0, st>>>(A, src, units);
+    }
+    launch_plane_scan(st, S.t_lastout.p, S.t_base.p, ntiles, (int)planes, kScanMaxExcl);
+    {
+        PROF("enc_lattice", st);
+        enc_lattice<<<tgrid_p, kEncThreads, 0, st>>>(A, (int)planes);
+    }
+    launch_plane_scan(st, S.t_nev.p, S.t_evoff.p, ntiles, (int)planes, kScanSumExcl);
+    {
+        PROF("enc_compact", st);
+        enc_compact<<<tgrid_p, kEncThreads, 0, st>>>(A, (int)planes);
     }
     {
-        PROF("enc_quantize", st);
-        enc_quantize<NP, Src><<<units, kEncThreads, sizeof(E1Smem<NP>), st>>>(E, src, units);
+        PROF("enc_chain", st);
+        enc_chain<<<(unsigned)planes, 32, 0, st>>>(A, (int)planes);
+    }
+    {
+        PROF("enc_verify", st);
+        enc_verify<<<tgrid_p, kEncThreads, 0, st>>>(A, (int)planes);
     }
     {
         PROF("enc_serial", st);
-        enc_serial<NP, Src><<<(unsigned)((planes + 31) / 32), 32, 0, st>>>(E, src, units);
+        enc_serial_x<<<(unsigned)((planes + 31) / 32), 32, 0, st>>>(A, (int)planes);
     }
 
-    TokPlanes T;
+    TokArgs T;
     T.sym = S.sym.p;
+    T.x = S.x.p;
     T.tsym = S.tsym.p;
     T.trep = S.trep.p;
+    T.opos = S.opos.p;
+    T.oval = S.oval.p;
+    T.ocount = S.ocount.p;
     T.ntok = S.ntok.p;
     T.hist = S.hist.p;
     T.hspecial = S.hspecial.p;
     T.symrange = S.symrange.p;
     T.gamma_bits = S.gamma.p;
     T.index = index;
+    T.t_firstb = S.t_firstb.p;
+    T.t_lastb = S.t_lastb.p;
+    T.t_nout = S.t_nout.p;
+    T.t_ooff = S.t_ooff.p;
+    T.t_prevb = S.t_prevb.p;
+    T.t_nextb = S.t_nextb.p;
+    T.t_ntok = S.t_ntok.p;
+    T.t_tokoff = S.t_tokoff.p;
     T.L = L;
+    T.ntiles = ntiles;
     T.log2C = log2C;
     T.qb = qb;
     {
-        PROF("enc_tokenize", st);
-        enc_tokenize<<<(unsigned)planes, kEncThreads, sizeof(TokSmem), st>>>(T, (int)planes);
+        PROF("tok_stats", st);
+        tok_stats<<<tgrid_p, kEncThreads, 0, st>>>(T, (int)planes);
+    }
+    launch_plane_scan(st, S.t_lastb.p, S.t_prevb.p, ntiles, (int)planes, kScanMaxExcl);
+    launch_plane_scan(st, S.t_firstb.p, S.t_nextb.p, ntiles, (int)planes, kScanMinExclRev);
+    launch_plane_scan(st, S.t_nout.p, S.t_ooff.p, ntiles, (int)planes, kScanSumExcl);
+    {
+        PROF("tok_count", st);
+        tok_count<<<tgrid_p, kEncThreads, 0, st>>>(T, (int)planes);
+    }
+    launch_plane_scan(st, S.t_ntok.p, S.t_tokoff.p, ntiles, (int)planes, kScanSumExcl);
+    {
+        PROF("tok_emit", st);
+        tok_emit<<<tgrid_p, kEncThreads, 0, st>>>(T, (int)planes);
     }
 
     CodeBook B;
     B.hist = S.hist.p;
     B.hspecial = S.hspecial.p;
     B.symrange = S.symrange.p;
-    B.gamma_bits = S.gamma.p;
+    B.gamma_bits = reinterpret_cast<const uint64_t *>(S.gamma.p);
     B.ocount = S.ocount.p;
     B.sym = S.cb_sym.p;
     B.cnt = S.cb_cnt.p;
@@ -360,58 +512,75 @@ EncodeResult encode_batch(cudaStream_t st, EncScratch &S, const Src &src, int un
     CK(cub::DeviceScan::InclusiveSum(S.cub_tmp.p, tmp_bytes, S.slot_bytes.p, S.slot_off.p + 1, (int)planes, st));
     // (cub scan kernels are library code: not counted in g_launches)
 
-    EncodeResult R;
-    std::vector<uint32_t> err(planes);
-    CK(cudaMemcpyAsync(&R.total, S.slot_off.p + planes, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(err.data(), S.err.p, planes * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    g_prof.flush();
-    CK(cudaGetLastError());
-    for (uint64_t p = 0; p < planes; ++p)
-        if (err[p] == kErrDepth) raise(QCSIM_CODEC, "prefix code depth out of range");
-    arena.ensure(R.total + 64);
+    PackArgs P;
+    P.tsym = S.tsym.p;
+    P.trep = S.trep.p;
+    P.ntok = S.ntok.p;
+    P.cb_sym = S.cb_sym.p;
+    P.cb_len = S.cb_len.p;
+    P.cb_code = S.cb_code.p;
+    P.nsym = S.nsym.p;
+    P.stream_bits = S.stream_bits.p;
+    P.block_bytes = S.block_bytes.p;
+    P.slot_off = S.slot_off.p;
+    P.opos = S.opos.p;
+    P.oval = S.oval.p;
+    P.ocount = S.ocount.p;
+    P.params = S.params.p;
+    P.index = index;
+    P.overflow = S.overflow.p;
+    P.blk_off = S.blk_off.p;
+    P.L = L;
+    P.cap = cap;
+    P.log2C = log2C;
+    P.qb = qb;
+    P.mode = cfg.mode;
+    P.predictor = cfg.predictor;
+    P.planes_total = (int)planes;
+    S.pack = P;
+    S.planes = planes;
+    CK(cudaMemsetAsync(S.overflow.p, 0, sizeof(uint32_t), st));
+    launch_pack(st, S, arena);
+    // results for the host, one batch of async copies into pinned memory
+    S.h_bytes.ensure(planes);
+    S.h_off.ensure(planes);
+    S.h_params.ensure(planes);
+    S.h_err.ensure(planes);
+    S.h_misc.ensure(2);
+    CK(cudaMemcpyAsync(S.h_bytes.p, S.block_bytes.p, planes * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(S.h_off.p, S.blk_off.p, planes * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(S.h_params.p, S.params.p, planes * sizeof(PlaneParams), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(S.h_err.p, S.err.p, planes * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(S.h_misc.p, S.slot_off.p + planes, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(S.h_misc.p + 1, S.overflow.p, 4, cudaMemcpyDeviceToHost, st));
+    if (sync_now) {
+        CK(cudaStreamSynchronize(st));
+        g_prof.flush();
+    }
+}
 
-    PackArgs A;
-    A.tsym = S.tsym.p;
-    A.trep = S.trep.p;
-    A.ntok = S.ntok.p;
-    A.cb_sym = S.cb_sym.p;
-    A.cb_len = S.cb_len.p;
-    A.cb_code = S.cb_code.p;
-    A.nsym = S.nsym.p;
-    A.stream_bits = S.stream_bits.p;
-    A.block_bytes = S.block_bytes.p;
-    A.slot_off = S.slot_off.p;
-    A.opos = S.opos.p;
-    A.oval = S.oval.p;
-    A.ocount = S.ocount.p;
-    A.params = S.params.p;
-    A.index = index;
-    A.arena = arena.p;
-    A.blk_off = S.blk_off.p;
-    A.L = L;
-    A.cap = cap;
-    A.log2C = log2C;
-    A.qb = qb;
-    A.mode = cfg.mode;
-    A.predictor = cfg.predictor;
-    {
-        PROF("enc_pack", st);
-        enc_pack<<<(unsigned)planes, 256, 0, st>>>(A, (int)planes);
-    }
-    R.block_bytes.resize(planes);
-    CK(cudaMemcpyAsync(R.block_bytes.data(), S.block_bytes.p, planes * sizeof(uint64_t), cudaMemcpyDeviceToHost,
-                       st));
-    if (want_offsets) {
-        R.blk_off.resize(planes);
-        CK(cudaMemcpyAsync(R.blk_off.data(), S.blk_off.p, planes * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-    }
-    std::vector<PlaneParams> prm(planes);
-    CK(cudaMemcpyAsync(prm.data(), S.params.p, planes * sizeof(PlaneParams), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    g_prof.flush();
+// After the stream has been synchronised: errors, arena overflow (grow and
+// re-pack; nothing was written), per-plane results.
+EncodeResult encode_finish(cudaStream_t st, EncScratch &S, DBuf<uint8_t> &arena) {
     CK(cudaGetLastError());
-    for (auto &p : prm) R.fallback += (p.flags & kFlagFallback) ? 1 : 0;
+    const uint64_t planes = S.planes;
+    for (uint64_t p = 0; p < planes; ++p)
+        if (S.h_err.p[p] == kErrDepth) raise(QCSIM_CODEC, "prefix code depth out of range");
+    EncodeResult R;
+    R.total = S.h_misc.p[0];
+    if ((uint32_t)S.h_misc.p[1]) {
+        arena.ensure(R.total + R.total / 2 + (1 << 20));
+        CK(cudaMemsetAsync(S.overflow.p, 0, sizeof(uint32_t), st));
+        launch_pack(st, S, arena, false);
+        CK(cudaMemcpyAsync(S.h_off.p, S.blk_off.p, planes * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(S.h_misc.p + 1, S.overflow.p, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        g_prof.flush();
+        if ((uint32_t)S.h_misc.p[1]) raise(QCSIM_NOMEM, "compressed arena overflow after growth");
+    }
+    R.block_bytes.assign(S.h_bytes.p, S.h_bytes.p + planes);
+    R.blk_off.assign(S.h_off.p, S.h_off.p + planes);
+    for (uint64_t p = 0; p < planes; ++p) R.fallback += (S.h_params.p[p].flags & kFlagFallback) ? 1 : 0;
     return R;
 }
 
@@ -454,10 +623,10 @@ void decode_batch(cudaStream_t st, DecScratch &S, const uint8_t *arena, const ui
         dec_prepare<<<planes, 256, 0, st>>>(D, T, planes);
     }
     const uint64_t nchunks = (L + (1ull << log2C) - 1) >> log2C;
-    const uint64_t threads = nchunks * planes;
+    const uint64_t groups = (nchunks + kDecThreads - 1) / kDecThreads;
     {
         PROF("dec_chunks", st);
-        dec_chunks<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(D, T, planes);
+        dec_chunks<<<(unsigned)(groups * planes), kDecThreads, 0, st>>>(D, T, planes);
     }
 }
 
@@ -586,7 +755,9 @@ struct qcsim_engine {
     DBuf<uint64_t> unit_slice;
     DBuf<double *> outptrs;
     DBuf<double> slice_sq;
-    DBuf<double> scale_d;
+    HBuf<double> h_sq;
+    DBuf<double *> imp_ptrs;
+    bool tables_ready = false, slot_local = true;
     // partner slices imported from other ranks: slice -> QCB1 bytes
     std::vector<std::pair<uint64_t, std::vector<uint8_t>>> imported;
     std::vector<double> sq_norm; // all S slices (global view)
@@ -676,14 +847,8 @@ template <class Src> void engine_store(qcsim_engine *e, const Src &src) {
     const uint64_t ntiles = (e->L + kTile - 1) / kTile;
     if (e->compressed) {
         e->index[nxt].ensure(2 * e->ns * e->nidx);
-        EncodeResult R = encode_batch<2, Src>(e->st, e->enc, src, units, e->L, e->cfg.codec, e->log2C,
-                                              e->index[nxt].p, e->arena[nxt], false, false);
-        e->blk_off[nxt].ensure(2 * e->ns);
-        CK(cudaMemcpyAsync(e->blk_off[nxt].p, e->enc.blk_off.p, 2 * e->ns * sizeof(uint64_t),
-                           cudaMemcpyDeviceToDevice, e->st));
-        e->blk_bytes_h = R.block_bytes;
-        e->fallback += R.fallback;
-        record_sizes(e, R.block_bytes);
+        encode_launch<2, Src>(e->st, e->enc, src, units, e->L, e->cfg.codec, e->log2C, e->index[nxt].p,
+                              e->arena[nxt], false, false);
     } else {
         e->dense[nxt].ensure(e->ns * 2 * e->L);
         e->enc.tilesum.ensure(e->ns * ntiles);
@@ -697,31 +862,65 @@ template <class Src> void engine_store(qcsim_engine *e, const Src &src) {
         PROF("slice_norms", e->st);
         slice_norms<<<(units + 127) / 128, 128, 0, e->st>>>(e->enc.tilesum.p, (int)ntiles, units, e->slice_sq.p);
     }
-    std::vector<double> sq(e->ns);
-    CK(cudaMemcpyAsync(sq.data(), e->slice_sq.p, e->ns * sizeof(double), cudaMemcpyDeviceToHost, e->st));
+    e->h_sq.ensure(e->ns);
+    CK(cudaMemcpyAsync(e->h_sq.p, e->slice_sq.p, e->ns * sizeof(double), cudaMemcpyDeviceToHost, e->st));
+    // the one host synchronisation of a gate pass
     CK(cudaStreamSynchronize(e->st));
     g_prof.flush();
     CK(cudaGetLastError());
-    for (uint64_t k = 0; k < e->ns; ++k) e->sq_norm[e->s0 + k] = sq[k];
+    if (e->compressed) {
+        EncodeResult R = encode_finish(e->st, e->enc, e->arena[nxt]);
+        e->blk_off[nxt].ensure(2 * e->ns);
+        CK(cudaMemcpyAsync(e->blk_off[nxt].p, e->enc.blk_off.p, 2 * e->ns * sizeof(uint64_t),
+                           cudaMemcpyDeviceToDevice, e->st));
+        e->blk_bytes_h = std::move(R.block_bytes);
+        e->fallback += R.fallback;
+        record_sizes(e, e->blk_bytes_h);
+    }
+    for (uint64_t k = 0; k < e->ns; ++k) e->sq_norm[e->s0 + k] = e->h_sq.p[k];
     e->cur = nxt;
     e->loaded = true;
+}
+
+// Static device tables of the local slices, uploaded once: decode output
+// pointers (slot k = local slice k), unit -> slice, slice -> slot.
+void engine_tables(qcsim_engine *e) {
+    if (e->tables_ready) return;
+    e->old.ensure(e->ns * 2 * e->L);
+    std::vector<double *> ptrs(2 * e->ns);
+    for (uint64_t k = 0; k < 2 * e->ns; ++k) ptrs[k] = e->old.p + k * e->L;
+    e->outptrs.ensure(2 * e->ns);
+    CK(cudaMemcpy(e->outptrs.p, ptrs.data(), ptrs.size() * sizeof(double *), cudaMemcpyHostToDevice));
+    std::vector<uint64_t> us(e->ns);
+    for (uint64_t k = 0; k < e->ns; ++k) us[k] = e->s0 + k;
+    e->unit_slice.ensure(e->ns);
+    CK(cudaMemcpy(e->unit_slice.p, us.data(), e->ns * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    std::vector<int32_t> slot(e->S, -1);
+    for (uint64_t k = 0; k < e->ns; ++k) slot[e->s0 + k] = (int32_t)k;
+    e->slot_of.ensure(e->S);
+    CK(cudaMemcpy(e->slot_of.p, slot.data(), e->S * sizeof(int32_t), cudaMemcpyHostToDevice));
+    e->slot_local = true;
+    e->tables_ready = true;
 }
 
 // Decodes the current state of the local slices (plus imported partner
 // slices) into e->old, slot k = local slice k, then imported ones.
 void engine_decode_old(qcsim_engine *e, bool need_imported) {
+    engine_tables(e);
     const uint64_t extra = need_imported ? e->imported.size() : 0;
-    const uint64_t slots = e->ns + extra;
-    e->old.ensure(slots * 2 * e->L);
+    if (extra) {
+        // grow `old` for the imported slots (keeps pointers of local slots valid
+        // only if no reallocation: re-upload the tables when it happens)
+        if (e->old.cap < (e->ns + extra) * 2 * e->L) {
+            e->old.ensure((e->ns + extra) * 2 * e->L);
+            e->tables_ready = false;
+            engine_tables(e);
+        }
+    }
     if (!e->compressed) {
         CK(cudaMemcpyAsync(e->old.p, e->dense[e->cur].p, e->ns * 2 * e->L * sizeof(double),
                            cudaMemcpyDeviceToDevice, e->st));
     } else {
-        std::vector<double *> ptrs(2 * e->ns);
-        for (uint64_t k = 0; k < 2 * e->ns; ++k) ptrs[k] = e->old.p + k * e->L;
-        e->outptrs.ensure(2 * slots);
-        CK(cudaMemcpyAsync(e->outptrs.p, ptrs.data(), ptrs.size() * sizeof(double *), cudaMemcpyHostToDevice,
-                           e->st));
         decode_batch(e->st, e->dec, e->arena[e->cur].p, e->blk_off[e->cur].p, e->index[e->cur].p, e->outptrs.p,
                      (int)(2 * e->ns), e->L, e->log2C, e->cfg.codec.quant_code_bits);
     }
@@ -745,18 +944,19 @@ void engine_decode_old(qcsim_engine *e, bool need_imported) {
         CK(cudaMemcpyAsync(e->imp_off.p, offs.data(), offs.size() * 8, cudaMemcpyHostToDevice, e->st));
         std::vector<double *> ptrs(offs.size());
         for (uint64_t k = 0; k < offs.size(); ++k) ptrs[k] = e->old.p + (2 * e->ns + k) * e->L;
-        DBuf<double *> dp;
-        dp.ensure(ptrs.size());
-        CK(cudaMemcpyAsync(dp.p, ptrs.data(), ptrs.size() * sizeof(double *), cudaMemcpyHostToDevice, e->st));
-        e->val.ensure(offs.size(), std::min<uint64_t>(e->L + 1, (1ull << e->cfg.codec.quant_code_bits) + 1));
+        e->imp_ptrs.ensure(ptrs.size());
+        CK(cudaMemcpyAsync(e->imp_ptrs.p, ptrs.data(), ptrs.size() * sizeof(double *), cudaMemcpyHostToDevice,
+                           e->st));
+        const uint64_t vcap = std::min<uint64_t>(e->L + 1, (1ull << e->cfg.codec.quant_code_bits) + 1);
+        e->val.ensure(offs.size(), vcap);
         ValArgs V;
         V.blocks = e->imp_bytes.p;
         V.blk_off = e->imp_off.p;
-        V.out = dp.p;
+        V.out = e->imp_ptrs.p;
         V.err = e->val.err.p;
         V.ssym = e->val.ssym.p;
         V.slen = e->val.slen.p;
-        V.cap = std::min<uint64_t>(e->L + 1, (1ull << e->cfg.codec.quant_code_bits) + 1);
+        V.cap = vcap;
         {
             PROF("dec_validate", e->st);
             dec_validate<<<(unsigned)((offs.size() + 31) / 32), 32, 0, e->st>>>(V, (int)offs.size());
@@ -791,13 +991,14 @@ void engine_gate(qcsim_engine *e, const qcsim_action &a) {
     }
     // which old slices are needed: local + partners (imported if remote)
     bool remote = false;
-    for (uint64_t k = 0; k < e->ns; ++k) {
+    for (uint64_t k = 0; k < e->ns && !remote; ++k) {
         const uint64_t pj = partner_slice(a, e->s, e->s0 + k);
         if (pj < e->s0 || pj >= e->s0 + e->ns) remote = true;
     }
-    std::vector<int32_t> slot(e->S, -1);
-    for (uint64_t k = 0; k < e->ns; ++k) slot[e->s0 + k] = (int32_t)k;
+    engine_decode_old(e, remote);
     if (remote) {
+        std::vector<int32_t> slot(e->S, -1);
+        for (uint64_t k = 0; k < e->ns; ++k) slot[e->s0 + k] = (int32_t)k;
         for (uint64_t k = 0; k < e->ns; ++k) {
             const uint64_t pj = partner_slice(a, e->s, e->s0 + k);
             if (pj >= e->s0 && pj < e->s0 + e->ns) continue;
@@ -809,23 +1010,21 @@ void engine_gate(qcsim_engine *e, const qcsim_action &a) {
                       "partner slice " + std::to_string(pj) + " not imported (multi-rank exchange missing)");
             slot[pj] = (int32_t)(e->ns + found);
         }
+        CK(cudaMemcpy(e->slot_of.p, slot.data(), e->S * sizeof(int32_t), cudaMemcpyHostToDevice));
+        e->slot_local = false;
+    } else if (!e->slot_local) {
+        std::vector<int32_t> slot(e->S, -1);
+        for (uint64_t k = 0; k < e->ns; ++k) slot[e->s0 + k] = (int32_t)k;
+        CK(cudaMemcpy(e->slot_of.p, slot.data(), e->S * sizeof(int32_t), cudaMemcpyHostToDevice));
+        e->slot_local = true;
     }
-    engine_decode_old(e, remote);
-    e->slot_of.ensure(e->S);
-    CK(cudaMemcpyAsync(e->slot_of.p, slot.data(), e->S * sizeof(int32_t), cudaMemcpyHostToDevice, e->st));
-    std::vector<uint64_t> us(e->ns);
-    for (uint64_t k = 0; k < e->ns; ++k) us[k] = e->s0 + k;
-    e->unit_slice.ensure(e->ns);
-    CK(cudaMemcpyAsync(e->unit_slice.p, us.data(), e->ns * sizeof(uint64_t), cudaMemcpyHostToDevice, e->st));
     e->enc.ensure(2 * e->ns, e->ns, e->L, e->cfg.codec.quant_code_bits);
-    // scale as a device scalar (read by every fetch)
-    e->scale_d.ensure(1);
-    CK(cudaMemcpyAsync(e->scale_d.p, &scale, sizeof(double), cudaMemcpyHostToDevice, e->st));
     GateSrc g;
     g.old = e->old.p;
     g.slot_of = e->slot_of.p;
     g.unit_slice = e->unit_slice.p;
-    g.scale = apply ? e->scale_d.p : nullptr;
+    g.scale = scale;
+    g.apply_scale = apply ? 1 : 0;
     g.act = to_dev(a);
     g.s = e->s;
     g.L = e->L;
@@ -1164,7 +1363,7 @@ qcsim_status qcsim_engine_load_amplitudes(qcsim_engine *e, const double *amps, u
                 planar[k * 2 * e->L + i] = amps[2 * g];
                 planar[k * 2 * e->L + e->L + i] = amps[2 * g + 1];
             }
-        e->old.ensure(planar.size());
+        engine_tables(e);
         CK(cudaMemcpyAsync(e->old.p, planar.data(), planar.size() * sizeof(double), cudaMemcpyHostToDevice, e->st));
         PlanarSrc src{e->old.p, e->L};
         engine_store(e, src);
