@@ -1,0 +1,80 @@
+// qcsim/engine.hpp -- Algorithm 1 of arXiv:1811.05630 on the GPU.
+//
+// The reference specifies the engine but ships no header
+// or source for it; names follow SPEC.md (EngineConfig, RunMetrics, run,
+// gather_state).  Every gate pass -- decode, normalize, apply the lowered
+// action, sq_norm, re-encode every slice -- runs on the device
+// (libqcsim_b200.so); the compressed state stays resident in HBM.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "qcsim/circuit.hpp"
+#include "qcsim/codec.hpp"
+#include "qcsim/statevec.hpp"
+
+struct qcsim_engine;
+
+namespace qcsim {
+
+enum class NormPolicy { EveryGate, EveryKGates, Off };
+
+struct EngineConfig {
+    int slice_bits = -1; // < 0: default_slice_bits(n)
+    CodecConfig codec{CodecMode::Absolute, 1e-5, 16, Predictor::PreviousValue};
+    bool compression_enabled = true;
+    int workers = 1; // accepted for API parity; all slices run concurrently
+    NormPolicy norm_policy = NormPolicy::EveryGate;
+    int norm_every_k = 1;
+    double norm_drift_tolerance = 0.02;
+    int device = 0;
+    int rank = 0, world = 1; // slice sharding
+};
+
+struct RunMetrics {
+    double min_compression_ratio = 0.0;
+    double mean_compression_ratio = 0.0;
+    std::vector<double> per_gate_min_ratio; // not tracked on the device path (empty)
+    double wall_seconds = 0.0;
+    double baseline_wall_seconds = 0.0;
+    double overhead_factor = 0.0;
+    uint64_t peak_compressed_bytes = 0;
+    uint64_t dense_bytes = 0;
+    double final_norm = 0.0;
+    uint64_t compress_calls = 0;
+    uint64_t gates = 0;
+    uint64_t index_bytes = 0;
+    uint64_t fallback_planes = 0;
+};
+
+class Engine {
+  public:
+    Engine(int num_qubits, const EngineConfig &config);
+    ~Engine();
+    Engine(const Engine &) = delete;
+    Engine &operator=(const Engine &) = delete;
+
+    void load(const StateVector &initial);        // dense or compressed slices
+    void load_basis(uint64_t basis_index);
+    RunMetrics run(const Circuit &circuit);        // gate passes
+    RunMetrics run(const std::vector<GateAction> &actions);
+    RunMetrics metrics() const;
+    StateVector gather_state(int guard_qubits = 28) const; // dense StateVector
+    std::vector<CompressedPlanes> compressed_slices() const; // checkpoint
+
+    int num_qubits() const { return n_; }
+    int slice_bits() const { return s_; }
+
+  private:
+    qcsim_engine *h_ = nullptr;
+    int n_ = 0, s_ = 0;
+};
+
+// compresses `initial`, applies every gate, returns the
+// engine holding the final compressed state plus the metrics.
+std::pair<std::unique_ptr<Engine>, RunMetrics> run(const Circuit &circuit, const EngineConfig &config,
+                                                   const StateVector &initial);
+
+} // namespace qcsim

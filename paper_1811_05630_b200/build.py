@@ -32,13 +32,30 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+API_LIB = os.path.join(HERE, "libqcsim.so")           # C++ API shim (include/qcsim/*.hpp)
+API_SRC = os.path.join(CSRC, "host", "qcsim_api.cpp")
+API_SMOKE_SRC = os.path.join(ROOT, "tests", "cpp", "api_smoke.cpp")
+API_SMOKE = os.path.join(ROOT, "tests", "cpp", "api_smoke")
+CXXFLAGS = ["-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextra", "-I" + os.path.join(ROOT, "include")]
+
+
+def _run(cmd, verbose):
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.check_call(cmd)
+
+
 def build(force: bool = False, verbose: bool = True) -> str:
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "qcsim_c.h")]
     if force or _stale(LIB, deps):
-        cmd = [NVCC] + NVFLAGS + ["-shared", "-o", LIB] + [os.path.join(CSRC, f) for f in SOURCES]
-        if verbose:
-            print(" ".join(cmd), flush=True)
-        subprocess.check_call(cmd, cwd=CSRC)
+        _run([NVCC] + NVFLAGS + ["-shared", "-o", LIB] + [os.path.join(CSRC, f) for f in SOURCES], verbose)
+    hdrs = [os.path.join(ROOT, "include", "qcsim", h) for h in os.listdir(os.path.join(ROOT, "include", "qcsim"))]
+    if force or _stale(API_LIB, [API_SRC, LIB] + hdrs):
+        _run(["g++"] + CXXFLAGS + ["-shared", "-o", API_LIB, API_SRC, "-L" + HERE, "-lqcsim_b200",
+                                   "-Wl,-rpath,$ORIGIN"], verbose)
+    if force or _stale(API_SMOKE, [API_SMOKE_SRC, API_LIB] + hdrs):
+        _run(["g++"] + CXXFLAGS + ["-o", API_SMOKE, API_SMOKE_SRC, "-L" + HERE, "-lqcsim", "-lqcsim_b200",
+                                   "-Wl,-rpath," + HERE], verbose)
     return LIB
 
 

@@ -63,3 +63,13 @@ def test_block_bound_is_upper_bound(oracle):
             x = planes.make_plane(kind, 3000, 5)
             blk = oracle.compress(x, CodecConfig.make(1, 1e-9, qb, 0))
             assert len(blk.data) <= lib.qcsim_block_bound(3000, qb)
+
+
+def test_cpp_api_shim_links():
+    """The C++ drop-in (include/qcsim/*.hpp -> libqcsim.so -> C-ABI) builds
+    and links; the GPU leg runs it (tests/test_gpu_engine.py)."""
+    from paper_1811_05630_b200 import build as b
+    b.build(verbose=False)
+    assert os.path.exists(b.API_LIB) and os.path.exists(b.API_SMOKE)
+    lib = ctypes.CDLL(b.API_LIB)
+    assert lib is not None

@@ -171,3 +171,12 @@ def test_gather_guard(q):
     eng.load_basis(0)
     with pytest.raises(q.CapacityError):
         eng.gather(guard_qubits=10)
+
+
+def test_cpp_api_smoke():
+    """The reference's C++ API surface end to end on the GPU."""
+    import subprocess
+    from paper_1811_05630_b200 import build as b
+    out = subprocess.run([b.API_SMOKE], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    assert "api_smoke ok" in out.stdout
