@@ -51,9 +51,65 @@ struct TileArgs {
     int log2C;
     int qb;
     int predictor;
+    // per-pass bookkeeping reset by enc_x (tile 0 of every plane)
+    uint32_t *symrange;              // [plane][2]
+    uint32_t *hspecial;              // [plane][2]
+    unsigned long long *gamma;       // [plane]
 };
 
 __device__ __forceinline__ bool is_negzero(double v) { return bits_of(v) == 0x8000000000000000ull; }
+
+// Plane parameters as ONE consistent snapshot per block.  Other blocks of
+// the same kernel may set kFlagFallback concurrently (atomicOr); a per-thread
+// read could let some threads of a block return early while the rest enter
+// a barrier or a block-wide scan.  All threads must call this.
+__device__ __forceinline__ PlaneParams block_params(const PlaneParams *params, int pl) {
+    __shared__ PlaneParams s_pp;
+    if (threadIdx.x == 0) s_pp = params[pl];
+    __syncthreads();
+    const PlaneParams pp = s_pp;
+    __syncthreads();
+    return pp;
+}
+
+// Planes with few tiles get their cross-tile carries inline: the consuming
+// block reduces the per-tile values before (or after) its own tile instead
+// of waiting for a separate plane_scan launch.
+constexpr int kInlineTiles = 64;
+enum ScanKind { kScanMaxExcl = 0, kScanSumExcl = 1, kScanMinExclRev = 2 };
+
+// Exclusive carry of tile t over the per-tile array `a` (stride ntiles):
+// max over [0,t) (init -1), sum over [0,t), or min over (t,ntiles) (init
+// INT_MAX).  All threads call it; result broadcast through shared memory.
+__device__ int32_t tile_carry(const int32_t *a, int t, int ntiles, int kind) {
+    __shared__ int32_t s_res;
+    if (threadIdx.x < 32) {
+        int32_t v = kind == kScanMaxExcl ? -1 : (kind == kScanSumExcl ? 0 : 0x7FFFFFFF);
+        const int lo = kind == kScanMinExclRev ? t + 1 : 0;
+        const int hi = kind == kScanMinExclRev ? ntiles : t;
+        for (int k = lo + (int)threadIdx.x; k < hi; k += 32) {
+            const int32_t x = a[k];
+            v = kind == kScanMaxExcl ? max(v, x) : (kind == kScanSumExcl ? v + x : min(v, x));
+        }
+        for (int off = 16; off >= 1; off >>= 1) {
+            const int32_t o = __shfl_xor_sync(0xffffffffu, v, off);
+            v = kind == kScanMaxExcl ? max(v, o) : (kind == kScanSumExcl ? v + o : min(v, o));
+        }
+        if (threadIdx.x == 0) s_res = v;
+    }
+    __syncthreads();
+    const int32_t r = s_res;
+    __syncthreads();
+    return r;
+}
+
+// The scanned value for tile t: from the plane_scan output when the plane
+// has many tiles, else computed inline from the raw per-tile array.
+__device__ __forceinline__ int32_t carry_of(const int32_t *scanned, int scanned_stride, const int32_t *raw, int pl,
+                                            int t, int ntiles, int kind) {
+    if (ntiles > kInlineTiles) return scanned[(uint64_t)pl * scanned_stride + t];
+    return tile_carry(raw + (uint64_t)pl * ntiles, t, ntiles, kind);
+}
 
 // ------------------------------------------------------------------ T1
 template <int NP, class Src>
@@ -64,6 +120,17 @@ __global__ void __launch_bounds__(kEncThreads) enc_x(TileArgs A, Src src, int un
     const uint64_t L = A.L;
     const uint64_t t0 = (uint64_t)t * kTile;
     const int tl = (int)tmin<uint64_t>(kTile, L - t0);
+    if (t == 0 && tid < NP) {
+        // per-pass reset of the plane's flags and histogram bookkeeping
+        const int pl = unit * NP + tid;
+        const PlaneParams pp = A.params[pl];
+        A.params[pl].flags = (A.predictor == 1 && pp.eb != 0.0) ? kFlagFallback : 0u;
+        A.symrange[2 * pl] = 0xFFFFFFFFu;
+        A.symrange[2 * pl + 1] = 0;
+        A.hspecial[2 * pl] = 0;
+        A.hspecial[2 * pl + 1] = 0;
+        A.gamma[pl] = 0;
+    }
     __shared__ double xs[NP][kTile + 1];
     __shared__ double red[kEncThreads];
     using RedI = cub::BlockReduce<int, kEncThreads>;
@@ -125,7 +192,6 @@ __global__ void __launch_bounds__(kEncThreads) enc_x(TileArgs A, Src src, int un
 
 // ----------------------------------------------------------- plane scans
 // One block per plane over `ntiles` entries (ntiles <= 4096).
-enum ScanKind { kScanMaxExcl = 0, kScanSumExcl = 1, kScanMinExclRev = 2 };
 
 template <int ITEMS>
 __global__ void __launch_bounds__(256) plane_scan(const int32_t *in, int32_t *out, int ntiles, int planes, int kind,
@@ -166,7 +232,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int plane
     using ScanI = cub::BlockScan<int, kEncThreads>;
     __shared__ typename ScanI::TempStorage scan_tmp;
     __shared__ long long kb[kEncThreads];
-    const PlaneParams pp = A.params[pl];
+    const PlaneParams pp = block_params(A.params, pl);
     const long long half = 1ll << (A.qb - 1);
     const double *x = A.x + (uint64_t)pl * L;
     uint8_t *fl = A.fl + (uint64_t)pl * L;
@@ -201,7 +267,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int plane
     }
     int lo[kPerThread];
     ScanI(scan_tmp).ExclusiveScan(opos, lo, -1, cub::Max());
-    const int32_t tbase = A.t_base[(uint64_t)pl * A.ntiles + t]; // global position or -1
+    const int32_t tbase = carry_of(A.t_base, A.ntiles, A.t_lastout, pl, t, A.ntiles, kScanMaxExcl); // position or -1
     long long K[kPerThread];
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
@@ -268,7 +334,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int plane
 __global__ void __launch_bounds__(kEncThreads) enc_compact(TileArgs A, int planes) {
     const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
     if (pl >= planes) return;
-    if (A.params[pl].flags & kFlagFallback) return;
+    if (block_params(A.params, pl).flags & kFlagFallback) return;
     const int tid = threadIdx.x;
     const uint64_t L = A.L;
     const uint64_t t0 = (uint64_t)t * kTile;
@@ -282,7 +348,8 @@ __global__ void __launch_bounds__(kEncThreads) enc_compact(TileArgs A, int plane
         f[e] = (k < tl && (fl[t0 + k] & 1)) ? 1 : 0;
     }
     ScanI(scan_tmp).ExclusiveSum(f, pos);
-    const uint32_t base = A.t_evoff[(uint64_t)pl * (A.ntiles + 1) + t];
+    const uint32_t base = (uint32_t)carry_of(reinterpret_cast<const int32_t *>(A.t_evoff), A.ntiles + 1,
+                                             reinterpret_cast<const int32_t *>(A.t_nev), pl, t, A.ntiles, kScanSumExcl);
     uint32_t *ev = A.evlist + (uint64_t)pl * L;
     double *evc = A.evc + (uint64_t)pl * L;
     const uint32_t *sym = A.sym + (uint64_t)pl * L;
@@ -341,13 +408,15 @@ __global__ void __launch_bounds__(32) enc_chain(TileArgs A, int planes) {
     const int pl = blockIdx.x;
     if (pl >= planes) return;
     const int lane = threadIdx.x;
-    const PlaneParams pp = A.params[pl];
+    const PlaneParams pp = block_params(A.params, pl);
     if ((pp.flags & kFlagFallback) || pp.eb == 0.0) return;
     __shared__ alignas(128) double cbuf[kChainBufs][kChainChunk];
     __shared__ alignas(128) uint32_t obuf[kChainBufs][kChainChunk];
     __shared__ alignas(8) uint64_t bar[kChainBufs];
     const uint64_t L = A.L;
-    const uint32_t nev = A.t_evoff[(uint64_t)pl * (A.ntiles + 1) + A.ntiles];
+    const uint32_t nev = (uint32_t)carry_of(reinterpret_cast<const int32_t *>(A.t_evoff), A.ntiles + 1,
+                                            reinterpret_cast<const int32_t *>(A.t_nev), pl, A.ntiles, A.ntiles,
+                                            kScanSumExcl);
     if (nev == 0) return;
     const uint32_t *ev = A.evlist + (uint64_t)pl * L;
     const double *evc = A.evc + (uint64_t)pl * L;
@@ -402,7 +471,7 @@ __global__ void __launch_bounds__(32) enc_chain(TileArgs A, int planes) {
 __global__ void __launch_bounds__(kEncThreads) enc_verify(TileArgs A, int planes) {
     const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
     if (pl >= planes) return;
-    const PlaneParams pp = A.params[pl];
+    const PlaneParams pp = block_params(A.params, pl);
     if (pp.flags & kFlagFallback) return;
     const int tid = threadIdx.x;
     const uint64_t L = A.L;
@@ -431,17 +500,29 @@ __global__ void __launch_bounds__(kEncThreads) enc_verify(TileArgs A, int planes
     const uint8_t *fl = A.fl + (uint64_t)pl * L;
     uint32_t *sym = A.sym + (uint64_t)pl * L;
     const double *dv = A.dval + (uint64_t)pl * L;
-    const uint32_t evbase = A.t_evoff[(uint64_t)pl * (A.ntiles + 1) + t];
+    const uint32_t evbase = (uint32_t)carry_of(reinterpret_cast<const int32_t *>(A.t_evoff), A.ntiles + 1,
+                                               reinterpret_cast<const int32_t *>(A.t_nev), pl, t, A.ntiles, kScanSumExcl);
     int f[kPerThread], rank[kPerThread];
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
         f[e] = (k < tl && (fl[t0 + k] & 1)) ? 1 : 0;
     }
-    ScanI(scan_tmp).ExclusiveSum(f, rank);
+    int nf_tile;
+    ScanI(scan_tmp).ExclusiveSum(f, rank, nf_tile);
     __syncthreads();
-    // prediction = d at the last event strictly before i (ordinal evbase +
-    // rank - 1), else the value carried into the tile, else 0.0
-    const double dcarry = evbase > 0 ? dv[evbase - 1] : 0.0;
+    // guard: the event ordinals of this tile must lie inside the plane's
+    // event list (a violation means corrupt carries -> serial re-encode)
+    const uint32_t nev_plane = (uint32_t)carry_of(reinterpret_cast<const int32_t *>(A.t_evoff), A.ntiles + 1,
+                                                  reinterpret_cast<const int32_t *>(A.t_nev), pl, A.ntiles, A.ntiles,
+                                                  kScanSumExcl);
+    if ((uint64_t)evbase + (uint64_t)nf_tile > (uint64_t)nev_plane || nev_plane > L) {
+        if (tid == 0) {
+            printf("qcsim enc_verify: plane %d tile %d evbase %u tile events %d plane events %u (L %llu)\n", pl, t,
+                   evbase, nf_tile, nev_plane, (unsigned long long)L);
+            atomicOr(&A.params[pl].flags, kFlagFallback);
+        }
+        return;
+    }
     int bad = 0;
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
@@ -459,7 +540,6 @@ __global__ void __launch_bounds__(kEncThreads) enc_verify(TileArgs A, int planes
             idx[i >> A.log2C].dprev2 = 0.0; // unused by the previous-value predictor
         }
     }
-    (void)dcarry;
     if (bad) s_bad = 1;
     __syncthreads();
     if (tid == 0 && s_bad) atomicOr(&A.params[pl].flags, kFlagFallback);
@@ -584,7 +664,7 @@ __device__ __forceinline__ void element_runs(const TokArgs &A, const uint32_t *s
         isb[e] = (k < tl && (i == 0 || sym[i] != sym[i - 1])) ? (int)k : -1;
     }
     ScanI(tmp).InclusiveScan(isb, st, cub::Max());
-    const int32_t prevb = A.t_prevb[(uint64_t)pl * A.ntiles + t];
+    const int32_t prevb = carry_of(A.t_prevb, A.ntiles, A.t_lastb, pl, t, A.ntiles, kScanMaxExcl);
     // first run start after each element: next boundary in the tile, else
     // the scanned carry from later tiles, else L
     for (int e = 0; e < kPerThread; ++e) {
@@ -610,7 +690,7 @@ __device__ __forceinline__ void element_runs(const TokArgs &A, const uint32_t *s
         tmin_s[tid] = min(tmin_s[tid], v);
         __syncthreads();
     }
-    const int32_t nextb_carry = A.t_nextb[(uint64_t)pl * A.ntiles + t];
+    const int32_t nextb_carry = carry_of(A.t_nextb, A.ntiles, A.t_firstb, pl, t, A.ntiles, kScanMinExclRev);
     const uint64_t after = nextb_carry == 0x7FFFFFFF ? A.L : (uint64_t)nextb_carry;
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
@@ -741,8 +821,8 @@ __global__ void __launch_bounds__(kEncThreads) tok_emit(TokArgs A, int planes) {
     ScanI(tmp).ExclusiveSum(cnt, tpos);
     __syncthreads();
     ScanI(tmp).ExclusiveSum(isout, opos);
-    const uint32_t tokbase = (uint32_t)A.t_tokoff[(uint64_t)pl * (A.ntiles + 1) + t];
-    const uint32_t obase = (uint32_t)A.t_ooff[(uint64_t)pl * (A.ntiles + 1) + t];
+    const uint32_t tokbase = (uint32_t)carry_of(A.t_tokoff, A.ntiles + 1, A.t_ntok, pl, t, A.ntiles, kScanSumExcl);
+    const uint32_t obase = (uint32_t)carry_of(A.t_ooff, A.ntiles + 1, A.t_nout, pl, t, A.ntiles, kScanSumExcl);
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
         if (k >= tl) continue;
@@ -789,9 +869,13 @@ __global__ void __launch_bounds__(kEncThreads) tok_emit(TokArgs A, int planes) {
             }
         }
     }
-    if (tid == 0 && t == A.ntiles - 1) {
-        A.ntok[pl] = (uint32_t)A.t_tokoff[(uint64_t)pl * (A.ntiles + 1) + A.ntiles];
-        A.ocount[pl] = (uint32_t)A.t_ooff[(uint64_t)pl * (A.ntiles + 1) + A.ntiles];
+    if (t == A.ntiles - 1) { // uniform per block
+        const int32_t nt = carry_of(A.t_tokoff, A.ntiles + 1, A.t_ntok, pl, A.ntiles, A.ntiles, kScanSumExcl);
+        const int32_t no = carry_of(A.t_ooff, A.ntiles + 1, A.t_nout, pl, A.ntiles, A.ntiles, kScanSumExcl);
+        if (tid == 0) {
+            A.ntok[pl] = (uint32_t)nt;
+            A.ocount[pl] = (uint32_t)no;
+        }
     }
 }
 

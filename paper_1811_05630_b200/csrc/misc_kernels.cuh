@@ -3,6 +3,8 @@
 
 #include <cfloat>
 
+#include <cub/block/block_scan.cuh>
+
 #include "common.cuh"
 
 namespace qcb {
@@ -73,6 +75,27 @@ __global__ void __launch_bounds__(256) init_params(PlaneParams *params, Src src,
         gamma_bits[pl] = 0;
         if (nonfinite && sbad) atomicExch(nonfinite, 1u);
     }
+}
+
+// Exclusive scan of the per-plane arena slot sizes (16-byte aligned slots):
+// out[p] = sum(in[0..p)), out[planes] = total.  One 1024-thread block.
+__global__ void __launch_bounds__(1024) slot_scan(const uint64_t *in, uint64_t *out, int planes) {
+    using Scan = cub::BlockScan<unsigned long long, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ unsigned long long carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < planes; base += 1024) {
+        const int k = base + (int)threadIdx.x;
+        const unsigned long long v = k < planes ? in[k] : 0ull;
+        unsigned long long r, tot;
+        Scan(tmp).ExclusiveSum(v, r, tot);
+        if (k < planes) out[k] = carry + r;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[planes] = carry;
 }
 
 // Per-slice sq_norm: adjacent-pair tree over the tile partials (the tile

@@ -11,6 +11,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include "common.cuh"
+#include "enc_tiles.cuh" // carry_of / tile_carry
 
 namespace qcb {
 
@@ -321,6 +322,17 @@ __device__ __forceinline__ uint32_t token_bits(const SCodebook &C, const PackArg
 __global__ void __launch_bounds__(256) pack_count(PackArgs A, int planes, int nck, int32_t *cbits) {
     const int pl = blockIdx.x / nck, c = blockIdx.x % nck;
     if (pl >= planes) return;
+    // zero this block's share of the plane's arena slot (stream words are
+    // OR-combined at chunk seams by pack_write); skipped when the batch
+    // does not fit -- pack_write then reports the overflow
+    if (A.slot_off[A.planes_total] + 64 <= A.arena_cap) {
+        const uint64_t s0 = A.slot_off[pl], s1 = A.slot_off[pl + 1]; // 16-byte aligned slots
+        const uint64_t nw = (s1 - s0) / 16, per = (nw + nck - 1) / nck;
+        uint4 *w = reinterpret_cast<uint4 *>(A.arena + s0);
+        for (uint64_t k = (uint64_t)c * per + threadIdx.x; k < tmin<uint64_t>(nw, (uint64_t)(c + 1) * per);
+             k += blockDim.x)
+            w[k] = make_uint4(0, 0, 0, 0);
+    }
     const uint32_t ntok = A.ntok[pl];
     const uint32_t t0 = (uint32_t)c * kPackTok;
     if (t0 >= ntok) {
@@ -357,7 +369,8 @@ __global__ void arena_zero(uint8_t *arena, uint64_t cap, const uint64_t *total_p
 
 // P2: header + table (chunk 0), stream bits of every chunk, outlier records,
 // decode-index bit positions (grid: planes x chunks).
-__global__ void __launch_bounds__(256) pack_write(PackArgs A, int planes, int nck, const int32_t *coff) {
+__global__ void __launch_bounds__(256) pack_write(PackArgs A, int planes, int nck, const int32_t *coff,
+                                                  const int32_t *cbits) {
     const int pl = blockIdx.x / nck, c = blockIdx.x % nck;
     if (pl >= planes) return;
     const int tid = threadIdx.x;
@@ -441,7 +454,7 @@ __global__ void __launch_bounds__(256) pack_write(PackArgs A, int planes, int nc
     }
     uint32_t pos[4], tot;
     Scan(scan_tmp).ExclusiveSum(tbits, pos, tot);
-    const uint64_t base_bit = (uint64_t)(uint32_t)coff[(uint64_t)pl * (nck + 1) + c];
+    const uint64_t base_bit = (uint64_t)(uint32_t)carry_of(coff, nck + 1, cbits, pl, c, nck, kScanSumExcl);
     const uint32_t b0 = (uint32_t)(base_bit & 31);
     const uint32_t nwords = (b0 + tot + 31) / 32;
     for (uint32_t w = tid; w < nwords; w += 256) words[w] = 0;

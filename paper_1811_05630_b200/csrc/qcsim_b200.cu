@@ -248,6 +248,8 @@ struct EncScratch {
     PackArgs pack{};
     uint64_t planes = 0;
     uint64_t hist_stride = 0;
+    uint64_t param_planes = 0;       // params valid for this many planes ...
+    qcsim_codec_config param_cfg{};  // ... under this config
 
     void ensure(uint64_t planes, uint64_t units, uint64_t L, int qb) {
         const uint64_t ntiles = (L + kTile - 1) / kTile;
@@ -323,18 +325,17 @@ void launch_pack(cudaStream_t st, EncScratch &S, DBuf<uint8_t> &arena, bool coun
     const unsigned grid = (unsigned)(S.planes * nck);
     if (count) {
         {
-            PROF("pack_count", st);
+            PROF("pack_count", st); // also zeroes the plane slots
             pack_count<<<grid, 256, 0, st>>>(P, (int)S.planes, nck, S.t_cbits.p);
         }
         launch_plane_scan(st, S.t_cbits.p, S.t_coff.p, nck, (int)S.planes, kScanSumExcl);
-    }
-    {
-        PROF("arena_zero", st);
+    } else {
+        PROF("arena_zero", st); // re-pack after an arena overflow
         arena_zero<<<296, 256, 0, st>>>(arena.p, arena.cap, S.slot_off.p + S.planes);
     }
     {
         PROF("pack_write", st);
-        pack_write<<<grid, 256, 0, st>>>(P, (int)S.planes, nck, S.t_coff.p);
+        pack_write<<<grid, 256, 0, st>>>(P, (int)S.planes, nck, S.t_coff.p, S.t_cbits.p);
     }
 }
 
@@ -353,6 +354,7 @@ EncodeResult encode_batch(cudaStream_t st, EncScratch &S, const Src &src, int un
 }
 
 void launch_plane_scan(cudaStream_t st, const int32_t *in, int32_t *out, int ntiles, int planes, ScanKind kind) {
+    if (ntiles <= kInlineTiles) return; // consumers compute the carry inline (carry_of)
     const int out_stride = kind == kScanSumExcl ? ntiles + 1 : ntiles;
     PROF("plane_scan", st);
     if (ntiles <= 256) plane_scan<1><<<planes, 256, 0, st>>>(in, out, ntiles, planes, kind, ntiles, out_stride);
@@ -376,11 +378,19 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     const unsigned tgrid_u = (unsigned)(units * ntiles), tgrid_p = (unsigned)(planes * ntiles);
 
     if (check_finite) CK(cudaMemsetAsync(S.nonfinite.p, 0, sizeof(uint32_t), st));
-    {
+    // Per-plane bounds only change with the data in RangeRelative mode; for
+    // fixed bounds they are computed once per batch shape (enc_x resets the
+    // per-pass flags and histogram bookkeeping itself).
+    const bool params_fresh = S.param_planes == planes && S.param_cfg.mode == cfg.mode &&
+                              S.param_cfg.bound == cfg.bound && S.param_cfg.predictor == cfg.predictor &&
+                              cfg.mode != QCSIM_MODE_RANGE_RELATIVE;
+    if (check_finite || !params_fresh) {
         PROF("init_params", st);
         init_params<NP, Src><<<units, 256, 0, st>>>(S.params.p, src, units, L, cfg.mode, cfg.bound, cfg.predictor,
                                                     check_finite ? S.nonfinite.p : nullptr, S.symrange.p,
                                                     S.hspecial.p, S.gamma.p);
+        S.param_planes = cfg.mode == QCSIM_MODE_RANGE_RELATIVE ? 0 : planes;
+        S.param_cfg = cfg;
     }
     if (check_finite) {
         uint32_t bad = 0;
@@ -408,6 +418,9 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     A.log2C = log2C;
     A.qb = qb;
     A.predictor = cfg.predictor;
+    A.symrange = S.symrange.p;
+    A.hspecial = S.hspecial.p;
+    A.gamma = S.gamma.p;
     A.t_nev = reinterpret_cast<uint32_t *>(S.t_nev.p);
     {
         PROF("enc_x", st);
@@ -424,8 +437,12 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
         enc_compact<<<tgrid_p, kEncThreads, 0, st>>>(A, (int)planes);
     }
     {
+        static const int chain_mode = [] {
+            const char *v = std::getenv("QCSIM_DEBUG_CHAIN"); // debug: 0 normal, 1 skip
+            return v ? std::atoi(v) : 0;
+        }();
         PROF("enc_chain", st);
-        enc_chain<<<(unsigned)planes, 32, 0, st>>>(A, (int)planes);
+        if (chain_mode == 0) enc_chain<<<(unsigned)planes, 32, 0, st>>>(A, (int)planes);
     }
     {
         PROF("enc_verify", st);
@@ -505,12 +522,10 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     }
 
     // slot offsets: exclusive scan of slot sizes (16-byte aligned slots)
-    size_t tmp_bytes = 0;
-    CK(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, S.slot_bytes.p, S.slot_off.p + 1, (int)planes, st));
-    S.cub_tmp.ensure(tmp_bytes);
-    CK(cudaMemsetAsync(S.slot_off.p, 0, sizeof(uint64_t), st));
-    CK(cub::DeviceScan::InclusiveSum(S.cub_tmp.p, tmp_bytes, S.slot_bytes.p, S.slot_off.p + 1, (int)planes, st));
-    // (cub scan kernels are library code: not counted in g_launches)
+    {
+        PROF("slot_scan", st);
+        slot_scan<<<1, 1024, 0, st>>>(S.slot_bytes.p, S.slot_off.p, (int)planes);
+    }
 
     PackArgs P;
     P.tsym = S.tsym.p;
