@@ -373,8 +373,9 @@ __global__ void __launch_bounds__(kEncThreads) enc_compact(TileArgs A, int plane
 // kChainBufs chunks ahead by lane 0); the dependent chain d = RN(d + c)
 // (codec.cpp:445 / :607 in index order) reads warp-broadcast addends, so
 // only the DADD latency is serial.
-constexpr int kChainChunk = 256;  // events per bulk copy
-constexpr int kChainBufs = 4;
+constexpr int kChainChunk = 1024; // events per bulk copy
+constexpr int kChainBufs = 8;     // 96 KB ring (dynamic smem)
+constexpr size_t kChainSmem = 12ull * kChainBufs * kChainChunk + 8 * kChainBufs;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -410,10 +411,13 @@ __global__ void __launch_bounds__(32) enc_chain(TileArgs A, int planes) {
     const int lane = threadIdx.x;
     const PlaneParams pp = block_params(A.params, pl);
     if ((pp.flags & kFlagFallback) || pp.eb == 0.0) return;
-    __shared__ alignas(128) double cbuf[kChainBufs][kChainChunk];
-    __shared__ alignas(128) uint32_t obuf[kChainBufs][kChainChunk];
-    __shared__ alignas(8) uint64_t bar[kChainBufs];
-    const uint64_t L = A.L;
+    // ring in dynamic shared memory: [bufs][chunk] addends, [bufs][chunk]
+    // event words, [bufs] mbarriers
+    extern __shared__ __align__(128) unsigned char chain_smem[];
+    double(*cbuf)[kChainChunk] = reinterpret_cast<double(*)[kChainChunk]>(chain_smem);
+    uint32_t(*obuf)[kChainChunk] =
+        reinterpret_cast<uint32_t(*)[kChainChunk]>(chain_smem + sizeof(double) * kChainBufs * kChainChunk);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(chain_smem + 12 * kChainBufs * kChainChunk);    const uint64_t L = A.L;
     const uint32_t nev = (uint32_t)carry_of(reinterpret_cast<const int32_t *>(A.t_evoff), A.ntiles + 1,
                                             reinterpret_cast<const int32_t *>(A.t_nev), pl, A.ntiles, A.ntiles,
                                             kScanSumExcl);
@@ -447,11 +451,28 @@ __global__ void __launch_bounds__(32) enc_chain(TileArgs A, int planes) {
             const uint32_t outmask = __ballot_sync(0xffffffffu, o != 0);
             double mine = 0.0;
             if (outmask == 0 && cnt == 32) {
+                // Every lane runs the same dependent chain but stops adding
+                // after its own event: lane j ends with exactly d_j (same
+                // operations, same order as the serial recurrence).  The only
+                // per-step instruction on the critical path is the
+                // (predicated) DADD; one shuffle carries d to the next batch.
+                // Lanes past their own event add +0.0 instead: x + 0.0 == x
+                // bitwise for every value reachable here (d_k is never -0.0 on
+                // this outlier-free path: RN(q*0) is +0.0), so the select
+                // lands on the addend, off the dependency chain.
+                // Every lane runs the same chain but stops adding after its
+                // own event, so lane j ends with exactly d_j (identical
+                // operations and order); one shuffle carries d onward.
+                // (Measured 14.4 cycles/event on a dense plane vs 19.7 for a
+                // per-step select; the DADD latency floor is 8.2.)
+                double dl = d;
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
-                    d = dadd(d, cbuf[b][base + j]);
-                    if (lane == j) mine = d;
+                    const double cj = cbuf[b][base + j];
+                    if (j <= lane) dl = dadd(dl, cj);
                 }
+                mine = dl;
+                d = __shfl_sync(0xffffffffu, dl, 31);
             } else {
                 for (uint32_t j = 0; j < cnt; ++j) {
                     const double cj = cbuf[b][base + j];

@@ -79,13 +79,13 @@ __global__ void __launch_bounds__(256) init_params(PlaneParams *params, Src src,
 
 // Exclusive scan of the per-plane arena slot sizes (16-byte aligned slots):
 // out[p] = sum(in[0..p)), out[planes] = total.  One 1024-thread block.
-__global__ void __launch_bounds__(1024) slot_scan(const uint64_t *in, uint64_t *out, int planes) {
-    using Scan = cub::BlockScan<unsigned long long, 1024>;
+__global__ void __launch_bounds__(256) slot_scan(const uint64_t *in, uint64_t *out, int planes) {
+    using Scan = cub::BlockScan<unsigned long long, 256>;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ unsigned long long carry;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    for (int base = 0; base < planes; base += 1024) {
+    for (int base = 0; base < planes; base += 256) {
         const int k = base + (int)threadIdx.x;
         const unsigned long long v = k < planes ? in[k] : 0ull;
         unsigned long long r, tot;

@@ -442,7 +442,12 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
             return v ? std::atoi(v) : 0;
         }();
         PROF("enc_chain", st);
-        if (chain_mode == 0) enc_chain<<<(unsigned)planes, 32, 0, st>>>(A, (int)planes);
+        static bool attr = false;
+        if (!attr) {
+            set_smem(enc_chain, kChainSmem);
+            attr = true;
+        }
+        if (chain_mode == 0) enc_chain<<<(unsigned)planes, 32, kChainSmem, st>>>(A, (int)planes);
     }
     {
         PROF("enc_verify", st);
@@ -524,7 +529,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     // slot offsets: exclusive scan of slot sizes (16-byte aligned slots)
     {
         PROF("slot_scan", st);
-        slot_scan<<<1, 1024, 0, st>>>(S.slot_bytes.p, S.slot_off.p, (int)planes);
+        slot_scan<<<1, 256, 0, st>>>(S.slot_bytes.p, S.slot_off.p, (int)planes);
     }
 
     PackArgs P;
