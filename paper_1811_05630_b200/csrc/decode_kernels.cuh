@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(256) dec_prepare(DecPlanes D, DecTables T, int
     __shared__ uint32_t cnt[kMaxCodeLen + 1];
     __shared__ uint64_t first[kMaxCodeLen + 1];
     __shared__ uint32_t basei[kMaxCodeLen + 1];
-    __shared__ uint32_t s_n, s_maxlen;
+    __shared__ uint32_t s_n;
     const uint8_t *blk = D.arena + D.blk_off[pl];
     const uint8_t *tab = blk + kHeaderBytes + 4;
     if (tid == 0) s_n = (uint32_t)load_le(blk + kHeaderBytes, 4);
@@ -76,7 +76,6 @@ __global__ void __launch_bounds__(256) dec_prepare(DecPlanes D, DecTables T, int
             prev = l;
             maxlen = l;
         }
-        s_maxlen = maxlen;
         // symbols in (len, sym) order: the table is in symbol order, so a
         // stable pass by length keeps symbol order inside each length
         uint32_t next[kMaxCodeLen + 1];

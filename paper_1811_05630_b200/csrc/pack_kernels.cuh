@@ -11,6 +11,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include "common.cuh"
+#include "decode_kernels.cuh" // DecTables
 #include "enc_tiles.cuh" // carry_of / tile_carry
 
 namespace qcb {
@@ -38,6 +39,7 @@ struct CodeBook {
     uint32_t *err;             // nonzero: codec error code
     uint64_t cap;
     int qb;
+    DecTables dec;             // optional: decode tables of the new blocks
 };
 
 enum : uint32_t { kErrDepth = 1 };
@@ -66,30 +68,93 @@ __device__ void block_bitonic(uint64_t *a, uint32_t n) {
     }
 }
 
-constexpr uint32_t kSmemSort = 4096;
+constexpr uint32_t kSmallN = 1024; // alphabets up to this size stay in shared memory
 
+// Decode tables of a block (PrefixDecoder, codec.cpp:251-273) written by the
+// encoder itself, so the next gate pass needs no table-parsing kernel.
+// entries: n symbols in ascending order with code lengths and canonical codes.
+__device__ void emit_dec_tables(const DecTables &T, int pl, uint32_t n, const uint32_t *sym, const uint8_t *len,
+                                const uint64_t *code, const uint32_t *lcount, const uint64_t *lfirst0) {
+    uint32_t *lut = T.lut + (uint64_t)pl * (1u << kLutBits);
+    for (int k = threadIdx.x; k < (1 << kLutBits); k += blockDim.x) lut[k] = 0;
+    __shared__ uint32_t basei[kMaxCodeLen + 2];
+    if (threadIdx.x == 0) {
+        uint32_t b = 0, maxlen = 0;
+        for (int l = 1; l <= kMaxCodeLen; ++l) {
+            basei[l] = b;
+            b += lcount[l];
+            if (lcount[l]) maxlen = l;
+            T.first[(uint64_t)pl * (kMaxCodeLen + 1) + l] = lcount[l] ? lfirst0[l] : 0;
+            T.count[(uint64_t)pl * (kMaxCodeLen + 1) + l] = lcount[l];
+            T.basei[(uint64_t)pl * (kMaxCodeLen + 1) + l] = basei[l];
+        }
+        T.first[(uint64_t)pl * (kMaxCodeLen + 1)] = 0;
+        T.count[(uint64_t)pl * (kMaxCodeLen + 1)] = 0;
+        T.basei[(uint64_t)pl * (kMaxCodeLen + 1)] = 0;
+        T.meta[4 * pl] = maxlen;
+        T.meta[4 * pl + 1] = n;
+    }
+    __syncthreads();
+    uint32_t *sorted = T.sorted + (uint64_t)pl * T.cap;
+    for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
+        const int l = len[r];
+        // (len, sym) order: position within the length = code - first code
+        sorted[basei[l] + (uint32_t)(code[r] - lfirst0[l])] = sym[r];
+        if (l <= kLutBits) {
+            const uint32_t lo = (uint32_t)(code[r] << (kLutBits - l));
+            const uint32_t hi = (uint32_t)((code[r] + 1) << (kLutBits - l));
+            const uint32_t e = (sym[r] << 6) | (uint32_t)l;
+            for (uint32_t k = lo; k < hi; ++k) lut[k] = e;
+        }
+    }
+}
+
+// One block per plane.  Working arrays live in shared memory for alphabets of
+// up to kSmallN symbols (the serial two-queue merge then runs on smem), in
+// per-plane global scratch beyond that.
 __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
     const int pl = blockIdx.x;
     if (pl >= planes) return;
     const int tid = threadIdx.x;
     using Scan = cub::BlockScan<int, 256>;
     __shared__ typename Scan::TempStorage scan_tmp;
-    __shared__ uint64_t skeys[kSmemSort];
+    __shared__ uint64_t k_s[kSmallN];
+    __shared__ uint32_t sym_s[kSmallN], cnt_s[kSmallN];
+    __shared__ uint32_t nc_s[2 * kSmallN];
+    __shared__ int32_t par_s[2 * kSmallN];
+    __shared__ uint8_t len_s[kSmallN];
+    __shared__ uint64_t code_s[kSmallN];
     __shared__ uint32_t s_n;
     __shared__ uint32_t lcount[kMaxCodeLen + 2];
-    __shared__ uint64_t lfirst[kMaxCodeLen + 2];
+    __shared__ uint64_t lfirst[kMaxCodeLen + 2], lfirst0[kMaxCodeLen + 2];
     __shared__ unsigned long long s_bits;
     __shared__ uint32_t s_err;
 
     const uint32_t rsym = 1u << B.qb;
     uint32_t *hist = B.hist + (uint64_t)pl * ((uint64_t)rsym + 1);
     const uint64_t cap = B.cap;
-    uint32_t *sym = B.sym + pl * cap;
-    uint64_t *cnt = B.cnt + pl * cap;
-    uint8_t *len = B.len + pl * cap;
-    uint64_t *code = B.code + pl * cap;
     const uint32_t h0 = B.hspecial[2 * pl], hrun = B.hspecial[2 * pl + 1];
     const uint32_t smin = B.symrange[2 * pl], smax = B.symrange[2 * pl + 1];
+    // alphabet size first (decides smem vs global working arrays)
+    __shared__ uint32_t s_cnt_total;
+    if (tid == 0) s_cnt_total = (h0 ? 1u : 0u) + (hrun ? 1u : 0u);
+    __syncthreads();
+    if (smin <= smax) {
+        uint32_t c = 0;
+        for (uint64_t s = smin + tid; s <= smax; s += 256) c += hist[s] != 0;
+        atomicAdd(&s_cnt_total, c);
+    }
+    if (tid < kMaxCodeLen + 2) lcount[tid] = 0;
+    __syncthreads();
+    const uint32_t n = s_cnt_total;
+    const bool small = n <= kSmallN;
+    uint32_t *sym = small ? sym_s : B.sym + pl * cap;
+    uint32_t *cnt = small ? cnt_s : reinterpret_cast<uint32_t *>(B.cnt + pl * cap);
+    uint8_t *len = small ? len_s : B.len + pl * cap;
+    uint64_t *code = small ? code_s : B.code + pl * cap;
+    uint64_t *keys = small ? k_s : B.key + pl * cap * 2;
+    uint32_t *nc = small ? nc_s : reinterpret_cast<uint32_t *>(B.ncnt + pl * cap * 2);
+    int32_t *par = small ? par_s : B.parent + pl * cap * 2;
 
     if (tid == 0) {
         s_n = 0;
@@ -101,9 +166,8 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
             s_n = 1;
         }
     }
-    if (tid < kMaxCodeLen + 2) lcount[tid] = 0;
     __syncthreads();
-    // 1) compaction of the symbol range, ascending
+    // 1) compaction of the symbol range, ascending (freq, codec.cpp:484-488)
     if (smin <= smax) {
         for (uint64_t c0 = smin; c0 <= smax; c0 += 256) {
             const uint64_t s = c0 + tid;
@@ -126,25 +190,21 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
         s_n += 1;
     }
     __syncthreads();
-    const uint32_t n = s_n;
     if (n == 0) { // unreachable for L >= 1
         if (tid == 0) B.err[pl] = 0;
         return;
     }
     // 2) leaves sorted by (count, symbol)
-    uint64_t *keys = n <= kSmemSort ? skeys : B.key + pl * cap * 2;
-    for (uint32_t i = tid; i < n; i += 256) keys[i] = (cnt[i] << 25) | sym[i];
+    for (uint32_t i = tid; i < n; i += 256) keys[i] = ((uint64_t)cnt[i] << 25) | sym[i];
     __syncthreads();
     if (n > 1) block_bitonic(keys, n);
-    // 3) two-queue merge (serial; ties prefer the leaf queue)
-    uint64_t *nc = B.ncnt + pl * cap * 2;
-    int32_t *par = B.parent + pl * cap * 2;
+    // 3) two-queue merge (codec.cpp:168-229; ties prefer the leaf queue)
     if (tid == 0) {
         if (n == 1) {
             par[0] = -1;
         } else {
             for (uint32_t i = 0; i < n; ++i) {
-                nc[i] = keys[i] >> 25;
+                nc[i] = (uint32_t)(keys[i] >> 25);
                 par[i] = -1;
             }
             uint32_t lp = 0, ip = n, nodes = n;
@@ -170,32 +230,34 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
     // 4) lengths in symbol order
     for (uint32_t i = tid; i < n; i += 256) {
         const uint32_t s = (uint32_t)(keys[i] & ((1ull << 25) - 1));
-        const uint64_t depth = n == 1 ? 1 : nc[i];
-        if (depth < 1 || depth > (uint64_t)kMaxCodeLen) atomicExch(&s_err, kErrDepth);
-        // rank of s in the ascending symbol list
-        uint32_t lo = 0, hi = n;
+        const uint32_t depth = n == 1 ? 1u : nc[i];
+        if (depth < 1 || depth > (uint32_t)kMaxCodeLen) atomicExch(&s_err, kErrDepth);
+        uint32_t lo = 0, hi = n; // rank of s in the ascending symbol list
         while (lo < hi) {
             const uint32_t mid = (lo + hi) >> 1;
             if (sym[mid] < s) lo = mid + 1;
             else hi = mid;
         }
-        const uint8_t l = (uint8_t)tmin<uint64_t>(depth, kMaxCodeLen);
+        const uint8_t l = (uint8_t)tmin<uint32_t>(depth, kMaxCodeLen);
         len[lo] = l;
         atomicAdd(&lcount[l], 1u);
-        atomicAdd(&s_bits, (unsigned long long)(cnt[lo] * l));
+        atomicAdd(&s_bits, (unsigned long long)cnt[lo] * l);
     }
     __syncthreads();
-    // 5) canonical codes: (len, sym) order == symbol order within a length
+    // 5) canonical codes (codec.cpp:233-249): (len, sym) order == symbol
+    //    order within a length
     if (tid == 0) {
         uint64_t c = 0;
         int prev = -1;
         for (int l = 1; l <= kMaxCodeLen; ++l) {
+            lfirst[l] = 0;
             if (!lcount[l]) continue;
             if (prev >= 0) c <<= (l - prev);
             lfirst[l] = c;
             c += lcount[l];
             prev = l;
         }
+        for (int l = 0; l <= kMaxCodeLen; ++l) lfirst0[l] = lfirst[l];
         for (uint32_t r = 0; r < n; ++r) code[r] = lfirst[len[r]]++;
         const uint64_t bits = s_bits + B.gamma_bits[pl];
         const uint64_t payload = 4 + 5ull * n + (bits + 7) / 8 + 16ull * B.ocount[pl];
@@ -206,6 +268,15 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
         B.slot_bytes[pl] = 16 + ((bytes + 15) & ~15ull);
         B.err[pl] = s_err;
     }
+    __syncthreads();
+    if (small) { // publish the codebook for the packer
+        for (uint32_t r = tid; r < n; r += 256) {
+            B.sym[pl * cap + r] = sym_s[r];
+            B.len[pl * cap + r] = len_s[r];
+            B.code[pl * cap + r] = code_s[r];
+        }
+    }
+    if (B.dec.lut) emit_dec_tables(B.dec, pl, n, sym, len, code, lcount, lfirst0);
 }
 
 // ------------------------------------------------------------------ E5

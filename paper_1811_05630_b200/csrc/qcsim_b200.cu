@@ -203,7 +203,7 @@ void validate_codec(const qcsim_codec_config &c) { // codec.cpp:331-341
 int auto_log2C(uint64_t L) {
     int s = 0;
     while ((1ull << s) < L) ++s;
-    return std::max(6, std::min(10, s - 7));
+    return std::max(5, std::min(10, s - 9)); // 2^14 planes: 512 chunks of 32
 }
 
 // Grow-only pinned host buffer.
@@ -250,6 +250,7 @@ struct EncScratch {
     uint64_t hist_stride = 0;
     uint64_t param_planes = 0;       // params valid for this many planes ...
     qcsim_codec_config param_cfg{};  // ... under this config
+    DecTables dec_out{};             // where enc_codebook writes decode tables (optional)
 
     void ensure(uint64_t planes, uint64_t units, uint64_t L, int qb) {
         const uint64_t ntiles = (L + kTile - 1) / kTile;
@@ -521,6 +522,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     B.err = S.err.p;
     B.cap = cap;
     B.qb = qb;
+    B.dec = S.dec_out;
     {
         PROF("enc_codebook", st);
         enc_codebook<<<(unsigned)planes, 256, 0, st>>>(B, (int)planes);
@@ -618,19 +620,26 @@ struct DecScratch {
         sorted.ensure(planes * cap);
         meta.ensure(planes * 4);
     }
+    DecTables tables() const {
+        DecTables T;
+        T.lut = lut.p;
+        T.first = first.p;
+        T.count = count.p;
+        T.basei = basei.p;
+        T.sorted = sorted.p;
+        T.meta = meta.p;
+        T.cap = cap;
+        return T;
+    }
 };
 
+// prepare = false: the tables were written by the encoder that produced the
+// blocks (enc_codebook -> emit_dec_tables), no table-parsing pass needed.
 void decode_batch(cudaStream_t st, DecScratch &S, const uint8_t *arena, const uint64_t *blk_off,
-                  const IndexRec *index, double *const *out, int planes, uint64_t L, int log2C, int qb) {
-    S.ensure(planes, L, qb);
-    DecTables T;
-    T.lut = S.lut.p;
-    T.first = S.first.p;
-    T.count = S.count.p;
-    T.basei = S.basei.p;
-    T.sorted = S.sorted.p;
-    T.meta = S.meta.p;
-    T.cap = S.cap;
+                  const IndexRec *index, double *const *out, int planes, uint64_t L, int log2C, int qb,
+                  bool prepare = true) {
+    if (prepare) S.ensure(planes, L, qb);
+    const DecTables T = S.tables();
     DecPlanes D;
     D.arena = arena;
     D.blk_off = blk_off;
@@ -638,7 +647,7 @@ void decode_batch(cudaStream_t st, DecScratch &S, const uint8_t *arena, const ui
     D.out = out;
     D.L = L;
     D.log2C = log2C;
-    {
+    if (prepare) {
         PROF("dec_prepare", st);
         dec_prepare<<<planes, 256, 0, st>>>(D, T, planes);
     }
@@ -782,7 +791,7 @@ struct qcsim_engine {
     std::vector<std::pair<uint64_t, std::vector<uint8_t>>> imported;
     std::vector<double> sq_norm; // all S slices (global view)
     EncScratch enc;
-    DecScratch dec;
+    DecScratch dec[2]; // decode tables of arena[0/1], written by the encoder
     ValScratch val;
     DBuf<uint8_t> imp_bytes;
     DBuf<uint64_t> imp_off;
@@ -867,8 +876,12 @@ template <class Src> void engine_store(qcsim_engine *e, const Src &src) {
     const uint64_t ntiles = (e->L + kTile - 1) / kTile;
     if (e->compressed) {
         e->index[nxt].ensure(2 * e->ns * e->nidx);
+        // the encoder also writes the decode tables of the blocks it packs
+        e->dec[nxt].ensure(2 * e->ns, e->L, e->cfg.codec.quant_code_bits);
+        e->enc.dec_out = e->dec[nxt].tables();
         encode_launch<2, Src>(e->st, e->enc, src, units, e->L, e->cfg.codec, e->log2C, e->index[nxt].p,
                               e->arena[nxt], false, false);
+        e->enc.dec_out = DecTables{};
     } else {
         e->dense[nxt].ensure(e->ns * 2 * e->L);
         e->enc.tilesum.ensure(e->ns * ntiles);
@@ -941,8 +954,8 @@ void engine_decode_old(qcsim_engine *e, bool need_imported) {
         CK(cudaMemcpyAsync(e->old.p, e->dense[e->cur].p, e->ns * 2 * e->L * sizeof(double),
                            cudaMemcpyDeviceToDevice, e->st));
     } else {
-        decode_batch(e->st, e->dec, e->arena[e->cur].p, e->blk_off[e->cur].p, e->index[e->cur].p, e->outptrs.p,
-                     (int)(2 * e->ns), e->L, e->log2C, e->cfg.codec.quant_code_bits);
+        decode_batch(e->st, e->dec[e->cur], e->arena[e->cur].p, e->blk_off[e->cur].p, e->index[e->cur].p, e->outptrs.p,
+                     (int)(2 * e->ns), e->L, e->log2C, e->cfg.codec.quant_code_bits, /*prepare=*/false);
     }
     if (extra) {
         // imported blocks: validating serial decode (they carry no index)
