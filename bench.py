@@ -205,6 +205,11 @@ def run_ours(args, wl, rank, world, dist):
         eng.run(wl["steps"](k % wl["max_steps"]))
     kprof = profile_end(lib, prof)
     mets = eng.metrics()
+    chain = None
+    if hasattr(lib, "qcsim_debug_chain_stats"):
+        cs = (ctypes.c_uint32 * 3)()
+        if lib.qcsim_debug_chain_stats(cs) == 0:
+            chain = {"resolve_points": int(cs[0]), "refuted_chunks": int(cs[1]), "serial_chunks": int(cs[2])}
 
     # e2e: the same step count through the C-ABI with host buffers
     e2e_t, h2d, d2h = 0.0, 0, 0
@@ -223,7 +228,7 @@ def run_ours(args, wl, rank, world, dist):
         e2e_t += time.perf_counter() - t0
         h2d += ctypes.sizeof(arr)
         d2h += len(blocks) + ctypes.sizeof(_native.RunMetricsC)
-    return dict(gates=gates, dev_s=dev_s, wall=wall, clocks=clk, launches=launches, metrics=mets, kprof=kprof,
+    return dict(gates=gates, dev_s=dev_s, wall=wall, clocks=clk, launches=launches, metrics=mets, kprof=kprof, chain=chain,
                 e2e_t=e2e_t, h2d=h2d // max(1, args.steps), d2h=d2h // max(1, args.steps))
 
 
@@ -326,7 +331,8 @@ def main():
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
             "traffic": None, "peak_kind": peak_kind,
             "basis": "per gate pass: sum of input+output QCB1 block bytes (SURVEY.md 8(d)) / device time per pass",
-            "dominant_kernel": dominant, "kernel_shares": kprof[:8]}
+            "dominant_kernel": dominant, "kernel_shares": kprof[:8],
+            "kernel_ms_total": sum(k["ms"] for k in kprof), "chain_scan": res.get("chain")}
     cpu = None
     if args.gpus == 1 and world == 1:
         try:

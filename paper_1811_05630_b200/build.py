@@ -22,7 +22,7 @@ NVFLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler"
 
 LIB = os.path.join(HERE, "libqcsim_b200.so")
 SOURCES = ["qcsim_b200.cu"]
-HEADERS = ["common.cuh", "enc_tiles.cuh", "sources.cuh", "pack_kernels.cuh", "decode_kernels.cuh", "misc_kernels.cuh"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith(".cuh"))
 
 
 def _stale(target, deps):

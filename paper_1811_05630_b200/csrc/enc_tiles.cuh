@@ -27,6 +27,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include "common.cuh"
+#include "align.cuh"
 
 namespace qcb {
 
@@ -39,6 +40,7 @@ struct TileArgs {
     uint32_t *evlist;      // [plane][L] event element indices (bit 31: outlier)
     double *evc;           // [plane][L] event addend q*m^ (outlier: its value)
     double *dval;          // [plane][L] chain value per event ordinal
+    double *evD;           // [plane][L] lattice estimate of d per event ordinal (chain_scan.cuh)
     IndexRec *index;       // [plane][nidx]
     // per plane-tile, stride ntiles (+1 for scanned arrays)
     int32_t *t_lastout;    // last speculative outlier in the tile (-1)
@@ -269,15 +271,20 @@ __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int plane
     ScanI(scan_tmp).ExclusiveScan(opos, lo, -1, cub::Max());
     const int32_t tbase = carry_of(A.t_base, A.ntiles, A.t_lastout, pl, t, A.ntiles, kScanMaxExcl); // position or -1
     long long K[kPerThread];
+    double *dhat = A.dval + (uint64_t)pl * L; // scratch until the chain overwrites dval
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
         if (opos[e] >= 0) {
             K[e] = 0;
+            if (k < tl) dhat[t0 + k] = xv[e];
         } else {
             double base;
             if (lo[e] >= 0) base = x[t0 + lo[e]];
             else base = tbase >= 0 ? x[tbase] : 0.0;
             K[e] = k < tl ? llround_exact(dmul(dsub(xv[e], base), pp.inv_q)) : 0;
+            // alignment of the lattice estimate of d (chain_scan.cuh)
+            // lattice estimate of the chain value (chain_scan.cuh)
+            if (k < tl) dhat[t0 + k] = dadd(base, dmul(pp.q, (double)K[e]));
         }
     }
     kb[tid] = K[kPerThread - 1];
@@ -352,6 +359,8 @@ __global__ void __launch_bounds__(kEncThreads) enc_compact(TileArgs A, int plane
                                              reinterpret_cast<const int32_t *>(A.t_nev), pl, t, A.ntiles, kScanSumExcl);
     uint32_t *ev = A.evlist + (uint64_t)pl * L;
     double *evc = A.evc + (uint64_t)pl * L;
+    double *evD = A.evD + (uint64_t)pl * L;
+    const double *dhat = A.dval + (uint64_t)pl * L;
     const uint32_t *sym = A.sym + (uint64_t)pl * L;
     const double *x = A.x + (uint64_t)pl * L;
     const double q = A.params[pl].q;
@@ -364,6 +373,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_compact(TileArgs A, int plane
         // and the element index with bit 31 = outlier
         ev[base + pos[e]] = (uint32_t)i | (out ? 0x80000000u : 0u);
         evc[base + pos[e]] = out ? x[i] : dmul(q, (double)((long long)sym[i] - half));
+        evD[base + pos[e]] = dhat[i];
     }
 }
 

@@ -13,6 +13,7 @@
 #include "common.cuh"
 #include "decode_kernels.cuh" // DecTables
 #include "enc_tiles.cuh" // carry_of / tile_carry
+#include "chain_scan.cuh"
 
 namespace qcb {
 

@@ -242,6 +242,10 @@ struct EncScratch {
     DBuf<uint32_t> cb_sym;
     DBuf<int32_t> cb_parent;
     DBuf<uint32_t> overflow;
+    DBuf<double> evD;
+    DBuf<double> chain_carry; // enc_chain_scan chunk hand-off
+    DBuf<uint32_t> chain_flag;
+    uint32_t chain_epoch = 0;
     HBuf<uint64_t> h_bytes, h_off, h_misc;
     HBuf<PlaneParams> h_params;
     HBuf<uint32_t> h_err;
@@ -261,6 +265,7 @@ struct EncScratch {
         dval.ensure(planes * L);
         evc.ensure(planes * L + 8);       // TMA chunks round up to 16 bytes
         evlist.ensure(planes * L + 8);
+        evD.ensure(planes * L + 8);
         sym.ensure(planes * L);
         fl.ensure(planes * L);
         opos.ensure(planes * L);
@@ -300,6 +305,18 @@ struct EncScratch {
         overflow.ensure(1);
     }
 };
+
+// enc_chain_scan counters: [0] resolve points, [1] refuted chunks redone
+// serially, [4] chunks run serially because the maps did not fit
+constexpr uint64_t kScanChainMaxPlanes = 4096;
+uint32_t *chain_stats() {
+    static DBuf<uint32_t> buf;
+    if (!buf.p) {
+        buf.ensure(8);
+        CK(cudaMemset(buf.p, 0, 8 * sizeof(uint32_t)));
+    }
+    return buf.p;
+}
 
 template <class K> void set_smem(K kernel, size_t bytes) {
     CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
@@ -409,6 +426,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     A.evlist = S.evlist.p;
     A.evc = S.evc.p;
     A.dval = S.dval.p;
+    A.evD = S.evD.p;
     A.index = index;
     A.t_lastout = S.t_lastout.p;
     A.t_base = S.t_base.p;
@@ -438,17 +456,63 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
         enc_compact<<<tgrid_p, kEncThreads, 0, st>>>(A, (int)planes);
     }
     {
+        // debug: dump one encode call's event lists (QCSIM_CHAIN_DUMP_AT = call
+        // number, QCSIM_CHAIN_DUMP_FILE = path)
+        static const long dump_at = std::getenv("QCSIM_CHAIN_DUMP_AT") ? std::atol(std::getenv("QCSIM_CHAIN_DUMP_AT")) : -1;
+        static long calls = 0;
+        if (dump_at >= 0 && calls++ == dump_at) {
+            CK(cudaStreamSynchronize(st));
+            const uint64_t nel = planes * L;
+            std::vector<uint32_t> h_ev(nel), h_nev(planes * ntiles);
+            std::vector<double> h_c(nel), h_d(nel);
+            std::vector<PlaneParams> h_pp(planes);
+            CK(cudaMemcpy(h_ev.data(), S.evlist.p, nel * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(h_c.data(), S.evc.p, nel * 8, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(h_d.data(), S.evD.p, nel * 8, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(h_nev.data(), S.t_nev.p, planes * ntiles * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(h_pp.data(), S.params.p, planes * sizeof(PlaneParams), cudaMemcpyDeviceToHost));
+            if (FILE *f = std::fopen(std::getenv("QCSIM_CHAIN_DUMP_FILE"), "wb")) {
+                const uint64_t hdr[3] = {planes, L, (uint64_t)ntiles};
+                std::fwrite(hdr, 8, 3, f);
+                std::fwrite(h_pp.data(), sizeof(PlaneParams), planes, f);
+                std::fwrite(h_nev.data(), 4, planes * ntiles, f);
+                std::fwrite(h_ev.data(), 4, nel, f);
+                std::fwrite(h_c.data(), 8, nel, f);
+                std::fwrite(h_d.data(), 8, nel, f);
+                std::fclose(f);
+            }
+        }
+    }
+    {
+        // 0 auto, 1 skip (debug), 2 serial warp chain, 3 block-parallel chain
         static const int chain_mode = [] {
-            const char *v = std::getenv("QCSIM_DEBUG_CHAIN"); // debug: 0 normal, 1 skip
+            const char *v = std::getenv("QCSIM_CHAIN");
             return v ? std::atoi(v) : 0;
         }();
-        PROF("enc_chain", st);
+        static const int chain_debug = std::getenv("QCSIM_CHAIN_DEBUG") ? 1 : 0;
         static bool attr = false;
         if (!attr) {
             set_smem(enc_chain, kChainSmem);
+            set_smem(enc_chain_scan, kChainScanSmem);
             attr = true;
         }
-        if (chain_mode == 0) enc_chain<<<(unsigned)planes, 32, kChainSmem, st>>>(A, (int)planes);
+        const bool scan = chain_mode == 3 || (chain_mode == 0 && planes <= kScanChainMaxPlanes);
+        if (chain_mode != 1 && scan) {
+            PROF("enc_chain_scan", st);
+            const int cmax = (int)((L + kCsChunk - 1) / kCsChunk);
+            S.chain_carry.ensure(planes * cmax);
+            if (S.chain_flag.ensure(planes * cmax, /*zero=*/true)) S.chain_epoch = 0;
+            ChainLink link{S.chain_carry.p, S.chain_flag.p, cmax, ++S.chain_epoch};
+            if (link.epoch == 0) { // wrapped: start over from clean flags
+                CK(cudaMemsetAsync(S.chain_flag.p, 0, S.chain_flag.cap * sizeof(uint32_t), st));
+                link.epoch = S.chain_epoch = 1;
+            }
+            enc_chain_scan<<<(unsigned)(planes * cmax), kCsThreads, kChainScanSmem, st>>>(A, (int)planes, link,
+                                                                                        chain_stats(), chain_debug);
+        } else if (chain_mode != 1) {
+            PROF("enc_chain", st);
+            enc_chain<<<(unsigned)planes, 32, kChainSmem, st>>>(A, (int)planes);
+        }
     }
     {
         PROF("enc_verify", st);
@@ -1095,6 +1159,20 @@ int qcsim_profile_read(char (*names)[64], double *ms, uint64_t *count, double *b
         ++k;
     }
     return k;
+}
+
+// Debug (not part of the public header): enc_chain_scan counters since the
+// last call ([0] resolve points, [1] refuted chunks, [2] serial chunks).
+qcsim_status qcsim_debug_chain_stats(uint32_t *out3) {
+    return guarded([&] {
+        CK(cudaDeviceSynchronize());
+        uint32_t v[8];
+        CK(cudaMemcpy(v, chain_stats(), sizeof v, cudaMemcpyDeviceToHost));
+        out3[0] = v[0];
+        out3[1] = v[1];
+        out3[2] = v[4];
+        CK(cudaMemset(chain_stats(), 0, sizeof v));
+    });
 }
 
 // Debug (not part of the public header): encoder intermediates for one plane.
