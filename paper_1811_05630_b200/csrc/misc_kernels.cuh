@@ -163,4 +163,102 @@ __global__ void __launch_bounds__(256) dense_gate(Src src, int units, uint64_t L
     if (tid == 0) tilesum[(uint64_t)unit * ntiles + t] = red[0];
 }
 
+// ------------------------------------------------ deferred engine bookkeeping
+// Gate passes that never wait for the host: the normalization scale and the
+// run metrics live on the device; errors are latched (first one wins) and
+// raised by the host when the run returns.
+enum : uint32_t { kEngOk = 0, kEngNumeric = 1, kEngDepth = 2, kEngOverflow = 3 };
+struct EngineDevStats {
+    double ratio_min, ratio_sum, norm_G;
+    unsigned long long calls, current, peak, fallback, status_gate;
+    uint32_t status, pad;
+};
+
+// G = pairwise tree over the S slice norms (the association of the host's
+// tree_sum_host / DESIGN.md §3.2), drift check, scale = 1/sqrt(G).
+__global__ void __launch_bounds__(256) engine_norm(const double *sq, double *b0, double *b1, uint64_t S, double tol10,
+                                                   unsigned long long gate, double *scale, EngineDevStats *st) {
+    const int tid = threadIdx.x;
+    for (uint64_t k = tid; k < S; k += 256) b0[k] = sq[k];
+    __syncthreads();
+    double *in = b0, *out = b1;
+    for (uint64_t w = S / 2; w >= 1; w /= 2) {
+        for (uint64_t k = tid; k < w; k += 256) out[k] = dadd(in[2 * k], in[2 * k + 1]);
+        __syncthreads();
+        double *t = in;
+        in = out;
+        out = t;
+    }
+    if (tid == 0) {
+        const double G = in[0];
+        if (!isfinite(G) || fabs(dsub(G, 1.0)) > tol10) {
+            if (st->status == kEngOk) {
+                st->status = kEngNumeric;
+                st->status_gate = gate;
+                st->norm_G = G;
+            }
+            *scale = 1.0;
+        } else {
+            *scale = ddiv(1.0, __dsqrt_rn(G));
+        }
+    }
+}
+
+// Per gate pass: compression ratio min / sum (plane order, as the host's
+// record_sizes), current and peak bytes, fallback planes, latched errors.
+__global__ void __launch_bounds__(256) engine_stats(const uint64_t *bytes, const uint32_t *err,
+                                                    const PlaneParams *params, const uint32_t *overflow, int planes,
+                                                    uint64_t L, unsigned long long gate, EngineDevStats *st) {
+    __shared__ double ratio[1024];
+    __shared__ unsigned long long tot_s, fb_s;
+    __shared__ uint32_t bad_s;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        tot_s = 0;
+        fb_s = 0;
+        bad_s = 0;
+    }
+    __syncthreads();
+    const double in_bytes = (double)(8 * L);
+    for (int base = 0; base < planes; base += 1024) {
+        const int m = min(1024, planes - base);
+        unsigned long long t = 0, f = 0;
+        for (int k = tid; k < m; k += 256) {
+            const uint64_t b = bytes[base + k];
+            ratio[k] = ddiv(in_bytes, (double)b);
+            t += b;
+            f += (params[base + k].flags & kFlagFallback) ? 1 : 0;
+            if (err[base + k] != 0) atomicExch(&bad_s, 1u);
+        }
+        atomicAdd(&tot_s, t);
+        atomicAdd(&fb_s, f);
+        __syncthreads();
+        if (tid == 0) { // plane order, in registers
+            double rmin = st->ratio_min, rsum = st->ratio_sum;
+            for (int k = 0; k < m; ++k) {
+                const double r = ratio[k];
+                if (r < rmin) rmin = r;
+                rsum = dadd(rsum, r);
+            }
+            st->ratio_min = rmin;
+            st->ratio_sum = rsum;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        st->calls += (unsigned long long)planes;
+        st->current = tot_s;
+        if (tot_s > st->peak) st->peak = tot_s;
+        st->fallback += fb_s;
+        if (st->status == kEngOk && bad_s) {
+            st->status = kEngDepth;
+            st->status_gate = gate;
+        }
+        if (st->status == kEngOk && *overflow) {
+            st->status = kEngOverflow;
+            st->status_gate = gate;
+        }
+    }
+}
+
 } // namespace qcb

@@ -361,7 +361,7 @@ void launch_pack(cudaStream_t st, EncScratch &S, DBuf<uint8_t> &arena, bool coun
 template <int NP, class Src>
 void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, uint64_t L,
                    const qcsim_codec_config &cfg, int log2C, IndexRec *index, DBuf<uint8_t> &arena,
-                   bool check_finite, bool sync_now);
+                   bool check_finite, bool sync_now, bool host_results = true);
 EncodeResult encode_finish(cudaStream_t st, EncScratch &S, DBuf<uint8_t> &arena);
 template <int NP, class Src>
 EncodeResult encode_batch(cudaStream_t st, EncScratch &S, const Src &src, int units, uint64_t L,
@@ -387,7 +387,7 @@ void launch_plane_scan(cudaStream_t st, const int32_t *in, int32_t *out, int nti
 template <int NP, class Src>
 void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, uint64_t L,
                    const qcsim_codec_config &cfg, int log2C, IndexRec *index, DBuf<uint8_t> &arena,
-                   bool check_finite, bool sync_now) {
+                   bool check_finite, bool sync_now, bool host_results) {
     const uint64_t planes = (uint64_t)units * NP;
     const int qb = cfg.quant_code_bits;
     S.ensure(planes, units, L, qb);
@@ -627,6 +627,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     S.planes = planes;
     CK(cudaMemsetAsync(S.overflow.p, 0, sizeof(uint32_t), st));
     launch_pack(st, S, arena);
+    if (!host_results) return; // deferred engine: engine_stats consumes them on the device
     // results for the host, one batch of async copies into pinned memory
     S.h_bytes.ensure(planes);
     S.h_off.ensure(planes);
@@ -859,6 +860,12 @@ struct qcsim_engine {
     ValScratch val;
     DBuf<uint8_t> imp_bytes;
     DBuf<uint64_t> imp_off;
+    // deferred gate loop (no host round trip per gate): device scale,
+    // device metrics, latched errors
+    bool deferred = false;
+    DBuf<double> norm_buf[2], dev_scale;
+    DBuf<EngineDevStats> dev_stats;
+    HBuf<EngineDevStats> h_stats;
     // metrics
     double ratio_min = INFINITY, ratio_sum = 0.0;
     uint64_t calls = 0, gates = 0, peak = 0, current = 0, fallback = 0;
@@ -938,6 +945,29 @@ template <class Src> void engine_store(qcsim_engine *e, const Src &src) {
     const int units = (int)e->ns;
     const int nxt = e->cur ^ 1;
     const uint64_t ntiles = (e->L + kTile - 1) / kTile;
+    if (e->deferred) { // no host round trip (qcsim_engine_run settles the books)
+        e->index[nxt].ensure(2 * e->ns * e->nidx);
+        e->dec[nxt].ensure(2 * e->ns, e->L, e->cfg.codec.quant_code_bits);
+        e->enc.dec_out = e->dec[nxt].tables();
+        encode_launch<2, Src>(e->st, e->enc, src, units, e->L, e->cfg.codec, e->log2C, e->index[nxt].p,
+                              e->arena[nxt], false, false, /*host_results=*/false);
+        e->enc.dec_out = DecTables{};
+        {
+            PROF("slice_norms", e->st);
+            slice_norms<<<(units + 127) / 128, 128, 0, e->st>>>(e->enc.tilesum.p, (int)ntiles, units, e->slice_sq.p);
+        }
+        {
+            PROF("engine_stats", e->st);
+            engine_stats<<<1, 256, 0, e->st>>>(e->enc.block_bytes.p, e->enc.err.p, e->enc.params.p, e->enc.overflow.p,
+                                               (int)(2 * e->ns), e->L, (unsigned long long)e->gates,
+                                               e->dev_stats.p);
+        }
+        e->blk_off[nxt].ensure(2 * e->ns);
+        CK(cudaMemcpyAsync(e->blk_off[nxt].p, e->enc.blk_off.p, 2 * e->ns * sizeof(uint64_t),
+                           cudaMemcpyDeviceToDevice, e->st));
+        e->cur = nxt;
+        return;
+    }
     if (e->compressed) {
         e->index[nxt].ensure(2 * e->ns * e->nidx);
         // the encoder also writes the decode tables of the blocks it packs
@@ -1076,7 +1106,12 @@ void engine_gate(qcsim_engine *e, const qcsim_action &a) {
     // deterministic tree over every slice's sq_norm
     const bool apply = e->cfg.norm_every > 0 && (e->gates % (uint64_t)e->cfg.norm_every) == 0;
     double scale = 1.0;
-    if (apply) {
+    if (apply && e->deferred) {
+        PROF("engine_norm", e->st);
+        engine_norm<<<1, 256, 0, e->st>>>(e->slice_sq.p, e->norm_buf[0].p, e->norm_buf[1].p, e->S,
+                                          10.0 * e->cfg.norm_drift_tolerance, (unsigned long long)e->gates,
+                                          e->dev_scale.p, e->dev_stats.p);
+    } else if (apply) {
         const double G = tree_sum_host(e->sq_norm.data(), e->S);
         if (!std::isfinite(G) || std::fabs(G - 1.0) > 10.0 * e->cfg.norm_drift_tolerance) {
             char buf[160];
@@ -1121,6 +1156,7 @@ void engine_gate(qcsim_engine *e, const qcsim_action &a) {
     g.slot_of = e->slot_of.p;
     g.unit_slice = e->unit_slice.p;
     g.scale = scale;
+    g.scale_dev = e->deferred ? e->dev_scale.p : nullptr;
     g.apply_scale = apply ? 1 : 0;
     g.act = to_dev(a);
     g.s = e->s;
@@ -1128,6 +1164,106 @@ void engine_gate(qcsim_engine *e, const qcsim_action &a) {
     engine_store(e, g);
     e->gates++;
     e->imported.clear();
+}
+
+// Worst-case arena bytes for one gate pass (every plane at qcsim_block_bound,
+// 16-byte slots): with arenas that large a pass cannot overflow, so the gate
+// loop needs no host round trip.
+uint64_t arena_worst(const qcsim_engine *e) {
+    const uint64_t L = e->L;
+    uint64_t nsym = (1ull << e->cfg.codec.quant_code_bits) + 1;
+    if (nsym > L + 1) nsym = L + 1;
+    const uint64_t bound = kHeaderBytes + 4 + 5 * nsym + (L * kMaxCodeLen + 7) / 8 + 16 + L * 16;
+    return 2 * e->ns * ((bound + 31) & ~15ull) + (1 << 20);
+}
+
+// Grows a buffer keeping its first `keep` bytes.
+void grow_keep(DBuf<uint8_t> &b, uint64_t want, uint64_t keep, cudaStream_t st) {
+    if (b.cap >= want) return;
+    DBuf<uint8_t> nb;
+    nb.ensure(want);
+    if (b.p && keep) CK(cudaMemcpyAsync(nb.p, b.p, keep, cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    b.swap(nb);
+}
+
+// Deferred gate loop: single rank, compressed, worst-case arenas within the
+// budget (QCSIM_SYNC_GATES=1 forces the per-gate host round trip).
+bool engine_defer_begin(qcsim_engine *e) {
+    static const bool forced_sync = std::getenv("QCSIM_SYNC_GATES") != nullptr;
+    constexpr uint64_t kBudget = 8ull << 30;
+    const uint64_t worst = arena_worst(e);
+    if (forced_sync || e->cfg.world > 1 || !e->compressed || 2 * worst > kBudget || !e->imported.empty()) return false;
+    CK(cudaStreamSynchronize(e->st));
+    uint64_t used = 0;
+    for (uint64_t k = 0; k < e->blk_bytes_h.size(); ++k) used = std::max(used, e->blk_bytes_h[k]);
+    {
+        // current arena: keep its contents (up to the highest slot end)
+        std::vector<uint64_t> off(2 * e->ns);
+        CK(cudaMemcpy(off.data(), e->blk_off[e->cur].p, off.size() * 8, cudaMemcpyDeviceToHost));
+        uint64_t hi = 0;
+        for (uint64_t k = 0; k < off.size(); ++k) hi = std::max(hi, off[k] + e->blk_bytes_h[k]);
+        grow_keep(e->arena[e->cur], worst, hi, e->st);
+        grow_keep(e->arena[e->cur ^ 1], worst, 0, e->st);
+    }
+    e->enc.ensure(2 * e->ns, e->ns, e->L, e->cfg.codec.quant_code_bits);
+    e->slice_sq.ensure(e->ns);
+    e->norm_buf[0].ensure(e->S);
+    e->norm_buf[1].ensure(e->S);
+    e->dev_scale.ensure(1);
+    e->dev_stats.ensure(1);
+    e->h_stats.ensure(1);
+    e->h_sq.ensure(e->ns);
+    // the host view is authoritative between runs
+    for (uint64_t k = 0; k < e->ns; ++k) e->h_sq.p[k] = e->sq_norm[e->s0 + k];
+    CK(cudaMemcpyAsync(e->slice_sq.p, e->h_sq.p, e->ns * sizeof(double), cudaMemcpyHostToDevice, e->st));
+    EngineDevStats &h = *e->h_stats.p;
+    std::memset(&h, 0, sizeof h);
+    h.ratio_min = e->ratio_min;
+    h.ratio_sum = e->ratio_sum;
+    h.calls = e->calls;
+    h.current = e->current;
+    h.peak = e->peak;
+    h.fallback = e->fallback;
+    CK(cudaMemcpyAsync(e->dev_stats.p, e->h_stats.p, sizeof h, cudaMemcpyHostToDevice, e->st));
+    CK(cudaStreamSynchronize(e->st));
+    e->deferred = true;
+    return true;
+}
+
+// Settles a deferred run: metrics, norms and block sizes back to the host,
+// latched errors raised.
+void engine_defer_end(qcsim_engine *e, bool raise_errors) {
+    e->deferred = false;
+    CK(cudaStreamSynchronize(e->st));
+    g_prof.flush();
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(e->h_stats.p, e->dev_stats.p, sizeof(EngineDevStats), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(e->h_sq.p, e->slice_sq.p, e->ns * sizeof(double), cudaMemcpyDeviceToHost));
+    const EngineDevStats h = *e->h_stats.p;
+    e->ratio_min = h.ratio_min;
+    e->ratio_sum = h.ratio_sum;
+    e->calls = h.calls;
+    e->current = h.current;
+    e->peak = h.peak;
+    e->fallback = h.fallback;
+    for (uint64_t k = 0; k < e->ns; ++k) e->sq_norm[e->s0 + k] = e->h_sq.p[k];
+    e->blk_bytes_h.resize(2 * e->ns);
+    CK(cudaMemcpy(e->blk_bytes_h.data(), e->enc.block_bytes.p, 2 * e->ns * 8, cudaMemcpyDeviceToHost));
+    if (!raise_errors) return;
+    if (h.status == kEngNumeric) {
+        // the gates queued after the failing one ran on an unnormalized
+        // state: the engine must be reloaded (the host-synchronous path keeps
+        // the failing gate's input instead)
+        e->gates = h.status_gate;
+        e->loaded = false;
+        char buf[160];
+        std::snprintf(buf, sizeof buf, "norm drift before gate %llu: global sq_norm %.17g",
+                      (unsigned long long)h.status_gate, h.norm_G);
+        raise(QCSIM_NUMERIC, buf);
+    }
+    if (h.status == kEngDepth) raise(QCSIM_CODEC, "prefix code depth out of range");
+    if (h.status == kEngOverflow) raise(QCSIM_NOMEM, "compressed arena overflow");
 }
 
 } // namespace
@@ -1488,13 +1624,20 @@ qcsim_status qcsim_engine_run(qcsim_engine *e, const qcsim_action *actions, uint
         if (!e->loaded) raise(QCSIM_INVALID_ARGUMENT, "engine has no state (load_basis / load_amplitudes first)");
         CK(cudaSetDevice(e->cfg.device));
         if (count) {
+            const bool deferred = engine_defer_begin(e);
             CK(cudaEventRecord(e->ev0, e->st));
-            for (uint64_t k = 0; k < count; ++k) engine_gate(e, actions[k]);
+            try {
+                for (uint64_t k = 0; k < count; ++k) engine_gate(e, actions[k]);
+            } catch (...) {
+                if (deferred) engine_defer_end(e, false);
+                throw;
+            }
             CK(cudaEventRecord(e->ev1, e->st));
             CK(cudaEventSynchronize(e->ev1));
             float ms = 0.f;
             CK(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
             e->wall += ms * 1e-3;
+            if (deferred) engine_defer_end(e, true);
         }
         if (m) {
             std::memset(m, 0, sizeof *m);

@@ -25,7 +25,8 @@ struct GateSrc {
     const double *old;          // dense old planes, [slot][re|im][L]
     const int32_t *slot_of;     // global slice -> slot in `old`
     const uint64_t *unit_slice; // unit -> global slice
-    double scale;               // 1/sqrt(G) (host-computed)
+    double scale;               // 1/sqrt(G) (host-computed) ...
+    const double *scale_dev;    // ... or device-computed (engine_norm) when set
     int apply_scale;            // 0: normalization skipped for this gate
     DevAction act;
     int s;
@@ -46,7 +47,7 @@ struct GateSrc {
     __device__ __forceinline__ void load(int unit, uint64_t i, double *v) const {
         const uint64_t g = (unit_slice[unit] << s) | i;
         const bool apply = apply_scale != 0;
-        const double sc = scale;
+        const double sc = scale_dev ? *scale_dev : scale;
         if (act.kind == 0) {
             double r, m;
             fetch(g, sc, apply, r, m);

@@ -1,4 +1,5 @@
-"""Short engine run for ncu captures: WORKLOAD setup + G gate passes."""
+"""Short engine run for ncu captures: WORKLOAD setup + SKIP untimed gate
+passes + G timed gate passes."""
 import os
 import sys
 
@@ -8,6 +9,7 @@ import paper_1811_05630_b200 as q  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "grover20"
 gates = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+skip = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 wl = bench.workload(name)
 eng = q.Engine(q.EngineConfig(num_qubits=wl["n"], slice_bits=wl["s"],
                               codec=q.CodecConfig(q.CodecMode.Absolute, wl["eb"])))
@@ -15,9 +17,12 @@ eng.load_basis(wl["basis"])
 eng.run(wl["setup"])
 acts = []
 k = 0
-while len(acts) < gates:
+while len(acts) < gates + skip:
     acts += wl["steps"](k)
     k += 1
-m = eng.run(acts[:gates])
-print(f"{name}: {gates} gates, device {m.wall_seconds*1e3:.2f} ms, min ratio {m.min_compression_ratio:.3f}, "
-      f"launches {q.kernel_launches()}")
+if skip:
+    eng.run(acts[:skip])
+m0 = eng.metrics().wall_seconds
+m = eng.run(acts[skip:skip + gates])
+print(f"{name}: {gates} gates after {skip}, device {(m.wall_seconds - m0)*1e3:.2f} ms, "
+      f"min ratio {m.min_compression_ratio:.3f}, launches {q.kernel_launches()}")
