@@ -132,13 +132,24 @@ __device__ __forceinline__ uint64_t peek64(const uint32_t *w, uint64_t bp) {
 }
 
 constexpr int kDecThreads = 128;             // chunks per block
-constexpr int kDecStageWords = 8192;         // 32 KB of stream staged per block
+constexpr int kDecStageWords = 4096;         // 16 KB of stream staged per block
+constexpr int kDecWin = 32;                  // output window per chunk (C is a multiple)
+struct DecSmem {
+    uint32_t lut[1 << kLutBits];
+    uint32_t sw[kDecStageWords + 4];
+    double sout[kDecThreads / 32][32][kDecWin + 1]; // per warp: 32 chunks x one window
+};
+constexpr size_t kDecSmem = sizeof(DecSmem);
 
 // One block per (plane, group of kDecThreads checkpoint chunks).  The
 // plane's 11-bit LUT and the group's stream bytes are staged in shared
 // memory; each thread then resumes from its IndexRec and reproduces
-// codec.cpp:591-626 for its chunk.
+// codec.cpp:591-626 for its chunk, kDecWin elements at a time: the warp
+// parks its 32 chunks' windows in shared memory and stores them row by row
+// (256-byte coalesced rows instead of 32 scattered 8-byte stores).
 __global__ void __launch_bounds__(kDecThreads) dec_chunks(DecPlanes D, DecTables T, int planes) {
+    extern __shared__ __align__(16) unsigned char dec_raw[];
+    DecSmem &S = *reinterpret_cast<DecSmem *>(dec_raw);
     const uint64_t nchunks = (D.L + (1ull << D.log2C) - 1) >> D.log2C;
     const uint32_t groups = (uint32_t)((nchunks + kDecThreads - 1) / kDecThreads);
     const int pl = (int)(blockIdx.x / groups);
@@ -147,8 +158,6 @@ __global__ void __launch_bounds__(kDecThreads) dec_chunks(DecPlanes D, DecTables
     const uint64_t j = j0 + threadIdx.x;
     const uint64_t jend = tmin<uint64_t>(j0 + kDecThreads, nchunks);
     const uint64_t nidx = (D.L >> D.log2C) + 1;
-    __shared__ uint32_t slut[1 << kLutBits];
-    __shared__ uint32_t sw[kDecStageWords + 4];
     const uint8_t *blk = D.arena + D.blk_off[pl];
     const uint8_t pred_kind = blk[6];
     const int qb = blk[7];
@@ -171,93 +180,120 @@ __global__ void __launch_bounds__(kDecThreads) dec_chunks(DecPlanes D, DecTables
     const uint32_t *sorted = T.sorted + (uint64_t)pl * T.cap;
     const IndexRec *idx = D.index + (uint64_t)pl * nidx;
 
-    for (int k = threadIdx.x; k < (1 << kLutBits); k += kDecThreads) slut[k] = glut[k];
+    {
+        const uint4 *g4 = reinterpret_cast<const uint4 *>(glut);
+        uint4 *s4 = reinterpret_cast<uint4 *>(S.lut);
+#pragma unroll
+        for (int k = threadIdx.x; k < (1 << kLutBits) / 4; k += kDecThreads) s4[k] = g4[k];
+    }
     // stream words this group reads: [bitpos(j0), bitpos(jend)) + lookahead
     const uint64_t w_lo = idx[j0].bitpos >> 5;
     const uint64_t bit_hi = jend < nchunks ? idx[jend].bitpos : sbytes * 8;
     const uint64_t w_hi = (bit_hi >> 5) + 3;
     const bool staged = w_hi - w_lo <= (uint64_t)kDecStageWords;
     if (staged)
-        for (uint64_t w = w_lo + threadIdx.x; w < w_hi; w += kDecThreads) sw[w - w_lo] = __ldg(stream + w);
+        for (uint64_t w = w_lo + threadIdx.x; w < w_hi; w += kDecThreads) S.sw[w - w_lo] = __ldg(stream + w);
     __syncthreads();
-    if (j >= jend) return;
 
-    const IndexRec r = idx[j];
+    const bool active = j < jend;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint64_t C = 1ull << D.log2C;
+    IndexRec r{};
+    if (active) r = idx[j];
     uint64_t bp = r.bitpos;
     uint32_t run_left = r.run_left;
     uint32_t last = r.last_lit;
     uint64_t ocur = r.ocur;
     double d1 = r.dprev, d2 = r.dprev2;
     const uint64_t e0 = j << D.log2C;
-    const uint64_t e1 = tmin<uint64_t>(e0 + (1ull << D.log2C), D.L);
+    const uint64_t e1 = active ? tmin<uint64_t>(e0 + C, D.L) : e0;
     double *out = D.out[pl];
     const uint64_t sbase = staged ? w_lo * 32 : 0;
+    const uint64_t jw = j0 + (uint64_t)wid * 32; // first chunk of this warp
+    double *row = S.sout[wid][lane];
 
     uint64_t i = e0;
-    auto emit = [&](uint32_t s) {
-        double v;
-        if (s == kOutlierSym) {
-            v = __longlong_as_double((long long)load_le(orec + 16 * ocur + 8, 8));
-            ++ocur;
-        } else {
-            double pred;
-            if (pred_kind == 0) pred = i > 0 ? d1 : 0.0;
-            else pred = i == 0 ? 0.0 : (i == 1 ? d1 : predict_linear(d1, d2));
-            const long long m = (long long)s - half;
-            v = eb == 0.0 ? pred : dadd(pred, dmul(q, (double)m));
-        }
-        out[i] = v;
-        d2 = d1;
-        d1 = v;
-        ++i;
-    };
-    while (i < e1) {
-        if (run_left > 0) {
-            // a run of a zero code with the previous-value predictor is a
-            // constant fill (d + 0.0 == d except -0.0, which emit() keeps)
-            if (pred_kind == 0 && last == (uint32_t)half && eb != 0.0 && bits_of(d1) != 0x8000000000000000ull &&
-                i > 0) {
-                const uint64_t stop = tmin<uint64_t>(e1, i + run_left);
-                const double v = d1;
-                run_left -= (uint32_t)(stop - i);
-                for (; i < stop; ++i) out[i] = v;
-                d2 = v;
+    bool dead = !active;
+    for (uint64_t w0 = 0; w0 < C; w0 += kDecWin) {
+        const uint64_t wb = e0 + w0;
+        const uint64_t wend = tmin<uint64_t>(wb + kDecWin, e1);
+        auto emit = [&](uint32_t s) {
+            double v;
+            if (s == kOutlierSym) {
+                v = __longlong_as_double((long long)load_le(orec + 16 * ocur + 8, 8));
+                ++ocur;
+            } else {
+                double pred;
+                if (pred_kind == 0) pred = i > 0 ? d1 : 0.0;
+                else pred = i == 0 ? 0.0 : (i == 1 ? d1 : predict_linear(d1, d2));
+                const long long m = (long long)s - half;
+                v = eb == 0.0 ? pred : dadd(pred, dmul(q, (double)m));
+            }
+            row[i - wb] = v;
+            d2 = d1;
+            d1 = v;
+            ++i;
+        };
+        while (!dead && i < wend) {
+            if (run_left > 0) {
+                // a run of a zero code with the previous-value predictor is a
+                // constant fill (d + 0.0 == d except -0.0, which emit() keeps)
+                if (pred_kind == 0 && last == (uint32_t)half && eb != 0.0 &&
+                    bits_of(d1) != 0x8000000000000000ull && i > 0) {
+                    const uint64_t stop = tmin<uint64_t>(wend, i + run_left);
+                    const double v = d1;
+                    run_left -= (uint32_t)(stop - i);
+                    for (; i < stop; ++i) row[i - wb] = v;
+                    d2 = v;
+                    continue;
+                }
+                emit(last);
+                --run_left;
                 continue;
             }
-            emit(last);
-            --run_left;
-            continue;
-        }
-        const uint64_t w = staged ? peek64<true>(sw, bp - sbase) : peek64<false>(stream, bp);
-        const uint32_t le = slut[w >> (64 - kLutBits)];
-        uint32_t s, l;
-        if (le & 63) {
-            l = le & 63;
-            s = le >> 6;
-        } else {
-            s = 0;
-            l = 0;
-            for (uint32_t ll = kLutBits + 1; ll <= maxlen; ++ll) {
-                if (!count[ll]) continue;
-                const uint64_t c = w >> (64 - ll);
-                if (c >= first[ll] && c - first[ll] < count[ll]) {
-                    s = sorted[basei[ll] + (uint32_t)(c - first[ll])];
-                    l = ll;
+            const uint64_t w = staged ? peek64<true>(S.sw, bp - sbase) : peek64<false>(stream, bp);
+            const uint32_t le = S.lut[w >> (64 - kLutBits)];
+            uint32_t s, l;
+            if (le & 63) {
+                l = le & 63;
+                s = le >> 6;
+            } else {
+                s = 0;
+                l = 0;
+                for (uint32_t ll = kLutBits + 1; ll <= maxlen; ++ll) {
+                    if (!count[ll]) continue;
+                    const uint64_t c = w >> (64 - ll);
+                    if (c >= first[ll] && c - first[ll] < count[ll]) {
+                        s = sorted[basei[ll] + (uint32_t)(c - first[ll])];
+                        l = ll;
+                        break;
+                    }
+                }
+                if (l == 0) { // corrupt (never for encoder-produced blocks)
+                    dead = true;
                     break;
                 }
             }
-            if (l == 0) return; // corrupt (never for encoder-produced blocks)
+            bp += l;
+            if (s == rsym) {
+                const uint64_t g = staged ? peek64<true>(S.sw, bp - sbase) : peek64<false>(stream, bp);
+                const int z = __clzll((long long)g);
+                run_left = (uint32_t)(g >> (64 - (2 * z + 1)));
+                bp += 2 * z + 1;
+            } else {
+                emit(s);
+                last = s;
+            }
         }
-        bp += l;
-        if (s == rsym) {
-            const uint64_t g = staged ? peek64<true>(sw, bp - sbase) : peek64<false>(stream, bp);
-            const int z = __clzll((long long)g);
-            run_left = (uint32_t)(g >> (64 - (2 * z + 1)));
-            bp += 2 * z + 1;
-        } else {
-            emit(s);
-            last = s;
+        __syncwarp();
+        // the warp's 32 chunk windows, one coalesced row per chunk
+        for (int rr = 0; rr < 32; ++rr) {
+            const uint64_t jr = jw + rr;
+            if (jr >= jend) break;
+            const uint64_t e = (jr << D.log2C) + w0 + lane;
+            if (w0 + lane < C && e < D.L) out[e] = S.sout[wid][rr][lane];
         }
+        __syncwarp();
     }
 }
 

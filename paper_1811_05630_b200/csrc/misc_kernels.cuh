@@ -3,6 +3,7 @@
 
 #include <cfloat>
 
+#include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
 #include "common.cuh"
@@ -209,48 +210,48 @@ __global__ void __launch_bounds__(256) engine_norm(const double *sq, double *b0,
 __global__ void __launch_bounds__(256) engine_stats(const uint64_t *bytes, const uint32_t *err,
                                                     const PlaneParams *params, const uint32_t *overflow, int planes,
                                                     uint64_t L, unsigned long long gate, EngineDevStats *st) {
+    using Red = cub::BlockReduce<unsigned long long, 256>;
+    __shared__ typename Red::TempStorage red;
     __shared__ double ratio[1024];
-    __shared__ unsigned long long tot_s, fb_s;
-    __shared__ uint32_t bad_s;
     const int tid = threadIdx.x;
-    if (tid == 0) {
-        tot_s = 0;
-        fb_s = 0;
-        bad_s = 0;
-    }
-    __syncthreads();
     const double in_bytes = (double)(8 * L);
+    unsigned long long tot = 0, fb = 0;
+    int bad = 0;
+    double rmin = 0.0, rsum = 0.0;
+    if (tid == 0) {
+        rmin = st->ratio_min;
+        rsum = st->ratio_sum;
+    }
     for (int base = 0; base < planes; base += 1024) {
         const int m = min(1024, planes - base);
-        unsigned long long t = 0, f = 0;
         for (int k = tid; k < m; k += 256) {
             const uint64_t b = bytes[base + k];
             ratio[k] = ddiv(in_bytes, (double)b);
-            t += b;
-            f += (params[base + k].flags & kFlagFallback) ? 1 : 0;
-            if (err[base + k] != 0) atomicExch(&bad_s, 1u);
+            tot += b;
+            fb += (params[base + k].flags & kFlagFallback) ? 1 : 0;
+            bad |= err[base + k] != 0;
         }
-        atomicAdd(&tot_s, t);
-        atomicAdd(&fb_s, f);
         __syncthreads();
-        if (tid == 0) { // plane order, in registers
-            double rmin = st->ratio_min, rsum = st->ratio_sum;
+        if (tid == 0) // plane order, in registers
             for (int k = 0; k < m; ++k) {
                 const double r = ratio[k];
                 if (r < rmin) rmin = r;
                 rsum = dadd(rsum, r);
             }
-            st->ratio_min = rmin;
-            st->ratio_sum = rsum;
-        }
         __syncthreads();
     }
+    tot = Red(red).Sum(tot);
+    __syncthreads();
+    fb = Red(red).Sum(fb);
+    bad = __syncthreads_or(bad);
     if (tid == 0) {
+        st->ratio_min = rmin;
+        st->ratio_sum = rsum;
         st->calls += (unsigned long long)planes;
-        st->current = tot_s;
-        if (tot_s > st->peak) st->peak = tot_s;
-        st->fallback += fb_s;
-        if (st->status == kEngOk && bad_s) {
+        st->current = tot;
+        if (tot > st->peak) st->peak = tot;
+        st->fallback += fb;
+        if (st->status == kEngOk && bad) {
             st->status = kEngDepth;
             st->status_gate = gate;
         }
@@ -260,5 +261,4 @@ __global__ void __launch_bounds__(256) engine_stats(const uint64_t *bytes, const
         }
     }
 }
-
 } // namespace qcb

@@ -77,7 +77,6 @@ constexpr uint32_t kSmallN = 1024; // alphabets up to this size stay in shared m
 __device__ void emit_dec_tables(const DecTables &T, int pl, uint32_t n, const uint32_t *sym, const uint8_t *len,
                                 const uint64_t *code, const uint32_t *lcount, const uint64_t *lfirst0) {
     uint32_t *lut = T.lut + (uint64_t)pl * (1u << kLutBits);
-    for (int k = threadIdx.x; k < (1 << kLutBits); k += blockDim.x) lut[k] = 0;
     __shared__ uint32_t basei[kMaxCodeLen + 2];
     if (threadIdx.x == 0) {
         uint32_t b = 0, maxlen = 0;
@@ -101,12 +100,22 @@ __device__ void emit_dec_tables(const DecTables &T, int pl, uint32_t n, const ui
         const int l = len[r];
         // (len, sym) order: position within the length = code - first code
         sorted[basei[l] + (uint32_t)(code[r] - lfirst0[l])] = sym[r];
-        if (l <= kLutBits) {
-            const uint32_t lo = (uint32_t)(code[r] << (kLutBits - l));
-            const uint32_t hi = (uint32_t)((code[r] + 1) << (kLutBits - l));
-            const uint32_t e = (sym[r] << 6) | (uint32_t)l;
-            for (uint32_t k = lo; k < hi; ++k) lut[k] = e;
+    }
+    __syncthreads();
+    // short codes -> LUT: every entry decodes its own kLutBits-bit window
+    // (canonical first/count per length), one store per entry
+    for (uint32_t k = threadIdx.x; k < (1u << kLutBits); k += blockDim.x) {
+        uint32_t e = 0;
+        for (int l = 1; l <= kLutBits; ++l) {
+            const uint32_t c = lcount[l];
+            if (!c) continue;
+            const uint64_t w = (uint64_t)(k >> (kLutBits - l));
+            if (w >= lfirst0[l] && w - lfirst0[l] < c) {
+                e = (sorted[basei[l] + (uint32_t)(w - lfirst0[l])] << 6) | (uint32_t)l;
+                break;
+            }
         }
+        lut[k] = e;
     }
 }
 

@@ -719,8 +719,13 @@ void decode_batch(cudaStream_t st, DecScratch &S, const uint8_t *arena, const ui
     const uint64_t nchunks = (L + (1ull << log2C) - 1) >> log2C;
     const uint64_t groups = (nchunks + kDecThreads - 1) / kDecThreads;
     {
+        static bool attr = false;
+        if (!attr) {
+            set_smem(dec_chunks, kDecSmem);
+            attr = true;
+        }
         PROF("dec_chunks", st);
-        dec_chunks<<<(unsigned)(groups * planes), kDecThreads, 0, st>>>(D, T, planes);
+        dec_chunks<<<(unsigned)(groups * planes), kDecThreads, kDecSmem, st>>>(D, T, planes);
     }
 }
 
