@@ -105,6 +105,50 @@ __device__ int32_t tile_carry(const int32_t *a, int t, int ntiles, int kind) {
     return r;
 }
 
+// Two exclusive carries of tile t in one warp pass and one barrier pair.
+__device__ __forceinline__ int32_t carry_reduce(int kind, int32_t v, int32_t x) {
+    return kind == kScanMaxExcl ? max(v, x) : (kind == kScanSumExcl ? v + x : min(v, x));
+}
+__device__ __forceinline__ int32_t carry_init(int kind) {
+    return kind == kScanMaxExcl ? -1 : (kind == kScanSumExcl ? 0 : 0x7FFFFFFF);
+}
+__device__ void tile_carry2(const int32_t *a1, int k1, const int32_t *a2, int k2, int t, int ntiles, int32_t &r1,
+                            int32_t &r2) {
+    __shared__ int32_t s_res2[2];
+    if (threadIdx.x < 32) {
+        int32_t v1 = carry_init(k1), v2 = carry_init(k2);
+        const int lo1 = k1 == kScanMinExclRev ? t + 1 : 0, hi1 = k1 == kScanMinExclRev ? ntiles : t;
+        const int lo2 = k2 == kScanMinExclRev ? t + 1 : 0, hi2 = k2 == kScanMinExclRev ? ntiles : t;
+        for (int k = (int)threadIdx.x; k < ntiles; k += 32) {
+            if (k >= lo1 && k < hi1) v1 = carry_reduce(k1, v1, a1[k]);
+            if (k >= lo2 && k < hi2) v2 = carry_reduce(k2, v2, a2[k]);
+        }
+        for (int off = 16; off >= 1; off >>= 1) {
+            v1 = carry_reduce(k1, v1, __shfl_xor_sync(0xffffffffu, v1, off));
+            v2 = carry_reduce(k2, v2, __shfl_xor_sync(0xffffffffu, v2, off));
+        }
+        if (threadIdx.x == 0) {
+            s_res2[0] = v1;
+            s_res2[1] = v2;
+        }
+    }
+    __syncthreads();
+    r1 = s_res2[0];
+    r2 = s_res2[1];
+    __syncthreads();
+}
+// carry_of for two arrays of the same plane / tile at once
+__device__ __forceinline__ void carry_of2(const int32_t *sc1, int st1, const int32_t *raw1, int k1, const int32_t *sc2,
+                                          int st2, const int32_t *raw2, int k2, int pl, int t, int ntiles,
+                                          int32_t &r1, int32_t &r2) {
+    if (ntiles > kInlineTiles) {
+        r1 = sc1[(uint64_t)pl * st1 + t];
+        r2 = sc2[(uint64_t)pl * st2 + t];
+        return;
+    }
+    tile_carry2(raw1 + (uint64_t)pl * ntiles, k1, raw2 + (uint64_t)pl * ntiles, k2, t, ntiles, r1, r2);
+}
+
 // The scanned value for tile t: from the plane_scan output when the plane
 // has many tiles, else computed inline from the raw per-tile array.
 __device__ __forceinline__ int32_t carry_of(const int32_t *scanned, int scanned_stride, const int32_t *raw, int pl,
@@ -689,13 +733,21 @@ __device__ __forceinline__ void element_runs(const TokArgs &A, const uint32_t *s
                                              uint64_t *start, uint64_t *end) {
     const int tid = threadIdx.x;
     int isb[kPerThread], st[kPerThread];
+    uint32_t sv[kPerThread + 1];
+    for (int e = 0; e < kPerThread; ++e) { // loads in flight across the carry pass
+        const int k = tid * kPerThread + e;
+        sv[e + 1] = k < tl ? sym[t0 + k] : 0u;
+    }
+    sv[0] = (t0 + tid * kPerThread > 0 && tid * kPerThread < tl) ? sym[t0 + tid * kPerThread - 1] : 0u;
+    int32_t prevb, nextb_carry;
+    carry_of2(A.t_prevb, A.ntiles, A.t_lastb, kScanMaxExcl, A.t_nextb, A.ntiles, A.t_firstb, kScanMinExclRev, pl, t,
+              A.ntiles, prevb, nextb_carry);
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
         const uint64_t i = t0 + k;
-        isb[e] = (k < tl && (i == 0 || sym[i] != sym[i - 1])) ? (int)k : -1;
+        isb[e] = (k < tl && (i == 0 || sv[e + 1] != sv[e])) ? (int)k : -1;
     }
     ScanI(tmp).InclusiveScan(isb, st, cub::Max());
-    const int32_t prevb = carry_of(A.t_prevb, A.ntiles, A.t_lastb, pl, t, A.ntiles, kScanMaxExcl);
     // first run start after each element: next boundary in the tile, else
     // the scanned carry from later tiles, else L
     for (int e = 0; e < kPerThread; ++e) {
@@ -707,21 +759,25 @@ __device__ __forceinline__ void element_runs(const TokArgs &A, const uint32_t *s
     // (small serial-free pass: each thread scans forward within its items,
     // then a block-wide reverse scan over thread minima)
     __shared__ int tmin_s[kEncThreads];
+    __shared__ int wmin_s[kEncThreads / 32];
     int m = 0x7FFFFFFF;
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
         if (k < tl && isb[e] >= 0) m = min(m, k);
     }
+    // reverse inclusive min-scan over threads: within the warp by shuffles,
+    // across warps through one shared-memory pass
+    const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_down_sync(0xffffffffu, m, off);
+        if (lane + off < 32) m = min(m, o);
+    }
+    if (lane == 0) wmin_s[wid] = m;
+    __syncthreads();
+    for (int w = wid + 1; w < kEncThreads / 32; ++w) m = min(m, wmin_s[w]);
     tmin_s[tid] = m;
     __syncthreads();
-    // reverse inclusive min-scan over threads (Hillis-Steele)
-    for (int off = 1; off < kEncThreads; off <<= 1) {
-        const int v = tid + off < kEncThreads ? tmin_s[tid + off] : 0x7FFFFFFF;
-        __syncthreads();
-        tmin_s[tid] = min(tmin_s[tid], v);
-        __syncthreads();
-    }
-    const int32_t nextb_carry = carry_of(A.t_nextb, A.ntiles, A.t_firstb, pl, t, A.ntiles, kScanMinExclRev);
     const uint64_t after = nextb_carry == 0x7FFFFFFF ? A.L : (uint64_t)nextb_carry;
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
@@ -750,21 +806,25 @@ __global__ void __launch_bounds__(kEncThreads) tok_count(TokArgs A, int planes) 
     __shared__ typename ScanI::TempStorage tmp;
     __shared__ typename RedI::TempStorage rtmp;
     __shared__ int s_next[kTile];
-    __shared__ uint32_t hist[kWin];
+    __shared__ __align__(16) uint32_t hist[kWin];
+    __shared__ uint16_t touched[kTile + 1]; // window bins this tile hit (first-touch list)
+    __shared__ uint32_t ntouched;
     __shared__ uint32_t h0, hrun, smin, smax;
     __shared__ unsigned long long gbits;
     const long long half = 1ll << (A.qb - 1);
     const uint32_t rsym = 1u << A.qb;
     const uint32_t wlo = (uint32_t)(half - kWin / 2);
     uint32_t *ghist = A.hist + (uint64_t)pl * ((uint64_t)rsym + 1);
-    for (int k = tid; k < kWin; k += kEncThreads) hist[k] = 0;
-    if (tid == 0) { h0 = 0; hrun = 0; smin = 0xFFFFFFFFu; smax = 0; gbits = 0; }
+    for (int k = tid; k < kWin / 4; k += kEncThreads) reinterpret_cast<uint4 *>(hist)[k] = make_uint4(0, 0, 0, 0);
+    if (tid == 0) { h0 = 0; hrun = 0; smin = 0xFFFFFFFFu; smax = 0; gbits = 0; ntouched = 0; }
     uint64_t start[kPerThread], end[kPerThread];
     element_runs<ScanI>(A, sym, pl, t, t0, tl, tmp, s_next, start, end);
     auto count = [&](uint32_t s, uint32_t n) {
         if (s == kOutlierSym) atomicAdd(&h0, n);
         else if (s == rsym) atomicAdd(&hrun, n);
-        else if (s - wlo < (uint32_t)kWin) atomicAdd(&hist[s - wlo], n);
+        else if (s - wlo < (uint32_t)kWin) {
+            if (atomicAdd(&hist[s - wlo], n) == 0) touched[atomicAdd(&ntouched, 1u)] = (uint16_t)(s - wlo);
+        }
         else {
             atomicAdd(&ghist[s], n);
             atomicMin(&smin, s);
@@ -799,10 +859,11 @@ __global__ void __launch_bounds__(kEncThreads) tok_count(TokArgs A, int planes) 
         if (hrun) atomicAdd(&A.hspecial[2 * pl + 1], hrun);
         if (gbits) atomicAdd(&A.gamma_bits[pl], gbits);
     }
-    for (int k = tid; k < kWin; k += kEncThreads) {
+    for (uint32_t m = tid; m < ntouched; m += kEncThreads) {
+        const uint32_t k = touched[m];
         const uint32_t v = hist[k];
         const uint32_t sy = wlo + k;
-        if (v && sy != kOutlierSym && sy < rsym) {
+        if (sy != kOutlierSym && sy < rsym) {
             atomicAdd(&ghist[sy], v);
             atomicMin(&smin, sy);
             atomicMax(&smax, sy);
@@ -852,8 +913,10 @@ __global__ void __launch_bounds__(kEncThreads) tok_emit(TokArgs A, int planes) {
     ScanI(tmp).ExclusiveSum(cnt, tpos);
     __syncthreads();
     ScanI(tmp).ExclusiveSum(isout, opos);
-    const uint32_t tokbase = (uint32_t)carry_of(A.t_tokoff, A.ntiles + 1, A.t_ntok, pl, t, A.ntiles, kScanSumExcl);
-    const uint32_t obase = (uint32_t)carry_of(A.t_ooff, A.ntiles + 1, A.t_nout, pl, t, A.ntiles, kScanSumExcl);
+    int32_t tokbase_i, obase_i;
+    carry_of2(A.t_tokoff, A.ntiles + 1, A.t_ntok, kScanSumExcl, A.t_ooff, A.ntiles + 1, A.t_nout, kScanSumExcl, pl, t,
+              A.ntiles, tokbase_i, obase_i);
+    const uint32_t tokbase = (uint32_t)tokbase_i, obase = (uint32_t)obase_i;
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
         if (k >= tl) continue;
