@@ -145,18 +145,18 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
     const uint64_t cap = B.cap;
     const uint32_t h0 = B.hspecial[2 * pl], hrun = B.hspecial[2 * pl + 1];
     const uint32_t smin = B.symrange[2 * pl], smax = B.symrange[2 * pl + 1];
-    // alphabet size first (decides smem vs global working arrays)
-    __shared__ uint32_t s_cnt_total;
-    if (tid == 0) s_cnt_total = (h0 ? 1u : 0u) + (hrun ? 1u : 0u);
-    __syncthreads();
-    if (smin <= smax) {
-        uint32_t c = 0;
-        for (uint64_t s = smin + tid; s <= smax; s += 256) c += hist[s] != 0;
-        atomicAdd(&s_cnt_total, c);
-    }
+    // alphabet size first (decides smem vs global working arrays): every
+    // thread owns a contiguous slice of the symbol range, counts its nonzero
+    // bins, and one block scan places each slice in the ascending list
+    const uint64_t R = smin <= smax ? (uint64_t)smax - smin + 1 : 0;
+    const uint64_t per = (R + 255) / 256;
+    const uint64_t b0 = (uint64_t)smin + tid * per, b1 = tmin<uint64_t>(b0 + per, (uint64_t)smin + R);
+    int mine = 0;
+    for (uint64_t s2 = b0; s2 < b1; ++s2) mine += hist[s2] != 0;
+    int pos_r = 0, tot_r = 0;
+    Scan(scan_tmp).ExclusiveSum(mine, pos_r, tot_r);
     if (tid < kMaxCodeLen + 2) lcount[tid] = 0;
-    __syncthreads();
-    const uint32_t n = s_cnt_total;
+    const uint32_t n = (h0 ? 1u : 0u) + (uint32_t)tot_r + (hrun ? 1u : 0u);
     const bool small = n <= kSmallN;
     uint32_t *sym = small ? sym_s : B.sym + pl * cap;
     uint32_t *cnt = small ? cnt_s : reinterpret_cast<uint32_t *>(B.cnt + pl * cap);
@@ -167,33 +167,28 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
     int32_t *par = small ? par_s : B.parent + pl * cap * 2;
 
     if (tid == 0) {
-        s_n = 0;
+        s_n = (h0 ? 1u : 0u) + (uint32_t)tot_r;
         s_bits = 0;
         s_err = 0;
         if (h0) {
             sym[0] = kOutlierSym;
             cnt[0] = h0;
-            s_n = 1;
+        }
+    }
+    // 1) compaction of the symbol range, ascending (freq, codec.cpp:484-488)
+    {
+        uint32_t o = (h0 ? 1u : 0u) + (uint32_t)pos_r;
+        for (uint64_t s2 = b0; s2 < b1; ++s2) {
+            const uint32_t v = hist[s2];
+            if (v) {
+                sym[o] = (uint32_t)s2;
+                cnt[o] = v;
+                ++o;
+                hist[s2] = 0; // restore the zero invariant
+            }
         }
     }
     __syncthreads();
-    // 1) compaction of the symbol range, ascending (freq, codec.cpp:484-488)
-    if (smin <= smax) {
-        for (uint64_t c0 = smin; c0 <= smax; c0 += 256) {
-            const uint64_t s = c0 + tid;
-            const uint32_t v = s <= smax ? hist[s] : 0u;
-            int f = v ? 1 : 0, pos, tot;
-            Scan(scan_tmp).ExclusiveSum(f, pos, tot);
-            if (v) {
-                sym[s_n + pos] = (uint32_t)s;
-                cnt[s_n + pos] = v;
-                hist[s] = 0; // restore the zero invariant
-            }
-            __syncthreads();
-            if (tid == 0) s_n += tot;
-            __syncthreads();
-        }
-    }
     if (tid == 0 && hrun) {
         sym[s_n] = rsym;
         cnt[s_n] = hrun;
@@ -268,7 +263,6 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
             prev = l;
         }
         for (int l = 0; l <= kMaxCodeLen; ++l) lfirst0[l] = lfirst[l];
-        for (uint32_t r = 0; r < n; ++r) code[r] = lfirst[len[r]]++;
         const uint64_t bits = s_bits + B.gamma_bits[pl];
         const uint64_t payload = 4 + 5ull * n + (bits + 7) / 8 + 16ull * B.ocount[pl];
         const uint64_t bytes = kHeaderBytes + payload;
@@ -277,6 +271,21 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
         B.block_bytes[pl] = bytes;
         B.slot_bytes[pl] = 16 + ((bytes + 15) & ~15ull);
         B.err[pl] = s_err;
+    }
+    __syncthreads();
+    // canonical codes in symbol order, one warp: a symbol's code is its
+    // length's next free code plus its rank among equal lengths in the group
+    if (tid < 32) {
+        for (uint32_t g0 = 0; g0 < n; g0 += 32) {
+            const uint32_t r = g0 + tid;
+            const int l = r < n ? len[r] : 0;
+            const unsigned peers = __match_any_sync(0xffffffffu, l);
+            const uint32_t rank = __popc(peers & ((1u << tid) - 1));
+            if (r < n) code[r] = lfirst[l] + rank;
+            __syncwarp();
+            if (r < n && rank == 0) lfirst[l] += __popc(peers);
+            __syncwarp();
+        }
     }
     __syncthreads();
     if (small) { // publish the codebook for the packer
@@ -563,6 +572,15 @@ __global__ void __launch_bounds__(256) pack_write(PackArgs A, int planes, int nc
         else gw[w0 + w] = v;
     }
     // decode-index bit positions for checkpoints resuming in this chunk
+    const bool last_chunk = c == (int)nchk - 1;
+    if (nchunks_idx <= 16u * 256u) { // few records: every thread filters its share in parallel
+        for (uint32_t j = 1 + tid; j < nchunks_idx; j += 256) {
+            const uint32_t tk = idx[j].tok;
+            if (tk >= t0 && (last_chunk || tk < t0 + tn))
+                idx[j].bitpos = tk >= t0 + tn ? base_bit + tot : base_bit + toff[tk - t0];
+        }
+        return;
+    }
     if (tid == 0) {
         uint32_t lo = 1, hi = nchunks_idx;
         while (lo < hi) {
@@ -571,7 +589,6 @@ __global__ void __launch_bounds__(256) pack_write(PackArgs A, int planes, int nc
             else hi = mid;
         }
         s_jlo = lo;
-        const bool last_chunk = c == (int)nchk - 1;
         hi = nchunks_idx;
         uint32_t lo2 = lo;
         while (lo2 < hi) {
