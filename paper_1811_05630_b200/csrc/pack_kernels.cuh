@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
     __shared__ int32_t par_s[2 * kSmallN];
     __shared__ uint8_t len_s[kSmallN];
     __shared__ uint64_t code_s[kSmallN];
-    __shared__ uint32_t s_n;
+    __shared__ uint32_t s_n, s_nodes;
     __shared__ uint32_t lcount[kMaxCodeLen + 2];
     __shared__ uint64_t lfirst[kMaxCodeLen + 2], lfirst0[kMaxCodeLen + 2];
     __shared__ unsigned long long s_bits;
@@ -212,23 +212,80 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
                 nc[i] = (uint32_t)(keys[i] >> 25);
                 par[i] = -1;
             }
+            // queue heads live in registers; internal nodes are appended in
+            // non-decreasing order, so the internal head is re-read only
+            // when it advances
             uint32_t lp = 0, ip = n, nodes = n;
+            uint32_t lv = nc[0], iv = 0;
             while ((n - lp) + (nodes - ip) >= 2) {
-                uint32_t pick[2];
+                uint32_t pick[2], pv[2];
                 for (int k = 0; k < 2; ++k) {
                     const bool leaf_ok = lp < n, int_ok = ip < nodes;
-                    const bool take_leaf = leaf_ok && (!int_ok || nc[lp] <= nc[ip]);
-                    pick[k] = take_leaf ? lp++ : ip++;
+                    const bool take_leaf = leaf_ok && (!int_ok || lv <= iv);
+                    if (take_leaf) {
+                        pick[k] = lp;
+                        pv[k] = lv;
+                        ++lp;
+                        lv = lp < n ? nc[lp] : 0u;
+                    } else {
+                        pick[k] = ip;
+                        pv[k] = iv;
+                        ++ip;
+                        iv = ip < nodes ? nc[ip] : 0u;
+                    }
                 }
-                nc[nodes] = nc[pick[0]] + nc[pick[1]];
-                par[nodes] = -1;
+                const uint32_t sum = pv[0] + pv[1];
+                nc[nodes] = sum;
                 par[pick[0]] = (int32_t)nodes;
                 par[pick[1]] = (int32_t)nodes;
+                if (ip == nodes) iv = sum; // the internal queue was empty
                 ++nodes;
             }
-            // depths top-down (parents have larger indices); stored in nc
-            nc[nodes - 1] = 0;
-            for (int64_t v = (int64_t)nodes - 2; v >= 0; --v) nc[v] = nc[par[v]] + 1;
+            par[nodes - 1] = -1;
+            s_nodes = nodes;
+            if (!small) { // large alphabet: depths top-down, serially
+                nc[nodes - 1] = 0;
+                for (int64_t v = (int64_t)nodes - 2; v >= 0; --v) nc[v] = nc[par[v]] + 1;
+            }
+        }
+    }
+    __syncthreads();
+    // depths by pointer jumping (parents have larger indices; root -> 0),
+    // stored in nc
+    if (n > 1 && small) {
+        const uint32_t nodes = s_nodes;
+        for (uint32_t v = tid; v < nodes; v += 256) {
+            nc[v] = par[v] < 0 ? 0u : 1u; // distance to the current ancestor
+        }
+        __syncthreads();
+        for (int round = 0; round < 32; ++round) {
+            int changed = 0;
+            for (uint32_t v = tid; v < nodes; v += 256) {
+                const int32_t a = par[v];
+                if (a >= 0 && par[a] >= 0) changed = 1;
+            }
+            if (!__syncthreads_or(changed)) break;
+            // one jump: read everything first, then write (separate phases)
+            uint32_t nd[(2 * kSmallN + 255) / 256];
+            int32_t na[(2 * kSmallN + 255) / 256];
+            int q = 0;
+            for (uint32_t v = tid; v < nodes && q < (2 * kSmallN + 255) / 256; v += 256, ++q) {
+                const int32_t a = par[v];
+                if (a >= 0 && par[a] >= 0) { // stop at the root: -1 marks only the root itself
+                    nd[q] = nc[v] + nc[a];
+                    na[q] = par[a];
+                } else {
+                    nd[q] = nc[v];
+                    na[q] = a;
+                }
+            }
+            __syncthreads();
+            q = 0;
+            for (uint32_t v = tid; v < nodes && q < (2 * kSmallN + 255) / 256; v += 256, ++q) {
+                nc[v] = nd[q];
+                par[v] = na[q];
+            }
+            __syncthreads();
         }
     }
     __syncthreads();
