@@ -341,6 +341,8 @@ __global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int 
                                             kScanSumExcl);
     const uint32_t c0 = (uint32_t)ck * kCsChunk;
     if (c0 >= nev) return;
+    if (ck == 0 && threadIdx.x == 0 && stats) // events of the pass (bench roofline)
+        atomicAdd(reinterpret_cast<unsigned long long *>(stats + 6), (unsigned long long)nev);
     if (nev <= kCsSerialMax) { // a handful of events: the plain recurrence is cheaper
         if (threadIdx.x < 32)
             chain_serial_warp(A.evc + (uint64_t)pl * A.L, A.evlist + (uint64_t)pl * A.L, A.dval + (uint64_t)pl * A.L,

@@ -1303,8 +1303,9 @@ int qcsim_profile_read(char (*names)[64], double *ms, uint64_t *count, double *b
 }
 
 // Debug (not part of the public header): enc_chain_scan counters since the
-// last call ([0] resolve points, [1] refuted chunks, [2] serial chunks).
-qcsim_status qcsim_debug_chain_stats(uint32_t *out3) {
+// last call ([0] resolve points, [1] refuted chunks, [2] serial chunks,
+// [3..4] events chained, u64 little-endian).
+qcsim_status qcsim_debug_chain_stats(uint32_t *out3) { // out3[5]
     return guarded([&] {
         CK(cudaDeviceSynchronize());
         uint32_t v[8];
@@ -1312,6 +1313,8 @@ qcsim_status qcsim_debug_chain_stats(uint32_t *out3) {
         out3[0] = v[0];
         out3[1] = v[1];
         out3[2] = v[4];
+        out3[3] = v[6]; // events (low, high words of a u64)
+        out3[4] = v[7];
         CK(cudaMemset(chain_stats(), 0, sizeof v));
     });
 }
