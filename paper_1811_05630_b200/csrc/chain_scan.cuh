@@ -208,12 +208,12 @@ __device__ __forceinline__ Clamp event_clamp(bool outlier, double c, double dh, 
 
 // ------------------------------------------------------ the kernel
 constexpr int kCsThreads = 256;
-constexpr int kCsEpt = 8;                         // events per thread
+constexpr int kCsEpt = 16;                        // events per thread
 constexpr int kCsChunk = kCsThreads * kCsEpt;     // events per block pass
 constexpr int kCsPad = kCsEpt + 1;                // bank-conflict-free rows
 constexpr int kCsWarps = kCsThreads / 32;
 constexpr uint32_t kCsSerialMax = 256;            // planes with fewer events run serially
-constexpr int kCsResolveMax = 24;                 // more resolve points: the chunk runs serially
+constexpr int kCsResolveMax = 48;                 // more resolve points: the chunk runs serially
 
 struct ChainElem {
     int kind; // 0 map of the chunk carry, 1 constant (T[0] = delta), 2 map of resolved thread `base`
