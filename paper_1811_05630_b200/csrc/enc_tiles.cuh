@@ -11,8 +11,7 @@
 //   S  scan          base (last outlier) before every tile
 //   T2 enc_lattice   lattice codes m^ = K_i - K_{i-1}, K relative to the
 //                    segment base, event flags
-//   S  scan          event offsets
-//   T3 enc_compact   event list in index order
+//   (T2 also writes the event list: tile offsets by decoupled look-back)
 //   C  enc_chain     exact d += RN(q*m^) over events (codec.cpp:445)
 //   T4 enc_verify    every decision re-evaluated with the exact prediction
 //                    (codec.cpp:440-451); refuted planes -> enc_serial_x
@@ -41,6 +40,8 @@ struct TileArgs {
     double *evc;           // [plane][L] event addend q*m^ (outlier: its value)
     double *dval;          // [plane][L] chain value per event ordinal
     double *evD;           // [plane][L] lattice estimate of d per event ordinal (chain_scan.cuh)
+    unsigned long long *lb; // [plane][ntiles] event-offset look-back slots (epoch-tagged)
+    uint32_t lb_epoch;
     IndexRec *index;       // [plane][nidx]
     // per plane-tile, stride ntiles (+1 for scanned arrays)
     int32_t *t_lastout;    // last speculative outlier in the tile (-1)
@@ -267,7 +268,61 @@ __global__ void __launch_bounds__(256) plane_scan(const int32_t *in, int32_t *ou
     if (tid == 0 && kind == kScanSumExcl) o[ntiles] = total;
 }
 
+// Decoupled look-back over the tiles of one plane (one thread per block):
+// publish this tile's count, add predecessors' counts until one with an
+// inclusive prefix, publish the inclusive prefix.  Slots carry the pass
+// epoch in their tag, so they never need clearing; blocks of a plane are
+// dispatched in tile order (block = plane * ntiles + tile).
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long lb_tag(uint32_t epoch, uint32_t status) {
+    return (unsigned long long)((epoch << 2) | status) << 32;
+}
+__device__ void lookback_publish_aggregate(unsigned long long *slots, uint32_t epoch, int t, uint32_t local) {
+    st_release_u64(&slots[t], lb_tag(epoch, 1) | local);
+}
+// Warp-wide: lanes read 32 predecessors at once; the window slides back
+// until it meets an inclusive prefix (or tile 0).  Call with a full warp;
+// the result is valid in every lane.
+__device__ uint32_t lookback_exclusive(unsigned long long *slots, uint32_t epoch, int t, uint32_t local) {
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) st_release_u64(&slots[t], lb_tag(epoch, t == 0 ? 2 : 1) | local);
+    uint32_t prefix = 0;
+    int hi = t - 1; // window [hi - 31, hi]
+    while (hi >= 0) {
+        const int k = hi - lane;
+        unsigned long long w = 0;
+        uint32_t st = 2; // below tile 0: acts as an inclusive zero
+        if (k >= 0) {
+            do {
+                w = ld_acquire_u64(&slots[k]);
+                st = ((uint32_t)(w >> 32) >> 2) == epoch ? ((uint32_t)(w >> 32) & 3) : 0;
+                if (st == 0) __nanosleep(32);
+            } while (st == 0);
+        }
+        // the nearest inclusive prefix in the window ends the walk
+        const unsigned incl = __ballot_sync(0xffffffffu, st == 2);
+        const int stop = incl ? __ffs(incl) - 1 : 32; // lanes [0, stop] contribute
+        uint32_t v = (lane <= stop && k >= 0) ? (uint32_t)w : 0u;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        prefix += v;
+        if (incl) break;
+        hi -= 32;
+    }
+    if (lane == 0 && t > 0) st_release_u64(&slots[t], lb_tag(epoch, 2) | (prefix + local));
+    return prefix;
+}
+
 // ------------------------------------------------------------------ T2
+// Lattice codes, flags and the plane's event list (the compaction is fused:
+// the tile's event offset comes from the look-back above).
 __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int planes) {
     const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
     if (pl >= planes) return;
@@ -283,8 +338,12 @@ __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int plane
     const double *x = A.x + (uint64_t)pl * L;
     uint8_t *fl = A.fl + (uint64_t)pl * L;
     uint32_t *sym = A.sym + (uint64_t)pl * L;
+    unsigned long long *lbs = A.lb + (uint64_t)pl * A.ntiles;
     if (pp.flags & kFlagFallback) {
-        if (tid == 0) A.t_nev[(uint64_t)pl * A.ntiles + t] = 0;
+        if (tid == 0) {
+            A.t_nev[(uint64_t)pl * A.ntiles + t] = 0;
+            lookback_publish_aggregate(lbs, A.lb_epoch, t, 0);
+        }
         return;
     }
     if (pp.eb == 0.0) {
@@ -300,7 +359,10 @@ __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int plane
             sym[i] = bits_of(x[i]) == bits_of(pred) ? (uint32_t)half : 0u;
             fl[i] = 0;
         }
-        if (tid == 0) A.t_nev[(uint64_t)pl * A.ntiles + t] = 0;
+        if (tid == 0) {
+            A.t_nev[(uint64_t)pl * A.ntiles + t] = 0;
+            lookback_publish_aggregate(lbs, A.lb_epoch, t, 0);
+        }
         return;
     }
     // speculative outliers of this tile and the element before it
@@ -315,20 +377,18 @@ __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int plane
     ScanI(scan_tmp).ExclusiveScan(opos, lo, -1, cub::Max());
     const int32_t tbase = carry_of(A.t_base, A.ntiles, A.t_lastout, pl, t, A.ntiles, kScanMaxExcl); // position or -1
     long long K[kPerThread];
-    double *dhat = A.dval + (uint64_t)pl * L; // scratch until the chain overwrites dval
+    double dh[kPerThread]; // lattice estimate of the chain value (chain_scan.cuh)
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
         if (opos[e] >= 0) {
             K[e] = 0;
-            if (k < tl) dhat[t0 + k] = xv[e];
+            dh[e] = xv[e];
         } else {
             double base;
             if (lo[e] >= 0) base = x[t0 + lo[e]];
             else base = tbase >= 0 ? x[tbase] : 0.0;
             K[e] = k < tl ? llround_exact(dmul(dsub(xv[e], base), pp.inv_q)) : 0;
-            // alignment of the lattice estimate of d (chain_scan.cuh)
-            // lattice estimate of the chain value (chain_scan.cuh)
-            if (k < tl) dhat[t0 + k] = dadd(base, dmul(pp.q, (double)K[e]));
+            dh[e] = dadd(base, dmul(pp.q, (double)K[e]));
         }
     }
     kb[tid] = K[kPerThread - 1];
@@ -347,6 +407,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int plane
     }
     __syncthreads();
     int evflag[kPerThread];
+    uint32_t esym[kPerThread];
     int bad = 0;
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
@@ -372,52 +433,37 @@ __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int plane
         }
         fl[t0 + k] = f;
         sym[t0 + k] = sy;
+        esym[e] = sy;
         evflag[e] = f & 1;
     }
     if (bad) atomicOr(&A.params[pl].flags, kFlagFallback);
-    using RedI = cub::BlockReduce<int, kEncThreads>;
-    __shared__ typename RedI::TempStorage red_tmp;
-    const int tot = RedI(red_tmp).Sum(evflag[0] + evflag[1] + evflag[2] + evflag[3]);
-    if (tid == 0) A.t_nev[(uint64_t)pl * A.ntiles + t] = (uint32_t)tot;
-}
-
-// ------------------------------------------------------------------ T3
-__global__ void __launch_bounds__(kEncThreads) enc_compact(TileArgs A, int planes) {
-    const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
-    if (pl >= planes) return;
-    if (block_params(A.params, pl).flags & kFlagFallback) return;
-    const int tid = threadIdx.x;
-    const uint64_t L = A.L;
-    const uint64_t t0 = (uint64_t)t * kTile;
-    const int tl = (int)tmin<uint64_t>(kTile, L - t0);
-    using ScanI = cub::BlockScan<int, kEncThreads>;
-    __shared__ typename ScanI::TempStorage scan_tmp;
-    const uint8_t *fl = A.fl + (uint64_t)pl * L;
-    int f[kPerThread], pos[kPerThread];
-    for (int e = 0; e < kPerThread; ++e) {
-        const int k = tid * kPerThread + e;
-        f[e] = (k < tl && (fl[t0 + k] & 1)) ? 1 : 0;
+    // event list: tile offset by look-back, in-tile positions by a block scan
+    int epos[kPerThread], tot;
+    __syncthreads();
+    ScanI(scan_tmp).ExclusiveSum(evflag, epos, tot);
+    __shared__ uint32_t s_evbase;
+    if (tid < 32) {
+        const uint32_t b = lookback_exclusive(lbs, A.lb_epoch, t, (uint32_t)tot);
+        if (tid == 0) {
+            A.t_nev[(uint64_t)pl * A.ntiles + t] = (uint32_t)tot;
+            s_evbase = b;
+        }
     }
-    ScanI(scan_tmp).ExclusiveSum(f, pos);
-    const uint32_t base = (uint32_t)carry_of(reinterpret_cast<const int32_t *>(A.t_evoff), A.ntiles + 1,
-                                             reinterpret_cast<const int32_t *>(A.t_nev), pl, t, A.ntiles, kScanSumExcl);
+    __syncthreads();
+    const uint32_t evb = s_evbase;
     uint32_t *ev = A.evlist + (uint64_t)pl * L;
     double *evc = A.evc + (uint64_t)pl * L;
     double *evD = A.evD + (uint64_t)pl * L;
-    const double *dhat = A.dval + (uint64_t)pl * L;
-    const uint32_t *sym = A.sym + (uint64_t)pl * L;
-    const double *x = A.x + (uint64_t)pl * L;
-    const double q = A.params[pl].q;
-    const long long half = 1ll << (A.qb - 1);
     for (int e = 0; e < kPerThread; ++e) {
-        if (!f[e]) continue;
-        const uint64_t i = t0 + tid * kPerThread + e;
-        const bool out = (fl[i] & 2) != 0;
-        // the event record the chain consumes: its addend (or outlier value)
-        // and the element index with bit 31 = outlier
-        ev[base + pos[e]] = (uint32_t)i | (out ? 0x80000000u : 0u);
-        evc[base + pos[e]] = out ? x[i] : dmul(q, (double)((long long)sym[i] - half));
-        evD[base + pos[e]] = dhat[i];
+        if (!evflag[e]) continue;
+        const uint32_t i = (uint32_t)(t0 + tid * kPerThread + e);
+        const bool out = opos[e] >= 0;
+        const uint32_t o = evb + (uint32_t)epos[e];
+        // the record the chain consumes: element index (bit 31 = outlier),
+        // addend q*m^ (or the outlier value), lattice estimate of d
+        ev[o] = i | (out ? 0x80000000u : 0u);
+        evc[o] = out ? xv[e] : dmul(pp.q, (double)((long long)esym[e] - half));
+        evD[o] = dh[e];
     }
 }
 

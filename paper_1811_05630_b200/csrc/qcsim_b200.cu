@@ -243,6 +243,8 @@ struct EncScratch {
     DBuf<int32_t> cb_parent;
     DBuf<uint32_t> overflow;
     DBuf<double> evD;
+    DBuf<unsigned long long> lb; // enc_lattice event-offset look-back
+    uint32_t lb_epoch = 0;
     DBuf<double> chain_carry; // enc_chain_scan chunk hand-off
     DBuf<uint32_t> chain_flag;
     uint32_t chain_epoch = 0;
@@ -447,14 +449,17 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     }
     launch_plane_scan(st, S.t_lastout.p, S.t_base.p, ntiles, (int)planes, kScanMaxExcl);
     {
+        if (S.lb.ensure(planes * ntiles, /*zero=*/true)) S.lb_epoch = 0;
+        if (++S.lb_epoch >= (1u << 30)) { // epoch wrapped: clean slots
+            CK(cudaMemsetAsync(S.lb.p, 0, S.lb.cap * sizeof(unsigned long long), st));
+            S.lb_epoch = 1;
+        }
+        A.lb = S.lb.p;
+        A.lb_epoch = S.lb_epoch;
         PROF("enc_lattice", st);
         enc_lattice<<<tgrid_p, kEncThreads, 0, st>>>(A, (int)planes);
     }
     launch_plane_scan(st, S.t_nev.p, S.t_evoff.p, ntiles, (int)planes, kScanSumExcl);
-    {
-        PROF("enc_compact", st);
-        enc_compact<<<tgrid_p, kEncThreads, 0, st>>>(A, (int)planes);
-    }
     {
         // debug: dump one encode call's event lists (QCSIM_CHAIN_DUMP_AT = call
         // number, QCSIM_CHAIN_DUMP_FILE = path)
