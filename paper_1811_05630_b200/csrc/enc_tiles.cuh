@@ -11,7 +11,8 @@
 //   S  scan          base (last outlier) before every tile
 //   T2 enc_lattice   lattice codes m^ = K_i - K_{i-1}, K relative to the
 //                    segment base, event flags
-//   (T2 also writes the event list: tile offsets by decoupled look-back)
+//   (T2 also writes the event list for planes of <= 64 tiles, tile
+//    offsets by decoupled look-back; larger planes: S scan + T3 enc_compact)
 //   C  enc_chain     exact d += RN(q*m^) over events (codec.cpp:445)
 //   T4 enc_verify    every decision re-evaluated with the exact prediction
 //                    (codec.cpp:440-451); refuted planes -> enc_serial_x
@@ -342,7 +343,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int plane
     if (pp.flags & kFlagFallback) {
         if (tid == 0) {
             A.t_nev[(uint64_t)pl * A.ntiles + t] = 0;
-            lookback_publish_aggregate(lbs, A.lb_epoch, t, 0);
+            if (A.ntiles <= kInlineTiles) lookback_publish_aggregate(lbs, A.lb_epoch, t, 0);
         }
         return;
     }
@@ -361,7 +362,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int plane
         }
         if (tid == 0) {
             A.t_nev[(uint64_t)pl * A.ntiles + t] = 0;
-            lookback_publish_aggregate(lbs, A.lb_epoch, t, 0);
+            if (A.ntiles <= kInlineTiles) lookback_publish_aggregate(lbs, A.lb_epoch, t, 0);
         }
         return;
     }
@@ -389,6 +390,14 @@ __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int plane
             else base = tbase >= 0 ? x[tbase] : 0.0;
             K[e] = k < tl ? llround_exact(dmul(dsub(xv[e], base), pp.inv_q)) : 0;
             dh[e] = dadd(base, dmul(pp.q, (double)K[e]));
+        }
+    }
+    const bool fused = A.ntiles <= kInlineTiles; // else enc_compact writes the events
+    if (!fused) {
+        double *dhat = A.dval + (uint64_t)pl * L; // scratch until the chain overwrites dval
+        for (int e = 0; e < kPerThread; ++e) {
+            const int k = tid * kPerThread + e;
+            if (k < tl) dhat[t0 + k] = dh[e];
         }
     }
     kb[tid] = K[kPerThread - 1];
@@ -441,6 +450,10 @@ __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int plane
     int epos[kPerThread], tot;
     __syncthreads();
     ScanI(scan_tmp).ExclusiveSum(evflag, epos, tot);
+    if (!fused) {
+        if (tid == 0) A.t_nev[(uint64_t)pl * A.ntiles + t] = (uint32_t)tot;
+        return;
+    }
     __shared__ uint32_t s_evbase;
     if (tid < 32) {
         const uint32_t b = lookback_exclusive(lbs, A.lb_epoch, t, (uint32_t)tot);
@@ -464,6 +477,48 @@ __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int plane
         ev[o] = i | (out ? 0x80000000u : 0u);
         evc[o] = out ? xv[e] : dmul(pp.q, (double)((long long)esym[e] - half));
         evD[o] = dh[e];
+    }
+}
+
+// ------------------------------------------------------------------ T3
+// Event list for planes with many tiles (the fused look-back in enc_lattice
+// would serialise hundreds of tiles): tile offsets from the plane scan.
+__global__ void __launch_bounds__(kEncThreads) enc_compact(TileArgs A, int planes) {
+    const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
+    if (pl >= planes) return;
+    if (block_params(A.params, pl).flags & kFlagFallback) return;
+    const int tid = threadIdx.x;
+    const uint64_t L = A.L;
+    const uint64_t t0 = (uint64_t)t * kTile;
+    const int tl = (int)tmin<uint64_t>(kTile, L - t0);
+    using ScanI = cub::BlockScan<int, kEncThreads>;
+    __shared__ typename ScanI::TempStorage scan_tmp;
+    const uint8_t *fl = A.fl + (uint64_t)pl * L;
+    int f[kPerThread], pos[kPerThread];
+    for (int e = 0; e < kPerThread; ++e) {
+        const int k = tid * kPerThread + e;
+        f[e] = (k < tl && (fl[t0 + k] & 1)) ? 1 : 0;
+    }
+    ScanI(scan_tmp).ExclusiveSum(f, pos);
+    const uint32_t base = (uint32_t)carry_of(reinterpret_cast<const int32_t *>(A.t_evoff), A.ntiles + 1,
+                                             reinterpret_cast<const int32_t *>(A.t_nev), pl, t, A.ntiles, kScanSumExcl);
+    uint32_t *ev = A.evlist + (uint64_t)pl * L;
+    double *evc = A.evc + (uint64_t)pl * L;
+    double *evD = A.evD + (uint64_t)pl * L;
+    const double *dhat = A.dval + (uint64_t)pl * L;
+    const uint32_t *sym = A.sym + (uint64_t)pl * L;
+    const double *x = A.x + (uint64_t)pl * L;
+    const double q = A.params[pl].q;
+    const long long half = 1ll << (A.qb - 1);
+    for (int e = 0; e < kPerThread; ++e) {
+        if (!f[e]) continue;
+        const uint64_t i = t0 + tid * kPerThread + e;
+        const bool out = (fl[i] & 2) != 0;
+        // the event record the chain consumes: its addend (or outlier value)
+        // and the element index with bit 31 = outlier
+        ev[base + pos[e]] = (uint32_t)i | (out ? 0x80000000u : 0u);
+        evc[base + pos[e]] = out ? x[i] : dmul(q, (double)((long long)sym[i] - half));
+        evD[base + pos[e]] = dhat[i];
     }
 }
 

@@ -310,7 +310,7 @@ struct EncScratch {
 
 // enc_chain_scan counters: [0] resolve points, [1] refuted chunks redone
 // serially, [4] chunks run serially because the maps did not fit
-constexpr uint64_t kScanChainMaxPlanes = 4096;
+constexpr uint64_t kScanChainMaxPlanes = 256; // more planes fill the GPU with serial warps
 uint32_t *chain_stats() {
     static DBuf<uint32_t> buf;
     if (!buf.p) {
@@ -460,6 +460,10 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
         enc_lattice<<<tgrid_p, kEncThreads, 0, st>>>(A, (int)planes);
     }
     launch_plane_scan(st, S.t_nev.p, S.t_evoff.p, ntiles, (int)planes, kScanSumExcl);
+    if (ntiles > kInlineTiles) {
+        PROF("enc_compact", st);
+        enc_compact<<<tgrid_p, kEncThreads, 0, st>>>(A, (int)planes);
+    }
     {
         // debug: dump one encode call's event lists (QCSIM_CHAIN_DUMP_AT = call
         // number, QCSIM_CHAIN_DUMP_FILE = path)
