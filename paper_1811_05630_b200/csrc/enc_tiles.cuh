@@ -529,8 +529,10 @@ __global__ void __launch_bounds__(kEncThreads) enc_compact(TileArgs A, int plane
 // (codec.cpp:445 / :607 in index order) reads warp-broadcast addends, so
 // only the DADD latency is serial.
 constexpr int kChainChunk = 1024; // events per bulk copy
-constexpr int kChainBufs = 8;     // 96 KB ring (dynamic smem)
-constexpr size_t kChainSmem = 12ull * kChainBufs * kChainChunk + 8 * kChainBufs;
+constexpr int kChainBufs = 8;     // ring depth with few planes (96 KB, dynamic smem); many
+                                  // planes use a 2-deep ring so more warps fit per SM
+__host__ __device__ constexpr size_t chain_smem_bytes(int bufs) { return 12ull * bufs * kChainChunk + 8 * bufs; }
+constexpr size_t kChainSmem = chain_smem_bytes(kChainBufs);
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -560,7 +562,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
         : "memory");
 }
 
-__global__ void __launch_bounds__(32) enc_chain(TileArgs A, int planes) {
+__global__ void __launch_bounds__(32) enc_chain(TileArgs A, int planes, int nbufs) {
     const int pl = blockIdx.x;
     if (pl >= planes) return;
     const int lane = threadIdx.x;
@@ -571,8 +573,9 @@ __global__ void __launch_bounds__(32) enc_chain(TileArgs A, int planes) {
     extern __shared__ __align__(128) unsigned char chain_smem[];
     double(*cbuf)[kChainChunk] = reinterpret_cast<double(*)[kChainChunk]>(chain_smem);
     uint32_t(*obuf)[kChainChunk] =
-        reinterpret_cast<uint32_t(*)[kChainChunk]>(chain_smem + sizeof(double) * kChainBufs * kChainChunk);
-    uint64_t *bar = reinterpret_cast<uint64_t *>(chain_smem + 12 * kChainBufs * kChainChunk);    const uint64_t L = A.L;
+        reinterpret_cast<uint32_t(*)[kChainChunk]>(chain_smem + sizeof(double) * nbufs * kChainChunk);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(chain_smem + 12 * nbufs * kChainChunk);
+    const uint64_t L = A.L;
     const uint32_t nev = (uint32_t)carry_of(reinterpret_cast<const int32_t *>(A.t_evoff), A.ntiles + 1,
                                             reinterpret_cast<const int32_t *>(A.t_nev), pl, A.ntiles, A.ntiles,
                                             kScanSumExcl);
@@ -582,7 +585,7 @@ __global__ void __launch_bounds__(32) enc_chain(TileArgs A, int planes) {
     double *dv = A.dval + (uint64_t)pl * L;
     const uint32_t nchunks = (nev + kChainChunk - 1) / kChainChunk;
     auto issue = [&](uint32_t ch) {
-        const int b = ch % kChainBufs;
+        const int b = ch % nbufs;
         const uint32_t n = tmin<uint32_t>(kChainChunk, nev - ch * kChainChunk);
         const uint32_t cb = (n * 8 + 15) & ~15u, ob = (n * 4 + 15) & ~15u; // buffers are padded
         mbar_expect_tx(&bar[b], cb + ob);
@@ -590,15 +593,15 @@ __global__ void __launch_bounds__(32) enc_chain(TileArgs A, int planes) {
         tma_load_1d(obuf[b], ev + (uint64_t)ch * kChainChunk, ob, &bar[b]);
     };
     if (lane == 0) {
-        for (int b = 0; b < kChainBufs; ++b) mbar_init(&bar[b], 1);
+        for (int b = 0; b < nbufs; ++b) mbar_init(&bar[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (uint32_t ch = 0; ch < nchunks && ch < (uint32_t)kChainBufs; ++ch) issue(ch);
+        for (uint32_t ch = 0; ch < nchunks && ch < (uint32_t)nbufs; ++ch) issue(ch);
     }
     __syncwarp();
     double d = 0.0;
     for (uint32_t ch = 0; ch < nchunks; ++ch) {
-        const int b = ch % kChainBufs;
-        mbar_wait(&bar[b], (ch / kChainBufs) & 1);
+        const int b = ch % nbufs;
+        mbar_wait(&bar[b], (ch / nbufs) & 1);
         const uint32_t n = tmin<uint32_t>(kChainChunk, nev - ch * kChainChunk);
         for (uint32_t base = 0; base < n; base += 32) {
             const uint32_t cnt = tmin<uint32_t>(32, n - base);
@@ -639,7 +642,7 @@ __global__ void __launch_bounds__(32) enc_chain(TileArgs A, int planes) {
             if (lane < (int)cnt) dv[(uint64_t)ch * kChainChunk + base + lane] = mine;
         }
         __syncwarp();
-        if (lane == 0 && ch + kChainBufs < nchunks) issue(ch + kChainBufs);
+        if (lane == 0 && ch + nbufs < nchunks) issue(ch + nbufs);
     }
 }
 

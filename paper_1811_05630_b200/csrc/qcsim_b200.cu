@@ -520,7 +520,8 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
                                                                                         chain_stats(), chain_debug);
         } else if (chain_mode != 1) {
             PROF("enc_chain", st);
-            enc_chain<<<(unsigned)planes, 32, kChainSmem, st>>>(A, (int)planes);
+            const int nbufs = planes > 2 * 148 ? 2 : kChainBufs; // latency hidden by other warps
+            enc_chain<<<(unsigned)planes, 32, chain_smem_bytes(nbufs), st>>>(A, (int)planes, nbufs);
         }
     }
     {
