@@ -173,10 +173,12 @@ def run_ours(args, wl, rank, world, dist):
     eng = ShardedEngine(cfg) if world > 1 else q.Engine(cfg)
     eng.load_basis(wl["basis"])
     eng.run(wl["setup"])
+    history = []  # every gate list run after the setup layer (accuracy check)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")  # > L2 (126 MB)
     lib = _native.lib()
     for k in range(args.warmup):
         eng.run(wl["steps"](k))
+        history.append(wl["steps"](k))
     gates = 0
     dev_s = 0.0
     wall = 0.0
@@ -194,6 +196,7 @@ def run_ours(args, wl, rank, world, dist):
         t0 = time.perf_counter()
         m = eng.run(acts)
         wall += time.perf_counter() - t0
+        history.append(acts)
         dev_s += m.wall_seconds - m0
         gates += len(acts)
     torch.cuda.synchronize()
@@ -205,6 +208,7 @@ def run_ours(args, wl, rank, world, dist):
     prof = profile_begin(lib)
     for k in range(args.warmup + args.steps, args.warmup + args.steps + max(1, args.steps // 2)):
         eng.run(wl["steps"](k % wl["max_steps"]))
+        history.append(wl["steps"](k % wl["max_steps"]))
     kprof = profile_end(lib, prof)
     mets = eng.metrics()
     chain = None
@@ -227,11 +231,27 @@ def run_ours(args, wl, rank, world, dist):
         pinned = torch.empty(ctypes.sizeof(arr), dtype=torch.uint8, pin_memory=True)
         ctypes.memmove(pinned.data_ptr(), ctypes.addressof(arr), ctypes.sizeof(arr))
         m = eng.run(acts)
+        history.append(acts)
         blocks = eng.export_blocks()[0] if world == 1 else eng.export_local_blocks()
         e2e_t += time.perf_counter() - t0
         h2d += ctypes.sizeof(arr)
         d2h += len(blocks) + ctypes.sizeof(_native.RunMetricsC)
+    # accuracy: the same gate sequence through a
+    # compression-off FP64 engine, compared on the device (outside all timing)
+    accuracy = None
+    if world == 1 and wl["n"] <= 30:
+        dense = q.Engine(q.EngineConfig(num_qubits=wl["n"], slice_bits=wl["s"], compression_enabled=False, device=dev))
+        dense.load_basis(wl["basis"])
+        dense.run(wl["setup"])
+        for acts in history:
+            dense.run(acts)
+        r = eng.compare(dense)
+        accuracy = {"max_abs_err_vs_fp64": r["max_abs_diff"], "fidelity_vs_fp64": r["fidelity"] / (r["norm_a"] * r["norm_b"]),
+                    "gates": len(wl["setup"]) + sum(len(a) for a in history),
+                    "basis": "same gates through a compression-off FP64 engine, compared on the device"}
+        del dense
     return dict(gates=gates, dev_s=dev_s, wall=wall, clocks=clk, launches=launches, metrics=mets, kprof=kprof, chain=chain,
+                accuracy=accuracy,
                 e2e_t=e2e_t, h2d=h2d // max(1, args.steps), d2h=d2h // max(1, args.steps))
 
 
@@ -371,6 +391,7 @@ def main():
             "compression": {"min_ratio": m.min_compression_ratio, "mean_ratio": m.mean_compression_ratio,
                             "compressed_bytes": m.current_compressed_bytes, "dense_bytes": m.dense_bytes,
                             "fallback_planes": m.fallback_planes},
+            "accuracy": res.get("accuracy"),
             "wall_ms_per_step": 1e3 * wall / args.steps}
     print(json.dumps(line), flush=True)
     if dist:

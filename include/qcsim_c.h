@@ -189,6 +189,20 @@ qcsim_status qcsim_engine_run(qcsim_engine *eng, const qcsim_action *actions,
 qcsim_status qcsim_engine_gather(qcsim_engine *eng, double *amps,
                                  uint64_t capacity, int32_t guard_qubits);
 
+/* On-device comparison of two engines' current states (same qubits, slice
+ * size and rank layout), e.g. a compressed run against a compression-off
+ * FP64 run of the same circuit: max |a_k - b_k| over every amplitude, the
+ * inner product <a|b> (statevec.hpp:83, conj(a).b), both squared norms and
+ * fidelity = |<a|b>|^2 (statevec.hpp:84).  Sums are fixed pairwise trees. */
+typedef struct qcsim_compare_result {
+    double max_abs_diff;
+    double inner_re, inner_im;
+    double norm_a, norm_b;
+    double fidelity;
+} qcsim_compare_result;
+qcsim_status qcsim_engine_compare(qcsim_engine *a, qcsim_engine *b,
+                                  qcsim_compare_result *out);
+
 /* Per-slice sq_norm cache (statevec.hpp:72) of this rank's slices. */
 qcsim_status qcsim_engine_slice_norms(qcsim_engine *eng, double *out,
                                       uint64_t capacity);

@@ -35,6 +35,11 @@ class EngineConfigC(C.Structure):
                 ("world", C.c_int32), ("checkpoint_bits", C.c_int32), ("wave_bytes", C.c_uint64)]
 
 
+class CompareC(C.Structure):
+    _fields_ = [("max_abs_diff", C.c_double), ("inner_re", C.c_double), ("inner_im", C.c_double),
+                ("norm_a", C.c_double), ("norm_b", C.c_double), ("fidelity", C.c_double)]
+
+
 class RunMetricsC(C.Structure):
     _fields_ = [("min_compression_ratio", C.c_double), ("mean_compression_ratio", C.c_double),
                 ("wall_seconds", C.c_double), ("final_norm", C.c_double),
@@ -66,6 +71,7 @@ SIGNATURES = [
     ("qcsim_engine_run", C.c_int, [C.c_void_p, P(ActionC), C.c_uint64, P(RunMetricsC)]),
     ("qcsim_engine_gather", C.c_int, [C.c_void_p, dp, C.c_uint64, C.c_int32]),
     ("qcsim_engine_slice_norms", C.c_int, [C.c_void_p, dp, C.c_uint64]),
+    ("qcsim_engine_compare", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     ("qcsim_engine_export_blocks", C.c_int, [C.c_void_p, u8p, C.c_uint64, u64p, u64p, C.c_uint64]),
     ("qcsim_engine_partner_blocks_needed", C.c_int, [C.c_void_p, P(ActionC), u64p, C.c_uint64, u64p]),
     ("qcsim_engine_export_slice", C.c_int, [C.c_void_p, C.c_uint64, u8p, C.c_uint64, u64p]),

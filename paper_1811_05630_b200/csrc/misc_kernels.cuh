@@ -261,4 +261,54 @@ __global__ void __launch_bounds__(256) engine_stats(const uint64_t *bytes, const
         }
     }
 }
+// ------------------------------------------------ on-device state comparison
+// Two decoded states ([slot][re|im][L], same layout): per 1024-element tile,
+// pairwise trees of conj(a).b (re, im), |a|^2, |b|^2 and the max |a - b|
+// (statevec.cpp:199-247 semantics; the host finishes the tile trees).
+__global__ void __launch_bounds__(256) state_compare(const double *a, const double *b, uint64_t L, int units,
+                                                     double *part) {
+    const int ntiles = (int)((L + kTile - 1) / kTile);
+    const int unit = blockIdx.x / ntiles, t = blockIdx.x % ntiles;
+    if (unit >= units) return;
+    __shared__ double red[4][256];
+    __shared__ double mx[256];
+    const int tid = threadIdx.x;
+    double s[4][4], m = 0.0;
+    for (int e = 0; e < 4; ++e) {
+        const uint64_t i = (uint64_t)t * kTile + tid * 4 + e;
+        s[0][e] = s[1][e] = s[2][e] = s[3][e] = 0.0;
+        if (i < L) {
+            const double ar = a[(uint64_t)unit * 2 * L + i], ai = a[(uint64_t)unit * 2 * L + L + i];
+            const double br = b[(uint64_t)unit * 2 * L + i], bi = b[(uint64_t)unit * 2 * L + L + i];
+            s[0][e] = dadd(dmul(ar, br), dmul(ai, bi));
+            s[1][e] = dsub(dmul(ar, bi), dmul(ai, br));
+            s[2][e] = dadd(dmul(ar, ar), dmul(ai, ai));
+            s[3][e] = dadd(dmul(br, br), dmul(bi, bi));
+            const double dr = dsub(ar, br), di = dsub(ai, bi);
+            m = fmax(m, __dsqrt_rn(dadd(dmul(dr, dr), dmul(di, di))));
+        }
+    }
+    for (int q = 0; q < 4; ++q) red[q][tid] = dadd(dadd(s[q][0], s[q][1]), dadd(s[q][2], s[q][3]));
+    mx[tid] = m;
+    __syncthreads();
+    for (int w = 128; w >= 1; w >>= 1) {
+        double v[4], vm = 0.0;
+        if (tid < w) {
+            for (int q = 0; q < 4; ++q) v[q] = dadd(red[q][2 * tid], red[q][2 * tid + 1]);
+            vm = fmax(mx[2 * tid], mx[2 * tid + 1]);
+        }
+        __syncthreads();
+        if (tid < w) {
+            for (int q = 0; q < 4; ++q) red[q][tid] = v[q];
+            mx[tid] = vm;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        double *o = part + 5 * ((uint64_t)unit * ntiles + t);
+        for (int q = 0; q < 4; ++q) o[q] = red[q][0];
+        o[4] = mx[0];
+    }
+}
+
 } // namespace qcb

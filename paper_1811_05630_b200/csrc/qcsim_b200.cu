@@ -1696,6 +1696,46 @@ qcsim_status qcsim_engine_gather(qcsim_engine *e, double *amps, uint64_t capacit
     });
 }
 
+qcsim_status qcsim_engine_compare(qcsim_engine *a, qcsim_engine *b, qcsim_compare_result *out) {
+    return guarded([&] {
+        if (!a || !b || !out) raise(QCSIM_INVALID_ARGUMENT, "null argument");
+        if (a->n != b->n || a->s != b->s || a->s0 != b->s0 || a->ns != b->ns || a->cfg.device != b->cfg.device)
+            raise(QCSIM_INVALID_ARGUMENT, "engines differ in qubits, slice size, slice range or device");
+        if (!a->loaded || !b->loaded) raise(QCSIM_INVALID_ARGUMENT, "engine has no state");
+        CK(cudaSetDevice(a->cfg.device));
+        engine_decode_old(a, false);
+        engine_decode_old(b, false);
+        CK(cudaStreamSynchronize(b->st));
+        CK(cudaStreamSynchronize(a->st));
+        const uint64_t ntiles = (a->L + kTile - 1) / kTile;
+        const uint64_t tiles = a->ns * ntiles;
+        DBuf<double> part;
+        part.ensure(5 * tiles);
+        {
+            PROF("state_compare", a->st);
+            state_compare<<<(unsigned)tiles, 256, 0, a->st>>>(a->old.p, b->old.p, a->L, (int)a->ns, part.p);
+        }
+        std::vector<double> h(5 * tiles);
+        CK(cudaMemcpyAsync(h.data(), part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, a->st));
+        CK(cudaStreamSynchronize(a->st));
+        CK(cudaGetLastError());
+        std::vector<double> col(tiles);
+        double r[4];
+        for (int q = 0; q < 4; ++q) {
+            for (uint64_t k = 0; k < tiles; ++k) col[k] = h[5 * k + q];
+            r[q] = tree_sum_host(col.data(), tiles);
+        }
+        double mx = 0.0;
+        for (uint64_t k = 0; k < tiles; ++k) mx = std::max(mx, h[5 * k + 4]);
+        out->max_abs_diff = mx;
+        out->inner_re = r[0];
+        out->inner_im = r[1];
+        out->norm_a = r[2];
+        out->norm_b = r[3];
+        out->fidelity = r[0] * r[0] + r[1] * r[1];
+    });
+}
+
 qcsim_status qcsim_engine_slice_norms(qcsim_engine *e, double *out, uint64_t capacity) {
     return guarded([&] {
         if (!e || !out) raise(QCSIM_INVALID_ARGUMENT, "null argument");

@@ -129,6 +129,15 @@ class Engine:
         g = self.gather(guard_qubits)
         return g[0::2] + 1j * g[1::2]
 
+    def compare(self, other: "Engine") -> dict:
+        """On-device comparison with another engine's current state (same
+        qubits and slicing): max |a - b|, <a|b>, both squared norms and
+        fidelity |<a|b>|^2 (statevec.hpp:83-84)."""
+        r = _native.CompareC()
+        self._ck(self.L.qcsim_engine_compare(self.h, other.h, C.byref(r)))
+        return {"max_abs_diff": r.max_abs_diff, "inner": complex(r.inner_re, r.inner_im), "norm_a": r.norm_a,
+                "norm_b": r.norm_b, "fidelity": r.fidelity}
+
     def slice_norms(self) -> np.ndarray:
         out = np.empty(self.local_slices, dtype=np.float64)
         self._ck(self.L.qcsim_engine_slice_norms(self.h, out.ctypes.data_as(_native.dp), out.size))

@@ -180,3 +180,27 @@ def test_cpp_api_smoke():
     out = subprocess.run([b.API_SMOKE], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr
     assert "api_smoke ok" in out.stdout
+
+
+def test_compare_against_dense_run(q):
+    """On-device max error / fidelity of a compressed run against the
+    compression-off FP64 run of the same circuit."""
+    n, s = 16, 12
+    acts = q.lower(q.build_qft(n))
+    comp = q.Engine(q.EngineConfig(num_qubits=n, slice_bits=s, codec=q.CodecConfig(q.CodecMode.Absolute, 1e-5)))
+    dense = q.Engine(q.EngineConfig(num_qubits=n, slice_bits=s, compression_enabled=False))
+    for e in (comp, dense):
+        e.load_basis(12345)
+        e.run(acts)
+    r = comp.compare(dense)
+    ref = comp.amplitudes() - dense.amplitudes()
+    assert r["max_abs_diff"] == pytest.approx(np.max(np.abs(ref)), rel=1e-12)
+    assert r["fidelity"] > 0.999 and r["max_abs_diff"] < 1e-3
+    assert r["norm_b"] == pytest.approx(1.0, abs=1e-9)
+    same = comp.compare(comp)
+    assert same["max_abs_diff"] == 0.0
+    assert same["fidelity"] == pytest.approx(same["norm_a"] ** 2, rel=1e-12)
+    twin = q.Engine(q.EngineConfig(num_qubits=n, slice_bits=s, codec=q.CodecConfig(q.CodecMode.Absolute, 1e-5)))
+    twin.load_basis(12345)
+    twin.run(acts)
+    assert comp.compare(twin)["max_abs_diff"] == 0.0  # deterministic, bit-identical
