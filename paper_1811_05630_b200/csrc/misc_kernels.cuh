@@ -175,11 +175,39 @@ struct EngineDevStats {
     uint32_t status, pad;
 };
 
-// G = pairwise tree over the S slice norms (the association of the host's
-// tree_sum_host / DESIGN.md §3.2), drift check, scale = 1/sqrt(G).
-__global__ void __launch_bounds__(256) engine_norm(const double *sq, double *b0, double *b1, uint64_t S, double tol10,
-                                                   unsigned long long gate, double *scale, EngineDevStats *st) {
+// Gate-pass prologue of the deferred loop: per-slice sq_norm of the previous
+// pass from its tile partials (the slice_norms tree), G = pairwise tree over
+// the S slice norms (the association of the host's tree_sum_host /
+// DESIGN.md §3.2), drift check, scale = 1/sqrt(G); also latches an arena
+// overflow of the previous pass.
+__global__ void __launch_bounds__(256) engine_norm(const double *tilesum, int ntiles, double *sq, double *b0,
+                                                   double *b1, uint64_t S, double tol10, unsigned long long gate,
+                                                   double *scale, const uint32_t *overflow, EngineDevStats *st) {
     const int tid = threadIdx.x;
+    // slice norms: one thread per slice over its (aligned power-of-two) tiles
+    // (tilesum == nullptr: `sq` already holds them)
+    for (uint64_t u = tid; tilesum && u < S; u += 256) {
+        const double *t = tilesum + u * ntiles;
+        double acc[64], buf[64];
+        if (ntiles <= 64) {
+            for (int k = 0; k < ntiles; ++k) buf[k] = t[k];
+            for (int w = ntiles / 2; w >= 1; w >>= 1)
+                for (int k = 0; k < w; ++k) buf[k] = dadd(buf[2 * k], buf[2 * k + 1]);
+            sq[u] = buf[0];
+        } else {
+            const int groups = ntiles / 64;
+            for (int g = 0; g < groups && g < 64; ++g) {
+                for (int k = 0; k < 64; ++k) buf[k] = t[g * 64 + k];
+                for (int w = 32; w >= 1; w >>= 1)
+                    for (int k = 0; k < w; ++k) buf[k] = dadd(buf[2 * k], buf[2 * k + 1]);
+                acc[g] = buf[0];
+            }
+            for (int w = groups / 2; w >= 1; w >>= 1)
+                for (int k = 0; k < w; ++k) acc[k] = dadd(acc[2 * k], acc[2 * k + 1]);
+            sq[u] = acc[0];
+        }
+    }
+    __syncthreads();
     for (uint64_t k = tid; k < S; k += 256) b0[k] = sq[k];
     __syncthreads();
     double *in = b0, *out = b1;
@@ -191,6 +219,10 @@ __global__ void __launch_bounds__(256) engine_norm(const double *sq, double *b0,
         out = t;
     }
     if (tid == 0) {
+        if (overflow && *overflow && st->status == kEngOk) {
+            st->status = kEngOverflow;
+            st->status_gate = gate - 1;
+        }
         const double G = in[0];
         if (!isfinite(G) || fabs(dsub(G, 1.0)) > tol10) {
             if (st->status == kEngOk) {
@@ -207,15 +239,36 @@ __global__ void __launch_bounds__(256) engine_norm(const double *sq, double *b0,
 
 // Per gate pass: compression ratio min / sum (plane order, as the host's
 // record_sizes), current and peak bytes, fallback planes, latched errors.
-__global__ void __launch_bounds__(256) engine_stats(const uint64_t *bytes, const uint32_t *err,
-                                                    const PlaneParams *params, const uint32_t *overflow, int planes,
-                                                    uint64_t L, unsigned long long gate, EngineDevStats *st) {
+// Fused with the slot-offset scan of the packer (one block, both read the
+// codebook's per-plane results).
+__global__ void __launch_bounds__(256) slot_scan_stats(const uint64_t *slot_bytes, uint64_t *slot_off,
+                                                       const uint64_t *bytes, const uint32_t *err,
+                                                       const PlaneParams *params, int planes, uint64_t L,
+                                                       unsigned long long gate, EngineDevStats *st) {
+    using Scan = cub::BlockScan<unsigned long long, 256>;
     using Red = cub::BlockReduce<unsigned long long, 256>;
-    __shared__ typename Red::TempStorage red;
+    __shared__ union {
+        typename Scan::TempStorage scan;
+        typename Red::TempStorage red;
+    } tmp;
+    __shared__ unsigned long long carry;
     __shared__ double ratio[1024];
     const int tid = threadIdx.x;
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < planes; base += 256) {
+        const int k = base + tid;
+        const unsigned long long v = k < planes ? slot_bytes[k] : 0ull;
+        unsigned long long r, tot;
+        Scan(tmp.scan).ExclusiveSum(v, r, tot);
+        if (k < planes) slot_off[k] = carry + r;
+        __syncthreads();
+        if (tid == 0) carry += tot;
+        __syncthreads();
+    }
+    if (tid == 0) slot_off[planes] = carry;
     const double in_bytes = (double)(8 * L);
-    unsigned long long tot = 0, fb = 0;
+    unsigned long long tsum = 0, fb = 0;
     int bad = 0;
     double rmin = 0.0, rsum = 0.0;
     if (tid == 0) {
@@ -227,7 +280,7 @@ __global__ void __launch_bounds__(256) engine_stats(const uint64_t *bytes, const
         for (int k = tid; k < m; k += 256) {
             const uint64_t b = bytes[base + k];
             ratio[k] = ddiv(in_bytes, (double)b);
-            tot += b;
+            tsum += b;
             fb += (params[base + k].flags & kFlagFallback) ? 1 : 0;
             bad |= err[base + k] != 0;
         }
@@ -240,27 +293,24 @@ __global__ void __launch_bounds__(256) engine_stats(const uint64_t *bytes, const
             }
         __syncthreads();
     }
-    tot = Red(red).Sum(tot);
+    tsum = Red(tmp.red).Sum(tsum);
     __syncthreads();
-    fb = Red(red).Sum(fb);
+    fb = Red(tmp.red).Sum(fb);
     bad = __syncthreads_or(bad);
     if (tid == 0) {
         st->ratio_min = rmin;
         st->ratio_sum = rsum;
         st->calls += (unsigned long long)planes;
-        st->current = tot;
-        if (tot > st->peak) st->peak = tot;
+        st->current = tsum;
+        if (tsum > st->peak) st->peak = tsum;
         st->fallback += fb;
         if (st->status == kEngOk && bad) {
             st->status = kEngDepth;
             st->status_gate = gate;
         }
-        if (st->status == kEngOk && *overflow) {
-            st->status = kEngOverflow;
-            st->status_gate = gate;
-        }
     }
 }
+
 // ------------------------------------------------ on-device state comparison
 // Two decoded states ([slot][re|im][L], same layout): per 1024-element tile,
 // pairwise trees of conj(a).b (re, im), |a|^2, |b|^2 and the max |a - b|

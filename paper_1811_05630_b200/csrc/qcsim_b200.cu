@@ -257,6 +257,8 @@ struct EncScratch {
     uint64_t param_planes = 0;       // params valid for this many planes ...
     qcsim_codec_config param_cfg{};  // ... under this config
     DecTables dec_out{};             // where enc_codebook writes decode tables (optional)
+    EngineDevStats *stats_out = nullptr; // deferred engine: run metrics fused into the slot scan
+    unsigned long long stats_gate = 0;
 
     void ensure(uint64_t planes, uint64_t units, uint64_t L, int qb) {
         const uint64_t ntiles = (L + kTile - 1) / kTile;
@@ -603,7 +605,11 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     }
 
     // slot offsets: exclusive scan of slot sizes (16-byte aligned slots)
-    {
+    if (S.stats_out) {
+        PROF("slot_scan_stats", st);
+        slot_scan_stats<<<1, 256, 0, st>>>(S.slot_bytes.p, S.slot_off.p, S.block_bytes.p, S.err.p, S.params.p,
+                                           (int)planes, L, S.stats_gate, S.stats_out);
+    } else {
         PROF("slot_scan", st);
         slot_scan<<<1, 256, 0, st>>>(S.slot_bytes.p, S.slot_off.p, (int)planes);
     }
@@ -637,7 +643,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     S.planes = planes;
     CK(cudaMemsetAsync(S.overflow.p, 0, sizeof(uint32_t), st));
     launch_pack(st, S, arena);
-    if (!host_results) return; // deferred engine: engine_stats consumes them on the device
+    if (!host_results) return; // deferred engine: slot_scan_stats consumes them on the device
     // results for the host, one batch of async copies into pinned memory
     S.h_bytes.ensure(planes);
     S.h_off.ensure(planes);
@@ -878,6 +884,7 @@ struct qcsim_engine {
     // deferred gate loop (no host round trip per gate): device scale,
     // device metrics, latched errors
     bool deferred = false;
+    bool defer_fresh = false; // no pass has run yet in this deferred run
     DBuf<double> norm_buf[2], dev_scale;
     DBuf<EngineDevStats> dev_stats;
     HBuf<EngineDevStats> h_stats;
@@ -964,19 +971,14 @@ template <class Src> void engine_store(qcsim_engine *e, const Src &src) {
         e->index[nxt].ensure(2 * e->ns * e->nidx);
         e->dec[nxt].ensure(2 * e->ns, e->L, e->cfg.codec.quant_code_bits);
         e->enc.dec_out = e->dec[nxt].tables();
+        e->enc.stats_out = e->dev_stats.p;
+        e->enc.stats_gate = e->gates;
         encode_launch<2, Src>(e->st, e->enc, src, units, e->L, e->cfg.codec, e->log2C, e->index[nxt].p,
                               e->arena[nxt], false, false, /*host_results=*/false);
         e->enc.dec_out = DecTables{};
-        {
-            PROF("slice_norms", e->st);
-            slice_norms<<<(units + 127) / 128, 128, 0, e->st>>>(e->enc.tilesum.p, (int)ntiles, units, e->slice_sq.p);
-        }
-        {
-            PROF("engine_stats", e->st);
-            engine_stats<<<1, 256, 0, e->st>>>(e->enc.block_bytes.p, e->enc.err.p, e->enc.params.p, e->enc.overflow.p,
-                                               (int)(2 * e->ns), e->L, (unsigned long long)e->gates,
-                                               e->dev_stats.p);
-        }
+        e->enc.stats_out = nullptr;
+        e->defer_fresh = false; // slice norms: next pass's engine_norm, or engine_defer_end
+        (void)ntiles;
         e->blk_off[nxt].ensure(2 * e->ns);
         CK(cudaMemcpyAsync(e->blk_off[nxt].p, e->enc.blk_off.p, 2 * e->ns * sizeof(uint64_t),
                            cudaMemcpyDeviceToDevice, e->st));
@@ -1123,9 +1125,14 @@ void engine_gate(qcsim_engine *e, const qcsim_action &a) {
     double scale = 1.0;
     if (apply && e->deferred) {
         PROF("engine_norm", e->st);
-        engine_norm<<<1, 256, 0, e->st>>>(e->slice_sq.p, e->norm_buf[0].p, e->norm_buf[1].p, e->S,
+        // slice norms of the previous pass from its tile partials (or, for the
+        // first gate of a run, the norms uploaded by engine_defer_begin)
+        const uint64_t ntl = (e->L + kTile - 1) / kTile;
+        engine_norm<<<1, 256, 0, e->st>>>(e->defer_fresh ? nullptr : e->enc.tilesum.p, (int)ntl, e->slice_sq.p,
+                                          e->norm_buf[0].p, e->norm_buf[1].p, e->S,
                                           10.0 * e->cfg.norm_drift_tolerance, (unsigned long long)e->gates,
-                                          e->dev_scale.p, e->dev_stats.p);
+                                          e->dev_scale.p, e->defer_fresh ? nullptr : e->enc.overflow.p,
+                                          e->dev_stats.p);
     } else if (apply) {
         const double G = tree_sum_host(e->sq_norm.data(), e->S);
         if (!std::isfinite(G) || std::fabs(G - 1.0) > 10.0 * e->cfg.norm_drift_tolerance) {
@@ -1243,6 +1250,7 @@ bool engine_defer_begin(qcsim_engine *e) {
     CK(cudaMemcpyAsync(e->dev_stats.p, e->h_stats.p, sizeof h, cudaMemcpyHostToDevice, e->st));
     CK(cudaStreamSynchronize(e->st));
     e->deferred = true;
+    e->defer_fresh = true;
     return true;
 }
 
@@ -1250,6 +1258,14 @@ bool engine_defer_begin(qcsim_engine *e) {
 // latched errors raised.
 void engine_defer_end(qcsim_engine *e, bool raise_errors) {
     e->deferred = false;
+    if (!e->defer_fresh) { // slice norms of the last pass, from its tile partials
+        const uint64_t ntiles = (e->L + kTile - 1) / kTile;
+        PROF("slice_norms", e->st);
+        slice_norms<<<(unsigned)((e->ns + 127) / 128), 128, 0, e->st>>>(e->enc.tilesum.p, (int)ntiles, (int)e->ns,
+                                                                         e->slice_sq.p);
+    }
+    uint32_t ovf = 0;
+    if (!e->defer_fresh) CK(cudaMemcpyAsync(&ovf, e->enc.overflow.p, 4, cudaMemcpyDeviceToHost, e->st));
     CK(cudaStreamSynchronize(e->st));
     g_prof.flush();
     CK(cudaGetLastError());
@@ -1278,7 +1294,7 @@ void engine_defer_end(qcsim_engine *e, bool raise_errors) {
         raise(QCSIM_NUMERIC, buf);
     }
     if (h.status == kEngDepth) raise(QCSIM_CODEC, "prefix code depth out of range");
-    if (h.status == kEngOverflow) raise(QCSIM_NOMEM, "compressed arena overflow");
+    if (h.status == kEngOverflow || ovf) raise(QCSIM_NOMEM, "compressed arena overflow");
 }
 
 } // namespace
