@@ -16,7 +16,7 @@
 //   C  enc_chain     exact d += RN(q*m^) over events (codec.cpp:445)
 //   T4 enc_verify    every decision re-evaluated with the exact prediction
 //                    (codec.cpp:440-451); refuted planes -> enc_serial_x
-//   TA tok_stats     run boundaries / outliers per tile (codec.cpp:468-482)
+//   (T4 also writes the tiles' run boundaries / outliers, codec.cpp:468-482)
 //   S  scans         run start/end across tiles, outlier offsets
 //   TB tok_count     tokens per element, histogram (codec.cpp:484-488)
 //   S  scan          token offsets
@@ -43,6 +43,10 @@ struct TileArgs {
     double *evD;           // [plane][L] lattice estimate of d per event ordinal (chain_scan.cuh)
     unsigned long long *lb; // [plane][ntiles] event-offset look-back slots (epoch-tagged)
     uint32_t lb_epoch;
+    // run statistics of the final symbols (tokenizer input, codec.cpp:468-482),
+    // written by enc_verify / enc_serial_x: first / last run start and
+    // outliers per tile
+    int32_t *t_firstb, *t_lastb, *t_nout;
     IndexRec *index;       // [plane][nidx]
     // per plane-tile, stride ntiles (+1 for scanned arrays)
     int32_t *t_lastout;    // last speculative outlier in the tile (-1)
@@ -660,6 +664,38 @@ __global__ void __launch_bounds__(kEncThreads) enc_verify(TileArgs A, int planes
     const uint64_t nidx = (L >> A.log2C) + 1;
     const double *x = A.x + (uint64_t)pl * L;
     IndexRec *idx = A.index + (uint64_t)pl * nidx;
+    __shared__ int s_fb, s_lb, s_no;
+    if (tid == 0) {
+        s_fb = 0x7FFFFFFF;
+        s_lb = -1;
+        s_no = 0;
+    }
+    __syncthreads();
+    const uint32_t *fsym = A.sym + (uint64_t)pl * L;
+    auto tile_stats = [&](const uint32_t *sv) { // sv[e]: final symbol of element tid*4+e
+        int fb = 0x7FFFFFFF, lb = -1, no = 0;
+        uint32_t prev = (t0 + tid * kPerThread > 0 && tid * kPerThread < tl) ? fsym[t0 + tid * kPerThread - 1] : 0u;
+        for (int e = 0; e < kPerThread; ++e) {
+            const int k = tid * kPerThread + e;
+            if (k >= tl) break;
+            const uint64_t i = t0 + k;
+            if (i == 0 || sv[e] != prev) {
+                fb = min(fb, (int)i);
+                lb = max(lb, (int)i);
+            }
+            no += sv[e] == kOutlierSym;
+            prev = sv[e];
+        }
+        if (fb != 0x7FFFFFFF) atomicMin(&s_fb, fb);
+        if (lb >= 0) atomicMax(&s_lb, lb);
+        if (no) atomicAdd(&s_no, no);
+        __syncthreads();
+        if (tid == 0) {
+            A.t_firstb[(uint64_t)pl * A.ntiles + t] = s_fb;
+            A.t_lastb[(uint64_t)pl * A.ntiles + t] = s_lb;
+            A.t_nout[(uint64_t)pl * A.ntiles + t] = s_no;
+        }
+    };
     if (pp.eb == 0.0) {
         // lossless: d == x; only the decode index needs d[e-1], d[e-2]
         for (int k = tid; k < tl; k += kEncThreads) {
@@ -669,6 +705,12 @@ __global__ void __launch_bounds__(kEncThreads) enc_verify(TileArgs A, int planes
                 idx[i >> A.log2C].dprev2 = i > 1 ? x[i - 2] : 0.0;
             }
         }
+        uint32_t sv[kPerThread];
+        for (int e = 0; e < kPerThread; ++e) {
+            const int k = tid * kPerThread + e;
+            sv[e] = k < tl ? fsym[t0 + k] : 0u;
+        }
+        tile_stats(sv);
         return;
     }
     using ScanI = cub::BlockScan<int, kEncThreads>;
@@ -703,8 +745,10 @@ __global__ void __launch_bounds__(kEncThreads) enc_verify(TileArgs A, int planes
         return;
     }
     int bad = 0;
+    uint32_t sv[kPerThread];
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
+        sv[e] = 0;
         if (k >= tl) continue;
         const uint64_t i = t0 + k;
         const uint32_t ord = evbase + (uint32_t)rank[e]; // events before i
@@ -713,14 +757,15 @@ __global__ void __launch_bounds__(kEncThreads) enc_verify(TileArgs A, int planes
         double rec = 0.0;
         const uint32_t sy = quantize(x[i], pred, pp.q, pp.inv_q, pp.eb, half, &rec);
         if (sy == kOutlierSym) rec = x[i];
-        if (sy != sym[i] || bits_of(rec) != bits_of(dspec)) bad = 1;
+        sv[e] = sym[i];
+        if (sy != sv[e] || bits_of(rec) != bits_of(dspec)) bad = 1;
         if ((i & (C - 1)) == 0) {
             idx[i >> A.log2C].dprev = pred;
             idx[i >> A.log2C].dprev2 = 0.0; // unused by the previous-value predictor
         }
     }
     if (bad) s_bad = 1;
-    __syncthreads();
+    tile_stats(sv); // (a refuted plane gets them again from enc_serial_x)
     if (tid == 0 && s_bad) atomicOr(&A.params[pl].flags, kFlagFallback);
 }
 
@@ -739,6 +784,8 @@ __global__ void enc_serial_x(TileArgs A, int planes) {
     uint32_t *sym = A.sym + (uint64_t)pl * L;
     IndexRec *idx = A.index + (uint64_t)pl * nidx;
     double d1 = 0.0, d2 = 0.0;
+    int fb = 0x7FFFFFFF, lb = -1, no = 0; // run statistics of the current tile
+    uint32_t prev = 0;
     for (uint64_t i = 0; i < L; ++i) {
         if ((i & (C - 1)) == 0) {
             idx[i >> A.log2C].dprev = d1;
@@ -766,6 +813,21 @@ __global__ void enc_serial_x(TileArgs A, int planes) {
         sym[i] = sy;
         d2 = d1;
         d1 = rec;
+        if (i == 0 || sy != prev) {
+            fb = min(fb, (int)i);
+            lb = max(lb, (int)i);
+        }
+        no += sy == kOutlierSym;
+        prev = sy;
+        if ((i + 1) % kTile == 0 || i + 1 == L) {
+            const uint64_t t = i / kTile;
+            A.t_firstb[(uint64_t)pl * A.ntiles + t] = fb;
+            A.t_lastb[(uint64_t)pl * A.ntiles + t] = lb;
+            A.t_nout[(uint64_t)pl * A.ntiles + t] = no;
+            fb = 0x7FFFFFFF;
+            lb = -1;
+            no = 0;
+        }
     }
 }
 
@@ -792,39 +854,6 @@ struct TokArgs {
     uint64_t L;
     int ntiles, log2C, qb;
 };
-
-// A run starts at i when i == 0 or sym[i] != sym[i-1].
-__global__ void __launch_bounds__(kEncThreads) tok_stats(TokArgs A, int planes) {
-    const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
-    if (pl >= planes) return;
-    const int tid = threadIdx.x;
-    const uint64_t L = A.L;
-    const uint64_t t0 = (uint64_t)t * kTile;
-    const int tl = (int)tmin<uint64_t>(kTile, L - t0);
-    const uint32_t *sym = A.sym + (uint64_t)pl * L;
-    using RedI = cub::BlockReduce<int, kEncThreads>;
-    __shared__ typename RedI::TempStorage r1, r2, r3;
-    int fb = 0x7FFFFFFF, lb = -1, no = 0;
-    for (int e = 0; e < kPerThread; ++e) {
-        const int k = tid * kPerThread + e;
-        if (k >= tl) continue;
-        const uint64_t i = t0 + k;
-        const uint32_t s = sym[i];
-        if (i == 0 || s != sym[i - 1]) {
-            fb = min(fb, (int)i);
-            lb = max(lb, (int)i);
-        }
-        no += s == kOutlierSym;
-    }
-    const int FB = RedI(r1).Reduce(fb, cub::Min());
-    const int LB = RedI(r2).Reduce(lb, cub::Max());
-    const int NO = RedI(r3).Sum(no);
-    if (tid == 0) {
-        A.t_firstb[(uint64_t)pl * A.ntiles + t] = FB;
-        A.t_lastb[(uint64_t)pl * A.ntiles + t] = LB;
-        A.t_nout[(uint64_t)pl * A.ntiles + t] = NO;
-    }
-}
 
 struct RunInfo {
     uint64_t start, end;

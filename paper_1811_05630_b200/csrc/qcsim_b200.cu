@@ -431,6 +431,9 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     A.evc = S.evc.p;
     A.dval = S.dval.p;
     A.evD = S.evD.p;
+    A.t_firstb = S.t_firstb.p;
+    A.t_lastb = S.t_lastb.p;
+    A.t_nout = S.t_nout.p;
     A.index = index;
     A.t_lastout = S.t_lastout.p;
     A.t_base = S.t_base.p;
@@ -561,10 +564,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     T.ntiles = ntiles;
     T.log2C = log2C;
     T.qb = qb;
-    {
-        PROF("tok_stats", st);
-        tok_stats<<<tgrid_p, kEncThreads, 0, st>>>(T, (int)planes);
-    }
+    // (tile run statistics: written by enc_verify / enc_serial_x)
     launch_plane_scan(st, S.t_lastb.p, S.t_prevb.p, ntiles, (int)planes, kScanMaxExcl);
     launch_plane_scan(st, S.t_firstb.p, S.t_nextb.p, ntiles, (int)planes, kScanMinExclRev);
     launch_plane_scan(st, S.t_nout.p, S.t_ooff.p, ntiles, (int)planes, kScanSumExcl);
