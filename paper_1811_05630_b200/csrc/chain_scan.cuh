@@ -327,7 +327,17 @@ struct ChainLink {
     uint32_t *flag;  // [plane][cmax]
     int cmax;        // chunks per plane in the grid
     uint32_t epoch;  // this launch's flag value
+    unsigned long long *trace; // debug: per block 8 phase times (%globaltimer ns), see CS_TRACE
 };
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// phases: 0 start, 4 loaded, 5 alignments, 6 folded, 1 maps scanned,
+// 2 carry in, 3 end
+#define CS_TRACE(k) \
+    if (link.trace && threadIdx.x == 0) link.trace[8ull * blockIdx.x + (k)] = gtimer()
 
 #define CS_FAIL(code) atomicOr(&S.fail, 1 << (code))
 __global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int planes, ChainLink link, uint32_t *stats,
@@ -352,6 +362,7 @@ __global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int 
     extern __shared__ __align__(16) unsigned char cs_raw[];
     ChainScanSmem &S = *reinterpret_cast<ChainScanSmem *>(cs_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    CS_TRACE(0);
     const uint32_t *ev = A.evlist + (uint64_t)pl * L;
     const double *evc = A.evc + (uint64_t)pl * L;
     const double *evD = A.evD + (uint64_t)pl * L;
@@ -373,6 +384,7 @@ __global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int 
     }
     __syncthreads();
 
+    CS_TRACE(4);
     // ---- alignments: clamp scan from the weakest claim about the carry
     const int k0 = tid * kCsEpt;
     const int cnt = max(0, min(kCsEpt, n - k0));
@@ -405,6 +417,7 @@ __global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int 
     }
     __syncthreads();
 
+    CS_TRACE(5);
     // ---- fold my events into one map on deviations (thread 0 is resolved
     // from the carry instead)
     const int lsl = (tid - 1) * kCsPad + kCsEpt - 1; // left neighbour's last slot
@@ -456,6 +469,7 @@ __global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int 
     if (lane == 0 && pm) atomicOr(&S.pmask[warp], pm);
     __syncthreads();
 
+    CS_TRACE(6);
     int npts = 0;
 #pragma unroll
     for (int w = 0; w < kCsWarps; ++w) npts += __popc(S.pmask[w]);
@@ -499,6 +513,7 @@ __global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int 
     };
 
     // ---- the exact value before this chunk
+    CS_TRACE(1);
     if (tid == 0) {
         double cd = 0.0;
         if (ck > 0) {
@@ -510,6 +525,7 @@ __global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int 
     }
     __syncthreads();
     const double carry_d = S.dend[kCsThreads - 1];
+    CS_TRACE(2);
 
     if (serial_chunk) {
         if (tid < 32) {
@@ -598,6 +614,7 @@ __global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int 
             link.carry[(uint64_t)pl * link.cmax + ck] = S.dend[nthr - 1];
             st_release(link.flag + (uint64_t)pl * link.cmax + ck, link.epoch);
         }
+        CS_TRACE(3);
         if (stats) {
             atomicAdd(&stats[0], nresolve);
             if (failed) atomicAdd(&stats[1], 1u);
@@ -605,4 +622,5 @@ __global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int 
     }
 }
 #undef CS_FAIL
+#undef CS_TRACE
 } // namespace qcb

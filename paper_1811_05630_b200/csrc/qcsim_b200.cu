@@ -516,13 +516,37 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
             const int cmax = (int)((L + kCsChunk - 1) / kCsChunk);
             S.chain_carry.ensure(planes * cmax);
             if (S.chain_flag.ensure(planes * cmax, /*zero=*/true)) S.chain_epoch = 0;
-            ChainLink link{S.chain_carry.p, S.chain_flag.p, cmax, ++S.chain_epoch};
+            // debug: QCSIM_CHAIN_TRACE_AT = launch number -> per-block phase times to
+            // QCSIM_CHAIN_TRACE_FILE
+            static const long trace_at = std::getenv("QCSIM_CHAIN_TRACE_AT") ? std::atol(std::getenv("QCSIM_CHAIN_TRACE_AT")) : -1;
+            static long scan_calls = 0;
+            static DBuf<unsigned long long> trace_buf;
+            const bool tracing = trace_at >= 0 && scan_calls++ == trace_at;
+            if (tracing) {
+                trace_buf.ensure(8 * planes * cmax);
+                CK(cudaMemsetAsync(trace_buf.p, 0, 8 * planes * cmax * 8, st));
+            }
+            ChainLink link{S.chain_carry.p, S.chain_flag.p, cmax, ++S.chain_epoch, tracing ? trace_buf.p : nullptr};
             if (link.epoch == 0) { // wrapped: start over from clean flags
                 CK(cudaMemsetAsync(S.chain_flag.p, 0, S.chain_flag.cap * sizeof(uint32_t), st));
                 link.epoch = S.chain_epoch = 1;
             }
             enc_chain_scan<<<(unsigned)(planes * cmax), kCsThreads, kChainScanSmem, st>>>(A, (int)planes, link,
                                                                                         chain_stats(), chain_debug);
+            if (tracing) {
+                std::vector<unsigned long long> h(8 * planes * cmax);
+                std::vector<uint32_t> hn(planes * ntiles);
+                CK(cudaMemcpyAsync(h.data(), trace_buf.p, h.size() * 8, cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(hn.data(), S.t_nev.p, hn.size() * 4, cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                if (FILE *f = std::fopen(std::getenv("QCSIM_CHAIN_TRACE_FILE"), "wb")) {
+                    const uint64_t hdr[3] = {planes, (uint64_t)cmax, (uint64_t)ntiles};
+                    std::fwrite(hdr, 8, 3, f);
+                    std::fwrite(hn.data(), 4, hn.size(), f);
+                    std::fwrite(h.data(), 8, h.size(), f);
+                    std::fclose(f);
+                }
+            }
         } else if (chain_mode != 1) {
             PROF("enc_chain", st);
             const int nbufs = planes > 2 * 148 ? 2 : kChainBufs; // latency hidden by other warps
