@@ -342,6 +342,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define CS_FAIL(code) atomicOr(&S.fail, 1 << (code))
 __global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int planes, ChainLink link, uint32_t *stats,
                                                                 int debug) {
+    pdl_begin();
     const int pl = blockIdx.x % planes, ck = blockIdx.x / planes; // chunk-major: every plane's chain advances
     const PlaneParams pp = block_params(A.params, pl);
     if ((pp.flags & kFlagFallback) || pp.eb == 0.0) return;

@@ -11,6 +11,14 @@
 
 namespace qcb {
 
+// Programmatic Dependent Launch (host: launch_k): wait until the previous
+// kernel of the stream has completed and its writes are visible, then let
+// the next kernel be scheduled as this one drains.  No-ops without PDL.
+__device__ __forceinline__ void pdl_begin() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // codec.cpp:32-40
 constexpr uint32_t kOutlierSym = 0;
 constexpr uint32_t kMinRunLen = 5; // kMinRunRepeats + 1

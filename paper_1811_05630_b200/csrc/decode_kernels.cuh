@@ -43,6 +43,7 @@ __device__ __forceinline__ uint64_t load_le(const uint8_t *p, int bytes) {
 }
 
 __global__ void __launch_bounds__(256) dec_prepare(DecPlanes D, DecTables T, int planes) {
+    pdl_begin();
     const int pl = blockIdx.x;
     if (pl >= planes) return;
     const int tid = threadIdx.x;
@@ -148,6 +149,7 @@ constexpr size_t kDecSmem = sizeof(DecSmem);
 // parks its 32 chunks' windows in shared memory and stores them row by row
 // (256-byte coalesced rows instead of 32 scattered 8-byte stores).
 __global__ void __launch_bounds__(kDecThreads) dec_chunks(DecPlanes D, DecTables T, int planes) {
+    pdl_begin();
     extern __shared__ __align__(16) unsigned char dec_raw[];
     DecSmem &S = *reinterpret_cast<DecSmem *>(dec_raw);
     const uint64_t nchunks = (D.L + (1ull << D.log2C) - 1) >> D.log2C;
@@ -346,6 +348,7 @@ struct ByteBits {
 // Header (from_bytes) checks are done by the caller; this is
 // decompress_plane's payload part.  One thread per plane.
 __global__ void dec_validate(ValArgs A, int planes) {
+    pdl_begin();
     const int pl = blockIdx.x * blockDim.x + threadIdx.x;
     if (pl >= planes) return;
     const uint8_t *blk = A.blocks + A.blk_off[pl];

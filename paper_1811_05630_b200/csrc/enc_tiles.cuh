@@ -166,6 +166,7 @@ __device__ __forceinline__ int32_t carry_of(const int32_t *scanned, int scanned_
 // ------------------------------------------------------------------ T1
 template <int NP, class Src>
 __global__ void __launch_bounds__(kEncThreads) enc_x(TileArgs A, Src src, int units) {
+    pdl_begin();
     const int unit = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
     if (unit >= units) return;
     const int tid = threadIdx.x;
@@ -248,6 +249,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_x(TileArgs A, Src src, int un
 template <int ITEMS>
 __global__ void __launch_bounds__(256) plane_scan(const int32_t *in, int32_t *out, int ntiles, int planes, int kind,
                                                   int in_stride, int out_stride) {
+    pdl_begin();
     const int pl = blockIdx.x;
     if (pl >= planes) return;
     using Scan = cub::BlockScan<int32_t, 256>;
@@ -329,6 +331,7 @@ __device__ uint32_t lookback_exclusive(unsigned long long *slots, uint32_t epoch
 // Lattice codes, flags and the plane's event list (the compaction is fused:
 // the tile's event offset comes from the look-back above).
 __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int planes) {
+    pdl_begin();
     const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
     if (pl >= planes) return;
     const int tid = threadIdx.x;
@@ -488,6 +491,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int plane
 // Event list for planes with many tiles (the fused look-back in enc_lattice
 // would serialise hundreds of tiles): tile offsets from the plane scan.
 __global__ void __launch_bounds__(kEncThreads) enc_compact(TileArgs A, int planes) {
+    pdl_begin();
     const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
     if (pl >= planes) return;
     if (block_params(A.params, pl).flags & kFlagFallback) return;
@@ -567,6 +571,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
 }
 
 __global__ void __launch_bounds__(32) enc_chain(TileArgs A, int planes, int nbufs) {
+    pdl_begin();
     const int pl = blockIdx.x;
     if (pl >= planes) return;
     const int lane = threadIdx.x;
@@ -652,6 +657,7 @@ __global__ void __launch_bounds__(32) enc_chain(TileArgs A, int planes, int nbuf
 
 // ------------------------------------------------------------------ T4
 __global__ void __launch_bounds__(kEncThreads) enc_verify(TileArgs A, int planes) {
+    pdl_begin();
     const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
     if (pl >= planes) return;
     const PlaneParams pp = block_params(A.params, pl);
@@ -771,6 +777,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_verify(TileArgs A, int planes
 
 // E1f: exact serial closed loop for refuted / linear planes (x from A.x).
 __global__ void enc_serial_x(TileArgs A, int planes) {
+    pdl_begin();
     const int pl = blockIdx.x * blockDim.x + threadIdx.x;
     if (pl >= planes) return;
     const PlaneParams pp = A.params[pl];
@@ -927,6 +934,7 @@ __device__ __forceinline__ void element_runs(const TokArgs &A, const uint32_t *s
 }
 
 __global__ void __launch_bounds__(kEncThreads) tok_count(TokArgs A, int planes) {
+    pdl_begin();
     const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
     if (pl >= planes) return;
     const int tid = threadIdx.x;
@@ -1010,6 +1018,7 @@ __global__ void __launch_bounds__(kEncThreads) tok_count(TokArgs A, int planes) 
 }
 
 __global__ void __launch_bounds__(kEncThreads) tok_emit(TokArgs A, int planes) {
+    pdl_begin();
     const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
     if (pl >= planes) return;
     const int tid = threadIdx.x;

@@ -17,6 +17,7 @@ __global__ void __launch_bounds__(256) init_params(PlaneParams *params, Src src,
                                                    int mode, double bound, int predictor, uint32_t *nonfinite,
                                                    uint32_t *symrange, uint32_t *hspecial,
                                                    unsigned long long *gamma_bits) {
+    pdl_begin();
     const int unit = blockIdx.x;
     if (unit >= units) return;
     __shared__ double smin[NP][256], smax[NP][256];
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(256) init_params(PlaneParams *params, Src src,
 // Exclusive scan of the per-plane arena slot sizes (16-byte aligned slots):
 // out[p] = sum(in[0..p)), out[planes] = total.  One 1024-thread block.
 __global__ void __launch_bounds__(256) slot_scan(const uint64_t *in, uint64_t *out, int planes) {
+    pdl_begin();
     using Scan = cub::BlockScan<unsigned long long, 256>;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ unsigned long long carry;
@@ -102,6 +104,7 @@ __global__ void __launch_bounds__(256) slot_scan(const uint64_t *in, uint64_t *o
 // Per-slice sq_norm: adjacent-pair tree over the tile partials (the tile
 // partials are themselves the lower levels of the same tree).
 __global__ void slice_norms(const double *tilesum, int ntiles, int units, double *out) {
+    pdl_begin();
     const int u = blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= units) return;
     // ntiles is a power of two (L and kTile are); iterative pairwise levels
@@ -135,6 +138,7 @@ __global__ void slice_norms(const double *tilesum, int ntiles, int units, double
 // plus the same per-tile sq-norm partials the encoder produces.
 template <class Src>
 __global__ void __launch_bounds__(256) dense_gate(Src src, int units, uint64_t L, double *out, double *tilesum) {
+    pdl_begin();
     const int ntiles = (int)((L + kTile - 1) / kTile);
     const int unit = blockIdx.x / ntiles, t = blockIdx.x % ntiles;
     if (unit >= units) return;
@@ -183,6 +187,7 @@ struct EngineDevStats {
 __global__ void __launch_bounds__(256) engine_norm(const double *tilesum, int ntiles, double *sq, double *b0,
                                                    double *b1, uint64_t S, double tol10, unsigned long long gate,
                                                    double *scale, const uint32_t *overflow, EngineDevStats *st) {
+    pdl_begin();
     const int tid = threadIdx.x;
     // slice norms: one thread per slice over its (aligned power-of-two) tiles
     // (tilesum == nullptr: `sq` already holds them)
@@ -245,6 +250,7 @@ __global__ void __launch_bounds__(256) slot_scan_stats(const uint64_t *slot_byte
                                                        const uint64_t *bytes, const uint32_t *err,
                                                        const PlaneParams *params, int planes, uint64_t L,
                                                        unsigned long long gate, EngineDevStats *st) {
+    pdl_begin();
     using Scan = cub::BlockScan<unsigned long long, 256>;
     using Red = cub::BlockReduce<unsigned long long, 256>;
     __shared__ union {
@@ -317,6 +323,7 @@ __global__ void __launch_bounds__(256) slot_scan_stats(const uint64_t *slot_byte
 // (statevec.cpp:199-247 semantics; the host finishes the tile trees).
 __global__ void __launch_bounds__(256) state_compare(const double *a, const double *b, uint64_t L, int units,
                                                      double *part) {
+    pdl_begin();
     const int ntiles = (int)((L + kTile - 1) / kTile);
     const int unit = blockIdx.x / ntiles, t = blockIdx.x % ntiles;
     if (unit >= units) return;

@@ -123,6 +123,7 @@ __device__ void emit_dec_tables(const DecTables &T, int pl, uint32_t n, const ui
 // up to kSmallN symbols (the serial two-queue merge then runs on smem), in
 // per-plane global scratch beyond that.
 __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
+    pdl_begin();
     const int pl = blockIdx.x;
     if (pl >= planes) return;
     const int tid = threadIdx.x;
@@ -467,6 +468,7 @@ __device__ __forceinline__ uint32_t token_bits(const SCodebook &C, const PackArg
 
 // P1: bits of every 1024-token chunk (grid: planes x chunks).
 __global__ void __launch_bounds__(256) pack_count(PackArgs A, int planes, int nck, int32_t *cbits) {
+    pdl_begin();
     const int pl = blockIdx.x / nck, c = blockIdx.x % nck;
     if (pl >= planes) return;
     // zero this block's share of the plane's arena slot (stream words are
@@ -505,6 +507,7 @@ __global__ void __launch_bounds__(256) pack_count(PackArgs A, int planes, int nc
 
 // Zero the batch's arena range (stream words are OR-combined at chunk seams).
 __global__ void arena_zero(uint8_t *arena, uint64_t cap, const uint64_t *total_ptr) {
+    pdl_begin();
     const uint64_t total = *total_ptr + 64;
     if (total > cap) return;
     uint4 *w = reinterpret_cast<uint4 *>(arena);
@@ -518,6 +521,7 @@ __global__ void arena_zero(uint8_t *arena, uint64_t cap, const uint64_t *total_p
 // decode-index bit positions (grid: planes x chunks).
 __global__ void __launch_bounds__(256) pack_write(PackArgs A, int planes, int nck, const int32_t *coff,
                                                   const int32_t *cbits) {
+    pdl_begin();
     const int pl = blockIdx.x / nck, c = blockIdx.x % nck;
     if (pl >= planes) return;
     const int tid = threadIdx.x;

@@ -322,6 +322,30 @@ uint32_t *chain_stats() {
     return buf.p;
 }
 
+
+// Every kernel launch goes through here: Programmatic Dependent Launch lets
+// the next kernel of the stream be scheduled while this one drains (each
+// kernel starts with pdl_wait(), so it still sees all of its predecessor's
+// writes).  QCSIM_PDL=0 turns it off.
+template <class... KArgs, class... Args>
+void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {
+    static const bool pdl = [] {
+        const char *v = std::getenv("QCSIM_PDL");
+        return !(v && v[0] == '0');
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 template <class K> void set_smem(K kernel, size_t bytes) {
     CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
@@ -348,16 +372,16 @@ void launch_pack(cudaStream_t st, EncScratch &S, DBuf<uint8_t> &arena, bool coun
     if (count) {
         {
             PROF("pack_count", st); // also zeroes the plane slots
-            pack_count<<<grid, 256, 0, st>>>(P, (int)S.planes, nck, S.t_cbits.p);
+            launch_k(pack_count, grid, 256, 0, st, P, (int)S.planes, nck, S.t_cbits.p);
         }
         launch_plane_scan(st, S.t_cbits.p, S.t_coff.p, nck, (int)S.planes, kScanSumExcl);
     } else {
         PROF("arena_zero", st); // re-pack after an arena overflow
-        arena_zero<<<296, 256, 0, st>>>(arena.p, arena.cap, S.slot_off.p + S.planes);
+        launch_k(arena_zero, 296, 256, 0, st, arena.p, arena.cap, S.slot_off.p + S.planes);
     }
     {
         PROF("pack_write", st);
-        pack_write<<<grid, 256, 0, st>>>(P, (int)S.planes, nck, S.t_coff.p, S.t_cbits.p);
+        launch_k(pack_write, grid, 256, 0, st, P, (int)S.planes, nck, S.t_coff.p, S.t_cbits.p);
     }
 }
 
@@ -379,10 +403,10 @@ void launch_plane_scan(cudaStream_t st, const int32_t *in, int32_t *out, int nti
     if (ntiles <= kInlineTiles) return; // consumers compute the carry inline (carry_of)
     const int out_stride = kind == kScanSumExcl ? ntiles + 1 : ntiles;
     PROF("plane_scan", st);
-    if (ntiles <= 256) plane_scan<1><<<planes, 256, 0, st>>>(in, out, ntiles, planes, kind, ntiles, out_stride);
-    else if (ntiles <= 1024) plane_scan<4><<<planes, 256, 0, st>>>(in, out, ntiles, planes, kind, ntiles, out_stride);
-    else if (ntiles <= 4096) plane_scan<16><<<planes, 256, 0, st>>>(in, out, ntiles, planes, kind, ntiles, out_stride);
-    else if (ntiles <= 8192) plane_scan<32><<<planes, 256, 0, st>>>(in, out, ntiles, planes, kind, ntiles, out_stride);
+    if (ntiles <= 256) launch_k(plane_scan<1>, planes, 256, 0, st, in, out, ntiles, planes, kind, ntiles, out_stride);
+    else if (ntiles <= 1024) launch_k(plane_scan<4>, planes, 256, 0, st, in, out, ntiles, planes, kind, ntiles, out_stride);
+    else if (ntiles <= 4096) launch_k(plane_scan<16>, planes, 256, 0, st, in, out, ntiles, planes, kind, ntiles, out_stride);
+    else if (ntiles <= 8192) launch_k(plane_scan<32>, planes, 256, 0, st, in, out, ntiles, planes, kind, ntiles, out_stride);
     else raise(QCSIM_CAPACITY, "planes longer than 2^22 elements are not supported on the device path");
 }
 
@@ -408,7 +432,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
                               cfg.mode != QCSIM_MODE_RANGE_RELATIVE;
     if (check_finite || !params_fresh) {
         PROF("init_params", st);
-        init_params<NP, Src><<<units, 256, 0, st>>>(S.params.p, src, units, L, cfg.mode, cfg.bound, cfg.predictor,
+        launch_k(init_params<NP, Src>, units, 256, 0, st, S.params.p, src, units, L, cfg.mode, cfg.bound, cfg.predictor,
                                                     check_finite ? S.nonfinite.p : nullptr, S.symrange.p,
                                                     S.hspecial.p, S.gamma.p);
         S.param_planes = cfg.mode == QCSIM_MODE_RANGE_RELATIVE ? 0 : planes;
@@ -450,7 +474,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     A.t_nev = reinterpret_cast<uint32_t *>(S.t_nev.p);
     {
         PROF("enc_x", st);
-        enc_x<NP, Src><<<tgrid_u, kEncThreads, 0, st>>>(A, src, units);
+        launch_k(enc_x<NP, Src>, tgrid_u, kEncThreads, 0, st, A, src, units);
     }
     launch_plane_scan(st, S.t_lastout.p, S.t_base.p, ntiles, (int)planes, kScanMaxExcl);
     {
@@ -462,12 +486,12 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
         A.lb = S.lb.p;
         A.lb_epoch = S.lb_epoch;
         PROF("enc_lattice", st);
-        enc_lattice<<<tgrid_p, kEncThreads, 0, st>>>(A, (int)planes);
+        launch_k(enc_lattice, tgrid_p, kEncThreads, 0, st, A, (int)planes);
     }
     launch_plane_scan(st, S.t_nev.p, S.t_evoff.p, ntiles, (int)planes, kScanSumExcl);
     if (ntiles > kInlineTiles) {
         PROF("enc_compact", st);
-        enc_compact<<<tgrid_p, kEncThreads, 0, st>>>(A, (int)planes);
+        launch_k(enc_compact, tgrid_p, kEncThreads, 0, st, A, (int)planes);
     }
     {
         // debug: dump one encode call's event lists (QCSIM_CHAIN_DUMP_AT = call
@@ -531,7 +555,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
                 CK(cudaMemsetAsync(S.chain_flag.p, 0, S.chain_flag.cap * sizeof(uint32_t), st));
                 link.epoch = S.chain_epoch = 1;
             }
-            enc_chain_scan<<<(unsigned)(planes * cmax), kCsThreads, kChainScanSmem, st>>>(A, (int)planes, link,
+            launch_k(enc_chain_scan, (unsigned)(planes * cmax), kCsThreads, kChainScanSmem, st, A, (int)planes, link,
                                                                                         chain_stats(), chain_debug);
             if (tracing) {
                 std::vector<unsigned long long> h(8 * planes * cmax);
@@ -550,16 +574,16 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
         } else if (chain_mode != 1) {
             PROF("enc_chain", st);
             const int nbufs = planes > 2 * 148 ? 2 : kChainBufs; // latency hidden by other warps
-            enc_chain<<<(unsigned)planes, 32, chain_smem_bytes(nbufs), st>>>(A, (int)planes, nbufs);
+            launch_k(enc_chain, (unsigned)planes, 32, chain_smem_bytes(nbufs), st, A, (int)planes, nbufs);
         }
     }
     {
         PROF("enc_verify", st);
-        enc_verify<<<tgrid_p, kEncThreads, 0, st>>>(A, (int)planes);
+        launch_k(enc_verify, tgrid_p, kEncThreads, 0, st, A, (int)planes);
     }
     {
         PROF("enc_serial", st);
-        enc_serial_x<<<(unsigned)((planes + 31) / 32), 32, 0, st>>>(A, (int)planes);
+        launch_k(enc_serial_x, (unsigned)((planes + 31) / 32), 32, 0, st, A, (int)planes);
     }
 
     TokArgs T;
@@ -594,12 +618,12 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     launch_plane_scan(st, S.t_nout.p, S.t_ooff.p, ntiles, (int)planes, kScanSumExcl);
     {
         PROF("tok_count", st);
-        tok_count<<<tgrid_p, kEncThreads, 0, st>>>(T, (int)planes);
+        launch_k(tok_count, tgrid_p, kEncThreads, 0, st, T, (int)planes);
     }
     launch_plane_scan(st, S.t_ntok.p, S.t_tokoff.p, ntiles, (int)planes, kScanSumExcl);
     {
         PROF("tok_emit", st);
-        tok_emit<<<tgrid_p, kEncThreads, 0, st>>>(T, (int)planes);
+        launch_k(tok_emit, tgrid_p, kEncThreads, 0, st, T, (int)planes);
     }
 
     CodeBook B;
@@ -625,17 +649,17 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     B.dec = S.dec_out;
     {
         PROF("enc_codebook", st);
-        enc_codebook<<<(unsigned)planes, 256, 0, st>>>(B, (int)planes);
+        launch_k(enc_codebook, (unsigned)planes, 256, 0, st, B, (int)planes);
     }
 
     // slot offsets: exclusive scan of slot sizes (16-byte aligned slots)
     if (S.stats_out) {
         PROF("slot_scan_stats", st);
-        slot_scan_stats<<<1, 256, 0, st>>>(S.slot_bytes.p, S.slot_off.p, S.block_bytes.p, S.err.p, S.params.p,
+        launch_k(slot_scan_stats, 1, 256, 0, st, S.slot_bytes.p, S.slot_off.p, S.block_bytes.p, S.err.p, S.params.p,
                                            (int)planes, L, S.stats_gate, S.stats_out);
     } else {
         PROF("slot_scan", st);
-        slot_scan<<<1, 256, 0, st>>>(S.slot_bytes.p, S.slot_off.p, (int)planes);
+        launch_k(slot_scan, 1, 256, 0, st, S.slot_bytes.p, S.slot_off.p, (int)planes);
     }
 
     PackArgs P;
@@ -754,7 +778,7 @@ void decode_batch(cudaStream_t st, DecScratch &S, const uint8_t *arena, const ui
     D.log2C = log2C;
     if (prepare) {
         PROF("dec_prepare", st);
-        dec_prepare<<<planes, 256, 0, st>>>(D, T, planes);
+        launch_k(dec_prepare, planes, 256, 0, st, D, T, planes);
     }
     const uint64_t nchunks = (L + (1ull << log2C) - 1) >> log2C;
     const uint64_t groups = (nchunks + kDecThreads - 1) / kDecThreads;
@@ -765,7 +789,7 @@ void decode_batch(cudaStream_t st, DecScratch &S, const uint8_t *arena, const ui
             attr = true;
         }
         PROF("dec_chunks", st);
-        dec_chunks<<<(unsigned)(groups * planes), kDecThreads, kDecSmem, st>>>(D, T, planes);
+        launch_k(dec_chunks, (unsigned)(groups * planes), kDecThreads, kDecSmem, st, D, T, planes);
     }
 }
 
@@ -1021,14 +1045,14 @@ template <class Src> void engine_store(qcsim_engine *e, const Src &src) {
         e->dense[nxt].ensure(e->ns * 2 * e->L);
         e->enc.tilesum.ensure(e->ns * ntiles);
         PROF("dense_gate", e->st);
-        dense_gate<Src><<<(unsigned)(units * ntiles), 256, 0, e->st>>>(src, units, e->L, e->dense[nxt].p,
+        launch_k(dense_gate<Src>, (unsigned)(units * ntiles), 256, 0, e->st, src, units, e->L, e->dense[nxt].p,
                                                                         e->enc.tilesum.p);
     }
     // per-slice sq_norm from the tile partials
     e->slice_sq.ensure(e->ns);
     {
         PROF("slice_norms", e->st);
-        slice_norms<<<(units + 127) / 128, 128, 0, e->st>>>(e->enc.tilesum.p, (int)ntiles, units, e->slice_sq.p);
+        launch_k(slice_norms, (units + 127) / 128, 128, 0, e->st, e->enc.tilesum.p, (int)ntiles, units, e->slice_sq.p);
     }
     e->h_sq.ensure(e->ns);
     CK(cudaMemcpyAsync(e->h_sq.p, e->slice_sq.p, e->ns * sizeof(double), cudaMemcpyDeviceToHost, e->st));
@@ -1127,7 +1151,7 @@ void engine_decode_old(qcsim_engine *e, bool need_imported) {
         V.cap = vcap;
         {
             PROF("dec_validate", e->st);
-            dec_validate<<<(unsigned)((offs.size() + 31) / 32), 32, 0, e->st>>>(V, (int)offs.size());
+            launch_k(dec_validate, (unsigned)((offs.size() + 31) / 32), 32, 0, e->st, V, (int)offs.size());
         }
         std::vector<uint32_t> errs(offs.size());
         CK(cudaMemcpyAsync(errs.data(), e->val.err.p, errs.size() * 4, cudaMemcpyDeviceToHost, e->st));
@@ -1152,7 +1176,7 @@ void engine_gate(qcsim_engine *e, const qcsim_action &a) {
         // slice norms of the previous pass from its tile partials (or, for the
         // first gate of a run, the norms uploaded by engine_defer_begin)
         const uint64_t ntl = (e->L + kTile - 1) / kTile;
-        engine_norm<<<1, 256, 0, e->st>>>(e->defer_fresh ? nullptr : e->enc.tilesum.p, (int)ntl, e->slice_sq.p,
+        launch_k(engine_norm, 1, 256, 0, e->st, e->defer_fresh ? nullptr : e->enc.tilesum.p, (int)ntl, e->slice_sq.p,
                                           e->norm_buf[0].p, e->norm_buf[1].p, e->S,
                                           10.0 * e->cfg.norm_drift_tolerance, (unsigned long long)e->gates,
                                           e->dev_scale.p, e->defer_fresh ? nullptr : e->enc.overflow.p,
@@ -1285,7 +1309,7 @@ void engine_defer_end(qcsim_engine *e, bool raise_errors) {
     if (!e->defer_fresh) { // slice norms of the last pass, from its tile partials
         const uint64_t ntiles = (e->L + kTile - 1) / kTile;
         PROF("slice_norms", e->st);
-        slice_norms<<<(unsigned)((e->ns + 127) / 128), 128, 0, e->st>>>(e->enc.tilesum.p, (int)ntiles, (int)e->ns,
+        launch_k(slice_norms, (unsigned)((e->ns + 127) / 128), 128, 0, e->st, e->enc.tilesum.p, (int)ntiles, (int)e->ns,
                                                                          e->slice_sq.p);
     }
     uint32_t ovf = 0;
@@ -1480,7 +1504,7 @@ qcsim_status qcsim_decompress_plane(const uint8_t *block, uint64_t len, double *
         V.cap = cap;
         {
             PROF("dec_validate", C.st);
-            dec_validate<<<1, 32, 0, C.st>>>(V, 1);
+            launch_k(dec_validate, 1, 32, 0, C.st, V, 1);
         }
         uint32_t e = 0;
         CK(cudaMemcpyAsync(&e, C.val.err.p, 4, cudaMemcpyDeviceToHost, C.st));
@@ -1573,7 +1597,7 @@ qcsim_status qcsim_decompress_planes_device(const uint8_t *blocks, const uint64_
         V.cap = maxtc;
         {
             PROF("dec_validate", st);
-            dec_validate<<<(planes + 31) / 32, 32, 0, st>>>(V, (int)planes);
+            launch_k(dec_validate, (planes + 31) / 32, 32, 0, st, V, (int)planes);
         }
         std::vector<uint32_t> errs(planes);
         CK(cudaMemcpyAsync(errs.data(), C.val.err.p, planes * 4, cudaMemcpyDeviceToHost, st));
@@ -1753,7 +1777,7 @@ qcsim_status qcsim_engine_compare(qcsim_engine *a, qcsim_engine *b, qcsim_compar
         part.ensure(5 * tiles);
         {
             PROF("state_compare", a->st);
-            state_compare<<<(unsigned)tiles, 256, 0, a->st>>>(a->old.p, b->old.p, a->L, (int)a->ns, part.p);
+            launch_k(state_compare, (unsigned)tiles, 256, 0, a->st, a->old.p, b->old.p, a->L, (int)a->ns, part.p);
         }
         std::vector<double> h(5 * tiles);
         CK(cudaMemcpyAsync(h.data(), part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, a->st));
