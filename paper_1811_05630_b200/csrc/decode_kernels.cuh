@@ -134,7 +134,7 @@ __device__ __forceinline__ uint64_t peek64(const uint32_t *w, uint64_t bp) {
 
 constexpr int kDecThreads = 128;             // chunks per block
 constexpr int kDecStageWords = 4096;         // 16 KB of stream staged per block
-constexpr int kDecWin = 32;                  // output window per chunk (C is a multiple)
+constexpr int kDecWin = 16;                  // output window per chunk (C is a multiple)
 struct DecSmem {
     uint32_t lut[1 << kLutBits];
     uint32_t sw[kDecStageWords + 4];
@@ -148,7 +148,7 @@ constexpr size_t kDecSmem = sizeof(DecSmem);
 // codec.cpp:591-626 for its chunk, kDecWin elements at a time: the warp
 // parks its 32 chunks' windows in shared memory and stores them row by row
 // (256-byte coalesced rows instead of 32 scattered 8-byte stores).
-__global__ void __launch_bounds__(kDecThreads) dec_chunks(DecPlanes D, DecTables T, int planes) {
+__global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTables T, int planes) {
     pdl_begin();
     extern __shared__ __align__(16) unsigned char dec_raw[];
     DecSmem &S = *reinterpret_cast<DecSmem *>(dec_raw);
@@ -288,12 +288,12 @@ __global__ void __launch_bounds__(kDecThreads) dec_chunks(DecPlanes D, DecTables
             }
         }
         __syncwarp();
-        // the warp's 32 chunk windows, one coalesced row per chunk
-        for (int rr = 0; rr < 32; ++rr) {
+        // the warp's 32 chunk windows, coalesced kDecWin-element rows
+        for (int q = lane; q < 32 * kDecWin; q += 32) {
+            const int rr = q / kDecWin, col = q % kDecWin;
             const uint64_t jr = jw + rr;
-            if (jr >= jend) break;
-            const uint64_t e = (jr << D.log2C) + w0 + lane;
-            if (w0 + lane < C && e < D.L) out[e] = S.sout[wid][rr][lane];
+            const uint64_t e = (jr << D.log2C) + w0 + col;
+            if (jr < jend && w0 + col < C && e < D.L) out[e] = S.sout[wid][rr][col];
         }
         __syncwarp();
     }
