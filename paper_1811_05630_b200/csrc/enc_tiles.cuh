@@ -143,6 +143,34 @@ __device__ void tile_carry2(const int32_t *a1, int k1, const int32_t *a2, int k2
     r2 = s_res2[1];
     __syncthreads();
 }
+// N exclusive carries of tile t in one warp pass and one barrier pair.
+template <int N>
+__device__ void tile_carryN(const int32_t *const *a, const int *kinds, int t, int ntiles, int32_t *r) {
+    __shared__ int32_t s_resn[N];
+    if (threadIdx.x < 32) {
+        int32_t v[N];
+#pragma unroll
+        for (int q = 0; q < N; ++q) v[q] = carry_init(kinds[q]);
+        for (int k = (int)threadIdx.x; k < ntiles; k += 32) {
+#pragma unroll
+            for (int q = 0; q < N; ++q) {
+                const bool rev = kinds[q] == kScanMinExclRev;
+                if (rev ? k > t : k < t) v[q] = carry_reduce(kinds[q], v[q], a[q][k]);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < N; ++q)
+            for (int off = 16; off >= 1; off >>= 1) v[q] = carry_reduce(kinds[q], v[q], __shfl_xor_sync(0xffffffffu, v[q], off));
+        if (threadIdx.x == 0)
+#pragma unroll
+            for (int q = 0; q < N; ++q) s_resn[q] = v[q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < N; ++q) r[q] = s_resn[q];
+    __syncthreads();
+}
+
 // carry_of for two arrays of the same plane / tile at once
 __device__ __forceinline__ void carry_of2(const int32_t *sc1, int st1, const int32_t *raw1, int k1, const int32_t *sc2,
                                           int st2, const int32_t *raw2, int k2, int pl, int t, int ntiles,
@@ -870,7 +898,7 @@ struct RunInfo {
 template <class ScanI>
 __device__ __forceinline__ void element_runs(const TokArgs &A, const uint32_t *sym, int pl, int t, uint64_t t0,
                                              int tl, typename ScanI::TempStorage &tmp, int *s_next,
-                                             uint64_t *start, uint64_t *end) {
+                                             uint64_t *start, uint64_t *end, int32_t *bases = nullptr) {
     const int tid = threadIdx.x;
     int isb[kPerThread], st[kPerThread];
     uint32_t sv[kPerThread + 1];
@@ -880,8 +908,23 @@ __device__ __forceinline__ void element_runs(const TokArgs &A, const uint32_t *s
     }
     sv[0] = (t0 + tid * kPerThread > 0 && tid * kPerThread < tl) ? sym[t0 + tid * kPerThread - 1] : 0u;
     int32_t prevb, nextb_carry;
-    carry_of2(A.t_prevb, A.ntiles, A.t_lastb, kScanMaxExcl, A.t_nextb, A.ntiles, A.t_firstb, kScanMinExclRev, pl, t,
-              A.ntiles, prevb, nextb_carry);
+    if (bases && A.ntiles <= kInlineTiles) { // + token / outlier offsets of the tile (tok_emit)
+        const uint64_t o = (uint64_t)pl * A.ntiles;
+        const int32_t *arr[4] = {A.t_lastb + o, A.t_firstb + o, A.t_ntok + o, A.t_nout + o};
+        const int kinds[4] = {kScanMaxExcl, kScanMinExclRev, kScanSumExcl, kScanSumExcl};
+        int32_t r[4];
+        tile_carryN<4>(arr, kinds, t, A.ntiles, r);
+        prevb = r[0];
+        nextb_carry = r[1];
+        bases[0] = r[2];
+        bases[1] = r[3];
+    } else {
+        carry_of2(A.t_prevb, A.ntiles, A.t_lastb, kScanMaxExcl, A.t_nextb, A.ntiles, A.t_firstb, kScanMinExclRev, pl,
+                  t, A.ntiles, prevb, nextb_carry);
+        if (bases)
+            carry_of2(A.t_tokoff, A.ntiles + 1, A.t_ntok, kScanSumExcl, A.t_ooff, A.ntiles + 1, A.t_nout,
+                      kScanSumExcl, pl, t, A.ntiles, bases[0], bases[1]);
+    }
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
         const uint64_t i = t0 + k;
@@ -1037,7 +1080,8 @@ __global__ void __launch_bounds__(kEncThreads) tok_emit(TokArgs A, int planes) {
     uint32_t *trep = A.trep + (uint64_t)pl * (L + 1);
     IndexRec *idx = A.index + (uint64_t)pl * nidx;
     uint64_t start[kPerThread], end[kPerThread];
-    element_runs<ScanI>(A, sym, pl, t, t0, tl, tmp, s_next, start, end);
+    int32_t bases[2];
+    element_runs<ScanI>(A, sym, pl, t, t0, tl, tmp, s_next, start, end, bases);
     int cnt[kPerThread], tpos[kPerThread], isout[kPerThread], opos[kPerThread];
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
@@ -1052,13 +1096,11 @@ __global__ void __launch_bounds__(kEncThreads) tok_emit(TokArgs A, int planes) {
         isout[e] = s == kOutlierSym;
     }
     __syncthreads();
-    ScanI(tmp).ExclusiveSum(cnt, tpos);
+    int tile_tok, tile_out;
+    ScanI(tmp).ExclusiveSum(cnt, tpos, tile_tok);
     __syncthreads();
-    ScanI(tmp).ExclusiveSum(isout, opos);
-    int32_t tokbase_i, obase_i;
-    carry_of2(A.t_tokoff, A.ntiles + 1, A.t_ntok, kScanSumExcl, A.t_ooff, A.ntiles + 1, A.t_nout, kScanSumExcl, pl, t,
-              A.ntiles, tokbase_i, obase_i);
-    const uint32_t tokbase = (uint32_t)tokbase_i, obase = (uint32_t)obase_i;
+    ScanI(tmp).ExclusiveSum(isout, opos, tile_out);
+    const uint32_t tokbase = (uint32_t)bases[0], obase = (uint32_t)bases[1];
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
         if (k >= tl) continue;
@@ -1105,13 +1147,9 @@ __global__ void __launch_bounds__(kEncThreads) tok_emit(TokArgs A, int planes) {
             }
         }
     }
-    if (t == A.ntiles - 1) { // uniform per block
-        const int32_t nt = carry_of(A.t_tokoff, A.ntiles + 1, A.t_ntok, pl, A.ntiles, A.ntiles, kScanSumExcl);
-        const int32_t no = carry_of(A.t_ooff, A.ntiles + 1, A.t_nout, pl, A.ntiles, A.ntiles, kScanSumExcl);
-        if (tid == 0) {
-            A.ntok[pl] = (uint32_t)nt;
-            A.ocount[pl] = (uint32_t)no;
-        }
+    if (t == A.ntiles - 1 && tid == 0) { // plane totals: the last tile's offsets + its own counts
+        A.ntok[pl] = tokbase + (uint32_t)tile_tok;
+        A.ocount[pl] = obase + (uint32_t)tile_out;
     }
 }
 
