@@ -171,6 +171,31 @@ __device__ void tile_carryN(const int32_t *const *a, const int *kinds, int t, in
     __syncthreads();
 }
 
+// Sum over tiles [0, t) and over all tiles of one per-tile array, one pass.
+__device__ void tile_excl_total(const int32_t *a, int t, int ntiles, int32_t &excl, int32_t &total) {
+    __shared__ int32_t s_et[2];
+    if (threadIdx.x < 32) {
+        int32_t v1 = 0, v2 = 0;
+        for (int k = (int)threadIdx.x; k < ntiles; k += 32) {
+            const int32_t x = a[k];
+            v2 += x;
+            if (k < t) v1 += x;
+        }
+        for (int off = 16; off >= 1; off >>= 1) {
+            v1 += __shfl_xor_sync(0xffffffffu, v1, off);
+            v2 += __shfl_xor_sync(0xffffffffu, v2, off);
+        }
+        if (threadIdx.x == 0) {
+            s_et[0] = v1;
+            s_et[1] = v2;
+        }
+    }
+    __syncthreads();
+    excl = s_et[0];
+    total = s_et[1];
+    __syncthreads();
+}
+
 // carry_of for two arrays of the same plane / tile at once
 __device__ __forceinline__ void carry_of2(const int32_t *sc1, int st1, const int32_t *raw1, int k1, const int32_t *sc2,
                                           int st2, const int32_t *raw2, int k2, int pl, int t, int ntiles,
@@ -755,21 +780,28 @@ __global__ void __launch_bounds__(kEncThreads) enc_verify(TileArgs A, int planes
     const uint8_t *fl = A.fl + (uint64_t)pl * L;
     uint32_t *sym = A.sym + (uint64_t)pl * L;
     const double *dv = A.dval + (uint64_t)pl * L;
-    const uint32_t evbase = (uint32_t)carry_of(reinterpret_cast<const int32_t *>(A.t_evoff), A.ntiles + 1,
-                                               reinterpret_cast<const int32_t *>(A.t_nev), pl, t, A.ntiles, kScanSumExcl);
     int f[kPerThread], rank[kPerThread];
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
         f[e] = (k < tl && (fl[t0 + k] & 1)) ? 1 : 0;
+    }
+    // event offset of the tile and the plane's event count, one carry pass
+    uint32_t evbase, nev_plane;
+    if (A.ntiles <= kInlineTiles) {
+        int32_t ex, tot;
+        tile_excl_total(reinterpret_cast<const int32_t *>(A.t_nev) + (uint64_t)pl * A.ntiles, t, A.ntiles, ex, tot);
+        evbase = (uint32_t)ex;
+        nev_plane = (uint32_t)tot;
+    } else {
+        const int32_t *eo = reinterpret_cast<const int32_t *>(A.t_evoff) + (uint64_t)pl * (A.ntiles + 1);
+        evbase = (uint32_t)eo[t];
+        nev_plane = (uint32_t)eo[A.ntiles];
     }
     int nf_tile;
     ScanI(scan_tmp).ExclusiveSum(f, rank, nf_tile);
     __syncthreads();
     // guard: the event ordinals of this tile must lie inside the plane's
     // event list (a violation means corrupt carries -> serial re-encode)
-    const uint32_t nev_plane = (uint32_t)carry_of(reinterpret_cast<const int32_t *>(A.t_evoff), A.ntiles + 1,
-                                                  reinterpret_cast<const int32_t *>(A.t_nev), pl, A.ntiles, A.ntiles,
-                                                  kScanSumExcl);
     if ((uint64_t)evbase + (uint64_t)nf_tile > (uint64_t)nev_plane || nev_plane > L) {
         if (tid == 0) {
             printf("qcsim enc_verify: plane %d tile %d evbase %u tile events %d plane events %u (L %llu)\n", pl, t,
