@@ -41,6 +41,7 @@ struct CodeBook {
     uint64_t cap;
     int qb;
     DecTables dec;             // optional: decode tables of the new blocks
+    unsigned long long *trace = nullptr; // debug phase stamps
 };
 
 enum : uint32_t { kErrDepth = 1 };
@@ -78,23 +79,27 @@ __device__ void emit_dec_tables(const DecTables &T, int pl, uint32_t n, const ui
                                 const uint64_t *code, const uint32_t *lcount, const uint64_t *lfirst0) {
     uint32_t *lut = T.lut + (uint64_t)pl * (1u << kLutBits);
     __shared__ uint32_t basei[kMaxCodeLen + 2];
-    if (threadIdx.x == 0) {
+    __shared__ uint32_t s_maxlen;
+    if (threadIdx.x == 0) { // shared memory only; the tables are written in parallel below
         uint32_t b = 0, maxlen = 0;
+        basei[0] = 0;
         for (int l = 1; l <= kMaxCodeLen; ++l) {
             basei[l] = b;
             b += lcount[l];
             if (lcount[l]) maxlen = l;
-            T.first[(uint64_t)pl * (kMaxCodeLen + 1) + l] = lcount[l] ? lfirst0[l] : 0;
-            T.count[(uint64_t)pl * (kMaxCodeLen + 1) + l] = lcount[l];
-            T.basei[(uint64_t)pl * (kMaxCodeLen + 1) + l] = basei[l];
         }
-        T.first[(uint64_t)pl * (kMaxCodeLen + 1)] = 0;
-        T.count[(uint64_t)pl * (kMaxCodeLen + 1)] = 0;
-        T.basei[(uint64_t)pl * (kMaxCodeLen + 1)] = 0;
+        s_maxlen = maxlen;
         T.meta[4 * pl] = maxlen;
         T.meta[4 * pl + 1] = n;
     }
     __syncthreads();
+    for (int l = threadIdx.x; l <= kMaxCodeLen; l += blockDim.x) {
+        const bool any = l > 0 && lcount[l];
+        T.first[(uint64_t)pl * (kMaxCodeLen + 1) + l] = any ? lfirst0[l] : 0;
+        T.count[(uint64_t)pl * (kMaxCodeLen + 1) + l] = l > 0 ? lcount[l] : 0;
+        T.basei[(uint64_t)pl * (kMaxCodeLen + 1) + l] = basei[l];
+    }
+    const int lmax = (int)min((uint32_t)kLutBits, s_maxlen);
     uint32_t *sorted = T.sorted + (uint64_t)pl * T.cap;
     for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
         const int l = len[r];
@@ -106,7 +111,7 @@ __device__ void emit_dec_tables(const DecTables &T, int pl, uint32_t n, const ui
     // (canonical first/count per length), one store per entry
     for (uint32_t k = threadIdx.x; k < (1u << kLutBits); k += blockDim.x) {
         uint32_t e = 0;
-        for (int l = 1; l <= kLutBits; ++l) {
+        for (int l = 1; l <= lmax; ++l) {
             const uint32_t c = lcount[l];
             if (!c) continue;
             const uint64_t w = (uint64_t)(k >> (kLutBits - l));
@@ -127,6 +132,14 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
     const int pl = blockIdx.x;
     if (pl >= planes) return;
     const int tid = threadIdx.x;
+    auto stamp = [&](int k) { // debug phase trace (B.trace: 16 stamps per plane)
+        if (B.trace && tid == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            B.trace[16ull * pl + k] = t;
+        }
+    };
+    stamp(0);
     using Scan = cub::BlockScan<int, 256>;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ uint64_t k_s[kSmallN];
@@ -135,7 +148,7 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
     __shared__ int32_t par_s[2 * kSmallN];
     __shared__ uint8_t len_s[kSmallN];
     __shared__ uint64_t code_s[kSmallN];
-    __shared__ uint32_t s_n, s_nodes;
+    __shared__ uint32_t s_n, s_nodes, s_lmax;
     __shared__ uint32_t lcount[kMaxCodeLen + 2];
     __shared__ uint64_t lfirst[kMaxCodeLen + 2], lfirst0[kMaxCodeLen + 2];
     __shared__ unsigned long long s_bits;
@@ -169,6 +182,7 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
 
     if (tid == 0) {
         s_n = (h0 ? 1u : 0u) + (uint32_t)tot_r;
+        s_lmax = 0;
         s_bits = 0;
         s_err = 0;
         if (h0) {
@@ -176,6 +190,7 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
             cnt[0] = h0;
         }
     }
+    stamp(1);
     // 1) compaction of the symbol range, ascending (freq, codec.cpp:484-488)
     {
         uint32_t o = (h0 ? 1u : 0u) + (uint32_t)pos_r;
@@ -200,10 +215,12 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
         if (tid == 0) B.err[pl] = 0;
         return;
     }
+    stamp(2);
     // 2) leaves sorted by (count, symbol)
     for (uint32_t i = tid; i < n; i += 256) keys[i] = ((uint64_t)cnt[i] << 25) | sym[i];
     __syncthreads();
     if (n > 1) block_bitonic(keys, n);
+    stamp(3);
     // 3) two-queue merge (codec.cpp:168-229; ties prefer the leaf queue)
     if (tid == 0) {
         if (n == 1) {
@@ -244,7 +261,7 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
             }
             par[nodes - 1] = -1;
             s_nodes = nodes;
-            if (!small) { // large alphabet: depths top-down, serially
+            if (!small || n <= 64) { // large or tiny alphabet: depths top-down, serially
                 nc[nodes - 1] = 0;
                 for (int64_t v = (int64_t)nodes - 2; v >= 0; --v) nc[v] = nc[par[v]] + 1;
             }
@@ -253,7 +270,7 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
     __syncthreads();
     // depths by pointer jumping (parents have larger indices; root -> 0),
     // stored in nc
-    if (n > 1 && small) {
+    if (n > 64 && small) {
         const uint32_t nodes = s_nodes;
         for (uint32_t v = tid; v < nodes; v += 256) {
             nc[v] = par[v] < 0 ? 0u : 1u; // distance to the current ancestor
@@ -290,6 +307,7 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
         }
     }
     __syncthreads();
+    stamp(4);
     // 4) lengths in symbol order
     for (uint32_t i = tid; i < n; i += 256) {
         const uint32_t s = (uint32_t)(keys[i] & ((1ull << 25) - 1));
@@ -304,16 +322,19 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
         const uint8_t l = (uint8_t)tmin<uint32_t>(depth, kMaxCodeLen);
         len[lo] = l;
         atomicAdd(&lcount[l], 1u);
+        atomicMax(&s_lmax, (uint32_t)l);
         atomicAdd(&s_bits, (unsigned long long)cnt[lo] * l);
     }
     __syncthreads();
+    stamp(5);
     // 5) canonical codes (codec.cpp:233-249): (len, sym) order == symbol
     //    order within a length
     if (tid == 0) {
         uint64_t c = 0;
         int prev = -1;
-        for (int l = 1; l <= kMaxCodeLen; ++l) {
-            lfirst[l] = 0;
+        const int lm = (int)s_lmax;
+        for (int l = 0; l <= kMaxCodeLen; ++l) lfirst[l] = 0;
+        for (int l = 1; l <= lm; ++l) {
             if (!lcount[l]) continue;
             if (prev >= 0) c <<= (l - prev);
             lfirst[l] = c;
@@ -346,6 +367,7 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
         }
     }
     __syncthreads();
+    stamp(6);
     if (small) { // publish the codebook for the packer
         for (uint32_t r = tid; r < n; r += 256) {
             B.sym[pl * cap + r] = sym_s[r];
@@ -353,7 +375,10 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
             B.code[pl * cap + r] = code_s[r];
         }
     }
+    stamp(7);
     if (B.dec.lut) emit_dec_tables(B.dec, pl, n, sym, len, code, lcount, lfirst0);
+    stamp(8);
+    if (B.trace && tid == 0) B.trace[16ull * pl + 9] = n;
 }
 
 // ------------------------------------------------------------------ E5

@@ -647,9 +647,28 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     B.cap = cap;
     B.qb = qb;
     B.dec = S.dec_out;
+    // debug: QCSIM_CB_TRACE_AT = encode call -> codebook phase stamps to QCSIM_CB_TRACE_FILE
+    static const long cb_at = std::getenv("QCSIM_CB_TRACE_AT") ? std::atol(std::getenv("QCSIM_CB_TRACE_AT")) : -1;
+    static long cb_calls = 0;
+    static DBuf<unsigned long long> cb_trace;
+    const bool cb_tracing = cb_at >= 0 && cb_calls++ == cb_at;
+    if (cb_tracing) {
+        cb_trace.ensure(16 * planes);
+        CK(cudaMemsetAsync(cb_trace.p, 0, 16 * planes * 8, st));
+        B.trace = cb_trace.p;
+    }
     {
         PROF("enc_codebook", st);
         launch_k(enc_codebook, (unsigned)planes, 256, 0, st, B, (int)planes);
+    }
+    if (cb_tracing) {
+        std::vector<unsigned long long> h(16 * planes);
+        CK(cudaMemcpyAsync(h.data(), cb_trace.p, h.size() * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (FILE *f = std::fopen(std::getenv("QCSIM_CB_TRACE_FILE"), "wb")) {
+            std::fwrite(h.data(), 8, h.size(), f);
+            std::fclose(f);
+        }
     }
 
     // slot offsets: exclusive scan of slot sizes (16-byte aligned slots)
