@@ -47,10 +47,12 @@ def measured_peaks():
 
 
 # ------------------------------------------------------------- workloads
-def workload(name):
+def workload(name, extra=0):
+    """extra: additional qubits (weak scaling: n + log2(world) keeps the
+    slices per GPU fixed)."""
     import paper_1811_05630_b200 as q
     if name == "grover20":
-        n, s, eb = 20, 14, 1e-5
+        n, s, eb = 20 + extra, 14, 1e-5
         marked = q.seeded_index(n, 20)
         iters = q.grover_optimal_iterations(n)
         oracle = q.build_grover_oracle(n, marked).gates
@@ -59,22 +61,23 @@ def workload(name):
         step = [q.to_action_c(q.gate_action(g)) for g in oracle + diff]
         setup = [q.to_action_c(q.gate_action(q.Gate.h(k))) for k in range(n)]
         return dict(name="grover20", n=n, s=s, eb=eb, basis=0, setup=setup, steps=lambda k: step,
-                    max_steps=iters, desc=f"grover n=20 marked={marked} iterations={iters}, slices 64x2^14")
+                    max_steps=iters, desc=f"grover n={n} marked={marked} iterations={iters}, slices {1 << (n - s)}x2^{s}")
     if name in ("qft28", "qft16"):
-        n = 28 if name == "qft28" else 16
-        s = 20 if n == 28 else 12
+        base = 28 if name == "qft28" else 16
+        n = base + extra
+        s = 20 if base == 28 else 12
         acts = q.lower(q.build_qft(n))
         x = q.seeded_index(n, n)
-        chunk = 35 if n == 28 else 12
+        chunk = 35 if base == 28 else 12
         return dict(name=name, n=n, s=s, eb=1e-5, basis=x, setup=[],
                     steps=lambda k: acts[k * chunk:(k + 1) * chunk], max_steps=len(acts) // chunk,
                     desc=f"qft n={n} basis={x}, slices {1 << (n - s)}x2^{s}, step = {chunk} gates")
     if name == "random30":
-        n, s = 30, 20
+        n, s = 30 + extra, 20
         acts = q.random_u3_circuit_actions(n, 20, seed=30)
         per = n + n // 2
         return dict(name=name, n=n, s=s, eb=1e-5, basis=0, setup=[], steps=lambda k: acts[k * per:(k + 1) * per],
-                    max_steps=20, desc="random U3+CZ n=30 depth 20, slices 1024x2^20, step = 1 layer")
+                    max_steps=20, desc=f"random U3+CZ n={n} depth 20, slices {1 << (n - s)}x2^20, step = 1 layer")
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -310,12 +313,14 @@ def main():
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         tdist.init_process_group("nccl")
         dist = tdist
-    wl = workload(args.workload)
+    extra = max(0, world.bit_length() - 1) if world > 1 else 0  # weak scaling: slices per GPU fixed
+    wl = workload(args.workload, extra)
     hbm, peak_kind = measured_peaks()
     config = {"workload": wl["name"], "detail": wl["desc"], "n_qubits": wl["n"], "slice_bits": wl["s"],
               "error_bound": wl["eb"], "mode": "absolute", "quant_code_bits": 16, "predictor": "previous",
               "step": "one Grover iteration" if wl["name"] == "grover20" else "gate chunk",
-              "l2": "flushed between timed steps (256 MiB write)", "norm": "every gate"}
+              "l2": "flushed between timed steps (256 MiB write)", "norm": "every gate",
+              "weak_scaling": "n = base qubits + log2(n_gpus): the slices (and work) per GPU are fixed"}
 
     if args.impl == "reference":
         if rank != 0:
