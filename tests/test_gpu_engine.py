@@ -204,3 +204,54 @@ def test_compare_against_dense_run(q):
     twin.load_basis(12345)
     twin.run(acts)
     assert comp.compare(twin)["max_abs_diff"] == 0.0  # deterministic, bit-identical
+
+
+_VARIANT_SCRIPT = r"""
+import hashlib, sys
+import paper_1811_05630_b200 as q
+n, s = 14, 10
+acts = q.lower(q.build_qft(n))
+eng = q.Engine(q.EngineConfig(num_qubits=n, slice_bits=s, codec=q.CodecConfig(q.CodecMode.Absolute, 1e-5)))
+eng.load_basis(1234)
+m = eng.run(acts + acts[:40])
+blob = eng.export_blocks()[0]
+print(hashlib.sha256(bytes(blob)).hexdigest(), repr(m.mean_compression_ratio), repr(m.min_compression_ratio))
+"""
+
+
+@pytest.mark.parametrize("env", [{"QCSIM_CHAIN": "2"}, {"QCSIM_SYNC_GATES": "1"}, {"QCSIM_PDL": "0"}])
+def test_pipeline_variants_bit_identical(env):
+    """The serial warp chain, the host-synchronous gate loop and plain
+    launches produce the same blocks and metrics as the default pipeline
+    (block-parallel chain, deferred loop, programmatic dependent launch)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+    def run(extra):
+        e = dict(os.environ)
+        for k in ("QCSIM_CHAIN", "QCSIM_SYNC_GATES", "QCSIM_PDL"):
+            e.pop(k, None)
+        e.update(extra)
+        r = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT], cwd=root, env=e, capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        return r.stdout.strip().splitlines()[-1]
+
+    assert run(env) == run({})
+
+
+def test_deferred_drift_error_unloads(q):
+    """A norm-drift error latched by the deferred loop leaves the engine
+    without a state (it must be reloaded)."""
+    eng = q.Engine(q.EngineConfig(num_qubits=6, slice_bits=3, codec=q.CodecConfig(q.CodecMode.Absolute, 1e-5)))
+    amps = np.zeros(2 << 6)
+    amps[0] = 2.0
+    eng.load_amplitudes(amps)
+    with pytest.raises(q.NumericError):
+        eng.run(q.lower(q.build_qft(6)))
+    with pytest.raises((q.NumericError, ValueError)):
+        eng.run(q.lower(q.build_qft(6)))
+    eng.load_basis(0)
+    eng.run(q.lower(q.build_qft(6)))
