@@ -239,12 +239,17 @@ constexpr size_t kChainScanSmem = sizeof(ChainScanSmem);
 // order); returns the last value on every lane.  Outlier-free batches of 32
 // use the per-lane prefix form of enc_chain: lane j runs the same chain and
 // stops adding after event j, so only the DADD latency is serial.
+struct IdentitySlot {
+    __device__ uint64_t operator()(uint32_t ord) const { return ord; }
+};
+template <class Slot = IdentitySlot>
 __device__ double chain_serial_warp(const double *evc, const uint32_t *ev, double *dv, uint32_t from, uint32_t to,
-                                    double d, int lane) {
+                                    double d, int lane, Slot slot = Slot()) {
     for (uint32_t base = from; base < to; base += 32) {
         const uint32_t cnt = tmin<uint32_t>(32, to - base);
-        const double cl = lane < (int)cnt ? evc[base + lane] : 0.0;
-        const uint32_t o = lane < (int)cnt ? ev[base + lane] >> 31 : 0u;
+        const uint64_t g = lane < (int)cnt ? slot(base + lane) : 0;
+        const double cl = lane < (int)cnt ? evc[g] : 0.0;
+        const uint32_t o = lane < (int)cnt ? ev[g] >> 31 : 0u;
         const unsigned om = __ballot_sync(0xffffffffu, o != 0);
         double mine = 0.0;
         if (om == 0 && cnt == 32) {
@@ -354,12 +359,7 @@ __global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int 
     if (c0 >= nev) return;
     if (ck == 0 && threadIdx.x == 0 && stats) // events of the pass (bench roofline)
         atomicAdd(reinterpret_cast<unsigned long long *>(stats + 6), (unsigned long long)nev);
-    if (nev <= kCsSerialMax) { // a handful of events: the plain recurrence is cheaper
-        if (threadIdx.x < 32)
-            chain_serial_warp(A.evc + (uint64_t)pl * A.L, A.evlist + (uint64_t)pl * A.L, A.dval + (uint64_t)pl * A.L,
-                              0, nev, 0.0, threadIdx.x);
-        return;
-    }
+
     extern __shared__ __align__(16) unsigned char cs_raw[];
     ChainScanSmem &S = *reinterpret_cast<ChainScanSmem *>(cs_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -371,6 +371,39 @@ __global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int 
     const int uq = ulp_exp(pp.q);
     const int n = (int)tmin<uint32_t>(kCsChunk, nev - c0);
     const int nthr = (n + kCsEpt - 1) / kCsEpt;
+    // event ordinal -> record slot (tile-local records, enc_lattice)
+    __shared__ uint32_t s_tpre[kInlineTiles + 1];
+    if (A.ev_tile_local && tid < 32) {
+        const int32_t *tn = reinterpret_cast<const int32_t *>(A.t_nev) + (uint64_t)pl * A.ntiles;
+        uint32_t carry = 0;
+        for (int b0 = 0; b0 < A.ntiles; b0 += 32) {
+            const uint32_t v = b0 + tid < A.ntiles ? (uint32_t)tn[b0 + tid] : 0u;
+            uint32_t incl = v;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+                if (tid >= off) incl += o;
+            }
+            if (b0 + tid < A.ntiles) s_tpre[b0 + tid] = carry + incl - v;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (tid == 0) s_tpre[A.ntiles] = carry;
+    }
+    __syncthreads();
+    auto slot_of = [&](uint32_t ord) -> uint64_t {
+        if (!A.ev_tile_local) return ord;
+        int lo = 0, hi = A.ntiles; // last tile with prefix <= ord
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_tpre[mid] <= ord) lo = mid;
+            else hi = mid;
+        }
+        return (uint64_t)lo * kTile + (ord - s_tpre[lo]);
+    };
+    if (nev <= kCsSerialMax) { // a handful of events: the plain recurrence is cheaper
+        if (threadIdx.x < 32) chain_serial_warp(evc, ev, dv, 0, nev, 0.0, threadIdx.x, slot_of);
+        return;
+    }
 
     if (tid == 0) {
         S.fail = 0;
@@ -379,9 +412,10 @@ __global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int 
     if (tid < kCsWarps) S.pmask[tid] = tid == 0 ? 1u : 0u; // thread 0 starts from the carry
     for (int j = tid; j < n; j += kCsThreads) {
         const int s = (j / kCsEpt) * kCsPad + (j % kCsEpt);
-        S.c[s] = evc[c0 + j];
-        S.kh[s] = __double_as_longlong(evD[c0 + j]);
-        S.out[s] = (uint8_t)(ev[c0 + j] >> 31);
+        const uint64_t g = slot_of(c0 + j);
+        S.c[s] = evc[g];
+        S.kh[s] = __double_as_longlong(evD[g]);
+        S.out[s] = (uint8_t)(ev[g] >> 31);
     }
     __syncthreads();
 
@@ -607,7 +641,7 @@ __global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int 
     if (failed && tid < 32) { // redo this chunk with the serial recurrence
         if (debug && tid == 0 && atomicAdd(&stats[3], 1u) < 16)
             printf("chain_scan: plane %d chunk %u fail mask %x\n", pl, c0, S.fail);
-        const double d = chain_serial_warp(evc, ev, dv, c0, c0 + n, carry_d, tid);
+        const double d = chain_serial_warp(evc, ev, dv, c0, c0 + n, carry_d, tid, slot_of);
         if (tid == 0) S.dend[nthr - 1] = d;
     }
     if (tid == 0) {

@@ -43,6 +43,9 @@ struct TileArgs {
     double *evD;           // [plane][L] lattice estimate of d per event ordinal (chain_scan.cuh)
     unsigned long long *lb; // [plane][ntiles] event-offset look-back slots (epoch-tagged)
     uint32_t lb_epoch;
+    unsigned long long *trace; // debug: enc_lattice phase stamps, 8 per block
+    int ev_tile_local;     // event records at tile-local slots (tile * kTile + rank), no
+                           // plane-wide offsets: the chain-scan kernel maps ordinals
     // run statistics of the final symbols (tokenizer input, codec.cpp:468-482),
     // written by enc_verify / enc_serial_x: first / last run start and
     // outliers per tile
@@ -387,6 +390,14 @@ __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int plane
     pdl_begin();
     const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
     if (pl >= planes) return;
+    auto stamp = [&](int k) {
+        if (A.trace && threadIdx.x == 0) {
+            unsigned long long tt;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+            A.trace[8ull * blockIdx.x + k] = tt;
+        }
+    };
+    stamp(0);
     const int tid = threadIdx.x;
     const uint64_t L = A.L;
     const uint64_t t0 = (uint64_t)t * kTile;
@@ -436,7 +447,9 @@ __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int plane
     }
     int lo[kPerThread];
     ScanI(scan_tmp).ExclusiveScan(opos, lo, -1, cub::Max());
+    stamp(1);
     const int32_t tbase = carry_of(A.t_base, A.ntiles, A.t_lastout, pl, t, A.ntiles, kScanMaxExcl); // position or -1
+    stamp(2);
     long long K[kPerThread];
     double dh[kPerThread]; // lattice estimate of the chain value (chain_scan.cuh)
     for (int e = 0; e < kPerThread; ++e) {
@@ -506,6 +519,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int plane
         evflag[e] = f & 1;
     }
     if (bad) atomicOr(&A.params[pl].flags, kFlagFallback);
+    stamp(3);
     // event list: tile offset by look-back, in-tile positions by a block scan
     int epos[kPerThread], tot;
     __syncthreads();
@@ -515,7 +529,10 @@ __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int plane
         return;
     }
     __shared__ uint32_t s_evbase;
-    if (tid < 32) {
+    if (A.ev_tile_local) { // no cross-tile wait: records at the tile's own slots
+        if (tid == 0) A.t_nev[(uint64_t)pl * A.ntiles + t] = (uint32_t)tot;
+        if (tid == 0) s_evbase = (uint32_t)t0;
+    } else if (tid < 32) {
         const uint32_t b = lookback_exclusive(lbs, A.lb_epoch, t, (uint32_t)tot);
         if (tid == 0) {
             A.t_nev[(uint64_t)pl * A.ntiles + t] = (uint32_t)tot;
@@ -524,6 +541,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int plane
     }
     __syncthreads();
     const uint32_t evb = s_evbase;
+    stamp(4);
     uint32_t *ev = A.evlist + (uint64_t)pl * L;
     double *evc = A.evc + (uint64_t)pl * L;
     double *evD = A.evD + (uint64_t)pl * L;
@@ -538,6 +556,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int plane
         evc[o] = out ? xv[e] : dmul(pp.q, (double)((long long)esym[e] - half));
         evD[o] = dh[e];
     }
+    stamp(5);
 }
 
 // ------------------------------------------------------------------ T3

@@ -346,6 +346,19 @@ void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
     CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 
+// 0 auto, 1 skip (debug), 2 serial warp chain, 3 block-parallel chain
+int chain_choice() {
+    static const int mode = [] {
+        const char *v = std::getenv("QCSIM_CHAIN");
+        return v ? std::atoi(v) : 0;
+    }();
+    return mode;
+}
+bool chain_scan_selected(uint64_t planes) {
+    const int m = chain_choice();
+    return m == 3 || (m == 0 && planes <= kScanChainMaxPlanes);
+}
+
 template <class K> void set_smem(K kernel, size_t bytes) {
     CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
@@ -477,6 +490,9 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
         launch_k(enc_x<NP, Src>, tgrid_u, kEncThreads, 0, st, A, src, units);
     }
     launch_plane_scan(st, S.t_lastout.p, S.t_base.p, ntiles, (int)planes, kScanMaxExcl);
+    // event records at tile-local slots when the block-parallel chain reads
+    // them (no look-back between the tiles of a plane)
+    A.ev_tile_local = (ntiles <= kInlineTiles && chain_scan_selected(planes)) ? 1 : 0;
     {
         if (S.lb.ensure(planes * ntiles, /*zero=*/true)) S.lb_epoch = 0;
         if (++S.lb_epoch >= (1u << 30)) { // epoch wrapped: clean slots
@@ -485,8 +501,28 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
         }
         A.lb = S.lb.p;
         A.lb_epoch = S.lb_epoch;
+        // debug: QCSIM_LAT_TRACE_AT = encode call -> phase stamps to QCSIM_LAT_TRACE_FILE
+        static const long lat_at = std::getenv("QCSIM_LAT_TRACE_AT") ? std::atol(std::getenv("QCSIM_LAT_TRACE_AT")) : -1;
+        static long lat_calls = 0;
+        static DBuf<unsigned long long> lat_trace;
+        A.trace = nullptr;
+        if (lat_at >= 0 && lat_calls++ == lat_at) {
+            lat_trace.ensure(8 * (uint64_t)tgrid_p);
+            CK(cudaMemsetAsync(lat_trace.p, 0, 8 * (uint64_t)tgrid_p * 8, st));
+            A.trace = lat_trace.p;
+        }
         PROF("enc_lattice", st);
         launch_k(enc_lattice, tgrid_p, kEncThreads, 0, st, A, (int)planes);
+        if (A.trace) {
+            std::vector<unsigned long long> h(8 * (uint64_t)tgrid_p);
+            CK(cudaMemcpyAsync(h.data(), A.trace, h.size() * 8, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            if (FILE *f = std::fopen(std::getenv("QCSIM_LAT_TRACE_FILE"), "wb")) {
+                std::fwrite(h.data(), 8, h.size(), f);
+                std::fclose(f);
+            }
+            A.trace = nullptr;
+        }
     }
     launch_plane_scan(st, S.t_nev.p, S.t_evoff.p, ntiles, (int)planes, kScanSumExcl);
     if (ntiles > kInlineTiles) {
@@ -522,11 +558,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
         }
     }
     {
-        // 0 auto, 1 skip (debug), 2 serial warp chain, 3 block-parallel chain
-        static const int chain_mode = [] {
-            const char *v = std::getenv("QCSIM_CHAIN");
-            return v ? std::atoi(v) : 0;
-        }();
+        // (chain_mode / scan: chosen before enc_lattice, see chain_choice)
         static const int chain_debug = std::getenv("QCSIM_CHAIN_DEBUG") ? 1 : 0;
         static bool attr = false;
         if (!attr) {
@@ -534,7 +566,8 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
             set_smem(enc_chain_scan, kChainScanSmem);
             attr = true;
         }
-        const bool scan = chain_mode == 3 || (chain_mode == 0 && planes <= kScanChainMaxPlanes);
+        const bool scan = chain_scan_selected(planes);
+        const int chain_mode = chain_choice();
         if (chain_mode != 1 && scan) {
             PROF("enc_chain_scan", st);
             const int cmax = (int)((L + kCsChunk - 1) / kCsChunk);
