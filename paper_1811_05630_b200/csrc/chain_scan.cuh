@@ -412,41 +412,28 @@ __global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int 
     if (tid < kCsWarps) S.pmask[tid] = tid == 0 ? 1u : 0u; // thread 0 starts from the carry
     CS_TRACE(7);
     {
-        // record slots first (ordinals rise by kCsThreads: walk the tile
-        // prefix forward), then every load at once so their latencies overlap
-        constexpr int kPer = kCsChunk / kCsThreads;
-        uint64_t g[kPer];
+        // ordinals rise by kCsThreads per iteration: walk the tile prefix forward
+        int tile = 0;
         if (A.ev_tile_local) {
-            int tile = 0;
-            {
-                int lo = 0, hi = A.ntiles;
-                const uint32_t o0 = c0 + tid;
-                while (hi - lo > 1) {
-                    const int mid = (lo + hi) >> 1;
-                    if (s_tpre[mid] <= o0) lo = mid;
-                    else hi = mid;
-                }
-                tile = lo;
+            int lo = 0, hi = A.ntiles;
+            const uint32_t o0 = c0 + tid;
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (s_tpre[mid] <= o0) lo = mid;
+                else hi = mid;
             }
-#pragma unroll
-            for (int q = 0; q < kPer; ++q) {
-                const uint32_t o = c0 + tid + q * kCsThreads;
-                while (tile + 1 < A.ntiles && s_tpre[tile + 1] <= o) ++tile;
-                g[q] = (uint64_t)tile * kTile + (o - s_tpre[tile]);
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q < kPer; ++q) g[q] = c0 + tid + q * kCsThreads;
+            tile = lo;
         }
-#pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-            const int j = tid + q * kCsThreads;
-            if (j < n) {
-                const int s = (j / kCsEpt) * kCsPad + (j % kCsEpt);
-                S.c[s] = evc[g[q]];
-                S.kh[s] = __double_as_longlong(evD[g[q]]);
-                S.out[s] = (uint8_t)(ev[g[q]] >> 31);
+        for (int j = tid; j < n; j += kCsThreads) {
+            const int s = (j / kCsEpt) * kCsPad + (j % kCsEpt);
+            uint64_t g = c0 + j;
+            if (A.ev_tile_local) {
+                while (tile + 1 < A.ntiles && s_tpre[tile + 1] <= c0 + j) ++tile;
+                g = (uint64_t)tile * kTile + (c0 + j - s_tpre[tile]);
             }
+            S.c[s] = evc[g];
+            S.kh[s] = __double_as_longlong(evD[g]);
+            S.out[s] = (uint8_t)(ev[g] >> 31);
         }
     }
     __syncthreads();

@@ -492,7 +492,8 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     launch_plane_scan(st, S.t_lastout.p, S.t_base.p, ntiles, (int)planes, kScanMaxExcl);
     // event records at tile-local slots when the block-parallel chain reads
     // them (no look-back between the tiles of a plane)
-    A.ev_tile_local = (ntiles <= kInlineTiles && chain_scan_selected(planes)) ? 1 : 0;
+    static const bool tile_local_off = std::getenv("QCSIM_EV_TILE_LOCAL") && std::getenv("QCSIM_EV_TILE_LOCAL")[0] == '0';
+    A.ev_tile_local = (ntiles <= kInlineTiles && chain_scan_selected(planes) && !tile_local_off) ? 1 : 0;
     {
         if (S.lb.ensure(planes * ntiles, /*zero=*/true)) S.lb_epoch = 0;
         if (++S.lb_epoch >= (1u << 30)) { // epoch wrapped: clean slots
