@@ -524,6 +524,7 @@ __global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int 
     __syncthreads();
 
     CS_TRACE(6);
+    if (debug && stats && cnt > 0) atomicAdd(&stats[8 + min(e.kind == 0 ? e.f.W : 4 + e.kind, 7)], 1u); // W histogram
     int npts = 0;
 #pragma unroll
     for (int w = 0; w < kCsWarps; ++w) npts += __popc(S.pmask[w]);

@@ -316,8 +316,8 @@ constexpr uint64_t kScanChainMaxPlanes = 256; // more planes fill the GPU with s
 uint32_t *chain_stats() {
     static DBuf<uint32_t> buf;
     if (!buf.p) {
-        buf.ensure(8);
-        CK(cudaMemset(buf.p, 0, 8 * sizeof(uint32_t)));
+        buf.ensure(16);
+        CK(cudaMemset(buf.p, 0, 16 * sizeof(uint32_t)));
     }
     return buf.p;
 }
@@ -1435,8 +1435,11 @@ int qcsim_profile_read(char (*names)[64], double *ms, uint64_t *count, double *b
 qcsim_status qcsim_debug_chain_stats(uint32_t *out3) { // out3[5]
     return guarded([&] {
         CK(cudaDeviceSynchronize());
-        uint32_t v[8];
+        uint32_t v[16];
         CK(cudaMemcpy(v, chain_stats(), sizeof v, cudaMemcpyDeviceToHost));
+        if (std::getenv("QCSIM_CHAIN_DEBUG"))
+            std::fprintf(stderr, "chain maps: W0 %u W1 %u W2 %u W3 %u const %u poison %u\n", v[8], v[9], v[10], v[11],
+                         v[13], v[14]);
         out3[0] = v[0];
         out3[1] = v[1];
         out3[2] = v[4];
