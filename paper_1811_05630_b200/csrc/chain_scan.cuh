@@ -424,16 +424,38 @@ __global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int 
             }
             tile = lo;
         }
-        for (int j = tid; j < n; j += kCsThreads) {
-            const int s = (j / kCsEpt) * kCsPad + (j % kCsEpt);
-            uint64_t g = c0 + j;
-            if (A.ev_tile_local) {
+        // slots first, then every load in flight at once, then the stores
+        uint64_t g[kCsEpt];
+#pragma unroll
+        for (int i = 0; i < kCsEpt; ++i) {
+            const int j = tid + i * kCsThreads;
+            g[i] = c0 + j;
+            if (A.ev_tile_local && j < n) {
                 while (tile + 1 < A.ntiles && s_tpre[tile + 1] <= c0 + j) ++tile;
-                g = (uint64_t)tile * kTile + (c0 + j - s_tpre[tile]);
+                g[i] = (uint64_t)tile * kTile + (c0 + j - s_tpre[tile]);
             }
-            S.c[s] = evc[g];
-            S.kh[s] = __double_as_longlong(evD[g]);
-            S.out[s] = (uint8_t)(ev[g] >> 31);
+        }
+        double cv[kCsEpt];
+        long long dv2[kCsEpt];
+        uint32_t evv[kCsEpt];
+#pragma unroll
+        for (int i = 0; i < kCsEpt; ++i) {
+            const int j = tid + i * kCsThreads;
+            if (j < n) {
+                cv[i] = __ldg(evc + g[i]);
+                dv2[i] = __double_as_longlong(__ldg(evD + g[i]));
+                evv[i] = __ldg(ev + g[i]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kCsEpt; ++i) {
+            const int j = tid + i * kCsThreads;
+            if (j < n) {
+                const int s = (j / kCsEpt) * kCsPad + (j % kCsEpt);
+                S.c[s] = cv[i];
+                S.kh[s] = dv2[i];
+                S.out[s] = (uint8_t)(evv[i] >> 31);
+            }
         }
     }
     __syncthreads();

@@ -1111,9 +1111,8 @@ __global__ void __launch_bounds__(kEncThreads) tok_count(TokArgs A, int planes) 
     }
 }
 
-__global__ void __launch_bounds__(kEncThreads) tok_emit(TokArgs A, int planes) {
-    pdl_begin();
-    const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
+__device__ __forceinline__ void tok_emit_tile(const TokArgs &A, int planes, int blk) {
+    const int pl = blk / A.ntiles, t = blk % A.ntiles;
     if (pl >= planes) return;
     const int tid = threadIdx.x;
     const uint64_t L = A.L;
@@ -1202,6 +1201,10 @@ __global__ void __launch_bounds__(kEncThreads) tok_emit(TokArgs A, int planes) {
         A.ntok[pl] = tokbase + (uint32_t)tile_tok;
         A.ocount[pl] = obase + (uint32_t)tile_out;
     }
+}
+__global__ void __launch_bounds__(kEncThreads) tok_emit(TokArgs A, int planes) {
+    pdl_begin();
+    tok_emit_tile(A, planes, blockIdx.x);
 }
 
 } // namespace qcb

@@ -124,12 +124,127 @@ __device__ void emit_dec_tables(const DecTables &T, int pl, uint32_t n, const ui
     }
 }
 
+// Two-queue Huffman merge (codec.cpp:168-229; ties prefer the leaf queue)
+// for n in [2, 64] leaves, one warp, everything in registers: leaf i and
+// internal node k live in lane i & 31 / k & 31 (register i >> 5).  Every lane
+// runs the same serial merge; the next two heads of both queues are fetched
+// by shuffles at the top of each step (independent of its picks), so only
+// the compare/select work is serial.  Writes par[0, 2n-1) (root: -1).
+__device__ __forceinline__ uint32_t wsel(uint32_t lo, uint32_t hi, uint32_t i) {
+    return __shfl_sync(0xffffffffu, i >= 32 ? hi : lo, i & 31);
+}
+__device__ void huff_merge_regs(const uint64_t *keys, uint32_t n, int32_t *par, int lane) {
+    const uint32_t L0 = (uint32_t)lane < n ? (uint32_t)(keys[lane] >> 25) : 0u;
+    const uint32_t L1 = (uint32_t)lane + 32 < n ? (uint32_t)(keys[lane + 32] >> 25) : 0u;
+    uint32_t I0 = 0, I1 = 0;                         // internal node counts
+    int32_t lp0 = -1, lp1 = -1, ip0 = -1, ip1 = -1;  // parents (global node index)
+    uint32_t lp = 0, ip = 0, ni = 0;                 // leaf head, internal head, internal nodes
+    uint32_t lv = wsel(L0, L1, 0), iv = 0;
+    while ((n - lp) + (ni - ip) >= 2) {
+        const uint32_t l1 = wsel(L0, L1, min(lp + 1, 63u)), l2 = wsel(L0, L1, min(lp + 2, 63u));
+        const uint32_t i1 = wsel(I0, I1, min(ip + 1, 63u)), i2 = wsel(I0, I1, min(ip + 2, 63u));
+        uint32_t pk[2], pv[2];
+        bool pl_[2];
+        uint32_t ln = l1, in = i1; // the heads after the current ones
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const bool take_leaf = lp < n && (ip >= ni || lv <= iv);
+            pl_[k] = take_leaf;
+            if (take_leaf) {
+                pk[k] = lp;
+                pv[k] = lv;
+                ++lp;
+                lv = ln;
+                ln = l2;
+            } else {
+                pk[k] = ip;
+                pv[k] = iv;
+                ++ip;
+                iv = in;
+                in = i2;
+            }
+        }
+        const uint32_t sum = pv[0] + pv[1];
+        const int32_t node = (int32_t)(n + ni);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const uint32_t q = pk[k];
+            if ((uint32_t)lane == (q & 31)) {
+                if (pl_[k]) {
+                    if (q < 32) lp0 = node; else lp1 = node;
+                } else {
+                    if (q < 32) ip0 = node; else ip1 = node;
+                }
+            }
+        }
+        if ((uint32_t)lane == (ni & 31)) {
+            if (ni < 32) I0 = sum; else I1 = sum;
+        }
+        if (ip == ni) iv = sum; // the internal queue was empty
+        ++ni;
+    }
+    if ((uint32_t)lane < n) par[lane] = lp0;
+    if ((uint32_t)lane + 32 < n) par[lane + 32] = lp1;
+    if ((uint32_t)lane < ni) par[n + lane] = ip0;
+    if ((uint32_t)lane + 32 < ni) par[n + lane + 32] = ip1;
+    __syncwarp();
+}
+
+// The same merge for larger alphabets (nc[0, n) = leaf counts, par[0, n) =
+// -1 on entry), one warp, up to 32 picks per round.  Internal nodes are
+// appended in non-decreasing order behind every node that already exists, so
+// as long as a round only takes internal nodes that existed when it started,
+// its picks are the plain merge of two sorted lists (leaves, known internal
+// nodes): lane j finds pick j by a merge-path search.  The round stops at the
+// first pick that would need a node created in the same round; picks are
+// paired in order into new nodes.
+template <class U32P, class I32P>
+__device__ void huff_merge_batched(U32P nc, I32P par, uint32_t n, int tid) {
+    uint32_t lp = 0, ip = n, nodes = n;
+    while ((n - lp) + (nodes - ip) >= 2) {
+        const uint32_t nA = n - lp, nB = nodes - ip, j = (uint32_t)tid;
+        // leaves among the first j picks (ties: the leaf goes first)
+        uint32_t lo = j > nB ? j - nB : 0u, hi = tmin<uint32_t>(j, nA);
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (nc[lp + mid] <= nc[ip + j - 1 - mid]) lo = mid + 1;
+            else hi = mid;
+        }
+        const uint32_t cL = lo, cI = j - lo;
+        // pick j exists among the known nodes, and no node created in this
+        // round can be the internal head yet (j < 2: none exists)
+        const bool valid = j < nA + nB && (cI < nB || j < 2);
+        const bool take_leaf = cL < nA && (cI >= nB || nc[lp + cL] <= nc[ip + cI]);
+        const uint32_t idx = valid ? (take_leaf ? lp + cL : ip + cI) : 0u;
+        const uint32_t val = valid ? nc[idx] : 0u;
+        const unsigned vm = __ballot_sync(0xffffffffu, valid);
+        uint32_t P = vm == 0xffffffffu ? 32u : (uint32_t)(__ffs(~vm) - 1); // leading valid picks
+        P &= ~1u;
+        const uint32_t pidx = __shfl_xor_sync(0xffffffffu, idx, 1);
+        const uint32_t pval = __shfl_xor_sync(0xffffffffu, val, 1);
+        const unsigned lm = __ballot_sync(0xffffffffu, valid && take_leaf) & (P >= 32 ? 0xffffffffu : ((1u << P) - 1u));
+        __syncwarp(); // every lane has read nc before the new nodes land
+        if (j < P && (j & 1) == 0) {
+            const uint32_t k = nodes + (j >> 1);
+            nc[k] = val + pval;
+            par[idx] = (int32_t)k;
+            par[pidx] = (int32_t)k;
+        }
+        const uint32_t nl = (uint32_t)__popc(lm);
+        lp += nl;
+        ip += P - nl;
+        nodes += P >> 1;
+        __syncwarp();
+    }
+    if (tid == 0) par[nodes - 1] = -1;
+    __syncwarp();
+}
+constexpr uint32_t kDepthSerialN = 12; // larger (shared-memory) alphabets: depths by pointer jumping
+
 // One block per plane.  Working arrays live in shared memory for alphabets of
 // up to kSmallN symbols (the serial two-queue merge then runs on smem), in
 // per-plane global scratch beyond that.
-__global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
-    pdl_begin();
-    const int pl = blockIdx.x;
+__device__ __forceinline__ void codebook_plane(const CodeBook &B, int planes, int pl) {
     if (pl >= planes) return;
     const int tid = threadIdx.x;
     auto stamp = [&](int k) { // debug phase trace (B.trace: 16 stamps per plane)
@@ -172,6 +287,7 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
     if (tid < kMaxCodeLen + 2) lcount[tid] = 0;
     const uint32_t n = (h0 ? 1u : 0u) + (uint32_t)tot_r + (hrun ? 1u : 0u);
     const bool small = n <= kSmallN;
+    if (B.trace && tid == 0) B.trace[16ull * pl + 15] = n; // debug: alphabet size
     uint32_t *sym = small ? sym_s : B.sym + pl * cap;
     uint32_t *cnt = small ? cnt_s : reinterpret_cast<uint32_t *>(B.cnt + pl * cap);
     uint8_t *len = small ? len_s : B.len + pl * cap;
@@ -221,47 +337,24 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
     __syncthreads();
     if (n > 1) block_bitonic(keys, n);
     stamp(3);
-    // 3) two-queue merge (codec.cpp:168-229; ties prefer the leaf queue)
-    if (tid == 0) {
+    // 3) two-queue merge (codec.cpp:168-229; ties prefer the leaf queue).
+    if (tid < 32) {
         if (n == 1) {
-            par[0] = -1;
+            if (tid == 0) par[0] = -1;
+        } else if (n <= 64) {
+            huff_merge_regs(keys, n, par, tid);
         } else {
-            for (uint32_t i = 0; i < n; ++i) {
+            for (uint32_t i = tid; i < n; i += 32) {
                 nc[i] = (uint32_t)(keys[i] >> 25);
                 par[i] = -1;
             }
-            // queue heads live in registers; internal nodes are appended in
-            // non-decreasing order, so the internal head is re-read only
-            // when it advances
-            uint32_t lp = 0, ip = n, nodes = n;
-            uint32_t lv = nc[0], iv = 0;
-            while ((n - lp) + (nodes - ip) >= 2) {
-                uint32_t pick[2], pv[2];
-                for (int k = 0; k < 2; ++k) {
-                    const bool leaf_ok = lp < n, int_ok = ip < nodes;
-                    const bool take_leaf = leaf_ok && (!int_ok || lv <= iv);
-                    if (take_leaf) {
-                        pick[k] = lp;
-                        pv[k] = lv;
-                        ++lp;
-                        lv = lp < n ? nc[lp] : 0u;
-                    } else {
-                        pick[k] = ip;
-                        pv[k] = iv;
-                        ++ip;
-                        iv = ip < nodes ? nc[ip] : 0u;
-                    }
-                }
-                const uint32_t sum = pv[0] + pv[1];
-                nc[nodes] = sum;
-                par[pick[0]] = (int32_t)nodes;
-                par[pick[1]] = (int32_t)nodes;
-                if (ip == nodes) iv = sum; // the internal queue was empty
-                ++nodes;
-            }
-            par[nodes - 1] = -1;
+            __syncwarp();
+            huff_merge_batched(nc, par, n, tid);
+        }
+        if (tid == 0 && n > 1) {
+            const uint32_t nodes = 2 * n - 1;
             s_nodes = nodes;
-            if (!small || n <= 64) { // large or tiny alphabet: depths top-down, serially
+            if (!small || n <= kDepthSerialN) { // large or tiny alphabet: depths top-down, serially
                 nc[nodes - 1] = 0;
                 for (int64_t v = (int64_t)nodes - 2; v >= 0; --v) nc[v] = nc[par[v]] + 1;
             }
@@ -270,7 +363,7 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
     __syncthreads();
     // depths by pointer jumping (parents have larger indices; root -> 0),
     // stored in nc
-    if (n > 64 && small) {
+    if (n > kDepthSerialN && small) {
         const uint32_t nodes = s_nodes;
         for (uint32_t v = tid; v < nodes; v += 256) {
             nc[v] = par[v] < 0 ? 0u : 1u; // distance to the current ancestor
@@ -343,7 +436,9 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
         }
         for (int l = 0; l <= kMaxCodeLen; ++l) lfirst0[l] = lfirst[l];
         const uint64_t bits = s_bits + B.gamma_bits[pl];
-        const uint64_t payload = 4 + 5ull * n + (bits + 7) / 8 + 16ull * B.ocount[pl];
+        // outliers are never run-collapsed: one outlier token (symbol 0) per
+        // outlier, so h0 is the plane's outlier count (codec.cpp:460-488)
+        const uint64_t payload = 4 + 5ull * n + (bits + 7) / 8 + 16ull * h0;
         const uint64_t bytes = kHeaderBytes + payload;
         B.nsym[pl] = n;
         B.stream_bits[pl] = bits;
@@ -379,6 +474,18 @@ __global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
     if (B.dec.lut) emit_dec_tables(B.dec, pl, n, sym, len, code, lcount, lfirst0);
     stamp(8);
     if (B.trace && tid == 0) B.trace[16ull * pl + 9] = n;
+}
+__global__ void __launch_bounds__(256) enc_codebook(CodeBook B, int planes) {
+    pdl_begin();
+    codebook_plane(B, planes, blockIdx.x);
+}
+// Tokens (tok_emit) and codebooks in one grid: both consume only tok_count's
+// outputs, so the codebook blocks (first in the grid, one per plane, short
+// serial phases) overlap the tile-parallel token emission.
+__global__ void __launch_bounds__(256) tok_emit_codebook(TokArgs A, CodeBook B, int planes) {
+    pdl_begin();
+    if ((int)blockIdx.x < planes) codebook_plane(B, planes, blockIdx.x);
+    else tok_emit_tile(A, planes, (int)blockIdx.x - planes);
 }
 
 // ------------------------------------------------------------------ E5

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -655,10 +656,6 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
         launch_k(tok_count, tgrid_p, kEncThreads, 0, st, T, (int)planes);
     }
     launch_plane_scan(st, S.t_ntok.p, S.t_tokoff.p, ntiles, (int)planes, kScanSumExcl);
-    {
-        PROF("tok_emit", st);
-        launch_k(tok_emit, tgrid_p, kEncThreads, 0, st, T, (int)planes);
-    }
 
     CodeBook B;
     B.hist = S.hist.p;
@@ -692,8 +689,9 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
         B.trace = cb_trace.p;
     }
     {
-        PROF("enc_codebook", st);
-        launch_k(enc_codebook, (unsigned)planes, 256, 0, st, B, (int)planes);
+        // tokens and codebooks in one grid (both only consume tok_count)
+        PROF("tok_emit_codebook", st);
+        launch_k(tok_emit_codebook, (unsigned)planes + tgrid_p, 256, 0, st, T, B, (int)planes);
     }
     if (cb_tracing) {
         std::vector<unsigned long long> h(16 * planes);
@@ -1764,16 +1762,22 @@ qcsim_status qcsim_engine_run(qcsim_engine *e, const qcsim_action *actions, uint
         if (count) {
             const bool deferred = engine_defer_begin(e);
             CK(cudaEventRecord(e->ev0, e->st));
+            const auto h0 = std::chrono::steady_clock::now();
             try {
                 for (uint64_t k = 0; k < count; ++k) engine_gate(e, actions[k]);
             } catch (...) {
                 if (deferred) engine_defer_end(e, false);
                 throw;
             }
+            const auto h1 = std::chrono::steady_clock::now();
             CK(cudaEventRecord(e->ev1, e->st));
             CK(cudaEventSynchronize(e->ev1));
             float ms = 0.f;
             CK(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+            static const bool enq_timing = std::getenv("QCSIM_ENQ_TIMING") != nullptr; // debug
+            if (enq_timing)
+                std::fprintf(stderr, "engine_run: %llu gates, host enqueue %.3f ms, device %.3f ms\n",
+                             (unsigned long long)count, std::chrono::duration<double, std::milli>(h1 - h0).count(), ms);
             e->wall += ms * 1e-3;
             if (deferred) engine_defer_end(e, true);
         }
