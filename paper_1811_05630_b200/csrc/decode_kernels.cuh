@@ -14,6 +14,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "norm.cuh"
 
 namespace qcb {
 
@@ -148,8 +149,15 @@ constexpr size_t kDecSmem = sizeof(DecSmem);
 // codec.cpp:591-626 for its chunk, kDecWin elements at a time: the warp
 // parks its 32 chunks' windows in shared memory and stores them row by row
 // (256-byte coalesced rows instead of 32 scattered 8-byte stores).
-__global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTables T, int planes) {
+// N.enabled: the grid's last block runs the engine's normalization for this
+// gate pass instead (it needs only the previous pass's norms; the gate kernel
+// that applies the scale runs after this grid).
+__global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTables T, int planes, NormArgs N) {
     pdl_begin();
+    if (N.enabled && blockIdx.x == gridDim.x - 1) {
+        engine_norm_body(N);
+        return;
+    }
     extern __shared__ __align__(16) unsigned char dec_raw[];
     DecSmem &S = *reinterpret_cast<DecSmem *>(dec_raw);
     const uint64_t nchunks = (D.L + (1ull << D.log2C) - 1) >> D.log2C;

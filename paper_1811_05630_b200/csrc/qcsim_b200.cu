@@ -817,7 +817,7 @@ struct DecScratch {
 // blocks (enc_codebook -> emit_dec_tables), no table-parsing pass needed.
 void decode_batch(cudaStream_t st, DecScratch &S, const uint8_t *arena, const uint64_t *blk_off,
                   const IndexRec *index, double *const *out, int planes, uint64_t L, int log2C, int qb,
-                  bool prepare = true) {
+                  bool prepare = true, const NormArgs *norm = nullptr) {
     if (prepare) S.ensure(planes, L, qb);
     const DecTables T = S.tables();
     DecPlanes D;
@@ -840,7 +840,10 @@ void decode_batch(cudaStream_t st, DecScratch &S, const uint8_t *arena, const ui
             attr = true;
         }
         PROF("dec_chunks", st);
-        launch_k(dec_chunks, (unsigned)(groups * planes), kDecThreads, kDecSmem, st, D, T, planes);
+        NormArgs N{};
+        if (norm) N = *norm;
+        launch_k(dec_chunks, (unsigned)(groups * planes) + (N.enabled ? 1u : 0u), kDecThreads, kDecSmem, st, D, T,
+                 planes, N);
     }
 }
 
@@ -983,6 +986,7 @@ struct qcsim_engine {
     // deferred gate loop (no host round trip per gate): device scale,
     // device metrics, latched errors
     bool deferred = false;
+    NormArgs norm{};          // this gate pass's deferred normalization (run by the decoder grid)
     bool defer_fresh = false; // no pass has run yet in this deferred run
     DBuf<double> norm_buf[2], dev_scale;
     DBuf<EngineDevStats> dev_stats;
@@ -1161,12 +1165,17 @@ void engine_decode_old(qcsim_engine *e, bool need_imported) {
         }
     }
     if (!e->compressed) {
+        if (e->norm.enabled) {
+            PROF("engine_norm", e->st);
+            launch_k(engine_norm, 1, 256, 0, e->st, e->norm);
+        }
         CK(cudaMemcpyAsync(e->old.p, e->dense[e->cur].p, e->ns * 2 * e->L * sizeof(double),
                            cudaMemcpyDeviceToDevice, e->st));
     } else {
         decode_batch(e->st, e->dec[e->cur], e->arena[e->cur].p, e->blk_off[e->cur].p, e->index[e->cur].p, e->outptrs.p,
-                     (int)(2 * e->ns), e->L, e->log2C, e->cfg.codec.quant_code_bits, /*prepare=*/false);
+                     (int)(2 * e->ns), e->L, e->log2C, e->cfg.codec.quant_code_bits, /*prepare=*/false, &e->norm);
     }
+    e->norm.enabled = 0;
     if (extra) {
         // imported blocks: validating serial decode (they carry no index)
         std::vector<uint8_t> all;
@@ -1222,16 +1231,15 @@ void engine_gate(qcsim_engine *e, const qcsim_action &a) {
     // deterministic tree over every slice's sq_norm
     const bool apply = e->cfg.norm_every > 0 && (e->gates % (uint64_t)e->cfg.norm_every) == 0;
     double scale = 1.0;
+    e->norm = NormArgs{};
     if (apply && e->deferred) {
-        PROF("engine_norm", e->st);
         // slice norms of the previous pass from its tile partials (or, for the
-        // first gate of a run, the norms uploaded by engine_defer_begin)
+        // first gate of a run, the norms uploaded by engine_defer_begin); run
+        // by the decoder grid's extra block (engine_decode_old)
         const uint64_t ntl = (e->L + kTile - 1) / kTile;
-        launch_k(engine_norm, 1, 256, 0, e->st, e->defer_fresh ? nullptr : e->enc.tilesum.p, (int)ntl, e->slice_sq.p,
-                                          e->norm_buf[0].p, e->norm_buf[1].p, e->S,
-                                          10.0 * e->cfg.norm_drift_tolerance, (unsigned long long)e->gates,
-                                          e->dev_scale.p, e->defer_fresh ? nullptr : e->enc.overflow.p,
-                                          e->dev_stats.p);
+        e->norm = NormArgs{e->defer_fresh ? nullptr : e->enc.tilesum.p, (int)ntl, e->slice_sq.p, e->norm_buf[0].p,
+                           e->norm_buf[1].p, e->S, 10.0 * e->cfg.norm_drift_tolerance, (unsigned long long)e->gates,
+                           e->dev_scale.p, e->defer_fresh ? nullptr : e->enc.overflow.p, e->dev_stats.p, 1};
     } else if (apply) {
         const double G = tree_sum_host(e->sq_norm.data(), e->S);
         if (!std::isfinite(G) || std::fabs(G - 1.0) > 10.0 * e->cfg.norm_drift_tolerance) {
