@@ -82,8 +82,11 @@ __global__ void __launch_bounds__(256) init_params(PlaneParams *params, Src src,
 
 // Exclusive scan of the per-plane arena slot sizes (16-byte aligned slots):
 // out[p] = sum(in[0..p)), out[planes] = total.  One 1024-thread block.
-__global__ void __launch_bounds__(256) slot_scan(const uint64_t *in, uint64_t *out, int planes) {
+// (also clears the packer's arena-overflow flag for this batch: a kernel
+// instead of a memset keeps the launch chain programmatic)
+__global__ void __launch_bounds__(256) slot_scan(const uint64_t *in, uint64_t *out, int planes, uint32_t *overflow) {
     pdl_begin();
+    if (threadIdx.x == 0) *overflow = 0u;
     using Scan = cub::BlockScan<unsigned long long, 256>;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ unsigned long long carry;
@@ -176,8 +179,10 @@ __global__ void __launch_bounds__(256) dense_gate(Src src, int units, uint64_t L
 __global__ void __launch_bounds__(256) slot_scan_stats(const uint64_t *slot_bytes, uint64_t *slot_off,
                                                        const uint64_t *bytes, const uint32_t *err,
                                                        const PlaneParams *params, int planes, uint64_t L,
-                                                       unsigned long long gate, EngineDevStats *st) {
+                                                       unsigned long long gate, EngineDevStats *st,
+                                                       uint32_t *overflow) {
     pdl_begin();
+    if (threadIdx.x == 0) *overflow = 0u;
     using Scan = cub::BlockScan<unsigned long long, 256>;
     using Red = cub::BlockReduce<unsigned long long, 256>;
     __shared__ union {

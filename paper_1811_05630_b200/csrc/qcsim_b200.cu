@@ -259,6 +259,7 @@ struct EncScratch {
     qcsim_codec_config param_cfg{};  // ... under this config
     DecTables dec_out{};             // where enc_codebook writes decode tables (optional)
     EngineDevStats *stats_out = nullptr; // deferred engine: run metrics fused into the slot scan
+    uint64_t *blk_off_out = nullptr;     // deferred engine: the packer writes block offsets here directly
     unsigned long long stats_gate = 0;
 
     void ensure(uint64_t planes, uint64_t units, uint64_t L, int qb) {
@@ -707,10 +708,10 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     if (S.stats_out) {
         PROF("slot_scan_stats", st);
         launch_k(slot_scan_stats, 1, 256, 0, st, S.slot_bytes.p, S.slot_off.p, S.block_bytes.p, S.err.p, S.params.p,
-                                           (int)planes, L, S.stats_gate, S.stats_out);
+                                           (int)planes, L, S.stats_gate, S.stats_out, S.overflow.p);
     } else {
         PROF("slot_scan", st);
-        launch_k(slot_scan, 1, 256, 0, st, S.slot_bytes.p, S.slot_off.p, (int)planes);
+        launch_k(slot_scan, 1, 256, 0, st, S.slot_bytes.p, S.slot_off.p, (int)planes, S.overflow.p);
     }
 
     PackArgs P;
@@ -730,7 +731,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     P.params = S.params.p;
     P.index = index;
     P.overflow = S.overflow.p;
-    P.blk_off = S.blk_off.p;
+    P.blk_off = S.blk_off_out ? S.blk_off_out : S.blk_off.p;
     P.L = L;
     P.cap = cap;
     P.log2C = log2C;
@@ -740,8 +741,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     P.planes_total = (int)planes;
     S.pack = P;
     S.planes = planes;
-    CK(cudaMemsetAsync(S.overflow.p, 0, sizeof(uint32_t), st));
-    launch_pack(st, S, arena);
+    launch_pack(st, S, arena); // (slot_scan cleared the overflow flag)
     if (!host_results) return; // deferred engine: slot_scan_stats consumes them on the device
     // results for the host, one batch of async copies into pinned memory
     S.h_bytes.ensure(planes);
@@ -1076,15 +1076,15 @@ template <class Src> void engine_store(qcsim_engine *e, const Src &src) {
         e->enc.dec_out = e->dec[nxt].tables();
         e->enc.stats_out = e->dev_stats.p;
         e->enc.stats_gate = e->gates;
+        e->blk_off[nxt].ensure(2 * e->ns);
+        e->enc.blk_off_out = e->blk_off[nxt].p;
         encode_launch<2, Src>(e->st, e->enc, src, units, e->L, e->cfg.codec, e->log2C, e->index[nxt].p,
                               e->arena[nxt], false, false, /*host_results=*/false);
         e->enc.dec_out = DecTables{};
         e->enc.stats_out = nullptr;
+        e->enc.blk_off_out = nullptr;
         e->defer_fresh = false; // slice norms: next pass's engine_norm, or engine_defer_end
         (void)ntiles;
-        e->blk_off[nxt].ensure(2 * e->ns);
-        CK(cudaMemcpyAsync(e->blk_off[nxt].p, e->enc.blk_off.p, 2 * e->ns * sizeof(uint64_t),
-                           cudaMemcpyDeviceToDevice, e->st));
         e->cur = nxt;
         return;
     }
