@@ -333,6 +333,12 @@ struct ChainLink {
     int cmax;        // chunks per plane in the grid
     uint32_t epoch;  // this launch's flag value
     unsigned long long *trace; // debug: per block 8 phase times (%globaltimer ns), see CS_TRACE
+    // per-plane completion for the consumer grid (enc_verify runs alongside,
+    // waiting per plane instead of for the whole grid): every block of plane
+    // p counts itself in cnt[p]; the last one resets it and raises done[p]
+    // to the epoch (nullptr: the consumer waits for the grid)
+    uint32_t *cnt;
+    uint32_t *done;
 };
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -345,9 +351,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
     if (link.trace && threadIdx.x == 0) link.trace[8ull * blockIdx.x + (k)] = gtimer()
 
 #define CS_FAIL(code) atomicOr(&S.fail, 1 << (code))
-__global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int planes, ChainLink link, uint32_t *stats,
-                                                                int debug) {
-    pdl_begin();
+__device__ __forceinline__ void chain_chunk(const TileArgs &A, int planes, const ChainLink &link, uint32_t *stats,
+                                            int debug) {
     const int pl = blockIdx.x % planes, ck = blockIdx.x / planes; // chunk-major: every plane's chain advances
     const PlaneParams pp = block_params(A.params, pl);
     if ((pp.flags & kFlagFallback) || pp.eb == 0.0) return;
@@ -695,6 +700,23 @@ __global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int 
         if (stats) {
             atomicAdd(&stats[0], nresolve);
             if (failed) atomicAdd(&stats[1], 1u);
+        }
+    }
+}
+__global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int planes, ChainLink link, uint32_t *stats,
+                                                                int debug) {
+    pdl_begin();
+    chain_chunk(A, planes, link, stats, debug);
+    if (!link.done) return;
+    __syncthreads(); // every chain value of this block is written
+    if (threadIdx.x == 0) {
+        const int pl = blockIdx.x % planes;
+        __threadfence();
+        const uint32_t old = atomicAdd(link.cnt + pl, 1u);
+        if (old + 1 == (uint32_t)link.cmax) { // the plane's last block
+            link.cnt[pl] = 0u;
+            __threadfence(); // acquire the other blocks' counts (and their values)
+            st_release(link.done + pl, link.epoch);
         }
     }
 }

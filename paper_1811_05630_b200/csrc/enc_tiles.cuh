@@ -728,12 +728,27 @@ __global__ void __launch_bounds__(32) enc_chain(TileArgs A, int planes, int nbuf
 }
 
 // ------------------------------------------------------------------ T4
-__global__ void __launch_bounds__(kEncThreads) enc_verify(TileArgs A, int planes) {
-    pdl_begin();
+// chain_done != nullptr: launched alongside enc_chain_scan (no grid-wide
+// wait); a tile waits for its own plane's chain (done[pl] == epoch) and
+// reads the chain values from L2.
+__global__ void __launch_bounds__(kEncThreads) enc_verify(TileArgs A, int planes, const uint32_t *chain_done,
+                                                          uint32_t epoch) {
+    if (chain_done) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    else pdl_begin();
     const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
     if (pl >= planes) return;
     const PlaneParams pp = block_params(A.params, pl);
     if (pp.flags & kFlagFallback) return;
+    if (chain_done && pp.eb != 0.0) {
+        if (threadIdx.x == 0) {
+            uint32_t v;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(chain_done + pl) : "memory");
+                if (v != epoch) __nanosleep(64);
+            } while (v != epoch);
+        }
+        __syncthreads();
+    }
     const int tid = threadIdx.x;
     const uint64_t L = A.L;
     const uint64_t t0 = (uint64_t)t * kTile;
@@ -837,8 +852,8 @@ __global__ void __launch_bounds__(kEncThreads) enc_verify(TileArgs A, int planes
         if (k >= tl) continue;
         const uint64_t i = t0 + k;
         const uint32_t ord = evbase + (uint32_t)rank[e]; // events before i
-        const double pred = ord > 0 ? dv[ord - 1] : 0.0;
-        const double dspec = f[e] ? dv[ord] : pred;
+        const double pred = ord > 0 ? __ldcg(dv + ord - 1) : 0.0;
+        const double dspec = f[e] ? __ldcg(dv + ord) : pred;
         double rec = 0.0;
         const uint32_t sy = quantize(x[i], pred, pp.q, pp.inv_q, pp.eb, half, &rec);
         if (sy == kOutlierSym) rec = x[i];

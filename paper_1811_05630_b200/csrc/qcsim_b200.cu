@@ -247,6 +247,7 @@ struct EncScratch {
     DBuf<unsigned long long> lb; // enc_lattice event-offset look-back
     uint32_t lb_epoch = 0;
     DBuf<double> chain_carry; // enc_chain_scan chunk hand-off
+    DBuf<uint32_t> chain_cnt, chain_done; // per-plane chain completion (enc_verify overlap)
     DBuf<uint32_t> chain_flag;
     uint32_t chain_epoch = 0;
     HBuf<uint64_t> h_bytes, h_off, h_misc;
@@ -348,6 +349,15 @@ void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
     CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 
+// enc_verify launched alongside the block-parallel chain, waiting per plane
+// (QCSIM_CHAIN_OVERLAP=0: wait for the whole chain grid)
+bool chain_overlap() {
+    static const bool on = [] {
+        const char *v = std::getenv("QCSIM_CHAIN_OVERLAP");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
 // 0 auto, 1 skip (debug), 2 serial warp chain, 3 block-parallel chain
 int chain_choice() {
     static const int mode = [] {
@@ -560,6 +570,8 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
             }
         }
     }
+    uint32_t *verify_done = nullptr; // per-plane chain completion (enc_verify overlaps the chain grid)
+    uint32_t verify_epoch = 0;
     {
         // (chain_mode / scan: chosen before enc_lattice, see chain_choice)
         static const int chain_debug = std::getenv("QCSIM_CHAIN_DEBUG") ? 1 : 0;
@@ -575,7 +587,15 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
             PROF("enc_chain_scan", st);
             const int cmax = (int)((L + kCsChunk - 1) / kCsChunk);
             S.chain_carry.ensure(planes * cmax);
-            if (S.chain_flag.ensure(planes * cmax, /*zero=*/true)) S.chain_epoch = 0;
+            bool fresh = S.chain_flag.ensure(planes * cmax, /*zero=*/true);
+            fresh |= S.chain_cnt.ensure(planes, /*zero=*/true);
+            fresh |= S.chain_done.ensure(planes, /*zero=*/true);
+            if (fresh) {
+                CK(cudaMemsetAsync(S.chain_flag.p, 0, S.chain_flag.cap * sizeof(uint32_t), st));
+                CK(cudaMemsetAsync(S.chain_cnt.p, 0, S.chain_cnt.cap * sizeof(uint32_t), st));
+                CK(cudaMemsetAsync(S.chain_done.p, 0, S.chain_done.cap * sizeof(uint32_t), st));
+                S.chain_epoch = 0;
+            }
             // debug: QCSIM_CHAIN_TRACE_AT = launch number -> per-block phase times to
             // QCSIM_CHAIN_TRACE_FILE
             static const long trace_at = std::getenv("QCSIM_CHAIN_TRACE_AT") ? std::atol(std::getenv("QCSIM_CHAIN_TRACE_AT")) : -1;
@@ -586,11 +606,16 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
                 trace_buf.ensure(8 * planes * cmax);
                 CK(cudaMemsetAsync(trace_buf.p, 0, 8 * planes * cmax * 8, st));
             }
-            ChainLink link{S.chain_carry.p, S.chain_flag.p, cmax, ++S.chain_epoch, tracing ? trace_buf.p : nullptr};
+            ChainLink link{S.chain_carry.p, S.chain_flag.p, cmax, ++S.chain_epoch, tracing ? trace_buf.p : nullptr,
+                           S.chain_cnt.p, S.chain_done.p};
             if (link.epoch == 0) { // wrapped: start over from clean flags
                 CK(cudaMemsetAsync(S.chain_flag.p, 0, S.chain_flag.cap * sizeof(uint32_t), st));
+                CK(cudaMemsetAsync(S.chain_done.p, 0, S.chain_done.cap * sizeof(uint32_t), st));
                 link.epoch = S.chain_epoch = 1;
             }
+            if (!chain_overlap()) link.cnt = link.done = nullptr;
+            verify_done = link.done;
+            verify_epoch = link.epoch;
             launch_k(enc_chain_scan, (unsigned)(planes * cmax), kCsThreads, kChainScanSmem, st, A, (int)planes, link,
                                                                                         chain_stats(), chain_debug);
             if (tracing) {
@@ -615,7 +640,8 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     }
     {
         PROF("enc_verify", st);
-        launch_k(enc_verify, tgrid_p, kEncThreads, 0, st, A, (int)planes);
+        launch_k(enc_verify, tgrid_p, kEncThreads, 0, st, A, (int)planes, (const uint32_t *)verify_done,
+                 verify_epoch);
     }
     {
         PROF("enc_serial", st);
