@@ -600,7 +600,8 @@ __device__ __forceinline__ void chain_chunk(const TileArgs &A, int planes, const
         double cd = 0.0;
         if (ck > 0) {
             const uint32_t *fp = link.flag + (uint64_t)pl * link.cmax + ck - 1;
-            while (ld_acquire(fp) != link.epoch) __nanosleep(20);
+            while (ld_acquire(fp) != link.epoch) {
+            }
             cd = link.carry[(uint64_t)pl * link.cmax + ck - 1];
         }
         S.dend[kCsThreads - 1] = cd; // parked until the final pass overwrites it
@@ -682,17 +683,24 @@ __device__ __forceinline__ void chain_chunk(const TileArgs &A, int planes, const
                    kh_in, q.kind == 2 ? S.resd[q.base] : -1ll, S.fail);
         }
     }
-    for (int j = tid; j < n; j += kCsThreads) dv[c0 + j] = S.c[(j / kCsEpt) * kCsPad + (j % kCsEpt)];
     __syncthreads();
     const bool failed = S.fail != 0;
-    if (failed && tid < 32) { // redo this chunk with the serial recurrence
+    // publish the exact last value for the next chunk first (its hand-off is
+    // the critical path), then store this chunk's values
+    if (!failed && tid == 0 && c0 + n < nev) {
+        link.carry[(uint64_t)pl * link.cmax + ck] = S.dend[nthr - 1];
+        st_release(link.flag + (uint64_t)pl * link.cmax + ck, link.epoch);
+    }
+    if (!failed) {
+        for (int j = tid; j < n; j += kCsThreads) dv[c0 + j] = S.c[(j / kCsEpt) * kCsPad + (j % kCsEpt)];
+    } else if (tid < 32) { // redo this chunk with the serial recurrence
         if (debug && tid == 0 && atomicAdd(&stats[3], 1u) < 16)
             printf("chain_scan: plane %d chunk %u fail mask %x\n", pl, c0, S.fail);
         const double d = chain_serial_warp(evc, ev, dv, c0, c0 + n, carry_d, tid, slot_of);
         if (tid == 0) S.dend[nthr - 1] = d;
     }
     if (tid == 0) {
-        if (c0 + n < nev) { // publish the exact last value for the next chunk
+        if (failed && c0 + n < nev) {
             link.carry[(uint64_t)pl * link.cmax + ck] = S.dend[nthr - 1];
             st_release(link.flag + (uint64_t)pl * link.cmax + ck, link.epoch);
         }
