@@ -83,6 +83,33 @@ __device__ __forceinline__ PlaneParams block_params(const PlaneParams *params, i
     return pp;
 }
 
+// Per-plane hand-off between grids that overlap (programmatic launch without
+// a grid-wide wait): every block of plane p of the producer arrives in
+// cnt[p]; the last one resets it and raises done[p] to the pass's epoch.  A
+// consumer block of plane p waits for done[p] == epoch and reads the
+// producer's data from L2.
+struct PlaneFlow {
+    uint32_t *cnt;
+    uint32_t *done;
+    uint32_t epoch;
+};
+__device__ __forceinline__ void flow_arrive(const PlaneFlow &F, int pl, uint32_t blocks) { // thread 0, after a barrier
+    __threadfence();
+    const uint32_t old = atomicAdd(F.cnt + pl, 1u);
+    if (old + 1 == blocks) {
+        F.cnt[pl] = 0u;
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(F.done + pl), "r"(F.epoch) : "memory");
+    }
+}
+__device__ __forceinline__ void flow_wait(const uint32_t *done, int pl, uint32_t epoch) { // one thread
+    uint32_t v;
+    do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(done + pl) : "memory");
+        if (v != epoch) __nanosleep(32);
+    } while (v != epoch);
+}
+
 // Planes with few tiles get their cross-tile carries inline: the consuming
 // block reduces the per-tile values before (or after) its own tile instead
 // of waiting for a separate plane_scan launch.
@@ -99,7 +126,7 @@ __device__ int32_t tile_carry(const int32_t *a, int t, int ntiles, int kind) {
         const int lo = kind == kScanMinExclRev ? t + 1 : 0;
         const int hi = kind == kScanMinExclRev ? ntiles : t;
         for (int k = lo + (int)threadIdx.x; k < hi; k += 32) {
-            const int32_t x = a[k];
+            const int32_t x = __ldcg(a + k);
             v = kind == kScanMaxExcl ? max(v, x) : (kind == kScanSumExcl ? v + x : min(v, x));
         }
         for (int off = 16; off >= 1; off >>= 1) {
@@ -129,8 +156,8 @@ __device__ void tile_carry2(const int32_t *a1, int k1, const int32_t *a2, int k2
         const int lo1 = k1 == kScanMinExclRev ? t + 1 : 0, hi1 = k1 == kScanMinExclRev ? ntiles : t;
         const int lo2 = k2 == kScanMinExclRev ? t + 1 : 0, hi2 = k2 == kScanMinExclRev ? ntiles : t;
         for (int k = (int)threadIdx.x; k < ntiles; k += 32) {
-            if (k >= lo1 && k < hi1) v1 = carry_reduce(k1, v1, a1[k]);
-            if (k >= lo2 && k < hi2) v2 = carry_reduce(k2, v2, a2[k]);
+            if (k >= lo1 && k < hi1) v1 = carry_reduce(k1, v1, __ldcg(a1 + k));
+            if (k >= lo2 && k < hi2) v2 = carry_reduce(k2, v2, __ldcg(a2 + k));
         }
         for (int off = 16; off >= 1; off >>= 1) {
             v1 = carry_reduce(k1, v1, __shfl_xor_sync(0xffffffffu, v1, off));
@@ -158,7 +185,7 @@ __device__ void tile_carryN(const int32_t *const *a, const int *kinds, int t, in
 #pragma unroll
             for (int q = 0; q < N; ++q) {
                 const bool rev = kinds[q] == kScanMinExclRev;
-                if (rev ? k > t : k < t) v[q] = carry_reduce(kinds[q], v[q], a[q][k]);
+                if (rev ? k > t : k < t) v[q] = carry_reduce(kinds[q], v[q], __ldcg(a[q] + k));
             }
         }
 #pragma unroll
@@ -180,7 +207,7 @@ __device__ void tile_excl_total(const int32_t *a, int t, int ntiles, int32_t &ex
     if (threadIdx.x < 32) {
         int32_t v1 = 0, v2 = 0;
         for (int k = (int)threadIdx.x; k < ntiles; k += 32) {
-            const int32_t x = a[k];
+            const int32_t x = __ldcg(a + k);
             v2 += x;
             if (k < t) v1 += x;
         }
@@ -731,10 +758,8 @@ __global__ void __launch_bounds__(32) enc_chain(TileArgs A, int planes, int nbuf
 // chain_done != nullptr: launched alongside enc_chain_scan (no grid-wide
 // wait); a tile waits for its own plane's chain (done[pl] == epoch) and
 // reads the chain values from L2.
-__global__ void __launch_bounds__(kEncThreads) enc_verify(TileArgs A, int planes, const uint32_t *chain_done,
-                                                          uint32_t epoch) {
-    if (chain_done) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    else pdl_begin();
+__device__ __forceinline__ void verify_tile(const TileArgs &A, int planes, const uint32_t *chain_done,
+                                            uint32_t epoch) {
     const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
     if (pl >= planes) return;
     const PlaneParams pp = block_params(A.params, pl);
@@ -868,13 +893,22 @@ __global__ void __launch_bounds__(kEncThreads) enc_verify(TileArgs A, int planes
     tile_stats(sv); // (a refuted plane gets them again from enc_serial_x)
     if (tid == 0 && s_bad) atomicOr(&A.params[pl].flags, kFlagFallback);
 }
+// flow.cnt != nullptr: the plane's tiles report completion (enc_serial_x
+// and tok_count then run alongside, per plane)
+__global__ void __launch_bounds__(kEncThreads) enc_verify(TileArgs A, int planes, const uint32_t *chain_done,
+                                                          uint32_t epoch, PlaneFlow flow) {
+    if (chain_done) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    else pdl_begin();
+    verify_tile(A, planes, chain_done, epoch);
+    if (!flow.cnt) return;
+    __syncthreads();
+    if (threadIdx.x == 0) flow_arrive(flow, blockIdx.x / A.ntiles, (uint32_t)A.ntiles);
+}
 
 // E1f: exact serial closed loop for refuted / linear planes (x from A.x).
-__global__ void enc_serial_x(TileArgs A, int planes) {
-    pdl_begin();
-    const int pl = blockIdx.x * blockDim.x + threadIdx.x;
-    if (pl >= planes) return;
-    const PlaneParams pp = A.params[pl];
+__device__ __forceinline__ void serial_plane(const TileArgs &A, int pl) {
+    PlaneParams pp = A.params[pl];
+    pp.flags = __ldcg(&A.params[pl].flags);
     if (!(pp.flags & kFlagFallback)) return;
     const uint64_t L = A.L;
     const long long half = 1ll << (A.qb - 1);
@@ -931,6 +965,21 @@ __global__ void enc_serial_x(TileArgs A, int planes) {
         }
     }
 }
+// ver_done != nullptr: runs alongside enc_verify; one thread per plane waits
+// for its plane's tiles, re-encodes a refuted plane, then raises
+// ser_done[pl] (tok_count's hand-off).
+__global__ void enc_serial_x(TileArgs A, int planes, const uint32_t *ver_done, uint32_t *ser_done, uint32_t epoch) {
+    if (ver_done) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    else pdl_begin();
+    const int pl = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pl >= planes) return;
+    if (ver_done) flow_wait(ver_done, pl, epoch);
+    serial_plane(A, pl);
+    if (ser_done) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ser_done + pl), "r"(epoch) : "memory");
+    }
+}
 
 // ------------------------------------------------------------ tokenizer
 struct TokArgs {
@@ -970,9 +1019,9 @@ __device__ __forceinline__ void element_runs(const TokArgs &A, const uint32_t *s
     uint32_t sv[kPerThread + 1];
     for (int e = 0; e < kPerThread; ++e) { // loads in flight across the carry pass
         const int k = tid * kPerThread + e;
-        sv[e + 1] = k < tl ? sym[t0 + k] : 0u;
+        sv[e + 1] = k < tl ? __ldcg(sym + t0 + k) : 0u;
     }
-    sv[0] = (t0 + tid * kPerThread > 0 && tid * kPerThread < tl) ? sym[t0 + tid * kPerThread - 1] : 0u;
+    sv[0] = (t0 + tid * kPerThread > 0 && tid * kPerThread < tl) ? __ldcg(sym + t0 + tid * kPerThread - 1) : 0u;
     int32_t prevb, nextb_carry;
     if (bases && A.ntiles <= kInlineTiles) { // + token / outlier offsets of the tile (tok_emit)
         const uint64_t o = (uint64_t)pl * A.ntiles;
@@ -1042,10 +1091,18 @@ __device__ __forceinline__ void element_runs(const TokArgs &A, const uint32_t *s
     }
 }
 
-__global__ void __launch_bounds__(kEncThreads) tok_count(TokArgs A, int planes) {
-    pdl_begin();
+// ser_done != nullptr: runs alongside enc_serial_x; a tile waits for its
+// plane's final symbols (ser_done[pl] == epoch) and reads them from L2.
+__global__ void __launch_bounds__(kEncThreads) tok_count(TokArgs A, int planes, const uint32_t *ser_done,
+                                                         uint32_t epoch) {
+    if (ser_done) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    else pdl_begin();
     const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
     if (pl >= planes) return;
+    if (ser_done) {
+        if (threadIdx.x == 0) flow_wait(ser_done, pl, epoch);
+        __syncthreads();
+    }
     const int tid = threadIdx.x;
     const uint64_t L = A.L;
     const uint64_t t0 = (uint64_t)t * kTile;
@@ -1086,7 +1143,7 @@ __global__ void __launch_bounds__(kEncThreads) tok_count(TokArgs A, int planes) 
         const int k = tid * kPerThread + e;
         if (k >= tl) continue;
         const uint64_t i = t0 + k;
-        const uint32_t s = sym[i];
+        const uint32_t s = __ldcg(sym + i);
         const uint64_t len = end[e] - start[e];
         const bool longrun = s != kOutlierSym && len >= kMinRunLen;
         if (longrun) {

@@ -248,6 +248,8 @@ struct EncScratch {
     uint32_t lb_epoch = 0;
     DBuf<double> chain_carry; // enc_chain_scan chunk hand-off
     DBuf<uint32_t> chain_cnt, chain_done; // per-plane chain completion (enc_verify overlap)
+    DBuf<uint32_t> ver_cnt, ver_done, ser_done; // per-plane verify / serial completion (tok_count overlap)
+    uint32_t flow_epoch = 0;
     DBuf<uint32_t> chain_flag;
     uint32_t chain_epoch = 0;
     HBuf<uint64_t> h_bytes, h_off, h_misc;
@@ -638,14 +640,33 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
             launch_k(enc_chain, (unsigned)planes, 32, chain_smem_bytes(nbufs), st, A, (int)planes, nbufs);
         }
     }
+    // verify -> serial -> tok_count hand-offs per plane (the scans between
+    // them are inline for planes of <= kInlineTiles tiles)
+    const bool flow = chain_overlap() && ntiles <= kInlineTiles;
+    PlaneFlow vflow{nullptr, nullptr, 0};
+    uint32_t flow_epoch = 0;
+    if (flow) {
+        bool fresh = S.ver_cnt.ensure(planes, /*zero=*/true);
+        fresh |= S.ver_done.ensure(planes, /*zero=*/true);
+        fresh |= S.ser_done.ensure(planes, /*zero=*/true);
+        if (fresh || ++S.flow_epoch == 0) {
+            CK(cudaMemsetAsync(S.ver_cnt.p, 0, S.ver_cnt.cap * sizeof(uint32_t), st));
+            CK(cudaMemsetAsync(S.ver_done.p, 0, S.ver_done.cap * sizeof(uint32_t), st));
+            CK(cudaMemsetAsync(S.ser_done.p, 0, S.ser_done.cap * sizeof(uint32_t), st));
+            S.flow_epoch = 1;
+        }
+        flow_epoch = S.flow_epoch;
+        vflow = PlaneFlow{S.ver_cnt.p, S.ver_done.p, flow_epoch};
+    }
     {
         PROF("enc_verify", st);
         launch_k(enc_verify, tgrid_p, kEncThreads, 0, st, A, (int)planes, (const uint32_t *)verify_done,
-                 verify_epoch);
+                 verify_epoch, vflow);
     }
     {
         PROF("enc_serial", st);
-        launch_k(enc_serial_x, (unsigned)((planes + 31) / 32), 32, 0, st, A, (int)planes);
+        launch_k(enc_serial_x, (unsigned)((planes + 31) / 32), 32, 0, st, A, (int)planes,
+                 (const uint32_t *)(flow ? S.ver_done.p : nullptr), flow ? S.ser_done.p : nullptr, flow_epoch);
     }
 
     TokArgs T;
@@ -680,7 +701,8 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     launch_plane_scan(st, S.t_nout.p, S.t_ooff.p, ntiles, (int)planes, kScanSumExcl);
     {
         PROF("tok_count", st);
-        launch_k(tok_count, tgrid_p, kEncThreads, 0, st, T, (int)planes);
+        launch_k(tok_count, tgrid_p, kEncThreads, 0, st, T, (int)planes,
+                 (const uint32_t *)(flow ? S.ser_done.p : nullptr), flow_epoch);
     }
     launch_plane_scan(st, S.t_ntok.p, S.t_tokoff.p, ntiles, (int)planes, kScanSumExcl);
 
