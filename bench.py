@@ -368,7 +368,7 @@ def main():
         algo_launch = 28.0 * chain["events"] / dominant["launches"]
         achieved = algo_launch / (dominant["ms"] * 1e-3 / dominant["launches"]) / 1e9
     traffic = None
-    tf = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_v6_chain_scan_ncu.json")
+    tf = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_v7_chain_scan_ncu.json")
     if os.path.exists(tf):
         with open(tf) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
