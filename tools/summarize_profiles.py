@@ -23,8 +23,9 @@ def shares(path, gates, label, out):
         lines = [ln for ln in f if ln.startswith('"')]
     rows = list(csv.DictReader(io.StringIO("".join(lines))))
     rows = [r for r in rows if r["Metric Name"] == "gpu__time_duration.sum"]
-    # a gate pass starts at engine_norm (deferred loop) -- take the last GATES of them
-    starts = [i for i, r in enumerate(rows) if short(r["Kernel Name"]) == "engine_norm"]
+    # a gate pass starts at engine_norm (v6) / dec_chunks (v7+) -- take the last GATES of them
+    marker = "engine_norm" if any(short(r["Kernel Name"]) == "engine_norm" for r in rows) else "dec_chunks"
+    starts = [i for i, r in enumerate(rows) if short(r["Kernel Name"]) == marker]
     first = starts[-gates] if len(starts) >= gates else 0
     agg = {}
     for r in rows[first:]:
