@@ -105,6 +105,17 @@ __global__ void __launch_bounds__(256) slot_scan(const uint64_t *in, uint64_t *o
     if (threadIdx.x == 0) out[planes] = carry;
 }
 
+// Packs blocks scattered over an arena (fixed slots) back to back:
+// meta = [src offset x P | dst offset x P | length x P], one block per block.
+__global__ void gather_blocks(const uint8_t *arena, const uint64_t *meta, int P, uint8_t *out) {
+    pdl_begin();
+    const int k = blockIdx.x;
+    if (k >= P) return;
+    const uint8_t *src = arena + meta[k];
+    uint8_t *dst = out + meta[P + k];
+    for (uint64_t i = threadIdx.x; i < meta[2 * P + k]; i += blockDim.x) dst[i] = src[i];
+}
+
 // Per-slice sq_norm: adjacent-pair tree over the tile partials (the tile
 // partials are themselves the lower levels of the same tree).
 __global__ void slice_norms(const double *tilesum, int ntiles, int units, double *out) {

@@ -20,6 +20,7 @@ struct EngineDevStats {
 };
 
 struct NormArgs {
+    int norm;              // run the normalization (norm_every)
     const double *tilesum; // [slice][ntiles] partial trees of the previous pass (nullptr: sq holds the norms)
     int ntiles;
     double *sq, *b0, *b1;  // slice norms, tree buffers
@@ -29,8 +30,76 @@ struct NormArgs {
     double *scale;
     const uint32_t *overflow;
     EngineDevStats *st;
-    int enabled;
+    int enabled;           // the extra block runs at all (norm or stats)
+    // run metrics of the previous encode pass (fixed-slot deferred loop: no
+    // slot scan), accumulated before the normalization
+    int stats;
+    const uint64_t *bytes;
+    const uint32_t *err;
+    const PlaneParams *params;
+    int planes;
+    uint64_t L;
+    unsigned long long stats_gate;
 };
+
+// Per encode pass: compression ratio min / sum in plane order (as the
+// host's record_sizes), current and peak bytes, fallback planes, latched
+// codec errors.  The whole block: ratios in parallel, the plane-order sum
+// by thread 0.
+__device__ void pass_stats(const uint64_t *bytes, const uint32_t *err, const PlaneParams *params, int planes,
+                           uint64_t L, unsigned long long gate, EngineDevStats *st) {
+    __shared__ double s_r[256];
+    __shared__ unsigned long long s_tsum, s_fb;
+    __shared__ int s_bad;
+    const int tid = threadIdx.x, nt = min((int)blockDim.x, 256);
+    const double in_bytes = (double)(8 * L);
+    if (tid == 0) {
+        s_tsum = 0;
+        s_fb = 0;
+        s_bad = 0;
+    }
+    double rmin = 0.0, rsum = 0.0;
+    if (tid == 0) {
+        rmin = st->ratio_min;
+        rsum = st->ratio_sum;
+    }
+    __syncthreads();
+    for (int base = 0; base < planes; base += nt) {
+        const int k = base + tid;
+        if (tid < nt && k < planes) {
+            const uint64_t b = bytes[k];
+            s_r[tid] = ddiv(in_bytes, (double)b);
+            atomicAdd(&s_tsum, (unsigned long long)b);
+            if (params[k].flags & kFlagFallback) atomicAdd(&s_fb, 1ull);
+            if (err[k] != 0) s_bad = 1;
+        }
+        __syncthreads();
+        if (tid == 0)
+            for (int j = 0; j < nt && base + j < planes; ++j) {
+                const double r = s_r[j];
+                if (r < rmin) rmin = r;
+                rsum = dadd(rsum, r);
+            }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        st->ratio_min = rmin;
+        st->ratio_sum = rsum;
+        st->calls += (unsigned long long)planes;
+        st->current = s_tsum;
+        if (s_tsum > st->peak) st->peak = s_tsum;
+        st->fallback += s_fb;
+        if (st->status == kEngOk && s_bad) {
+            st->status = kEngDepth;
+            st->status_gate = gate;
+        }
+    }
+    __syncthreads();
+}
+__global__ void pass_stats_kernel(NormArgs N) {
+    pdl_begin();
+    pass_stats(N.bytes, N.err, N.params, N.planes, N.L, N.stats_gate, N.st);
+}
 
 
 // Gate-pass prologue of the deferred loop: per-slice sq_norm of the previous
@@ -49,6 +118,8 @@ __device__ void engine_norm_body(const NormArgs &N) {
     const uint32_t *overflow = N.overflow;
     EngineDevStats *st = N.st;
     const int tid = threadIdx.x, nt = blockDim.x;
+    if (N.stats) pass_stats(N.bytes, N.err, N.params, N.planes, N.L, N.stats_gate, st);
+    if (!N.norm) return;
     // slice norms: one thread per slice over its (aligned power-of-two) tiles
     // (tilesum == nullptr: `sq` already holds them)
     for (uint64_t u = tid; tilesum && u < S; u += nt) {

@@ -41,6 +41,8 @@ struct CodeBook {
     uint64_t cap;
     int qb;
     DecTables dec;             // optional: decode tables of the new blocks
+    uint8_t *zero_arena = nullptr; // fixed slots (plane p at p * zero_W): zero the plane's slot for the packer
+    uint64_t zero_W = 0;
     unsigned long long *trace = nullptr; // debug phase stamps
 };
 
@@ -268,6 +270,7 @@ __device__ __forceinline__ void codebook_plane(const CodeBook &B, int planes, in
     __shared__ uint64_t lfirst[kMaxCodeLen + 2], lfirst0[kMaxCodeLen + 2];
     __shared__ unsigned long long s_bits;
     __shared__ uint32_t s_err;
+    __shared__ uint64_t s_slotb;
 
     const uint32_t rsym = 1u << B.qb;
     uint32_t *hist = B.hist + (uint64_t)pl * ((uint64_t)rsym + 1);
@@ -445,8 +448,13 @@ __device__ __forceinline__ void codebook_plane(const CodeBook &B, int planes, in
         B.block_bytes[pl] = bytes;
         B.slot_bytes[pl] = 16 + ((bytes + 15) & ~15ull);
         B.err[pl] = s_err;
+        s_slotb = 16 + ((bytes + 15) & ~15ull);
     }
     __syncthreads();
+    if (B.zero_arena) { // stream words are OR-combined at chunk seams
+        uint4 *w = reinterpret_cast<uint4 *>(B.zero_arena + (uint64_t)pl * B.zero_W);
+        for (uint64_t k = tid; k < s_slotb / 16; k += 256) w[k] = make_uint4(0, 0, 0, 0);
+    }
     // canonical codes in symbol order, one warp: a symbol's code is its
     // length's next free code plus its rank among equal lengths in the group
     if (tid < 32) {
@@ -508,6 +516,8 @@ struct PackArgs {
     uint64_t L, cap;
     int log2C, qb, mode, predictor;
     int planes_total;                     // slot_off[planes_total] = bytes needed
+    unsigned long long *lb;               // != nullptr: chunk bit offsets by decoupled look-back
+    uint32_t lb_epoch;                    //   (no pack_count pass; slots pre-zeroed)
 };
 
 __device__ __forceinline__ void put_bits_smem(uint32_t *w, uint32_t o, uint64_t v, int n) {
@@ -737,7 +747,18 @@ __global__ void __launch_bounds__(256) pack_write(PackArgs A, int planes, int nc
     }
     uint32_t pos[4], tot;
     Scan(scan_tmp).ExclusiveSum(tbits, pos, tot);
-    const uint64_t base_bit = (uint64_t)(uint32_t)carry_of(coff, nck + 1, cbits, pl, c, nck, kScanSumExcl);
+    uint64_t base_bit;
+    if (A.lb) { // this chunk's bits -> look-back over the plane's earlier chunks
+        __shared__ uint32_t s_base;
+        if (tid < 32) {
+            const uint32_t b = lookback_exclusive(A.lb + (uint64_t)pl * nck, A.lb_epoch, c, tot);
+            if (tid == 0) s_base = b;
+        }
+        __syncthreads();
+        base_bit = s_base;
+    } else {
+        base_bit = (uint64_t)(uint32_t)carry_of(coff, nck + 1, cbits, pl, c, nck, kScanSumExcl);
+    }
     const uint32_t b0 = (uint32_t)(base_bit & 31);
     const uint32_t nwords = (b0 + tot + 31) / 32;
     for (uint32_t w = tid; w < nwords; w += 256) words[w] = 0;

@@ -263,6 +263,11 @@ struct EncScratch {
     DecTables dec_out{};             // where enc_codebook writes decode tables (optional)
     EngineDevStats *stats_out = nullptr; // deferred engine: run metrics fused into the slot scan
     uint64_t *blk_off_out = nullptr;     // deferred engine: the packer writes block offsets here directly
+    uint64_t fixed_W = 0;                // deferred engine: plane p's slot at p * fixed_W (no slot scan)
+    uint64_t fixed_planes = 0, fixed_at = 0;
+    DBuf<uint64_t> fixed_off;
+    DBuf<unsigned long long> pack_lb;    // pack_write look-back slots [plane][chunk]
+    uint32_t pack_lb_epoch = 0;
     unsigned long long stats_gate = 0;
 
     void ensure(uint64_t planes, uint64_t units, uint64_t L, int qb) {
@@ -396,7 +401,15 @@ void launch_pack(cudaStream_t st, EncScratch &S, DBuf<uint8_t> &arena, bool coun
     P.arena_cap = arena.cap;
     const int nck = (int)((P.L + 1 + kPackTok - 1) / kPackTok);
     const unsigned grid = (unsigned)(S.planes * nck);
-    if (count) {
+    if (S.fixed_W && count) { // slots zeroed by the codebook; chunk offsets by look-back
+        if (S.pack_lb.ensure(S.planes * nck, /*zero=*/true)) S.pack_lb_epoch = 0;
+        if (++S.pack_lb_epoch >= (1u << 29)) {
+            CK(cudaMemsetAsync(S.pack_lb.p, 0, S.pack_lb.cap * sizeof(unsigned long long), st));
+            S.pack_lb_epoch = 1;
+        }
+        P.lb = S.pack_lb.p;
+        P.lb_epoch = S.pack_lb_epoch;
+    } else if (count) {
         {
             PROF("pack_count", st); // also zeroes the plane slots
             launch_k(pack_count, grid, 256, 0, st, P, (int)S.planes, nck, S.t_cbits.p);
@@ -727,6 +740,20 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     B.cap = cap;
     B.qb = qb;
     B.dec = S.dec_out;
+    if (S.fixed_W) {
+        if (S.fixed_planes != planes || S.fixed_at != S.fixed_W) {
+            std::vector<uint64_t> off(planes + 1);
+            for (uint64_t k = 0; k <= planes; ++k) off[k] = k * S.fixed_W;
+            S.fixed_off.ensure(planes + 1);
+            CK(cudaMemcpyAsync(S.fixed_off.p, off.data(), off.size() * 8, cudaMemcpyHostToDevice, st));
+            CK(cudaStreamSynchronize(st));
+            S.fixed_planes = planes;
+            S.fixed_at = S.fixed_W;
+        }
+        if (!arena.p || arena.cap < planes * S.fixed_W + 64) raise(QCSIM_NOMEM, "fixed-slot arena too small");
+        B.zero_arena = arena.p;
+        B.zero_W = S.fixed_W;
+    }
     // debug: QCSIM_CB_TRACE_AT = encode call -> codebook phase stamps to QCSIM_CB_TRACE_FILE
     static const long cb_at = std::getenv("QCSIM_CB_TRACE_AT") ? std::atol(std::getenv("QCSIM_CB_TRACE_AT")) : -1;
     static long cb_calls = 0;
@@ -752,8 +779,10 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
         }
     }
 
-    // slot offsets: exclusive scan of slot sizes (16-byte aligned slots)
-    if (S.stats_out) {
+    // slot offsets: exclusive scan of slot sizes (16-byte aligned slots);
+    // fixed slots: none (run metrics: the next pass's decoder grid)
+    if (S.fixed_W) {
+    } else if (S.stats_out) {
         PROF("slot_scan_stats", st);
         launch_k(slot_scan_stats, 1, 256, 0, st, S.slot_bytes.p, S.slot_off.p, S.block_bytes.p, S.err.p, S.params.p,
                                            (int)planes, L, S.stats_gate, S.stats_out, S.overflow.p);
@@ -772,7 +801,9 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     P.nsym = S.nsym.p;
     P.stream_bits = S.stream_bits.p;
     P.block_bytes = S.block_bytes.p;
-    P.slot_off = S.slot_off.p;
+    P.slot_off = S.fixed_W ? S.fixed_off.p : S.slot_off.p;
+    P.lb = nullptr;
+    P.lb_epoch = 0;
     P.opos = S.opos.p;
     P.oval = S.oval.p;
     P.ocount = S.ocount.p;
@@ -1035,6 +1066,8 @@ struct qcsim_engine {
     // device metrics, latched errors
     bool deferred = false;
     NormArgs norm{};          // this gate pass's deferred normalization (run by the decoder grid)
+    DBuf<uint64_t> exp_meta;  // export_blocks gather: source / destination offsets, lengths
+    DBuf<uint8_t> exp_buf;
     bool defer_fresh = false; // no pass has run yet in this deferred run
     DBuf<double> norm_buf[2], dev_scale;
     DBuf<EngineDevStats> dev_stats;
@@ -1280,14 +1313,33 @@ void engine_gate(qcsim_engine *e, const qcsim_action &a) {
     const bool apply = e->cfg.norm_every > 0 && (e->gates % (uint64_t)e->cfg.norm_every) == 0;
     double scale = 1.0;
     e->norm = NormArgs{};
-    if (apply && e->deferred) {
-        // slice norms of the previous pass from its tile partials (or, for the
-        // first gate of a run, the norms uploaded by engine_defer_begin); run
-        // by the decoder grid's extra block (engine_decode_old)
-        const uint64_t ntl = (e->L + kTile - 1) / kTile;
-        e->norm = NormArgs{e->defer_fresh ? nullptr : e->enc.tilesum.p, (int)ntl, e->slice_sq.p, e->norm_buf[0].p,
-                           e->norm_buf[1].p, e->S, 10.0 * e->cfg.norm_drift_tolerance, (unsigned long long)e->gates,
-                           e->dev_scale.p, e->defer_fresh ? nullptr : e->enc.overflow.p, e->dev_stats.p, 1};
+    if (e->deferred) {
+        // run by the decoder grid's extra block (engine_decode_old):
+        // the previous pass's run metrics (none before the first pass), then
+        // the slice norms of the previous pass from its tile partials (or,
+        // for the first gate of a run, the norms uploaded by
+        // engine_defer_begin) and the scale
+        NormArgs &N = e->norm;
+        N.norm = apply ? 1 : 0;
+        N.tilesum = e->defer_fresh ? nullptr : e->enc.tilesum.p;
+        N.ntiles = (int)((e->L + kTile - 1) / kTile);
+        N.sq = e->slice_sq.p;
+        N.b0 = e->norm_buf[0].p;
+        N.b1 = e->norm_buf[1].p;
+        N.S = e->S;
+        N.tol10 = 10.0 * e->cfg.norm_drift_tolerance;
+        N.gate = (unsigned long long)e->gates;
+        N.scale = e->dev_scale.p;
+        N.overflow = e->defer_fresh ? nullptr : e->enc.overflow.p;
+        N.st = e->dev_stats.p;
+        N.stats = e->defer_fresh ? 0 : 1;
+        N.bytes = e->enc.block_bytes.p;
+        N.err = e->enc.err.p;
+        N.params = e->enc.params.p;
+        N.planes = (int)(2 * e->ns);
+        N.L = e->L;
+        N.stats_gate = (unsigned long long)e->gates - 1;
+        N.enabled = N.norm || N.stats;
     } else if (apply) {
         const double G = tree_sum_host(e->sq_norm.data(), e->S);
         if (!std::isfinite(G) || std::fabs(G - 1.0) > 10.0 * e->cfg.norm_drift_tolerance) {
@@ -1346,6 +1398,13 @@ void engine_gate(qcsim_engine *e, const qcsim_action &a) {
 // Worst-case arena bytes for one gate pass (every plane at qcsim_block_bound,
 // 16-byte slots): with arenas that large a pass cannot overflow, so the gate
 // loop needs no host round trip.
+uint64_t fixed_slot_bytes(const qcsim_engine *e) {
+    const uint64_t L = e->L;
+    uint64_t nsym = (1ull << e->cfg.codec.quant_code_bits) + 1;
+    if (nsym > L + 1) nsym = L + 1;
+    const uint64_t bound = kHeaderBytes + 4 + 5 * nsym + (L * kMaxCodeLen + 7) / 8 + 16 + L * 16;
+    return (bound + 31) & ~15ull; // >= 16 + round_up(block bytes, 16): every slot_bytes fits
+}
 uint64_t arena_worst(const qcsim_engine *e) {
     const uint64_t L = e->L;
     uint64_t nsym = (1ull << e->cfg.codec.quant_code_bits) + 1;
@@ -1406,6 +1465,7 @@ bool engine_defer_begin(qcsim_engine *e) {
     CK(cudaStreamSynchronize(e->st));
     e->deferred = true;
     e->defer_fresh = true;
+    e->enc.fixed_W = fixed_slot_bytes(e); // one worst-case slot per plane: no slot scan per pass
     return true;
 }
 
@@ -1413,6 +1473,20 @@ bool engine_defer_begin(qcsim_engine *e) {
 // latched errors raised.
 void engine_defer_end(qcsim_engine *e, bool raise_errors) {
     e->deferred = false;
+    e->enc.fixed_W = 0;
+    if (!e->defer_fresh) { // run metrics of the last pass (the others: the next pass's decoder grid)
+        NormArgs N{};
+        N.st = e->dev_stats.p;
+        N.stats = 1;
+        N.bytes = e->enc.block_bytes.p;
+        N.err = e->enc.err.p;
+        N.params = e->enc.params.p;
+        N.planes = (int)(2 * e->ns);
+        N.L = e->L;
+        N.stats_gate = (unsigned long long)e->gates - 1;
+        PROF("pass_stats", e->st);
+        launch_k(pass_stats_kernel, 1, 256, 0, e->st, N);
+    }
     if (!e->defer_fresh) { // slice norms of the last pass, from its tile partials
         const uint64_t ntiles = (e->L + kTile - 1) / kTile;
         PROF("slice_norms", e->st);
@@ -1942,9 +2016,25 @@ qcsim_status qcsim_engine_export_blocks(qcsim_engine *e, uint8_t *out, uint64_t 
         std::vector<uint64_t> off(P);
         CK(cudaMemcpyAsync(off.data(), e->blk_off[e->cur].p, P * 8, cudaMemcpyDeviceToHost, e->st));
         CK(cudaStreamSynchronize(e->st));
-        // one contiguous device->host copy of the arena, then gather on host
         uint64_t hi = 0;
         for (uint64_t k = 0; k < P; ++k) hi = std::max(hi, off[k] + e->blk_bytes_h[k]);
+        if (hi > 2 * tot + (1u << 20)) { // sparse arena (fixed slots): gather on the device, one copy
+            std::vector<uint64_t> meta(3 * P);
+            for (uint64_t k = 0; k < P; ++k) {
+                meta[k] = off[k];
+                meta[P + k] = (k ? meta[P + k - 1] + e->blk_bytes_h[k - 1] : 0);
+                meta[2 * P + k] = e->blk_bytes_h[k];
+            }
+            e->exp_meta.ensure(3 * P);
+            e->exp_buf.ensure(tot + 16);
+            CK(cudaMemcpyAsync(e->exp_meta.p, meta.data(), meta.size() * 8, cudaMemcpyHostToDevice, e->st));
+            launch_k(gather_blocks, (unsigned)P, 256, 0, e->st, (const uint8_t *)e->arena[e->cur].p,
+                     (const uint64_t *)e->exp_meta.p, (int)P, e->exp_buf.p);
+            CK(cudaMemcpyAsync(out, e->exp_buf.p, tot, cudaMemcpyDeviceToHost, e->st));
+            CK(cudaStreamSynchronize(e->st));
+            return;
+        }
+        // one contiguous device->host copy of the arena, then gather on host
         std::vector<uint8_t> host(hi);
         CK(cudaMemcpyAsync(host.data(), e->arena[e->cur].p, hi, cudaMemcpyDeviceToHost, e->st));
         CK(cudaStreamSynchronize(e->st));
