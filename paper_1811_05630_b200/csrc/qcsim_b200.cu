@@ -357,13 +357,12 @@ void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
 }
 
 // enc_verify launched alongside the block-parallel chain, waiting per plane
-// (QCSIM_CHAIN_OVERLAP=0: wait for the whole chain grid)
-bool chain_overlap() {
-    static const bool on = [] {
-        const char *v = std::getenv("QCSIM_CHAIN_OVERLAP");
-        return !(v && v[0] == '0');
-    }();
-    return on;
+// (QCSIM_CHAIN_OVERLAP=0/1 forces it off/on)
+bool chain_overlap(uint64_t planes) {
+    static const int env = std::getenv("QCSIM_CHAIN_OVERLAP") ? std::atoi(std::getenv("QCSIM_CHAIN_OVERLAP")) : -1;
+    // auto: batches of >= 64 planes (small batches finish faster with
+    // grid-wide waits than with polled per-plane flags)
+    return env >= 0 ? env != 0 : planes >= 64;
 }
 // 0 auto, 1 skip (debug), 2 serial warp chain, 3 block-parallel chain
 int chain_choice() {
@@ -628,7 +627,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
                 CK(cudaMemsetAsync(S.chain_done.p, 0, S.chain_done.cap * sizeof(uint32_t), st));
                 link.epoch = S.chain_epoch = 1;
             }
-            if (!chain_overlap()) link.cnt = link.done = nullptr;
+            if (!chain_overlap(planes)) link.cnt = link.done = nullptr;
             verify_done = link.done;
             verify_epoch = link.epoch;
             launch_k(enc_chain_scan, (unsigned)(planes * cmax), kCsThreads, kChainScanSmem, st, A, (int)planes, link,
@@ -655,7 +654,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     }
     // verify -> serial -> tok_count hand-offs per plane (the scans between
     // them are inline for planes of <= kInlineTiles tiles)
-    const bool flow = chain_overlap() && ntiles <= kInlineTiles;
+    const bool flow = chain_overlap(planes) && ntiles <= kInlineTiles;
     PlaneFlow vflow{nullptr, nullptr, 0};
     uint32_t flow_epoch = 0;
     if (flow) {
@@ -1465,7 +1464,11 @@ bool engine_defer_begin(qcsim_engine *e) {
     CK(cudaStreamSynchronize(e->st));
     e->deferred = true;
     e->defer_fresh = true;
-    e->enc.fixed_W = fixed_slot_bytes(e); // one worst-case slot per plane: no slot scan per pass
+    // one worst-case slot per plane: no slot scan per pass (QCSIM_FIXED_SLOTS=0
+    // keeps the packed layout)
+    static const int fixed_env = std::getenv("QCSIM_FIXED_SLOTS") ? std::atoi(std::getenv("QCSIM_FIXED_SLOTS")) : 1;
+    const bool fixed = fixed_env != 0;
+    e->enc.fixed_W = fixed ? fixed_slot_bytes(e) : 0;
     return true;
 }
 
