@@ -1301,7 +1301,9 @@ void engine_decode_old(qcsim_engine *e, bool need_imported) {
     }
 }
 
+double g_host_t[4] = {0, 0, 0, 0}; // debug (QCSIM_ENQ_TIMING): gate prologue, decode, encode, total
 void engine_gate(qcsim_engine *e, const qcsim_action &a) {
+    const auto ht0 = std::chrono::steady_clock::now();
     if (a.kind > 2) raise(QCSIM_INVALID_ARGUMENT, "unknown action kind");
     if (a.kind == QCSIM_ACTION_BUTTERFLY && (a.target < 0 || a.target >= e->n))
         raise(QCSIM_INVALID_ARGUMENT, "action qubit out of range");
@@ -1355,7 +1357,9 @@ void engine_gate(qcsim_engine *e, const qcsim_action &a) {
         const uint64_t pj = partner_slice(a, e->s, e->s0 + k);
         if (pj < e->s0 || pj >= e->s0 + e->ns) remote = true;
     }
+    const auto ht1 = std::chrono::steady_clock::now();
     engine_decode_old(e, remote);
+    const auto ht2 = std::chrono::steady_clock::now();
     if (remote) {
         std::vector<int32_t> slot(e->S, -1);
         for (uint64_t k = 0; k < e->ns; ++k) slot[e->s0 + k] = (int32_t)k;
@@ -1389,7 +1393,13 @@ void engine_gate(qcsim_engine *e, const qcsim_action &a) {
     g.act = to_dev(a);
     g.s = e->s;
     g.L = e->L;
+    const auto ht3 = std::chrono::steady_clock::now();
     engine_store(e, g);
+    const auto ht4 = std::chrono::steady_clock::now();
+    g_host_t[0] += std::chrono::duration<double, std::micro>(ht1 - ht0).count();
+    g_host_t[1] += std::chrono::duration<double, std::micro>(ht2 - ht1).count();
+    g_host_t[2] += std::chrono::duration<double, std::micro>(ht4 - ht3).count();
+    g_host_t[3] += std::chrono::duration<double, std::micro>(ht4 - ht0).count();
     e->gates++;
     e->imported.clear();
 }
@@ -1908,9 +1918,13 @@ qcsim_status qcsim_engine_run(qcsim_engine *e, const qcsim_action *actions, uint
             float ms = 0.f;
             CK(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
             static const bool enq_timing = std::getenv("QCSIM_ENQ_TIMING") != nullptr; // debug
-            if (enq_timing)
-                std::fprintf(stderr, "engine_run: %llu gates, host enqueue %.3f ms, device %.3f ms\n",
-                             (unsigned long long)count, std::chrono::duration<double, std::milli>(h1 - h0).count(), ms);
+            if (enq_timing) {
+                std::fprintf(stderr, "engine_run: %llu gates, host enqueue %.3f ms, device %.3f ms | per gate us: "
+                             "prologue %.1f decode %.1f encode %.1f total %.1f\n",
+                             (unsigned long long)count, std::chrono::duration<double, std::milli>(h1 - h0).count(), ms,
+                             g_host_t[0] / count, g_host_t[1] / count, g_host_t[2] / count, g_host_t[3] / count);
+                for (double &v : g_host_t) v = 0;
+            }
             e->wall += ms * 1e-3;
             if (deferred) engine_defer_end(e, true);
         }
