@@ -126,74 +126,62 @@ __device__ void emit_dec_tables(const DecTables &T, int pl, uint32_t n, const ui
     }
 }
 
-// Two-queue Huffman merge (codec.cpp:168-229; ties prefer the leaf queue)
-// for n in [2, 64] leaves, one warp, everything in registers: leaf i and
-// internal node k live in lane i & 31 / k & 31 (register i >> 5).  Every lane
-// runs the same serial merge; the next two heads of both queues are fetched
-// by shuffles at the top of each step (independent of its picks), so only
-// the compare/select work is serial.  Writes par[0, 2n-1) (root: -1).
-__device__ __forceinline__ uint32_t wsel(uint32_t lo, uint32_t hi, uint32_t i) {
-    return __shfl_sync(0xffffffffu, i >= 32 ? hi : lo, i & 31);
-}
-__device__ void huff_merge_regs(const uint64_t *keys, uint32_t n, int32_t *par, int lane) {
-    const uint32_t L0 = (uint32_t)lane < n ? (uint32_t)(keys[lane] >> 25) : 0u;
-    const uint32_t L1 = (uint32_t)lane + 32 < n ? (uint32_t)(keys[lane + 32] >> 25) : 0u;
-    uint32_t I0 = 0, I1 = 0;                         // internal node counts
-    int32_t lp0 = -1, lp1 = -1, ip0 = -1, ip1 = -1;  // parents (global node index)
-    uint32_t lp = 0, ip = 0, ni = 0;                 // leaf head, internal head, internal nodes
-    uint32_t lv = wsel(L0, L1, 0), iv = 0;
-    while ((n - lp) + (ni - ip) >= 2) {
-        const uint32_t l1 = wsel(L0, L1, min(lp + 1, 63u)), l2 = wsel(L0, L1, min(lp + 2, 63u));
-        const uint32_t i1 = wsel(I0, I1, min(ip + 1, 63u)), i2 = wsel(I0, I1, min(ip + 2, 63u));
-        uint32_t pk[2], pv[2];
-        bool pl_[2];
-        uint32_t ln = l1, in = i1; // the heads after the current ones
+// Two-queue Huffman merge (codec.cpp:168-229; ties prefer the leaf queue) by
+// one thread, with both queue heads held in 4-deep register windows that
+// are refilled three picks ahead, so the shared-memory latency stays off the
+// serial compare/select path.  nc[0, n) = leaf counts (sorted by (count,
+// sym)); internal node counts are appended at nc[n...]; par[] receives the
+// parent of every node (root: -1).  Returns the node count.
+template <class U32P, class I32P>
+__device__ uint32_t huff_merge_serial(U32P nc, I32P par, uint32_t n) {
+    uint32_t lp = 0, ip = n, nodes = n;
+    uint32_t L[4], I[4];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const bool take_leaf = lp < n && (ip >= ni || lv <= iv);
-            pl_[k] = take_leaf;
-            if (take_leaf) {
-                pk[k] = lp;
-                pv[k] = lv;
-                ++lp;
-                lv = ln;
-                ln = l2;
-            } else {
-                pk[k] = ip;
-                pv[k] = iv;
-                ++ip;
-                iv = in;
-                in = i2;
-            }
-        }
-        const uint32_t sum = pv[0] + pv[1];
-        const int32_t node = (int32_t)(n + ni);
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const uint32_t q = pk[k];
-            if ((uint32_t)lane == (q & 31)) {
-                if (pl_[k]) {
-                    if (q < 32) lp0 = node; else lp1 = node;
-                } else {
-                    if (q < 32) ip0 = node; else ip1 = node;
-                }
-            }
-        }
-        if ((uint32_t)lane == (ni & 31)) {
-            if (ni < 32) I0 = sum; else I1 = sum;
-        }
-        if (ip == ni) iv = sum; // the internal queue was empty
-        ++ni;
+    for (int k = 0; k < 4; ++k) {
+        L[k] = lp + k < n ? nc[lp + k] : 0u;
+        I[k] = 0u;
     }
-    if ((uint32_t)lane < n) par[lane] = lp0;
-    if ((uint32_t)lane + 32 < n) par[lane + 32] = lp1;
-    if ((uint32_t)lane < ni) par[n + lane] = ip0;
-    if ((uint32_t)lane + 32 < ni) par[n + lane + 32] = ip1;
-    __syncwarp();
+    while ((n - lp) + (nodes - ip) >= 2) {
+        uint32_t v[2], q[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const bool leaf = lp < n && (ip >= nodes || L[0] <= I[0]);
+            if (leaf) {
+                v[k] = L[0];
+                q[k] = lp;
+                ++lp;
+                L[0] = L[1];
+                L[1] = L[2];
+                L[2] = L[3];
+                L[3] = lp + 3 < n ? nc[lp + 3] : 0u;
+            } else {
+                v[k] = I[0];
+                q[k] = ip;
+                ++ip;
+                I[0] = I[1];
+                I[1] = I[2];
+                I[2] = I[3];
+                I[3] = ip + 3 < nodes ? nc[ip + 3] : 0u;
+            }
+        }
+        const uint32_t sum = v[0] + v[1];
+        nc[nodes] = sum;
+        par[q[0]] = (int32_t)nodes;
+        par[q[1]] = (int32_t)nodes;
+        // the new node joins the internal window if it lands inside it
+        const uint32_t d = nodes - ip;
+        if (d == 0) I[0] = sum;
+        else if (d == 1) I[1] = sum;
+        else if (d == 2) I[2] = sum;
+        else if (d == 3) I[3] = sum;
+        ++nodes;
+    }
+    par[nodes - 1] = -1;
+    return nodes;
 }
 
 // The same merge for larger alphabets (nc[0, n) = leaf counts, par[0, n) =
-// -1 on entry), one warp, up to 32 picks per round.  Internal nodes are
+// -1 on entry) by one warp, up to 32 picks per round.  Internal nodes are
 // appended in non-decreasing order behind every node that already exists, so
 // as long as a round only takes internal nodes that existed when it started,
 // its picks are the plain merge of two sorted lists (leaves, known internal
@@ -344,15 +332,20 @@ __device__ __forceinline__ void codebook_plane(const CodeBook &B, int planes, in
     if (tid < 32) {
         if (n == 1) {
             if (tid == 0) par[0] = -1;
-        } else if (n <= 64) {
-            huff_merge_regs(keys, n, par, tid);
         } else {
             for (uint32_t i = tid; i < n; i += 32) {
                 nc[i] = (uint32_t)(keys[i] >> 25);
                 par[i] = -1;
             }
             __syncwarp();
-            huff_merge_batched(nc, par, n, tid);
+            // small alphabets (skewed trees, one pick pair per step): one
+            // thread; larger ones: the warp-batched merge
+            if (n <= 64) {
+                if (tid == 0) huff_merge_serial(nc, par, n);
+                __syncwarp();
+            } else {
+                huff_merge_batched(nc, par, n, tid);
+            }
         }
         if (tid == 0 && n > 1) {
             const uint32_t nodes = 2 * n - 1;

@@ -121,6 +121,60 @@ __device__ void huff_merge_regs(const uint64_t *keys, uint32_t n, int32_t *par, 
 }
 
 
+// Two-queue Huffman merge (codec.cpp:168-229; ties prefer the leaf queue) by
+// one thread, with both queue heads held in 4-deep register windows that
+// are refilled three picks ahead, so the shared-memory latency stays off the
+// serial compare/select path.  nc[0, n) = leaf counts (sorted by (count,
+// sym)); internal node counts are appended at nc[n...]; par[] receives the
+// parent of every node (root: -1).  Returns the node count.
+template <class U32P, class I32P>
+__device__ uint32_t huff_merge_serial(U32P nc, I32P par, uint32_t n) {
+    uint32_t lp = 0, ip = n, nodes = n;
+    uint32_t L[4], I[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        L[k] = lp + k < n ? nc[lp + k] : 0u;
+        I[k] = 0u;
+    }
+    while ((n - lp) + (nodes - ip) >= 2) {
+        uint32_t v[2], q[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const bool leaf = lp < n && (ip >= nodes || L[0] <= I[0]);
+            if (leaf) {
+                v[k] = L[0];
+                q[k] = lp;
+                ++lp;
+                L[0] = L[1];
+                L[1] = L[2];
+                L[2] = L[3];
+                L[3] = lp + 3 < n ? nc[lp + 3] : 0u;
+            } else {
+                v[k] = I[0];
+                q[k] = ip;
+                ++ip;
+                I[0] = I[1];
+                I[1] = I[2];
+                I[2] = I[3];
+                I[3] = ip + 3 < nodes ? nc[ip + 3] : 0u;
+            }
+        }
+        const uint32_t sum = v[0] + v[1];
+        nc[nodes] = sum;
+        par[q[0]] = (int32_t)nodes;
+        par[q[1]] = (int32_t)nodes;
+        // the new node joins the internal window if it lands inside it
+        const uint32_t d = nodes - ip;
+        if (d == 0) I[0] = sum;
+        else if (d == 1) I[1] = sum;
+        else if (d == 2) I[2] = sum;
+        else if (d == 3) I[3] = sum;
+        ++nodes;
+    }
+    par[nodes - 1] = -1;
+    return nodes;
+}
+
 __global__ void bench(int mode, uint32_t n, uint32_t *gscratch, long long *cyc, unsigned long long *ns, uint32_t *out) {
     __shared__ uint32_t nc_s[2048];
     __shared__ int32_t par_s[2048];
@@ -135,7 +189,7 @@ __global__ void bench(int mode, uint32_t n, uint32_t *gscratch, long long *cyc, 
     uint32_t nodes = 0;
     if ((mode & 3) == 0) { if (tid == 0) nodes = merge_serial(nc, par, n); }
     else if ((mode & 3) == 1) { if (tid < 32) nodes = merge_warp(nc, par, n, tid); }
-    else if ((mode & 3) == 2) { if (tid < 32 && n <= 64) { __shared__ uint64_t ks[64]; for (uint32_t i = tid; i < n; i += 32) ks[i] = ((uint64_t)nc[i] << 25) | i; __syncwarp(); huff_merge_regs(ks, n, par, tid); nodes = 2 * n - 1; } }
+    else if ((mode & 3) == 2) { if (tid == 0) nodes = huff_merge_serial(nc_s, par_s, n); }
     else { if (tid < 32) nodes = merge_warp(nc_s, par_s, n, tid); }
     __syncthreads();
     long long t1 = clock64();
@@ -146,7 +200,7 @@ __global__ void bench(int mode, uint32_t n, uint32_t *gscratch, long long *cyc, 
 int main() {
     uint32_t *g, *out; long long *cyc; unsigned long long *ns;
     cudaMalloc(&g, 128 * 4096 * 4); cudaMalloc(&out, 128 * 4); cudaMalloc(&cyc, 128 * 8); cudaMalloc(&ns, 128 * 8);
-    const char *names[] = {"serial/generic", "warp/generic", "regs(n<=64)", "warp/smem"};
+    const char *names[] = {"serial/generic", "warp/generic", "serial/prefetch", "warp/smem"};
     for (uint32_t n : {8u, 38u, 200u, 1000u})
         for (int mode = 0; mode < 8; ++mode) {
             for (int rep = 0; rep < 3; ++rep) bench<<<128, 256>>>(mode, n, g, cyc, ns, out);
