@@ -1333,7 +1333,7 @@ void engine_gate(qcsim_engine *e, const qcsim_action &a) {
         N.scale = e->dev_scale.p;
         N.overflow = e->defer_fresh ? nullptr : e->enc.overflow.p;
         N.st = e->dev_stats.p;
-        N.stats = e->defer_fresh ? 0 : 1;
+        N.stats = (e->defer_fresh || !e->enc.fixed_W) ? 0 : 1; // (packed slots: slot_scan_stats counts)
         N.bytes = e->enc.block_bytes.p;
         N.err = e->enc.err.p;
         N.params = e->enc.params.p;
@@ -1486,8 +1486,9 @@ bool engine_defer_begin(qcsim_engine *e) {
 // latched errors raised.
 void engine_defer_end(qcsim_engine *e, bool raise_errors) {
     e->deferred = false;
+    const bool fixed = e->enc.fixed_W != 0;
     e->enc.fixed_W = 0;
-    if (!e->defer_fresh) { // run metrics of the last pass (the others: the next pass's decoder grid)
+    if (!e->defer_fresh && fixed) { // run metrics of the last pass (the others: the next pass's decoder grid)
         NormArgs N{};
         N.st = e->dev_stats.p;
         N.stats = 1;

@@ -122,6 +122,20 @@ def test_grover_vs_oracle(q, oracle):
     _run_both(q, oracle, n, s, acts, per_gate=True)
 
 
+def test_grover_many_planes_vs_oracle(q, oracle):
+    """128 planes: the per-plane hand-offs (chain -> verify -> serial ->
+    tok_count) and fixed-slot packing of the deferred loop are active."""
+    n, s = 12, 6
+    marked = q.seeded_index(n, 7)
+    acts = q.lower(q.build_grover(n, marked, 2))
+    eng, oe = _run_both(q, oracle, n, s, acts)
+    m = eng.metrics()
+    om = oe.run([])
+    assert m.min_compression_ratio == om.min_compression_ratio
+    assert m.mean_compression_ratio == pytest.approx(om.mean_compression_ratio, rel=1e-15)
+    assert m.compress_calls == om.compress_calls
+
+
 def test_cross_slice_gates(q, oracle):
     """Butterflies/swaps/controls on slice-index bits (pairing)."""
     n, s = 9, 4
@@ -209,7 +223,7 @@ def test_compare_against_dense_run(q):
 _VARIANT_SCRIPT = r"""
 import hashlib, sys
 import paper_1811_05630_b200 as q
-n, s = 14, 10
+n, s = 14, 8  # 128 planes: per-plane hand-offs active by default
 acts = q.lower(q.build_qft(n))
 eng = q.Engine(q.EngineConfig(num_qubits=n, slice_bits=s, codec=q.CodecConfig(q.CodecMode.Absolute, 1e-5)))
 eng.load_basis(1234)
@@ -219,11 +233,14 @@ print(hashlib.sha256(bytes(blob)).hexdigest(), repr(m.mean_compression_ratio), r
 """
 
 
-@pytest.mark.parametrize("env", [{"QCSIM_CHAIN": "2"}, {"QCSIM_SYNC_GATES": "1"}, {"QCSIM_PDL": "0"}])
+@pytest.mark.parametrize("env", [{"QCSIM_CHAIN": "2"}, {"QCSIM_SYNC_GATES": "1"}, {"QCSIM_PDL": "0"},
+                                 {"QCSIM_CHAIN_OVERLAP": "0"}, {"QCSIM_FIXED_SLOTS": "0"}])
 def test_pipeline_variants_bit_identical(env):
-    """The serial warp chain, the host-synchronous gate loop and plain
-    launches produce the same blocks and metrics as the default pipeline
-    (block-parallel chain, deferred loop, programmatic dependent launch)."""
+    """The serial warp chain, the host-synchronous gate loop, plain launches,
+    grid-wide waits instead of per-plane hand-offs and the packed (scanned)
+    slot layout produce the same blocks and metrics as the default pipeline
+    (block-parallel chain, deferred loop, programmatic dependent launch,
+    per-plane hand-offs, fixed slots)."""
     import os
     import subprocess
     import sys
@@ -231,7 +248,7 @@ def test_pipeline_variants_bit_identical(env):
 
     def run(extra):
         e = dict(os.environ)
-        for k in ("QCSIM_CHAIN", "QCSIM_SYNC_GATES", "QCSIM_PDL"):
+        for k in ("QCSIM_CHAIN", "QCSIM_SYNC_GATES", "QCSIM_PDL", "QCSIM_CHAIN_OVERLAP", "QCSIM_FIXED_SLOTS"):
             e.pop(k, None)
         e.update(extra)
         r = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT], cwd=root, env=e, capture_output=True,
