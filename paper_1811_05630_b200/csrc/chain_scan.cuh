@@ -207,13 +207,16 @@ __device__ __forceinline__ Clamp event_clamp(bool outlier, double c, double dh, 
 }
 
 // ------------------------------------------------------ the kernel
-constexpr int kCsThreads = 256;
+#ifndef QCSIM_CS_THREADS
+#define QCSIM_CS_THREADS 256
+#endif
+constexpr int kCsThreads = QCSIM_CS_THREADS;        // (512, i.e. 8192-event chunks, measured slower: 39.3 vs 37.2 ms)
 constexpr int kCsEpt = 16;                        // events per thread
 constexpr int kCsChunk = kCsThreads * kCsEpt;     // events per block pass
 constexpr int kCsPad = kCsEpt + 1;                // bank-conflict-free rows
 constexpr int kCsWarps = kCsThreads / 32;
 constexpr uint32_t kCsSerialMax = 256;            // planes with fewer events run serially
-constexpr int kCsResolveMax = 48;                 // more resolve points: the chunk runs serially
+constexpr int kCsResolveMax = 48 * kCsThreads / 256; // more resolve points: the chunk runs serially
 
 struct ChainElem {
     int kind; // 0 map of the chunk carry, 1 constant (T[0] = delta), 2 map of resolved thread `base`
@@ -711,7 +714,7 @@ __device__ __forceinline__ void chain_chunk(const TileArgs &A, int planes, const
         }
     }
 }
-__global__ void __launch_bounds__(kCsThreads, 2) enc_chain_scan(TileArgs A, int planes, ChainLink link, uint32_t *stats,
+__global__ void __launch_bounds__(kCsThreads, kCsThreads >= 512 ? 1 : 2) enc_chain_scan(TileArgs A, int planes, ChainLink link, uint32_t *stats,
                                                                 int debug) {
     pdl_begin();
     chain_chunk(A, planes, link, stats, debug);
