@@ -602,9 +602,7 @@ __device__ __forceinline__ uint32_t token_bits(const SCodebook &C, const PackArg
 }
 
 // P1: bits of every 1024-token chunk (grid: planes x chunks).
-__global__ void __launch_bounds__(256) pack_count(PackArgs A, int planes, int nck, int32_t *cbits) {
-    pdl_begin();
-    const int pl = blockIdx.x / nck, c = blockIdx.x % nck;
+__device__ __forceinline__ void pack_count_item(const PackArgs &A, int planes, int nck, int32_t *cbits, int pl, int c) {
     if (pl >= planes) return;
     // zero this block's share of the plane's arena slot (stream words are
     // OR-combined at chunk seams by pack_write); skipped when the batch
@@ -654,10 +652,8 @@ __global__ void arena_zero(uint8_t *arena, uint64_t cap, const uint64_t *total_p
 
 // P2: header + table (chunk 0), stream bits of every chunk, outlier records,
 // decode-index bit positions (grid: planes x chunks).
-__global__ void __launch_bounds__(256) pack_write(PackArgs A, int planes, int nck, const int32_t *coff,
-                                                  const int32_t *cbits) {
-    pdl_begin();
-    const int pl = blockIdx.x / nck, c = blockIdx.x % nck;
+__device__ __forceinline__ void pack_write_item(const PackArgs &A, int planes, int nck, const int32_t *coff,
+                                                const int32_t *cbits, int pl, int c) {
     if (pl >= planes) return;
     const int tid = threadIdx.x;
     if (A.slot_off[A.planes_total] + 64 > A.arena_cap) {
@@ -809,6 +805,44 @@ __global__ void __launch_bounds__(256) pack_write(PackArgs A, int planes, int nc
     for (uint32_t j = s_jlo + tid; j < s_jhi; j += 256) {
         const uint32_t tk = idx[j].tok;
         idx[j].bitpos = tk >= t0 + tn ? base_bit + tot : base_bit + toff[tk - t0];
+    }
+}
+
+// Both packer grids are (plane, K) blocks; block (p, y) takes the plane's
+// chunks y, y + K, ... and stops after the last chunk holding tokens (or
+// slot words to zero).  A 2^20-element plane has 1025 chunk slots, but a
+// well-compressed plane fills a handful: looping replaces hundreds of
+// thousands of empty blocks.  A block takes its chunks in increasing order,
+// and a plane's blocks are dispatched in order, so a look-back wait
+// (pack_write) always targets a dispatched chunk.
+__global__ void __launch_bounds__(256) pack_count(PackArgs A, int planes, int nck, int K, int32_t *cbits) {
+    pdl_begin();
+    const int pl = blockIdx.x / K, y = blockIdx.x % K;
+    if (pl >= planes) return;
+    const uint32_t ntok = A.ntok[pl];
+    int cend = (int)((ntok + kPackTok - 1) / kPackTok); // chunks with tokens
+    if (A.slot_off[A.planes_total] + 64 <= A.arena_cap) { // chunks with slot words to zero
+        const uint64_t nw = (A.slot_off[pl + 1] - A.slot_off[pl]) / 16, per = (nw + nck - 1) / nck;
+        if (per) cend = max(cend, (int)((nw + per - 1) / per));
+    }
+    for (int c = y; c < nck; c += K) {
+        if (c >= cend) { // nothing to zero or count: a zero bit count
+            cbits[(uint64_t)pl * nck + c] = 0;
+            continue;
+        }
+        pack_count_item(A, planes, nck, cbits, pl, c);
+        __syncthreads();
+    }
+}
+__global__ void __launch_bounds__(256) pack_write(PackArgs A, int planes, int nck, int K, const int32_t *coff,
+                                                  const int32_t *cbits) {
+    pdl_begin();
+    const int pl = blockIdx.x / K, y = blockIdx.x % K;
+    if (pl >= planes) return;
+    const int nchk = (int)((A.ntok[pl] + kPackTok - 1) / kPackTok);
+    for (int c = y; c < nchk; c += K) {
+        pack_write_item(A, planes, nck, coff, cbits, pl, c);
+        __syncthreads();
     }
 }
 

@@ -399,7 +399,9 @@ void launch_pack(cudaStream_t st, EncScratch &S, DBuf<uint8_t> &arena, bool coun
     P.arena = arena.p;
     P.arena_cap = arena.cap;
     const int nck = (int)((P.L + 1 + kPackTok - 1) / kPackTok);
-    const unsigned grid = (unsigned)(S.planes * nck);
+    // (plane, K) blocks looping over the plane's chunks (pack_count / pack_write)
+    const int K = std::min(nck, 32);
+    const unsigned grid = (unsigned)(S.planes * K);
     if (S.fixed_W && count) { // slots zeroed by the codebook; chunk offsets by look-back
         if (S.pack_lb.ensure(S.planes * nck, /*zero=*/true)) S.pack_lb_epoch = 0;
         if (++S.pack_lb_epoch >= (1u << 29)) {
@@ -411,7 +413,7 @@ void launch_pack(cudaStream_t st, EncScratch &S, DBuf<uint8_t> &arena, bool coun
     } else if (count) {
         {
             PROF("pack_count", st); // also zeroes the plane slots
-            launch_k(pack_count, grid, 256, 0, st, P, (int)S.planes, nck, S.t_cbits.p);
+            launch_k(pack_count, grid, 256, 0, st, P, (int)S.planes, nck, K, S.t_cbits.p);
         }
         launch_plane_scan(st, S.t_cbits.p, S.t_coff.p, nck, (int)S.planes, kScanSumExcl);
     } else {
@@ -420,7 +422,7 @@ void launch_pack(cudaStream_t st, EncScratch &S, DBuf<uint8_t> &arena, bool coun
     }
     {
         PROF("pack_write", st);
-        launch_k(pack_write, grid, 256, 0, st, P, (int)S.planes, nck, S.t_coff.p, S.t_cbits.p);
+        launch_k(pack_write, grid, 256, 0, st, P, (int)S.planes, nck, K, S.t_coff.p, S.t_cbits.p);
     }
 }
 
