@@ -364,14 +364,36 @@ def main():
     dominant = kprof[0] if kprof else None
     chain = res.get("chain") or {}
     achieved, algo_launch = None, None
+    prof_dir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles")
+    traffic, basis = None, None
+    elem_planes = 2.0 * (1 << wl["n"]) / world  # re + im planes of this rank (one pass)
+    ntiles = ((1 << wl["s"]) + 1023) // 1024
     if dominant and dominant["kernel"] == "enc_chain_scan" and chain.get("events"):
         algo_launch = 28.0 * chain["events"] / dominant["launches"]
+        basis = "enc_chain_scan: 28 B per chained event (device-counted) / mean launch time"
+        tf = os.path.join(prof_dir, "r01_v7_chain_scan_ncu.json")
+        if os.path.exists(tf):
+            with open(tf) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+    elif dominant and dominant["kernel"] == "enc_lattice" and ntiles > 64:
+        # dense pass (planes of > 64 tiles): x (8 B) and flags (1 B) in;
+        # symbols (4 B), flags (1 B) and the lattice estimate (8 B) out per
+        # element of every plane; events are negligible at these ratios
+        algo_launch = 22.0 * elem_planes
+        basis = "enc_lattice: 22 B per element-plane (x, flags in; symbols, flags, lattice estimate out) / mean launch time"
+        tf = os.path.join(prof_dir, "r01_v8_qft28_pass_dram.json")
+        if os.path.exists(tf) and wl["name"] == "qft28":
+            with open(tf) as f:
+                for ln in json.load(f)["launches"]:
+                    if ln["kernel"] == "enc_lattice":
+                        traffic = ln["dram_read_bytes"] + ln["dram_write_bytes"]
+    elif dominant and dominant["kernel"] == "dec_chunks":
+        # dense write of every decoded value (8 B per element-plane) plus
+        # the compressed stream read
+        algo_launch = 8.0 * elem_planes + float(m.current_compressed_bytes * world)
+        basis = "dec_chunks: 8 B written per element-plane + the compressed blocks read / mean launch time"
+    if algo_launch is not None:
         achieved = algo_launch / (dominant["ms"] * 1e-3 / dominant["launches"]) / 1e9
-    traffic = None
-    tf = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_v7_chain_scan_ncu.json")
-    if os.path.exists(tf):
-        with open(tf) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
     # SURVEY.md §8(d) pass basis: input + output compressed block bytes per
     # gate pass / device time per pass
     algo_per_pass = 2.0 * m.current_compressed_bytes * world
@@ -379,7 +401,7 @@ def main():
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": (achieved / hbm) if achieved is not None else None, "traffic": traffic, "peak_kind": peak_kind,
             "kernel": dominant["kernel"] if dominant else None, "algo_bytes_per_launch": algo_launch,
-            "basis": "enc_chain_scan: 28 B per chained event (device-counted) / mean launch time",
+            "basis": basis,
             "pass_basis": {"achieved": pass_achieved, "frac": pass_achieved / hbm,
                            "basis": "per gate pass: input+output QCB1 block bytes (SURVEY.md 8(d)) / device time"},
             "dense_equivalent": {"achieved": 32.0 * (1 << wl["n"]) * res["gates"] / dev_s / 1e9,
