@@ -387,6 +387,18 @@ def main():
                 for ln in json.load(f)["launches"]:
                     if ln["kernel"] == "enc_lattice":
                         traffic = ln["dram_read_bytes"] + ln["dram_write_bytes"]
+    elif dominant and dominant["kernel"] == "enc_verify" and ntiles > 64:
+        # dense pass: x (8 B), flags (1 B) and the speculated symbol (4 B) read
+        # per element of every plane (chain values and index records are
+        # negligible at these ratios)
+        algo_launch = 13.0 * elem_planes
+        basis = "enc_verify: 13 B per element-plane (x, flags, symbol in) / mean launch time"
+        tf = os.path.join(prof_dir, "r01_v8_qft28_pass_dram.json")
+        if os.path.exists(tf) and wl["name"] == "qft28":
+            with open(tf) as f:
+                for ln in json.load(f)["launches"]:
+                    if ln["kernel"] == "enc_verify":
+                        traffic = ln["dram_read_bytes"] + ln["dram_write_bytes"]
     elif dominant and dominant["kernel"] == "dec_chunks":
         # dense write of every decoded value (8 B per element-plane) plus
         # the compressed stream read

@@ -413,7 +413,7 @@ __device__ uint32_t lookback_exclusive(unsigned long long *slots, uint32_t epoch
 // ------------------------------------------------------------------ T2
 // Lattice codes, flags and the plane's event list (the compaction is fused:
 // the tile's event offset comes from the look-back above).
-__global__ void __launch_bounds__(kEncThreads) enc_lattice(TileArgs A, int planes) {
+__global__ void __launch_bounds__(kEncThreads, 5) enc_lattice(TileArgs A, int planes) {
     pdl_begin();
     const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
     if (pl >= planes) return;
