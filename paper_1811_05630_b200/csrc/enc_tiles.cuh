@@ -1091,6 +1091,33 @@ __device__ __forceinline__ void element_runs(const TokArgs &A, const uint32_t *s
     }
 }
 
+// A tile is "flat" when no run starts inside it: every element equals its
+// predecessor (so the tile lies inside one run that began in an earlier
+// tile).  Such a tile emits no token and counts nothing (a run longer than
+// the tile is always collapsed, codec.cpp:460-482); only its decode-index
+// records need the run's end.  Block-uniform result; sym via L2.
+__device__ __forceinline__ bool tile_is_flat(const uint32_t *sym, uint64_t t0, int tl, uint32_t &s_out) {
+    bool flat = t0 > 0 && tl >= (int)kMinRunLen;
+    const int k0 = threadIdx.x * kPerThread;
+    uint32_t s = 0;
+    if (flat && k0 < tl) {
+        uint32_t prev = __ldcg(sym + t0 + k0 - 1);
+        for (int e = 0; e < kPerThread && k0 + e < tl; ++e) {
+            const uint32_t v = __ldcg(sym + t0 + k0 + e);
+            flat &= v == prev;
+            prev = v;
+        }
+        s = prev;
+    }
+    flat = __syncthreads_and(flat);
+    if (flat) {
+        s = __ldcg(sym + t0);
+        flat = s != kOutlierSym;
+    }
+    s_out = s;
+    return flat;
+}
+
 // ser_done != nullptr: runs alongside enc_serial_x; a tile waits for its
 // plane's final symbols (ser_done[pl] == epoch) and reads them from L2.
 __global__ void __launch_bounds__(kEncThreads) tok_count(TokArgs A, int planes, const uint32_t *ser_done,
@@ -1108,6 +1135,13 @@ __global__ void __launch_bounds__(kEncThreads) tok_count(TokArgs A, int planes, 
     const uint64_t t0 = (uint64_t)t * kTile;
     const int tl = (int)tmin<uint64_t>(kTile, L - t0);
     const uint32_t *sym = A.sym + (uint64_t)pl * L;
+    {
+        uint32_t fs;
+        if (tile_is_flat(sym, t0, tl, fs)) { // inside one long run: no tokens, no counts
+            if (tid == 0) A.t_ntok[(uint64_t)pl * A.ntiles + t] = 0;
+            return;
+        }
+    }
     using ScanI = cub::BlockScan<int, kEncThreads>;
     using RedI = cub::BlockReduce<int, kEncThreads>;
     __shared__ typename ScanI::TempStorage tmp;
@@ -1201,6 +1235,41 @@ __device__ __forceinline__ void tok_emit_tile(const TokArgs &A, int planes, int 
     uint32_t *tsym = A.tsym + (uint64_t)pl * (L + 1);
     uint32_t *trep = A.trep + (uint64_t)pl * (L + 1);
     IndexRec *idx = A.index + (uint64_t)pl * nidx;
+    {
+        uint32_t fs;
+        if (tile_is_flat(sym, t0, tl, fs)) {
+            // inside one long run: no tokens or outliers; the index records
+            // resume after the run's literal + RUN tokens
+            int32_t nextb, tokb, ob;
+            if (A.ntiles <= kInlineTiles) {
+                const uint64_t o = (uint64_t)pl * A.ntiles;
+                const int32_t *arr[3] = {A.t_firstb + o, A.t_ntok + o, A.t_nout + o};
+                const int kinds[3] = {kScanMinExclRev, kScanSumExcl, kScanSumExcl};
+                int32_t r[3];
+                tile_carryN<3>(arr, kinds, t, A.ntiles, r);
+                nextb = r[0];
+                tokb = r[1];
+                ob = r[2];
+            } else {
+                nextb = __ldcg(A.t_nextb + (uint64_t)pl * A.ntiles + t);
+                tokb = __ldcg(A.t_tokoff + (uint64_t)pl * (A.ntiles + 1) + t);
+                ob = __ldcg(A.t_ooff + (uint64_t)pl * (A.ntiles + 1) + t);
+            }
+            const uint64_t end = nextb == 0x7FFFFFFF ? L : (uint64_t)nextb;
+            for (uint64_t i = ((t0 + C - 1) & ~(C - 1)) + (uint64_t)tid * C; i < t0 + tl; i += (uint64_t)kEncThreads * C) {
+                IndexRec *r = idx + (i >> A.log2C);
+                r->last_lit = fs;
+                r->ocur = (uint32_t)ob;
+                r->tok = (uint32_t)tokb;
+                r->run_left = (uint32_t)(end - i);
+            }
+            if (t == A.ntiles - 1 && tid == 0) {
+                A.ntok[pl] = (uint32_t)tokb;
+                A.ocount[pl] = (uint32_t)ob;
+            }
+            return;
+        }
+    }
     uint64_t start[kPerThread], end[kPerThread];
     int32_t bases[2];
     element_runs<ScanI>(A, sym, pl, t, t0, tl, tmp, s_next, start, end, bases);
