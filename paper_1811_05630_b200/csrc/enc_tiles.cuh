@@ -493,13 +493,6 @@ __global__ void __launch_bounds__(kEncThreads, 5) enc_lattice(TileArgs A, int pl
         }
     }
     const bool fused = A.ntiles <= kInlineTiles; // else enc_compact writes the events
-    if (!fused) {
-        double *dhat = A.dval + (uint64_t)pl * L; // scratch until the chain overwrites dval
-        for (int e = 0; e < kPerThread; ++e) {
-            const int k = tid * kPerThread + e;
-            if (k < tl) dhat[t0 + k] = dh[e];
-        }
-    }
     kb[tid] = K[kPerThread - 1];
     // K and outlier status of element t0-1 (for the first element)
     long long kprev0 = 0;
@@ -552,6 +545,11 @@ __global__ void __launch_bounds__(kEncThreads, 5) enc_lattice(TileArgs A, int pl
     __syncthreads();
     ScanI(scan_tmp).ExclusiveSum(evflag, epos, tot);
     if (!fused) {
+        // lattice estimates of the events only (enc_compact reads them there;
+        // dval is scratch until the chain overwrites it)
+        double *dhat = A.dval + (uint64_t)pl * L;
+        for (int e = 0; e < kPerThread; ++e)
+            if (evflag[e]) dhat[t0 + tid * kPerThread + e] = dh[e];
         if (tid == 0) A.t_nev[(uint64_t)pl * A.ntiles + t] = (uint32_t)tot;
         return;
     }
@@ -594,6 +592,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_compact(TileArgs A, int plane
     const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
     if (pl >= planes) return;
     if (block_params(A.params, pl).flags & kFlagFallback) return;
+    if (A.t_nev[(uint64_t)pl * A.ntiles + t] == 0) return; // no events in this tile
     const int tid = threadIdx.x;
     const uint64_t L = A.L;
     const uint64_t t0 = (uint64_t)t * kTile;
