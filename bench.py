@@ -377,11 +377,12 @@ def main():
                 traffic = json.load(f).get("dram_bytes_per_launch")
     elif dominant and dominant["kernel"] == "enc_lattice" and ntiles > 64:
         # dense pass (planes of > 64 tiles): x (8 B) and flags (1 B) in;
-        # symbols (4 B), flags (1 B) and the lattice estimate (8 B) out per
-        # element of every plane; events are negligible at these ratios
-        algo_launch = 22.0 * elem_planes
-        basis = "enc_lattice: 22 B per element-plane (x, flags in; symbols, flags, lattice estimate out) / mean launch time"
-        tf = os.path.join(prof_dir, "r01_v8_qft28_pass_dram.json")
+        # symbols (4 B) and flags (1 B) out per element of every plane (the
+        # lattice estimates are written at events only; events are
+        # negligible at these ratios)
+        algo_launch = 14.0 * elem_planes
+        basis = "enc_lattice: 14 B per element-plane (x, flags in; symbols, flags out) / mean launch time"
+        tf = os.path.join(prof_dir, "r01_v9_qft28_pass_dram.json")
         if os.path.exists(tf) and wl["name"] == "qft28":
             with open(tf) as f:
                 for ln in json.load(f)["launches"]:
@@ -393,7 +394,7 @@ def main():
         # negligible at these ratios)
         algo_launch = 13.0 * elem_planes
         basis = "enc_verify: 13 B per element-plane (x, flags, symbol in) / mean launch time"
-        tf = os.path.join(prof_dir, "r01_v8_qft28_pass_dram.json")
+        tf = os.path.join(prof_dir, "r01_v9_qft28_pass_dram.json")
         if os.path.exists(tf) and wl["name"] == "qft28":
             with open(tf) as f:
                 for ln in json.load(f)["launches"]:
