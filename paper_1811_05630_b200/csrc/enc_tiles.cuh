@@ -473,7 +473,17 @@ __global__ void __launch_bounds__(kEncThreads, 5) enc_lattice(TileArgs A, int pl
         xv[e] = k < tl ? x[t0 + k] : 0.0;
     }
     int lo[kPerThread];
-    ScanI(scan_tmp).ExclusiveScan(opos, lo, -1, cub::Max());
+    {
+        // (no speculative outlier in the tile: every element's segment base
+        // comes from the carry)
+        bool anyout = false;
+        for (int e = 0; e < kPerThread; ++e) anyout |= opos[e] >= 0;
+        if (__syncthreads_or(anyout)) {
+            ScanI(scan_tmp).ExclusiveScan(opos, lo, -1, cub::Max());
+        } else {
+            for (int e = 0; e < kPerThread; ++e) lo[e] = -1;
+        }
+    }
     stamp(1);
     const int32_t tbase = carry_of(A.t_base, A.ntiles, A.t_lastout, pl, t, A.ntiles, kScanMaxExcl); // position or -1
     stamp(2);
@@ -543,7 +553,19 @@ __global__ void __launch_bounds__(kEncThreads, 5) enc_lattice(TileArgs A, int pl
     // event list: tile offset by look-back, in-tile positions by a block scan
     int epos[kPerThread], tot;
     __syncthreads();
-    ScanI(scan_tmp).ExclusiveSum(evflag, epos, tot);
+    if (!fused) { // the event count only (enc_compact places the records)
+        __shared__ int s_tot;
+        int mine = 0;
+        for (int e = 0; e < kPerThread; ++e) mine += evflag[e];
+        mine = __reduce_add_sync(0xffffffffu, mine);
+        if (tid == 0) s_tot = 0;
+        __syncthreads();
+        if ((tid & 31) == 0 && mine) atomicAdd(&s_tot, mine);
+        __syncthreads();
+        tot = s_tot;
+    } else {
+        ScanI(scan_tmp).ExclusiveSum(evflag, epos, tot);
+    }
     if (!fused) {
         // lattice estimates of the events only (enc_compact reads them there;
         // dval is scratch until the chain overwrites it)
