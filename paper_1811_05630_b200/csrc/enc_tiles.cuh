@@ -609,12 +609,7 @@ __global__ void __launch_bounds__(kEncThreads, 5) enc_lattice(TileArgs A, int pl
 // ------------------------------------------------------------------ T3
 // Event list for planes with many tiles (the fused look-back in enc_lattice
 // would serialise hundreds of tiles): tile offsets from the plane scan.
-__global__ void __launch_bounds__(kEncThreads) enc_compact(TileArgs A, int planes) {
-    pdl_begin();
-    const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
-    if (pl >= planes) return;
-    if (block_params(A.params, pl).flags & kFlagFallback) return;
-    if (A.t_nev[(uint64_t)pl * A.ntiles + t] == 0) return; // no events in this tile
+__device__ __forceinline__ void compact_tile(const TileArgs &A, int pl, int t) {
     const int tid = threadIdx.x;
     const uint64_t L = A.L;
     const uint64_t t0 = (uint64_t)t * kTile;
@@ -647,6 +642,19 @@ __global__ void __launch_bounds__(kEncThreads) enc_compact(TileArgs A, int plane
         ev[base + pos[e]] = (uint32_t)i | (out ? 0x80000000u : 0u);
         evc[base + pos[e]] = out ? x[i] : dmul(q, (double)((long long)sym[i] - half));
         evD[base + pos[e]] = dhat[i];
+    }
+}
+// Grid of (plane, K) blocks; block (p, y) takes the plane's tiles y, y + K,
+// ... and skips event-free tiles without touching their data.
+__global__ void __launch_bounds__(kEncThreads) enc_compact(TileArgs A, int planes, int K) {
+    pdl_begin();
+    const int pl = blockIdx.x / K, y = blockIdx.x % K;
+    if (pl >= planes) return;
+    if (block_params(A.params, pl).flags & kFlagFallback) return;
+    for (int t = y; t < A.ntiles; t += K) {
+        if (A.t_nev[(uint64_t)pl * A.ntiles + t] == 0) continue; // no events in this tile
+        compact_tile(A, pl, t);
+        __syncthreads();
     }
 }
 
@@ -1034,6 +1042,8 @@ struct TokArgs {
     int32_t *t_prevb;            // scanned: last run start strictly before the tile
     int32_t *t_nextb;            // scanned: first run start strictly after the tile
     int32_t *t_ntok, *t_tokoff;  // tokens per tile, scanned (+1)
+    const uint32_t *t_nev;       // lattice events per tile (0: every symbol is m = 0)
+    const PlaneParams *params;   // kFlagFallback: symbols re-encoded serially
     uint64_t L;
     int ntiles, log2C, qb;
 };
@@ -1046,15 +1056,11 @@ struct RunInfo {
 template <class ScanI>
 __device__ __forceinline__ void element_runs(const TokArgs &A, const uint32_t *sym, int pl, int t, uint64_t t0,
                                              int tl, typename ScanI::TempStorage &tmp, int *s_next,
-                                             uint64_t *start, uint64_t *end, int32_t *bases = nullptr) {
+                                             uint64_t *start, uint64_t *end, const uint32_t *sv,
+                                             int32_t *bases = nullptr) {
+    // sv: this thread's symbols as loaded by tile_is_flat
     const int tid = threadIdx.x;
     int isb[kPerThread], st[kPerThread];
-    uint32_t sv[kPerThread + 1];
-    for (int e = 0; e < kPerThread; ++e) { // loads in flight across the carry pass
-        const int k = tid * kPerThread + e;
-        sv[e + 1] = k < tl ? __ldcg(sym + t0 + k) : 0u;
-    }
-    sv[0] = (t0 + tid * kPerThread > 0 && tid * kPerThread < tl) ? __ldcg(sym + t0 + tid * kPerThread - 1) : 0u;
     int32_t prevb, nextb_carry;
     if (bases && A.ntiles <= kInlineTiles) { // + token / outlier offsets of the tile (tok_emit)
         const uint64_t o = (uint64_t)pl * A.ntiles;
@@ -1129,20 +1135,18 @@ __device__ __forceinline__ void element_runs(const TokArgs &A, const uint32_t *s
 // tile).  Such a tile emits no token and counts nothing (a run longer than
 // the tile is always collapsed, codec.cpp:460-482); only its decode-index
 // records need the run's end.  Block-uniform result; sym via L2.
-__device__ __forceinline__ bool tile_is_flat(const uint32_t *sym, uint64_t t0, int tl, uint32_t &s_out) {
-    bool flat = t0 > 0 && tl >= (int)kMinRunLen;
+__device__ __forceinline__ bool tile_is_flat(const uint32_t *sym, uint64_t t0, int tl, uint32_t *sv,
+                                             uint32_t &s_out) {
+    // sv[0] = the element before this thread's, sv[1..kPerThread] = its own
+    // (the layout element_runs consumes), read from L2 once
     const int k0 = threadIdx.x * kPerThread;
-    uint32_t s = 0;
-    if (flat && k0 < tl) {
-        uint32_t prev = __ldcg(sym + t0 + k0 - 1);
-        for (int e = 0; e < kPerThread && k0 + e < tl; ++e) {
-            const uint32_t v = __ldcg(sym + t0 + k0 + e);
-            flat &= v == prev;
-            prev = v;
-        }
-        s = prev;
-    }
+    for (int e = 0; e < kPerThread; ++e) sv[e + 1] = k0 + e < tl ? __ldcg(sym + t0 + k0 + e) : 0u;
+    sv[0] = (t0 + k0 > 0 && k0 < tl) ? __ldcg(sym + t0 + k0 - 1) : 0u;
+    bool flat = t0 > 0 && tl >= (int)kMinRunLen;
+    for (int e = 0; e < kPerThread; ++e)
+        if (k0 + e < tl) flat &= sv[e + 1] == sv[e];
     flat = __syncthreads_and(flat);
+    uint32_t s = 0;
     if (flat) {
         s = __ldcg(sym + t0);
         flat = s != kOutlierSym;
@@ -1168,9 +1172,10 @@ __global__ void __launch_bounds__(kEncThreads) tok_count(TokArgs A, int planes, 
     const uint64_t t0 = (uint64_t)t * kTile;
     const int tl = (int)tmin<uint64_t>(kTile, L - t0);
     const uint32_t *sym = A.sym + (uint64_t)pl * L;
+    uint32_t sv[kPerThread + 1];
     {
         uint32_t fs;
-        if (tile_is_flat(sym, t0, tl, fs)) { // inside one long run: no tokens, no counts
+        if (tile_is_flat(sym, t0, tl, sv, fs)) { // inside one long run: no tokens, no counts
             if (tid == 0) A.t_ntok[(uint64_t)pl * A.ntiles + t] = 0;
             return;
         }
@@ -1192,7 +1197,7 @@ __global__ void __launch_bounds__(kEncThreads) tok_count(TokArgs A, int planes, 
     for (int k = tid; k < kWin / 4; k += kEncThreads) reinterpret_cast<uint4 *>(hist)[k] = make_uint4(0, 0, 0, 0);
     if (tid == 0) { h0 = 0; hrun = 0; smin = 0xFFFFFFFFu; smax = 0; gbits = 0; ntouched = 0; }
     uint64_t start[kPerThread], end[kPerThread];
-    element_runs<ScanI>(A, sym, pl, t, t0, tl, tmp, s_next, start, end);
+    element_runs<ScanI>(A, sym, pl, t, t0, tl, tmp, s_next, start, end, sv);
     auto count = [&](uint32_t s, uint32_t n) {
         if (s == kOutlierSym) atomicAdd(&h0, n);
         else if (s == rsym) atomicAdd(&hrun, n);
@@ -1210,7 +1215,7 @@ __global__ void __launch_bounds__(kEncThreads) tok_count(TokArgs A, int planes, 
         const int k = tid * kPerThread + e;
         if (k >= tl) continue;
         const uint64_t i = t0 + k;
-        const uint32_t s = __ldcg(sym + i);
+        const uint32_t s = sv[e + 1];
         const uint64_t len = end[e] - start[e];
         const bool longrun = s != kOutlierSym && len >= kMinRunLen;
         if (longrun) {
@@ -1268,9 +1273,10 @@ __device__ __forceinline__ void tok_emit_tile(const TokArgs &A, int planes, int 
     uint32_t *tsym = A.tsym + (uint64_t)pl * (L + 1);
     uint32_t *trep = A.trep + (uint64_t)pl * (L + 1);
     IndexRec *idx = A.index + (uint64_t)pl * nidx;
+    uint32_t sv[kPerThread + 1];
     {
         uint32_t fs;
-        if (tile_is_flat(sym, t0, tl, fs)) {
+        if (tile_is_flat(sym, t0, tl, sv, fs)) {
             // inside one long run: no tokens or outliers; the index records
             // resume after the run's literal + RUN tokens
             int32_t nextb, tokb, ob;
@@ -1305,7 +1311,7 @@ __device__ __forceinline__ void tok_emit_tile(const TokArgs &A, int planes, int 
     }
     uint64_t start[kPerThread], end[kPerThread];
     int32_t bases[2];
-    element_runs<ScanI>(A, sym, pl, t, t0, tl, tmp, s_next, start, end, bases);
+    element_runs<ScanI>(A, sym, pl, t, t0, tl, tmp, s_next, start, end, sv, bases);
     int cnt[kPerThread], tpos[kPerThread], isout[kPerThread], opos[kPerThread];
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
@@ -1313,7 +1319,7 @@ __device__ __forceinline__ void tok_emit_tile(const TokArgs &A, int planes, int 
         isout[e] = 0;
         if (k >= tl) continue;
         const uint64_t i = t0 + k;
-        const uint32_t s = sym[i];
+        const uint32_t s = sv[e + 1];
         const uint64_t len = end[e] - start[e];
         const bool longrun = s != kOutlierSym && len >= kMinRunLen;
         cnt[e] = longrun ? (i == start[e] ? 2 : 0) : 1;
@@ -1329,7 +1335,7 @@ __device__ __forceinline__ void tok_emit_tile(const TokArgs &A, int planes, int 
         const int k = tid * kPerThread + e;
         if (k >= tl) continue;
         const uint64_t i = t0 + k;
-        const uint32_t s = sym[i];
+        const uint32_t s = sv[e + 1];
         const uint32_t tk = tokbase + (uint32_t)tpos[e];
         const uint64_t len = end[e] - start[e];
         const bool longrun = s != kOutlierSym && len >= kMinRunLen;

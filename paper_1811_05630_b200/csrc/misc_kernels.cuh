@@ -118,6 +118,27 @@ __global__ void gather_blocks(const uint8_t *arena, const uint64_t *meta, int P,
 
 // Per-slice sq_norm: adjacent-pair tree over the tile partials (the tile
 // partials are themselves the lower levels of the same tree).
+// One block per slice for slices of many tiles: the same adjacent-pair tree
+// (levels in shared memory), ntiles <= 4096.
+__global__ void __launch_bounds__(256) slice_norms_block(const double *tilesum, int ntiles, int units, double *out) {
+    pdl_begin();
+    __shared__ double buf[4096];
+    const int u = blockIdx.x;
+    if (u >= units) return;
+    const double *t = tilesum + (uint64_t)u * ntiles;
+    for (int k = threadIdx.x; k < ntiles; k += blockDim.x) buf[k] = t[k];
+    __syncthreads();
+    for (int w = ntiles / 2; w >= 1; w >>= 1) {
+        double v[16];
+        int n = 0;
+        for (int k = threadIdx.x; k < w; k += blockDim.x) v[n++] = dadd(buf[2 * k], buf[2 * k + 1]);
+        __syncthreads();
+        n = 0;
+        for (int k = threadIdx.x; k < w; k += blockDim.x) buf[k] = v[n++];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[u] = buf[0];
+}
 __global__ void slice_norms(const double *tilesum, int ntiles, int units, double *out) {
     pdl_begin();
     const int u = blockIdx.x * blockDim.x + threadIdx.x;

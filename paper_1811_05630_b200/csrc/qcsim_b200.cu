@@ -556,7 +556,8 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     launch_plane_scan(st, S.t_nev.p, S.t_evoff.p, ntiles, (int)planes, kScanSumExcl);
     if (ntiles > kInlineTiles) {
         PROF("enc_compact", st);
-        launch_k(enc_compact, tgrid_p, kEncThreads, 0, st, A, (int)planes);
+        const int K = std::min(ntiles, 32);
+        launch_k(enc_compact, (unsigned)(planes * K), kEncThreads, 0, st, A, (int)planes, K);
     }
     {
         // debug: dump one encode call's event lists (QCSIM_CHAIN_DUMP_AT = call
@@ -705,6 +706,8 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     T.t_nextb = S.t_nextb.p;
     T.t_ntok = S.t_ntok.p;
     T.t_tokoff = S.t_tokoff.p;
+    T.t_nev = reinterpret_cast<const uint32_t *>(S.t_nev.p);
+    T.params = S.params.p;
     T.L = L;
     T.ntiles = ntiles;
     T.log2C = log2C;
@@ -1189,7 +1192,10 @@ template <class Src> void engine_store(qcsim_engine *e, const Src &src) {
     e->slice_sq.ensure(e->ns);
     {
         PROF("slice_norms", e->st);
-        launch_k(slice_norms, (units + 127) / 128, 128, 0, e->st, e->enc.tilesum.p, (int)ntiles, units, e->slice_sq.p);
+        if (ntiles > 64 && ntiles <= 4096)
+            launch_k(slice_norms_block, (unsigned)units, 256, 0, e->st, e->enc.tilesum.p, (int)ntiles, units, e->slice_sq.p);
+        else
+            launch_k(slice_norms, (units + 127) / 128, 128, 0, e->st, e->enc.tilesum.p, (int)ntiles, units, e->slice_sq.p);
     }
     e->h_sq.ensure(e->ns);
     CK(cudaMemcpyAsync(e->h_sq.p, e->slice_sq.p, e->ns * sizeof(double), cudaMemcpyDeviceToHost, e->st));
