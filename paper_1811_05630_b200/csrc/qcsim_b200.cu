@@ -556,7 +556,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     launch_plane_scan(st, S.t_nev.p, S.t_evoff.p, ntiles, (int)planes, kScanSumExcl);
     if (ntiles > kInlineTiles) {
         PROF("enc_compact", st);
-        const int K = std::min(ntiles, 32);
+        const int K = std::min(ntiles, 256);
         launch_k(enc_compact, (unsigned)(planes * K), kEncThreads, 0, st, A, (int)planes, K);
     }
     {
