@@ -886,7 +886,16 @@ __device__ __forceinline__ void verify_tile(const TileArgs &A, int planes, const
         nev_plane = (uint32_t)eo[A.ntiles];
     }
     int nf_tile;
-    ScanI(scan_tmp).ExclusiveSum(f, rank, nf_tile);
+    {
+        bool anyf = false; // (an event-free tile: every rank is 0)
+        for (int e = 0; e < kPerThread; ++e) anyf |= f[e] != 0;
+        if (__syncthreads_or(anyf)) {
+            ScanI(scan_tmp).ExclusiveSum(f, rank, nf_tile);
+        } else {
+            for (int e = 0; e < kPerThread; ++e) rank[e] = 0;
+            nf_tile = 0;
+        }
+    }
     __syncthreads();
     // guard: the event ordinals of this tile must lie inside the plane's
     // event list (a violation means corrupt carries -> serial re-encode)
