@@ -371,7 +371,7 @@ def main():
     if dominant and dominant["kernel"] == "enc_chain_scan" and chain.get("events"):
         algo_launch = 28.0 * chain["events"] / dominant["launches"]
         basis = "enc_chain_scan: 28 B per chained event (device-counted) / mean launch time"
-        tf = os.path.join(prof_dir, "r01_v7_chain_scan_ncu.json")
+        tf = os.path.join(prof_dir, "r01_v10_chain_scan_ncu.json")
         if os.path.exists(tf):
             with open(tf) as f:
                 traffic = json.load(f).get("dram_bytes_per_launch")
@@ -382,7 +382,7 @@ def main():
         # negligible at these ratios)
         algo_launch = 14.0 * elem_planes
         basis = "enc_lattice: 14 B per element-plane (x, flags in; symbols, flags out) / mean launch time"
-        tf = os.path.join(prof_dir, "r01_v9_qft28_pass_dram.json")
+        tf = os.path.join(prof_dir, "r01_v10_qft28_pass_dram.json")
         if os.path.exists(tf) and wl["name"] == "qft28":
             with open(tf) as f:
                 for ln in json.load(f)["launches"]:
@@ -394,7 +394,7 @@ def main():
         # negligible at these ratios)
         algo_launch = 13.0 * elem_planes
         basis = "enc_verify: 13 B per element-plane (x, flags, symbol in) / mean launch time"
-        tf = os.path.join(prof_dir, "r01_v9_qft28_pass_dram.json")
+        tf = os.path.join(prof_dir, "r01_v10_qft28_pass_dram.json")
         if os.path.exists(tf) and wl["name"] == "qft28":
             with open(tf) as f:
                 for ln in json.load(f)["launches"]:
