@@ -254,6 +254,7 @@ struct ChainScanSmem {
     uint32_t pmask[kCsWarps];          // resolve points
     int fail;
     int firstbad;
+    int tent;                          // a tentative last value was published
 };
 constexpr size_t kChainScanSmem = sizeof(ChainScanSmem);
 
@@ -350,8 +351,10 @@ __device__ __forceinline__ void st_release(uint32_t *p, uint32_t v) {
 // a waiter's predecessor always has a smaller block index (dispatched
 // earlier) and the resident blocks advance every plane's chain at once.
 struct ChainLink {
-    double *carry;   // [plane][cmax]
-    uint32_t *flag;  // [plane][cmax]
+    double *carry;   // [plane][cmax] exact last value of a chunk ...
+    uint32_t *flag;  // [plane][cmax] ... released when it is final (epoch)
+    double *tcarry;  // [plane][cmax] tentative last value (from the maps, before the
+    uint32_t *tflag; //   chunk's own verification): the successor starts on it
     int cmax;        // chunks per plane in the grid
     uint32_t epoch;  // this launch's flag value
     unsigned long long *trace; // debug: per block 8 phase times (%globaltimer ns), see CS_TRACE
@@ -663,13 +666,17 @@ __device__ __forceinline__ void chain_chunk(const TileArgs &A, int planes, const
 
     // ---- the exact value before this chunk
     CS_TRACE(1);
+    // (the map path starts on the predecessor's tentative value and checks
+    // it against the final one before publishing its own final value; a
+    // serial chunk waits for the final value)
+    const uint64_t lk = (uint64_t)pl * link.cmax + ck;
     if (tid == 0) {
         double cd = 0.0;
         if (ck > 0) {
-            const uint32_t *fp = link.flag + (uint64_t)pl * link.cmax + ck - 1;
+            const uint32_t *fp = (serial_chunk ? link.flag : link.tflag) + lk - 1;
             while (ld_acquire(fp) != link.epoch) {
             }
-            cd = link.carry[(uint64_t)pl * link.cmax + ck - 1];
+            cd = serial_chunk ? link.carry[lk - 1] : link.tcarry[lk - 1];
         }
         S.dend[kCsThreads - 1] = cd; // parked until the final pass overwrites it
     }
@@ -682,8 +689,10 @@ __device__ __forceinline__ void chain_chunk(const TileArgs &A, int planes, const
             const double d = chain_serial_smem(S, dv + c0, n, carry_d, tid);
             if (tid == 0) {
                 if (c0 + n < nev) {
-                    link.carry[(uint64_t)pl * link.cmax + ck] = d;
-                    st_release(link.flag + (uint64_t)pl * link.cmax + ck, link.epoch);
+                    link.carry[lk] = d;
+                    link.tcarry[lk] = d;
+                    st_release(link.flag + lk, link.epoch);
+                    st_release(link.tflag + lk, link.epoch);
                 }
                 if (stats) atomicAdd(&stats[4], 1u);
             }
@@ -715,6 +724,19 @@ __device__ __forceinline__ void chain_chunk(const TileArgs &A, int planes, const
                 long long K = 0;
                 if (!d_to_k(d, S.A[ls], K)) CS_FAIL(4);
                 S.resd[p] = K - S.kh[ls];
+            }
+        }
+        // tentative last value from the maps: the successor starts on it
+        // while this chunk verifies itself
+        if (c0 + n < nev) {
+            const int lls = (nthr - 1) * kCsPad + (n - (nthr - 1) * kCsEpt) - 1;
+            double dt = 0.0;
+            if (S.fail == 0 && delta_to_d(S.kh[lls], delta_before(nthr), S.A[lls], dt)) {
+                link.tcarry[lk] = dt;
+                st_release(link.tflag + lk, link.epoch);
+                S.tent = 1;
+            } else {
+                S.tent = 0;
             }
         }
     }
@@ -750,26 +772,46 @@ __device__ __forceinline__ void chain_chunk(const TileArgs &A, int planes, const
                    kh_in, q.kind == 2 ? S.resd[q.base] : -1ll, S.fail);
         }
     }
+    // the carry this chunk started from must be the predecessor's final value
+    if (tid == 0 && ck > 0) {
+        const uint32_t *fp = link.flag + lk - 1;
+        while (ld_acquire(fp) != link.epoch) {
+        }
+        const double fin = link.carry[lk - 1];
+        if (bits_of(fin) != bits_of(carry_d)) {
+            CS_FAIL(7);
+            S.dend[kCsThreads - 1] = fin; // (read back below as the redo's start)
+        }
+    }
     __syncthreads();
     const bool failed = S.fail != 0;
+    const double carry_fin = (failed && ck > 0 && (S.fail & (1 << 7))) ? S.dend[kCsThreads - 1] : carry_d;
     // publish the exact last value for the next chunk first (its hand-off is
     // the critical path), then store this chunk's values
     if (!failed && tid == 0 && c0 + n < nev) {
-        link.carry[(uint64_t)pl * link.cmax + ck] = S.dend[nthr - 1];
-        st_release(link.flag + (uint64_t)pl * link.cmax + ck, link.epoch);
+        link.carry[lk] = S.dend[nthr - 1];
+        st_release(link.flag + lk, link.epoch);
+        if (!S.tent) { // nothing tentative went out: the final value serves both
+            link.tcarry[lk] = S.dend[nthr - 1];
+            st_release(link.tflag + lk, link.epoch);
+        }
     }
     if (!failed) {
         for (int j = tid; j < n; j += kCsThreads) dv[c0 + j] = S.c[(j / kCsEpt) * kCsPad + (j % kCsEpt)];
     } else if (tid < 32) { // redo this chunk with the serial recurrence
         if (debug && tid == 0 && atomicAdd(&stats[3], 1u) < 16)
             printf("chain_scan: plane %d chunk %u fail mask %x\n", pl, c0, S.fail);
-        const double d = chain_serial_warp(evc, ev, dv, c0, c0 + n, carry_d, tid, slot_of);
+        const double d = chain_serial_warp(evc, ev, dv, c0, c0 + n, carry_fin, tid, slot_of);
         if (tid == 0) S.dend[nthr - 1] = d;
     }
     if (tid == 0) {
         if (failed && c0 + n < nev) {
-            link.carry[(uint64_t)pl * link.cmax + ck] = S.dend[nthr - 1];
-            st_release(link.flag + (uint64_t)pl * link.cmax + ck, link.epoch);
+            link.carry[lk] = S.dend[nthr - 1];
+            st_release(link.flag + lk, link.epoch);
+            if (!S.tent) {
+                link.tcarry[lk] = S.dend[nthr - 1];
+                st_release(link.tflag + lk, link.epoch);
+            }
         }
         CS_TRACE(3);
         if (stats) {

@@ -247,6 +247,8 @@ struct EncScratch {
     DBuf<unsigned long long> lb; // enc_lattice event-offset look-back
     uint32_t lb_epoch = 0;
     DBuf<double> chain_carry; // enc_chain_scan chunk hand-off
+    DBuf<double> chain_tcarry;   // tentative chunk values (from the maps)
+    DBuf<uint32_t> chain_tflag;
     DBuf<uint32_t> chain_cnt, chain_done; // per-plane chain completion (enc_verify overlap)
     DBuf<uint32_t> ver_cnt, ver_done, ser_done; // per-plane verify / serial completion (tok_count overlap)
     uint32_t flow_epoch = 0;
@@ -604,11 +606,14 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
             PROF("enc_chain_scan", st);
             const int cmax = (int)((L + kCsChunk - 1) / kCsChunk);
             S.chain_carry.ensure(planes * cmax);
+            S.chain_tcarry.ensure(planes * cmax);
             bool fresh = S.chain_flag.ensure(planes * cmax, /*zero=*/true);
+            fresh |= S.chain_tflag.ensure(planes * cmax, /*zero=*/true);
             fresh |= S.chain_cnt.ensure(planes, /*zero=*/true);
             fresh |= S.chain_done.ensure(planes, /*zero=*/true);
             if (fresh) {
                 CK(cudaMemsetAsync(S.chain_flag.p, 0, S.chain_flag.cap * sizeof(uint32_t), st));
+                CK(cudaMemsetAsync(S.chain_tflag.p, 0, S.chain_tflag.cap * sizeof(uint32_t), st));
                 CK(cudaMemsetAsync(S.chain_cnt.p, 0, S.chain_cnt.cap * sizeof(uint32_t), st));
                 CK(cudaMemsetAsync(S.chain_done.p, 0, S.chain_done.cap * sizeof(uint32_t), st));
                 S.chain_epoch = 0;
@@ -623,10 +628,11 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
                 trace_buf.ensure(8 * planes * cmax);
                 CK(cudaMemsetAsync(trace_buf.p, 0, 8 * planes * cmax * 8, st));
             }
-            ChainLink link{S.chain_carry.p, S.chain_flag.p, cmax, ++S.chain_epoch, tracing ? trace_buf.p : nullptr,
-                           S.chain_cnt.p, S.chain_done.p};
+            ChainLink link{S.chain_carry.p, S.chain_flag.p, S.chain_tcarry.p, S.chain_tflag.p, cmax, ++S.chain_epoch,
+                           tracing ? trace_buf.p : nullptr, S.chain_cnt.p, S.chain_done.p};
             if (link.epoch == 0) { // wrapped: start over from clean flags
                 CK(cudaMemsetAsync(S.chain_flag.p, 0, S.chain_flag.cap * sizeof(uint32_t), st));
+                CK(cudaMemsetAsync(S.chain_tflag.p, 0, S.chain_tflag.cap * sizeof(uint32_t), st));
                 CK(cudaMemsetAsync(S.chain_done.p, 0, S.chain_done.cap * sizeof(uint32_t), st));
                 link.epoch = S.chain_epoch = 1;
             }
