@@ -63,7 +63,10 @@ __device__ __forceinline__ int16_t outlier_align(double x, int uq) {
     return (int16_t)max(ulp_exp(x), segment_mu(x, uq));
 }
 
-constexpr int kMaxW = 3;             // chain map tables of up to 8 entries
+#ifndef QCSIM_CS_MAXW
+#define QCSIM_CS_MAXW 2
+#endif
+constexpr int kMaxW = QCSIM_CS_MAXW;  // chain map tables of up to 2^kMaxW entries
 constexpr int kTab = 1 << kMaxW;
 
 // Reference K for an estimate dh at alignment A (A >= ulp(dh)): floor to a
