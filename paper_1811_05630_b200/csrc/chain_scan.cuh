@@ -820,7 +820,7 @@ __device__ __forceinline__ void chain_chunk(const TileArgs &A, int planes, const
         }
     }
 }
-__global__ void __launch_bounds__(kCsThreads, kCsThreads >= 512 ? 1 : 2) enc_chain_scan(TileArgs A, int planes, ChainLink link, uint32_t *stats,
+__global__ void __launch_bounds__(kCsThreads, kCsThreads * kCsEpt > 4096 ? 1 : 2) enc_chain_scan(TileArgs A, int planes, ChainLink link, uint32_t *stats,
                                                                 int debug) {
     pdl_begin();
     chain_chunk(A, planes, link, stats, debug);
