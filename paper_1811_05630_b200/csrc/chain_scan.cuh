@@ -16,7 +16,7 @@
 //
 // Maps of this shape are closed under composition (the composed W only
 // grows with the net rise in magnitude), so a thread folds its events into
-// one map (W <= 3 here: 8-entry tables), the block scans the maps, and each
+// one map (W <= kMaxW = 2: 4-entry tables), the block scans the maps, and each
 // thread gets its exact start value.  Steps a map cannot express (a jump up
 // by several binades, huge cancellations) "poison" their thread: a serial
 // resolver pass computes those threads with plain FP64 once their start is
