@@ -291,16 +291,24 @@ __global__ void __launch_bounds__(kEncThreads) enc_x(TileArgs A, Src src, int un
             const double b = dmul(xs[NP - 1][k], xs[NP - 1][k]);
             acc[e] = dadd(a, b);
         }
-        red[tid] = dadd(dadd(acc[0], acc[1]), dadd(acc[2], acc[3]));
-        __syncthreads();
-        for (int w = kEncThreads / 2; w >= 1; w >>= 1) {
-            double v = 0.0;
-            if (tid < w) v = dadd(red[2 * tid], red[2 * tid + 1]);
-            __syncthreads();
-            if (tid < w) red[tid] = v;
-            __syncthreads();
+        // the tile's adjacent-pair tree: 5 levels inside each warp by
+        // shuffles (left operand = lower index, as the reference tree), then
+        // the 8 warp sums
+        double v = dadd(dadd(acc[0], acc[1]), dadd(acc[2], acc[3]));
+        const int lane = tid & 31;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const double o = __shfl_down_sync(0xffffffffu, v, off);
+            if ((lane & (2 * off - 1)) == 0) v = dadd(v, o);
         }
-        if (tid == 0) A.tilesum[(uint64_t)unit * A.ntiles + t] = red[0];
+        if (lane == 0) red[tid >> 5] = v;
+        __syncthreads();
+        if (tid == 0) {
+            static_assert(kEncThreads == 256, "8 warp sums");
+            const double s01 = dadd(red[0], red[1]), s23 = dadd(red[2], red[3]);
+            const double s45 = dadd(red[4], red[5]), s67 = dadd(red[6], red[7]);
+            A.tilesum[(uint64_t)unit * A.ntiles + t] = dadd(dadd(s01, s23), dadd(s45, s67));
+        }
     }
     // speculative outliers
     const double hh = (double)(1ll << (A.qb - 1));
