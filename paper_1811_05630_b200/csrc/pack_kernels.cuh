@@ -229,7 +229,7 @@ __device__ void huff_merge_batched(U32P nc, I32P par, uint32_t n, int tid) {
     if (tid == 0) par[nodes - 1] = -1;
     __syncwarp();
 }
-constexpr uint32_t kDepthSerialN = 12; // larger (shared-memory) alphabets: depths by pointer jumping
+constexpr uint32_t kDepthSerialN = 64; // larger (shared-memory) alphabets: depths by pointer jumping
 
 // One block per plane.  Working arrays live in shared memory for alphabets of
 // up to kSmallN symbols (the serial two-queue merge then runs on smem), in
