@@ -136,6 +136,22 @@ def test_grover_many_planes_vs_oracle(q, oracle):
     assert m.compress_calls == om.compress_calls
 
 
+@pytest.mark.parametrize("n,s,norm_every", [(12, 6, 3), (10, 5, 1), (10, 5, 0)])
+def test_deferred_variants_vs_oracle(q, oracle, n, s, norm_every):
+    """Deferred-loop bookkeeping at the edges: passes without normalization
+    (run metrics still accumulated by the decoder-grid block) and a batch of
+    exactly 64 planes (the smallest with per-plane hand-offs)."""
+    marked = q.seeded_index(n, 11)
+    acts = q.lower(q.build_grover(n, marked, 2))
+    eng, oe = _run_both(q, oracle, n, s, acts, norm_every=norm_every)
+    m = eng.metrics()
+    om = oe.run([])
+    assert m.min_compression_ratio == om.min_compression_ratio
+    assert m.mean_compression_ratio == pytest.approx(om.mean_compression_ratio, rel=1e-15)
+    assert m.compress_calls == om.compress_calls
+    assert m.peak_compressed_bytes == om.peak_compressed_bytes
+
+
 def test_cross_slice_gates(q, oracle):
     """Butterflies/swaps/controls on slice-index bits (pairing)."""
     n, s = 9, 4
