@@ -953,14 +953,27 @@ __device__ __forceinline__ void verify_tile(const TileArgs &A, int planes, const
 }
 // flow.cnt != nullptr: the plane's tiles report completion (enc_serial_x
 // and tok_count then run alongside, per plane)
+// ser_done != nullptr: the plane's last tile also releases tok_count directly
+// when the plane was not refuted (enc_serial_x releases the refuted ones).
 __global__ void __launch_bounds__(kEncThreads) enc_verify(TileArgs A, int planes, const uint32_t *chain_done,
-                                                          uint32_t epoch, PlaneFlow flow) {
+                                                          uint32_t epoch, PlaneFlow flow, uint32_t *ser_done) {
     if (chain_done) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     else pdl_begin();
     verify_tile(A, planes, chain_done, epoch);
     if (!flow.cnt) return;
     __syncthreads();
-    if (threadIdx.x == 0) flow_arrive(flow, blockIdx.x / A.ntiles, (uint32_t)A.ntiles);
+    if (threadIdx.x == 0) {
+        const int pl = blockIdx.x / A.ntiles;
+        __threadfence();
+        const uint32_t old = atomicAdd(flow.cnt + pl, 1u);
+        if (old + 1 == (uint32_t)A.ntiles) {
+            flow.cnt[pl] = 0u;
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flow.done + pl), "r"(flow.epoch) : "memory");
+            if (ser_done && !(__ldcg(&A.params[pl].flags) & kFlagFallback))
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ser_done + pl), "r"(flow.epoch) : "memory");
+        }
+    }
 }
 
 // E1f: exact serial closed loop for refuted / linear planes (x from A.x).

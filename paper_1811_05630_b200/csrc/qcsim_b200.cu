@@ -683,7 +683,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     {
         PROF("enc_verify", st);
         launch_k(enc_verify, tgrid_p, kEncThreads, 0, st, A, (int)planes, (const uint32_t *)verify_done,
-                 verify_epoch, vflow);
+                 verify_epoch, vflow, flow ? S.ser_done.p : nullptr);
     }
     {
         PROF("enc_serial", st);
