@@ -1072,8 +1072,6 @@ struct TokArgs {
     int32_t *t_prevb;            // scanned: last run start strictly before the tile
     int32_t *t_nextb;            // scanned: first run start strictly after the tile
     int32_t *t_ntok, *t_tokoff;  // tokens per tile, scanned (+1)
-    const uint32_t *t_nev;       // lattice events per tile (0: every symbol is m = 0)
-    const PlaneParams *params;   // kFlagFallback: symbols re-encoded serially
     uint64_t L;
     int ntiles, log2C, qb;
 };

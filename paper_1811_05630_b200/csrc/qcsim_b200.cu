@@ -713,8 +713,6 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     T.t_nextb = S.t_nextb.p;
     T.t_ntok = S.t_ntok.p;
     T.t_tokoff = S.t_tokoff.p;
-    T.t_nev = reinterpret_cast<const uint32_t *>(S.t_nev.p);
-    T.params = S.params.p;
     T.L = L;
     T.ntiles = ntiles;
     T.log2C = log2C;
