@@ -133,6 +133,37 @@ __device__ __forceinline__ uint64_t peek64(const uint32_t *w, uint64_t bp) {
     return (hi << b) | (bswap32(w2) >> (32 - b));
 }
 
+// MSB-first bit window over a word stream: `acc` holds the next n valid bits
+// (32 < n <= 64 between symbols), `pre` the next word, loaded one refill
+// ahead, so a symbol costs shifts instead of dependent word loads.
+struct BitWindow {
+    uint64_t acc;
+    int n;
+    const uint32_t *src; // next word after `pre`
+    uint32_t pre;
+    __device__ __forceinline__ void init(const uint32_t *words, uint64_t bitpos) {
+        const uint64_t wi = bitpos >> 5;
+        const int b = (int)(bitpos & 31);
+        acc = (((uint64_t)bswap32(words[wi]) << 32) | bswap32(words[wi + 1])) << b;
+        n = 64 - b;
+        pre = words[wi + 2];
+        src = words + wi + 3;
+        refill();
+    }
+    __device__ __forceinline__ void refill() {
+        while (n <= 32) {
+            acc |= (uint64_t)bswap32(pre) << (32 - n);
+            n += 32;
+            pre = *src++;
+        }
+    }
+    __device__ __forceinline__ void skip(int l) { // l <= n
+        acc = l < 64 ? acc << l : 0ull;
+        n -= l;
+        refill();
+    }
+};
+
 constexpr int kDecThreads = 128;             // chunks per block
 constexpr int kDecStageWords = 4096;         // 16 KB of stream staged per block
 constexpr int kDecWin = 16;                  // output window per chunk (C is a multiple)
@@ -201,6 +232,7 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
     const uint64_t bit_hi = jend < nchunks ? idx[jend].bitpos : sbytes * 8;
     const uint64_t w_hi = (bit_hi >> 5) + 3;
     const bool staged = w_hi - w_lo <= (uint64_t)kDecStageWords;
+    const uint64_t sbase0 = staged ? w_lo * 32 : 0;
     if (staged)
         for (uint64_t w = w_lo + threadIdx.x; w < w_hi; w += kDecThreads) S.sw[w - w_lo] = __ldg(stream + w);
     __syncthreads();
@@ -212,6 +244,11 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
     if (active) r = idx[j];
     uint64_t bp = r.bitpos;
     uint32_t run_left = r.run_left;
+    const uint32_t *wsrc = staged ? S.sw : stream; // the window's word source ...
+    const uint64_t wbase = staged ? sbase0 : 0;     // ... and its first bit
+    // (unstaged groups only: staged words are cheap shared-memory peeks)
+    BitWindow bw;
+    if (active && !staged) bw.init(wsrc, bp - wbase);
     uint32_t last = r.last_lit;
     uint64_t ocur = r.ocur;
     double d1 = r.dprev, d2 = r.dprev2;
@@ -261,13 +298,18 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
                 --run_left;
                 continue;
             }
-            const uint64_t w = staged ? peek64<true>(S.sw, bp - sbase) : peek64<false>(stream, bp);
-            const uint32_t le = S.lut[w >> (64 - kLutBits)];
+            const uint64_t wtop = staged ? peek64<true>(S.sw, bp - sbase) : bw.acc;
+            const uint32_t le = S.lut[wtop >> (64 - kLutBits)];
             uint32_t s, l;
             if (le & 63) {
                 l = le & 63;
                 s = le >> 6;
+                if (!staged) bw.skip((int)l);
             } else {
+                // a code longer than the LUT: from the window when it holds
+                // maxlen bits, else from the stream (then the window restarts)
+                const bool inwin = staged || (int)maxlen <= bw.n;
+                const uint64_t w = inwin ? wtop : peek64<false>(stream, bp);
                 s = 0;
                 l = 0;
                 for (uint32_t ll = kLutBits + 1; ll <= maxlen; ++ll) {
@@ -283,13 +325,26 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
                     dead = true;
                     break;
                 }
+                if (!staged) {
+                    if (inwin) bw.skip((int)l);
+                    else bw.init(wsrc, bp + l - wbase);
+                }
             }
             bp += l;
             if (s == rsym) {
-                const uint64_t g = staged ? peek64<true>(S.sw, bp - sbase) : peek64<false>(stream, bp);
-                const int z = __clzll((long long)g);
-                run_left = (uint32_t)(g >> (64 - (2 * z + 1)));
-                bp += 2 * z + 1;
+                // Elias gamma: z zeros, then the value in z + 1 bits
+                const int z = staged ? 64 : __clzll((long long)bw.acc);
+                if (!staged && 2 * z + 1 <= bw.n) {
+                    run_left = (uint32_t)(bw.acc >> (64 - (2 * z + 1)));
+                    bw.skip(2 * z + 1);
+                    bp += 2 * z + 1;
+                } else {
+                    const uint64_t g = staged ? peek64<true>(S.sw, bp - sbase) : peek64<false>(stream, bp);
+                    const int zz = __clzll((long long)g);
+                    run_left = (uint32_t)(g >> (64 - (2 * zz + 1)));
+                    bp += 2 * zz + 1;
+                    if (!staged) bw.init(wsrc, bp - wbase);
+                }
             } else {
                 emit(s);
                 last = s;
