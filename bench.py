@@ -400,6 +400,13 @@ def main():
                 for ln in json.load(f)["launches"]:
                     if ln["kernel"] == "enc_verify":
                         traffic = ln["dram_read_bytes"] + ln["dram_write_bytes"]
+    elif dominant and dominant["kernel"] == "enc_compact" and chain.get("events"):
+        # per element-plane: the flags (1 B); per event: flags, symbol and
+        # lattice estimate (13 B) read (x only at outliers) and the record
+        # (index 4 B, addend 8 B, estimate 8 B) written; events counted on
+        # the device
+        algo_launch = (1.0 * elem_planes * dominant["launches"] + 33.0 * chain["events"]) / dominant["launches"]
+        basis = "enc_compact: 1 B per element-plane + 33 B per event (device-counted) / mean launch time"
     elif dominant and dominant["kernel"] == "dec_chunks":
         # dense write of every decoded value (8 B per element-plane) plus
         # the compressed stream read

@@ -654,16 +654,22 @@ __device__ __forceinline__ void compact_tile(const TileArgs &A, int pl, int t) {
 }
 // Grid of (plane, K) blocks; block (p, y) takes the plane's tiles y, y + K,
 // ... and skips event-free tiles without touching their data.
-__global__ void __launch_bounds__(kEncThreads) enc_compact(TileArgs A, int planes, int K) {
+// evcount != nullptr: the events placed are counted (bench roofline).
+__global__ void __launch_bounds__(kEncThreads) enc_compact(TileArgs A, int planes, int K,
+                                                           unsigned long long *evcount) {
     pdl_begin();
     const int pl = blockIdx.x / K, y = blockIdx.x % K;
     if (pl >= planes) return;
     if (block_params(A.params, pl).flags & kFlagFallback) return;
+    unsigned long long placed = 0;
     for (int t = y; t < A.ntiles; t += K) {
-        if (A.t_nev[(uint64_t)pl * A.ntiles + t] == 0) continue; // no events in this tile
+        const uint32_t ne = A.t_nev[(uint64_t)pl * A.ntiles + t];
+        if (ne == 0) continue; // no events in this tile
+        placed += ne;
         compact_tile(A, pl, t);
         __syncthreads();
     }
+    if (evcount && threadIdx.x == 0 && placed) atomicAdd(evcount, placed);
 }
 
 // ------------------------------------------------------------------ chain

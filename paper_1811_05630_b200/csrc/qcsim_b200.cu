@@ -560,7 +560,8 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     if (ntiles > kInlineTiles) {
         PROF("enc_compact", st);
         const int K = std::min(ntiles, 256);
-        launch_k(enc_compact, (unsigned)(planes * K), kEncThreads, 0, st, A, (int)planes, K);
+        launch_k(enc_compact, (unsigned)(planes * K), kEncThreads, 0, st, A, (int)planes, K,
+                 reinterpret_cast<unsigned long long *>(chain_stats() + 6));
     }
     {
         // debug: dump one encode call's event lists (QCSIM_CHAIN_DUMP_AT = call
