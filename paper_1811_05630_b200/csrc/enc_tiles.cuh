@@ -110,6 +110,45 @@ __device__ __forceinline__ void flow_wait(const uint32_t *done, int pl, uint32_t
     } while (v != epoch);
 }
 
+// A thread's kPerThread (= 4) consecutive elements of a tile in one or two
+// vector loads (tile starts are 1024-element aligned); scalar at a ragged end.
+static_assert(kPerThread == 4, "vector tile loads assume 4 elements per thread");
+__device__ __forceinline__ void load4(const uint8_t *p, int k0, int tl, uint32_t *v) {
+    if (k0 + 4 <= tl) {
+        const uint32_t w = *reinterpret_cast<const uint32_t *>(p + k0);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = (w >> (8 * e)) & 0xFF;
+    } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = k0 + e < tl ? p[k0 + e] : 0u;
+    }
+}
+__device__ __forceinline__ void load4(const uint32_t *p, int k0, int tl, uint32_t *v) {
+    if (k0 + 4 <= tl) {
+        const uint4 w = *reinterpret_cast<const uint4 *>(p + k0);
+        v[0] = w.x;
+        v[1] = w.y;
+        v[2] = w.z;
+        v[3] = w.w;
+    } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = k0 + e < tl ? p[k0 + e] : 0u;
+    }
+}
+__device__ __forceinline__ void load4(const double *p, int k0, int tl, double *v) {
+    if (k0 + 4 <= tl) {
+        const double2 a = *reinterpret_cast<const double2 *>(p + k0);
+        const double2 b = *reinterpret_cast<const double2 *>(p + k0 + 2);
+        v[0] = a.x;
+        v[1] = a.y;
+        v[2] = b.x;
+        v[3] = b.y;
+    } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = k0 + e < tl ? p[k0 + e] : 0.0;
+    }
+}
+
 // Planes with few tiles get their cross-tile carries inline: the consuming
 // block reduces the per-tile values before (or after) its own tile instead
 // of waiting for a separate plane_scan launch.
@@ -883,9 +922,14 @@ __device__ __forceinline__ void verify_tile(const TileArgs &A, int planes, const
     uint32_t *sym = A.sym + (uint64_t)pl * L;
     const double *dv = A.dval + (uint64_t)pl * L;
     int f[kPerThread], rank[kPerThread];
-    for (int e = 0; e < kPerThread; ++e) {
-        const int k = tid * kPerThread + e;
-        f[e] = (k < tl && (fl[t0 + k] & 1)) ? 1 : 0;
+    double xv[kPerThread];
+    uint32_t symv[kPerThread];
+    {
+        uint32_t fv[kPerThread];
+        load4(fl + t0, tid * kPerThread, tl, fv);
+        load4(x + t0, tid * kPerThread, tl, xv);
+        load4(sym + t0, tid * kPerThread, tl, symv);
+        for (int e = 0; e < kPerThread; ++e) f[e] = (fv[e] & 1) ? 1 : 0;
     }
     // event offset of the tile and the plane's event count, one carry pass
     uint32_t evbase, nev_plane;
@@ -933,7 +977,7 @@ __device__ __forceinline__ void verify_tile(const TileArgs &A, int planes, const
         const double pred = ord > 0 ? (chain_done ? __ldcg(dv + ord - 1) : __ldg(dv + ord - 1)) : 0.0;
         const double dspec = f[e] ? (chain_done ? __ldcg(dv + ord) : __ldg(dv + ord)) : pred;
         double rec = 0.0;
-        const double xi = x[i];
+        const double xi = xv[e];
         uint32_t sy;
         const double r0 = dmul(dsub(xi, pred), pp.inv_q);
         if (fabs(r0) < 0.49) {
@@ -946,7 +990,7 @@ __device__ __forceinline__ void verify_tile(const TileArgs &A, int planes, const
             sy = quantize(xi, pred, pp.q, pp.inv_q, pp.eb, half, &rec);
         }
         if (sy == kOutlierSym) rec = xi;
-        sv[e] = sym[i];
+        sv[e] = symv[e];
         if (sy != sv[e] || bits_of(rec) != bits_of(dspec)) bad = 1;
         if ((i & (C - 1)) == 0) {
             idx[i >> A.log2C].dprev = pred;
@@ -961,7 +1005,7 @@ __device__ __forceinline__ void verify_tile(const TileArgs &A, int planes, const
 // and tok_count then run alongside, per plane)
 // ser_done != nullptr: the plane's last tile also releases tok_count directly
 // when the plane was not refuted (enc_serial_x releases the refuted ones).
-__global__ void __launch_bounds__(kEncThreads) enc_verify(TileArgs A, int planes, const uint32_t *chain_done,
+__global__ void __launch_bounds__(kEncThreads, 5) enc_verify(TileArgs A, int planes, const uint32_t *chain_done,
                                                           uint32_t epoch, PlaneFlow flow, uint32_t *ser_done) {
     if (chain_done) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     else pdl_begin();
