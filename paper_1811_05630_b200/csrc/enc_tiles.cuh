@@ -1218,7 +1218,16 @@ __device__ __forceinline__ bool tile_is_flat(const uint32_t *sym, uint64_t t0, i
     // sv[0] = the element before this thread's, sv[1..kPerThread] = its own
     // (the layout element_runs consumes), read from L2 once
     const int k0 = threadIdx.x * kPerThread;
-    for (int e = 0; e < kPerThread; ++e) sv[e + 1] = k0 + e < tl ? __ldcg(sym + t0 + k0 + e) : 0u;
+    if (k0 + kPerThread <= tl) { // one 16-byte load (tile starts are 1024-element aligned)
+        static_assert(kPerThread == 4, "uint4 symbol loads");
+        const uint4 w = __ldcg(reinterpret_cast<const uint4 *>(sym + t0 + k0));
+        sv[1] = w.x;
+        sv[2] = w.y;
+        sv[3] = w.z;
+        sv[4] = w.w;
+    } else {
+        for (int e = 0; e < kPerThread; ++e) sv[e + 1] = k0 + e < tl ? __ldcg(sym + t0 + k0 + e) : 0u;
+    }
     sv[0] = (t0 + k0 > 0 && k0 < tl) ? __ldcg(sym + t0 + k0 - 1) : 0u;
     bool flat = t0 > 0 && tl >= (int)kMinRunLen;
     for (int e = 0; e < kPerThread; ++e)
