@@ -567,10 +567,12 @@ __global__ void __launch_bounds__(kEncThreads, 5) enc_lattice(TileArgs A, int pl
     __syncthreads();
     int evflag[kPerThread];
     uint32_t esym[kPerThread];
+    uint32_t fword = 0; // this thread's 4 flag bytes (one 32-bit store)
     int bad = 0;
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
         evflag[e] = 0;
+        esym[e] = 0;
         if (k >= tl) continue;
         long long kprev;
         bool prev_out;
@@ -590,10 +592,21 @@ __global__ void __launch_bounds__(kEncThreads, 5) enc_lattice(TileArgs A, int pl
             sy = (uint32_t)(m + half);
             f = (m != 0 || (prev_out && is_negzero(xp))) ? 1 : 0;
         }
-        fl[t0 + k] = f;
-        sym[t0 + k] = sy;
+        fword |= (uint32_t)f << (8 * e);
         esym[e] = sy;
         evflag[e] = f & 1;
+    }
+    {
+        const int k0 = tid * kPerThread;
+        if (k0 + kPerThread <= tl) { // flags and symbols: one 4-byte and one 16-byte store
+            *reinterpret_cast<uint32_t *>(fl + t0 + k0) = fword;
+            *reinterpret_cast<uint4 *>(sym + t0 + k0) = make_uint4(esym[0], esym[1], esym[2], esym[3]);
+        } else {
+            for (int e = 0; e < kPerThread && k0 + e < tl; ++e) {
+                fl[t0 + k0 + e] = (uint8_t)(fword >> (8 * e));
+                sym[t0 + k0 + e] = esym[e];
+            }
+        }
     }
     if (bad) atomicOr(&A.params[pl].flags, kFlagFallback);
     stamp(3);
