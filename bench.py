@@ -382,7 +382,7 @@ def main():
         # negligible at these ratios)
         algo_launch = 14.0 * elem_planes
         basis = "enc_lattice: 14 B per element-plane (x, flags in; symbols, flags out) / mean launch time"
-        tf = os.path.join(prof_dir, "r01_v15_qft28_pass_dram.json")
+        tf = os.path.join(prof_dir, "r01_v16_qft28_pass_dram.json")
         if os.path.exists(tf) and wl["name"] == "qft28":
             with open(tf) as f:
                 for ln in json.load(f)["launches"]:
@@ -394,7 +394,7 @@ def main():
         # negligible at these ratios)
         algo_launch = 13.0 * elem_planes
         basis = "enc_verify: 13 B per element-plane (x, flags, symbol in) / mean launch time"
-        tf = os.path.join(prof_dir, "r01_v15_qft28_pass_dram.json")
+        tf = os.path.join(prof_dir, "r01_v16_qft28_pass_dram.json")
         if os.path.exists(tf) and wl["name"] == "qft28":
             with open(tf) as f:
                 for ln in json.load(f)["launches"]:
