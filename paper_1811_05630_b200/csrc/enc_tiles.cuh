@@ -1148,12 +1148,20 @@ template <class ScanI>
 __device__ __forceinline__ void element_runs(const TokArgs &A, const uint32_t *sym, int pl, int t, uint64_t t0,
                                              int tl, typename ScanI::TempStorage &tmp, int *s_next,
                                              uint64_t *start, uint64_t *end, const uint32_t *sv,
-                                             int32_t *bases = nullptr) {
-    // sv: this thread's symbols as loaded by tile_is_flat
+                                             int32_t *bases = nullptr, const int32_t *carries = nullptr) {
+    // sv: this thread's symbols as loaded by tile_load_syms; carries: the
+    // tile_carries() result when the caller computed it already
     const int tid = threadIdx.x;
     int isb[kPerThread], st[kPerThread];
     int32_t prevb, nextb_carry;
-    if (bases && A.ntiles <= kInlineTiles) { // + token / outlier offsets of the tile (tok_emit)
+    if (carries) {
+        prevb = carries[0];
+        nextb_carry = carries[1];
+        if (bases) {
+            bases[0] = carries[2];
+            bases[1] = carries[3];
+        }
+    } else if (bases && A.ntiles <= kInlineTiles) { // + token / outlier offsets of the tile (tok_emit)
         const uint64_t o = (uint64_t)pl * A.ntiles;
         const int32_t *arr[4] = {A.t_lastb + o, A.t_firstb + o, A.t_ntok + o, A.t_nout + o};
         const int kinds[4] = {kScanMaxExcl, kScanMinExclRev, kScanSumExcl, kScanSumExcl};
@@ -1226,10 +1234,9 @@ __device__ __forceinline__ void element_runs(const TokArgs &A, const uint32_t *s
 // tile).  Such a tile emits no token and counts nothing (a run longer than
 // the tile is always collapsed, codec.cpp:460-482); only its decode-index
 // records need the run's end.  Block-uniform result; sym via L2.
-__device__ __forceinline__ bool tile_is_flat(const uint32_t *sym, uint64_t t0, int tl, uint32_t *sv,
-                                             uint32_t &s_out) {
-    // sv[0] = the element before this thread's, sv[1..kPerThread] = its own
-    // (the layout element_runs consumes), read from L2 once
+// This thread's symbols, sv[0] = the element before them, sv[1..kPerThread]
+// = its own (the layout element_runs consumes), from L2; no barrier.
+__device__ __forceinline__ void tile_load_syms(const uint32_t *sym, uint64_t t0, int tl, uint32_t *sv) {
     const int k0 = threadIdx.x * kPerThread;
     if (k0 + kPerThread <= tl) { // one 16-byte load (tile starts are 1024-element aligned)
         static_assert(kPerThread == 4, "uint4 symbol loads");
@@ -1242,6 +1249,11 @@ __device__ __forceinline__ bool tile_is_flat(const uint32_t *sym, uint64_t t0, i
         for (int e = 0; e < kPerThread; ++e) sv[e + 1] = k0 + e < tl ? __ldcg(sym + t0 + k0 + e) : 0u;
     }
     sv[0] = (t0 + k0 > 0 && k0 < tl) ? __ldcg(sym + t0 + k0 - 1) : 0u;
+}
+// Flatness of the tile from the loaded symbols (block-uniform).
+__device__ __forceinline__ bool tile_flat(const uint32_t *sym, uint64_t t0, int tl, const uint32_t *sv,
+                                          uint32_t &s_out) {
+    const int k0 = threadIdx.x * kPerThread;
     bool flat = t0 > 0 && tl >= (int)kMinRunLen;
     for (int e = 0; e < kPerThread; ++e)
         if (k0 + e < tl) flat &= sv[e + 1] == sv[e];
@@ -1253,6 +1265,25 @@ __device__ __forceinline__ bool tile_is_flat(const uint32_t *sym, uint64_t t0, i
     }
     s_out = s;
     return flat;
+}
+__device__ __forceinline__ bool tile_is_flat(const uint32_t *sym, uint64_t t0, int tl, uint32_t *sv,
+                                             uint32_t &s_out) {
+    tile_load_syms(sym, t0, tl, sv);
+    return tile_flat(sym, t0, tl, sv, s_out);
+}
+// prevb, nextb, token base, outlier base of tile t (element_runs' carries).
+__device__ __forceinline__ void tile_carries(const TokArgs &A, int pl, int t, int32_t *r) {
+    if (A.ntiles <= kInlineTiles) {
+        const uint64_t o = (uint64_t)pl * A.ntiles;
+        const int32_t *arr[4] = {A.t_lastb + o, A.t_firstb + o, A.t_ntok + o, A.t_nout + o};
+        const int kinds[4] = {kScanMaxExcl, kScanMinExclRev, kScanSumExcl, kScanSumExcl};
+        tile_carryN<4>(arr, kinds, t, A.ntiles, r);
+    } else {
+        carry_of2(A.t_prevb, A.ntiles, A.t_lastb, kScanMaxExcl, A.t_nextb, A.ntiles, A.t_firstb, kScanMinExclRev, pl,
+                  t, A.ntiles, r[0], r[1]);
+        carry_of2(A.t_tokoff, A.ntiles + 1, A.t_ntok, kScanSumExcl, A.t_ooff, A.ntiles + 1, A.t_nout, kScanSumExcl,
+                  pl, t, A.ntiles, r[2], r[3]);
+    }
 }
 
 // ser_done != nullptr: runs alongside enc_serial_x; a tile waits for its
@@ -1374,26 +1405,15 @@ __device__ __forceinline__ void tok_emit_tile(const TokArgs &A, int planes, int 
     uint32_t *trep = A.trep + (uint64_t)pl * (L + 1);
     IndexRec *idx = A.index + (uint64_t)pl * nidx;
     uint32_t sv[kPerThread + 1];
+    int32_t carries[4];
+    tile_load_syms(sym, t0, tl, sv); // in flight while warp 0 gathers the carries
+    tile_carries(A, pl, t, carries);
     {
         uint32_t fs;
-        if (tile_is_flat(sym, t0, tl, sv, fs)) {
+        if (tile_flat(sym, t0, tl, sv, fs)) {
             // inside one long run: no tokens or outliers; the index records
             // resume after the run's literal + RUN tokens
-            int32_t nextb, tokb, ob;
-            if (A.ntiles <= kInlineTiles) {
-                const uint64_t o = (uint64_t)pl * A.ntiles;
-                const int32_t *arr[3] = {A.t_firstb + o, A.t_ntok + o, A.t_nout + o};
-                const int kinds[3] = {kScanMinExclRev, kScanSumExcl, kScanSumExcl};
-                int32_t r[3];
-                tile_carryN<3>(arr, kinds, t, A.ntiles, r);
-                nextb = r[0];
-                tokb = r[1];
-                ob = r[2];
-            } else {
-                nextb = __ldcg(A.t_nextb + (uint64_t)pl * A.ntiles + t);
-                tokb = __ldcg(A.t_tokoff + (uint64_t)pl * (A.ntiles + 1) + t);
-                ob = __ldcg(A.t_ooff + (uint64_t)pl * (A.ntiles + 1) + t);
-            }
+            const int32_t nextb = carries[1], tokb = carries[2], ob = carries[3];
             const uint64_t end = nextb == 0x7FFFFFFF ? L : (uint64_t)nextb;
             for (uint64_t i = ((t0 + C - 1) & ~(C - 1)) + (uint64_t)tid * C; i < t0 + tl; i += (uint64_t)kEncThreads * C) {
                 IndexRec *r = idx + (i >> A.log2C);
@@ -1411,7 +1431,7 @@ __device__ __forceinline__ void tok_emit_tile(const TokArgs &A, int planes, int 
     }
     uint64_t start[kPerThread], end[kPerThread];
     int32_t bases[2];
-    element_runs<ScanI>(A, sym, pl, t, t0, tl, tmp, s_next, start, end, sv, bases);
+    element_runs<ScanI>(A, sym, pl, t, t0, tl, tmp, s_next, start, end, sv, bases, carries);
     int cnt[kPerThread], tpos[kPerThread], isout[kPerThread], opos[kPerThread];
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
