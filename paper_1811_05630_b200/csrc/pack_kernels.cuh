@@ -737,25 +737,31 @@ __device__ __forceinline__ void pack_write_item(const PackArgs &A, int planes, i
     uint32_t pos[4], tot;
     Scan(scan_tmp).ExclusiveSum(tbits, pos, tot);
     uint64_t base_bit;
-    if (A.lb) { // this chunk's bits -> look-back over the plane's earlier chunks
-        __shared__ uint32_t s_base;
-        if (tid < 32) {
-            const uint32_t b = lookback_exclusive(A.lb + (uint64_t)pl * nck, A.lb_epoch, c, tot);
-            if (tid == 0) s_base = b;
-        }
-        __syncthreads();
-        base_bit = s_base;
-    } else {
-        base_bit = (uint64_t)(uint32_t)carry_of(coff, nck + 1, cbits, pl, c, nck, kScanSumExcl);
-    }
-    const uint32_t b0 = (uint32_t)(base_bit & 31);
-    const uint32_t nwords = (b0 + tot + 31) / 32;
-    for (uint32_t w = tid; w < nwords; w += 256) words[w] = 0;
+    // the word buffer (bounded for any bit offset) and the token offsets do
+    // not depend on where the chunk starts: the other warps fill them while
+    // warp 0 looks back
+    const uint32_t nw_max = (tot + 62) / 32;
     for (int e = 0; e < 4; ++e) {
         const uint32_t k = tid * 4 + e;
         if (k <= tn) toff[k] = pos[e];
     }
     if (tid == 255) toff[tn] = tot;
+    if (A.lb) { // this chunk's bits -> look-back over the plane's earlier chunks
+        __shared__ uint32_t s_base;
+        if (tid < 32) {
+            const uint32_t b = lookback_exclusive(A.lb + (uint64_t)pl * nck, A.lb_epoch, c, tot);
+            if (tid == 0) s_base = b;
+        } else {
+            for (uint32_t w = tid - 32; w < nw_max; w += 224) words[w] = 0;
+        }
+        __syncthreads();
+        base_bit = s_base;
+    } else {
+        for (uint32_t w = tid; w < nw_max; w += 256) words[w] = 0;
+        base_bit = (uint64_t)(uint32_t)carry_of(coff, nck + 1, cbits, pl, c, nck, kScanSumExcl);
+    }
+    const uint32_t b0 = (uint32_t)(base_bit & 31);
+    const uint32_t nwords = (b0 + tot + 31) / 32;
     __syncthreads();
     for (int e = 0; e < 4; ++e) {
         const uint32_t k = tid * 4 + e;
