@@ -1018,7 +1018,7 @@ __device__ __forceinline__ void verify_tile(const TileArgs &A, int planes, const
 // and tok_count then run alongside, per plane)
 // ser_done != nullptr: the plane's last tile also releases tok_count directly
 // when the plane was not refuted (enc_serial_x releases the refuted ones).
-__global__ void __launch_bounds__(kEncThreads, 5) enc_verify(TileArgs A, int planes, const uint32_t *chain_done,
+__global__ void __launch_bounds__(kEncThreads, 6) enc_verify(TileArgs A, int planes, const uint32_t *chain_done,
                                                           uint32_t epoch, PlaneFlow flow, uint32_t *ser_done) {
     if (chain_done) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     else pdl_begin();
