@@ -375,6 +375,11 @@ def main():
         if os.path.exists(tf):
             with open(tf) as f:
                 traffic = json.load(f).get("dram_bytes_per_launch")
+    elif dominant and dominant["kernel"] == "enc_chain" and chain.get("events"):
+        # serial warp chain (one warp per plane): the same 28 B per event as
+        # the scan form, streamed through its TMA ring
+        algo_launch = 28.0 * chain["events"] / dominant["launches"]
+        basis = "enc_chain: 28 B per chained event (device-counted) / mean launch time"
     elif dominant and dominant["kernel"] == "enc_lattice" and ntiles > 64:
         # dense pass (planes of > 64 tiles): x (8 B) and flags (1 B) in;
         # symbols (4 B) and flags (1 B) out per element of every plane (the
