@@ -371,7 +371,7 @@ def main():
     if dominant and dominant["kernel"] == "enc_chain_scan" and chain.get("events"):
         algo_launch = 28.0 * chain["events"] / dominant["launches"]
         basis = "enc_chain_scan: 28 B per chained event (device-counted) / mean launch time"
-        tf = os.path.join(prof_dir, "r01_v12_chain_scan_ncu.json")
+        tf = os.path.join(prof_dir, "r01_v18_chain_scan_ncu.json")
         if os.path.exists(tf):
             with open(tf) as f:
                 traffic = json.load(f).get("dram_bytes_per_launch")
