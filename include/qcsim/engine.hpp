@@ -9,6 +9,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "qcsim/circuit.hpp"
@@ -31,15 +32,16 @@ struct EngineConfig {
     double norm_drift_tolerance = 0.02;
     int device = 0;
     int rank = 0, world = 1; // slice sharding
+    uint64_t wave_bytes = 0; // dense working-set budget of a gate pass (0: 45% of the device)
 };
 
 struct RunMetrics {
     double min_compression_ratio = 0.0;
     double mean_compression_ratio = 0.0;
-    std::vector<double> per_gate_min_ratio; // not tracked on the device path (empty)
+    std::vector<double> per_gate_min_ratio; // one entry per gate pass since the load
     double wall_seconds = 0.0;
-    double baseline_wall_seconds = 0.0;
-    double overhead_factor = 0.0;
+    double baseline_wall_seconds = 0.0; // measure_overhead: the compression-off run
+    double overhead_factor = 0.0;       // measure_overhead: wall_seconds / baseline_wall_seconds
     uint64_t peak_compressed_bytes = 0;
     uint64_t dense_bytes = 0;
     double final_norm = 0.0;
@@ -47,6 +49,15 @@ struct RunMetrics {
     uint64_t gates = 0;
     uint64_t index_bytes = 0;
     uint64_t fallback_planes = 0;
+};
+
+// One row of the per-gate report (SPEC.md:383 CSV: gate_index, min_ratio,
+// mean_ratio, seconds) plus the state's bytes after the pass.  Row 0 is the
+// initial compression (gate_index -1).
+struct GateMetrics {
+    long long gate_index = 0;
+    double min_ratio = 0.0, mean_ratio = 0.0, seconds = 0.0;
+    uint64_t compressed_bytes = 0, index_bytes = 0;
 };
 
 class Engine {
@@ -61,6 +72,7 @@ class Engine {
     RunMetrics run(const Circuit &circuit);        // gate passes
     RunMetrics run(const std::vector<GateAction> &actions);
     RunMetrics metrics() const;
+    std::vector<GateMetrics> gate_metrics() const;
     StateVector gather_state(int guard_qubits = 28) const; // dense StateVector
     std::vector<CompressedPlanes> compressed_slices() const; // checkpoint
 
@@ -76,5 +88,16 @@ class Engine {
 // engine holding the final compressed state plus the metrics.
 std::pair<std::unique_ptr<Engine>, RunMetrics> run(const Circuit &circuit, const EngineConfig &config,
                                                    const StateVector &initial);
+
+// SPEC.md:353-361 (Fig. 2): runs the circuit twice on the same
+// device -- compression on (config) and off -- and returns the compressed
+// run's metrics with baseline_wall_seconds / overhead_factor filled.
+RunMetrics measure_overhead(const Circuit &circuit, const EngineConfig &config, const StateVector &initial);
+
+// Metrics report: a JSON object with every RunMetrics field
+// plus the per-gate rows, and the CSV export (gate_index, min_ratio,
+// mean_ratio, seconds).
+std::string metrics_json(const RunMetrics &m, const std::vector<GateMetrics> &rows);
+std::string metrics_csv(const std::vector<GateMetrics> &rows);
 
 } // namespace qcsim

@@ -145,7 +145,9 @@ typedef struct qcsim_engine_config {
     int32_t rank;                /* slice shard: this rank owns slices   */
     int32_t world;               /*   [rank*S/world, (rank+1)*S/world)   */
     int32_t checkpoint_bits;     /* decode index granularity, 0 = auto   */
-    uint64_t wave_bytes;         /* dense working-set budget, 0 = auto   */
+    uint64_t wave_bytes;         /* dense working-set budget of a gate   */
+                                 /* pass (slices are processed in waves  */
+                                 /* that fit it); 0 = 45% of the device  */
 } qcsim_engine_config;
 
 /* RunMetrics, accumulated over every compress call. */
@@ -163,6 +165,32 @@ typedef struct qcsim_run_metrics {
     uint64_t fallback_planes;      /* planes re-encoded on the serial path */
     uint64_t kernel_launches;      /* kernels launched by run()           */
 } qcsim_run_metrics;
+
+/* Per-gate row of RunMetrics (SPEC.md:310 per_gate_min_ratio; the CSV
+ * report's gate_index, min_ratio, mean_ratio, seconds): one row
+ * per compression pass since the last load -- row 0 is the load's initial
+ * compression, row k the state after gate k-1 of the loaded state.
+ * compressed_bytes / index_bytes: the state's QCB1 bytes and decode-index
+ * bytes after that pass.  Compression-off engines report ratio 0. */
+typedef struct qcsim_gate_metrics {
+    double min_ratio;
+    double mean_ratio;
+    double seconds;             /* device time of the pass                 */
+    uint64_t compressed_bytes;
+    uint64_t index_bytes;
+    uint64_t compress_calls;
+} qcsim_gate_metrics;
+
+/* Layout of an engine's gate pass: its local slices are processed in
+ * `waves` batches of `wave_slices` slices (the dense working set is
+ * O(wave), sized by qcsim_engine_config.wave_bytes). */
+typedef struct qcsim_engine_info_t {
+    uint64_t local_slices;
+    uint64_t wave_slices;
+    uint64_t waves;
+    int32_t checkpoint_bits;
+    int32_t reserved;
+} qcsim_engine_info_t;
 
 qcsim_status qcsim_engine_create(const qcsim_engine_config *cfg,
                                  qcsim_engine **out);
@@ -182,6 +210,18 @@ qcsim_status qcsim_engine_load_amplitudes(qcsim_engine *eng,
  * Metrics accumulate across calls; `metrics` (optional) receives the totals. */
 qcsim_status qcsim_engine_run(qcsim_engine *eng, const qcsim_action *actions,
                               uint64_t count, qcsim_run_metrics *metrics);
+
+/* Per-gate rows since the last load (pass rows = NULL to query `*count`). */
+qcsim_status qcsim_engine_gate_metrics(qcsim_engine *eng, qcsim_gate_metrics *rows,
+                                       uint64_t capacity, uint64_t *count);
+
+/* Wave layout of the engine (see qcsim_engine_info_t). */
+qcsim_status qcsim_engine_info(qcsim_engine *eng, qcsim_engine_info_t *info);
+
+/* Device bytes held by the library's buffers: current and the high-water
+ * mark (reset to the current value when reset_peak != 0). */
+qcsim_status qcsim_device_memory(uint64_t *current, uint64_t *peak,
+                                 int32_t reset_peak);
 
 /* to_amplitudes / gather_state (statevec.hpp:128-129):
  * interleaved (re, im) of this rank's slices into host memory. Guarded by

@@ -13,7 +13,8 @@ from .circuit import (Amplitude, ButterflyOp, Circuit, DiagonalOp, Gate, GateKin
                       validate_circuit)
 from .codec import (CodecConfig, CodecMode, CodecStats, CompressedBlock, Predictor, compress_plane,  # noqa: F401
                     compress_plane_bytes, compression_ratio, decompress_bytes, decompress_plane)
-from .engine import Engine, EngineConfig, RunMetrics, kernel_launches  # noqa: F401
+from .engine import (Engine, EngineConfig, RunMetrics, device_memory, kernel_launches,  # noqa: F401
+                     measure_overhead)
 from .errors import CapacityError, CodecError, CudaError, NumericError, ParseError, QcsimError  # noqa: F401
 
 __version__ = "0.1.0"

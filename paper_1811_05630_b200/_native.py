@@ -49,6 +49,16 @@ class RunMetricsC(C.Structure):
                 ("fallback_planes", C.c_uint64), ("kernel_launches", C.c_uint64)]
 
 
+class GateMetricsC(C.Structure):
+    _fields_ = [("min_ratio", C.c_double), ("mean_ratio", C.c_double), ("seconds", C.c_double),
+                ("compressed_bytes", C.c_uint64), ("index_bytes", C.c_uint64), ("compress_calls", C.c_uint64)]
+
+
+class EngineInfoC(C.Structure):
+    _fields_ = [("local_slices", C.c_uint64), ("wave_slices", C.c_uint64), ("waves", C.c_uint64),
+                ("checkpoint_bits", C.c_int32), ("reserved", C.c_int32)]
+
+
 P = C.POINTER
 u8p, dp, u64p = P(C.c_uint8), P(C.c_double), P(C.c_uint64)
 
@@ -77,6 +87,9 @@ SIGNATURES = [
     ("qcsim_engine_export_slice", C.c_int, [C.c_void_p, C.c_uint64, u8p, C.c_uint64, u64p]),
     ("qcsim_engine_import_partner", C.c_int, [C.c_void_p, C.c_uint64, u8p, C.c_uint64]),
     ("qcsim_engine_set_global_norms", C.c_int, [C.c_void_p, dp, C.c_uint64]),
+    ("qcsim_engine_gate_metrics", C.c_int, [C.c_void_p, P(GateMetricsC), C.c_uint64, u64p]),
+    ("qcsim_engine_info", C.c_int, [C.c_void_p, P(EngineInfoC)]),
+    ("qcsim_device_memory", C.c_int, [u64p, u64p, C.c_int32]),
 ]
 EXTRA = [("qcsim_kernel_launches", C.c_uint64, [])]
 

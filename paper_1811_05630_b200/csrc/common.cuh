@@ -48,6 +48,37 @@ struct IndexRec {
 };
 static_assert(sizeof(IndexRec) == 40, "IndexRec layout");
 
+// Decode index stored next to its block: the block's arena
+// slot is [QCB1 block | pad to 16 | IndexRec x (chunks - 1)], the record of
+// chunk j >= 1 at position j - 1 (chunk 0 starts from the initial decoder
+// state).  The chunk size is a power of two >= 2^log2Cmin chosen from the
+// block size alone, so the encoder (which knows the exact block size before
+// packing) and any decoder agree without extra metadata: one chunk per
+// kIdxBlockBytesPerChunk block bytes, i.e. the index is <= 40/512 = 7.8% of
+// the block.  The QCB1 bytes themselves are untouched.
+constexpr uint64_t kIdxBlockBytesPerChunk = 512;
+__host__ __device__ __forceinline__ int ceil_log2_u64(uint64_t v) {
+    int l = 0;
+    while ((1ull << l) < v) ++l;
+    return l;
+}
+__host__ __device__ __forceinline__ int chunk_log2(uint64_t n, uint64_t block_bytes, int log2Cmin) {
+    const uint64_t t = block_bytes / kIdxBlockBytesPerChunk; // target chunk count
+    int lt = 0;
+    while (lt < 62 && (2ull << lt) <= t) ++lt;                // floor(log2(t)), 0 for t <= 1
+    const int c = ceil_log2_u64(n) - lt;
+    return c > log2Cmin ? c : log2Cmin;
+}
+__host__ __device__ __forceinline__ uint64_t index_records(uint64_t n, uint64_t block_bytes, int log2Cmin) {
+    const int lc = chunk_log2(n, block_bytes, log2Cmin);
+    return ((n + (1ull << lc) - 1) >> lc) - 1;
+}
+// byte offset of the index records of the block at `blk_off` (slot-relative
+// arithmetic: slots start 16-byte aligned)
+__host__ __device__ __forceinline__ uint64_t index_offset(uint64_t blk_off, uint64_t block_bytes) {
+    return (blk_off + block_bytes + 15) & ~15ull;
+}
+
 // Per-plane codec parameters resolved on the device.
 struct PlaneParams {
     double eb;       // effective absolute bound

@@ -30,11 +30,10 @@ struct DecTables {
 
 struct DecPlanes {
     const uint8_t *arena;
-    const uint64_t *blk_off;   // [plane] block start in the arena
-    const IndexRec *index;     // [plane][nidx]
+    const uint64_t *blk_off;   // [plane] block start in the arena (its decode index follows it)
     double *const *out;        // [plane] output plane
     uint64_t L;
-    int log2C;
+    int log2C;                 // finest index chunk (chunk_log2, common.cuh)
 };
 
 __device__ __forceinline__ uint64_t load_le(const uint8_t *p, int bytes) {
@@ -167,19 +166,35 @@ struct BitWindow {
 constexpr int kDecThreads = 128;             // chunks per block
 constexpr int kDecStageWords = 4096;         // 16 KB of stream staged per block
 constexpr int kDecWin = 16;                  // output window per chunk (C is a multiple)
+constexpr int kDecFills = 64;                // deferred constant-run fills per block
+constexpr int kDecFillMin = 4 * kDecWin;     // shortest run worth deferring
+struct DecFill {
+    uint64_t start;
+    uint64_t len;
+    double v;
+};
 struct DecSmem {
     uint32_t lut[1 << kLutBits];
     uint32_t sw[kDecStageWords + 4];
     double sout[kDecThreads / 32][32][kDecWin + 1]; // per warp: 32 chunks x one window
+    DecFill fill[kDecFills];
+    uint32_t skip[kDecThreads / 32][32];           // per lane: its row holds the current window
+    uint32_t nfill;
 };
 constexpr size_t kDecSmem = sizeof(DecSmem);
 
-// One block per (plane, group of kDecThreads checkpoint chunks).  The
-// plane's 11-bit LUT and the group's stream bytes are staged in shared
-// memory; each thread then resumes from its IndexRec and reproduces
-// codec.cpp:591-626 for its chunk, kDecWin elements at a time: the warp
-// parks its 32 chunks' windows in shared memory and stores them row by row
-// (256-byte coalesced rows instead of 32 scattered 8-byte stores).
+// One block per (plane, group of kDecThreads index chunks).  The plane's
+// chunk size follows from its block size (chunk_log2), the records come
+// from the index stored after the block in its slot; blocks past the plane's
+// chunk count exit.  The plane's 11-bit LUT and the group's stream bytes are
+// staged in shared memory; each thread then resumes from its record and
+// reproduces codec.cpp:591-626 for its chunk, kDecWin elements at a time:
+// the warp parks its 32 chunks' windows in shared memory and stores them row
+// by row (coalesced rows instead of scattered 8-byte stores).  A zero-code
+// run with the previous-value predictor is a constant fill: a lane standing
+// at a window start inside such a run hands the whole windows it covers to
+// the block (shared fill list, written coalesced by all threads at the end)
+// and the warp skips windows every lane has handed off.
 // N.enabled: the grid's last block runs the engine's normalization for this
 // gate pass instead (it needs only the previous pass's norms; the gate kernel
 // that applies the scale runs after this grid).
@@ -191,15 +206,20 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
     }
     extern __shared__ __align__(16) unsigned char dec_raw[];
     DecSmem &S = *reinterpret_cast<DecSmem *>(dec_raw);
-    const uint64_t nchunks = (D.L + (1ull << D.log2C) - 1) >> D.log2C;
-    const uint32_t groups = (uint32_t)((nchunks + kDecThreads - 1) / kDecThreads);
+    const uint64_t nchunks_max = (D.L + (1ull << D.log2C) - 1) >> D.log2C;
+    const uint32_t groups = (uint32_t)((nchunks_max + kDecThreads - 1) / kDecThreads);
     const int pl = (int)(blockIdx.x / groups);
     if (pl >= planes) return;
+    const uint8_t *blk = D.arena + D.blk_off[pl];
+    const uint64_t payload = load_le(blk + 32, 8);
+    const uint64_t bbytes = kHeaderBytes + payload;
+    const int log2Cp = chunk_log2(D.L, bbytes, D.log2C);
+    const uint64_t C = 1ull << log2Cp;
+    const uint64_t nchunks = (D.L + C - 1) >> log2Cp;
     const uint64_t j0 = (uint64_t)(blockIdx.x % groups) * kDecThreads;
+    if (j0 >= nchunks) return;
     const uint64_t j = j0 + threadIdx.x;
     const uint64_t jend = tmin<uint64_t>(j0 + kDecThreads, nchunks);
-    const uint64_t nidx = (D.L >> D.log2C) + 1;
-    const uint8_t *blk = D.arena + D.blk_off[pl];
     const uint8_t pred_kind = blk[6];
     const int qb = blk[7];
     const long long half = 1ll << (qb - 1);
@@ -207,7 +227,6 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
     const double eb = __longlong_as_double((long long)load_le(blk + 16, 8));
     const double q = dmul(2.0, eb);
     const uint64_t nout = load_le(blk + 24, 8);
-    const uint64_t payload = load_le(blk + 32, 8);
     const uint32_t n = T.meta[4 * pl + 1];
     const uint32_t maxlen = T.meta[4 * pl];
     const uint64_t table_bytes = 4 + 5ull * n;
@@ -219,7 +238,8 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
     const uint32_t *count = T.count + (uint64_t)pl * (kMaxCodeLen + 1);
     const uint32_t *basei = T.basei + (uint64_t)pl * (kMaxCodeLen + 1);
     const uint32_t *sorted = T.sorted + (uint64_t)pl * T.cap;
-    const IndexRec *idx = D.index + (uint64_t)pl * nidx;
+    const IndexRec *sidx = reinterpret_cast<const IndexRec *>(D.arena + index_offset(D.blk_off[pl], bbytes));
+    auto rec_bitpos = [&](uint64_t jj) -> uint64_t { return jj == 0 ? 0ull : sidx[jj - 1].bitpos; };
 
     {
         const uint4 *g4 = reinterpret_cast<const uint4 *>(glut);
@@ -227,9 +247,10 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
 #pragma unroll
         for (int k = threadIdx.x; k < (1 << kLutBits) / 4; k += kDecThreads) s4[k] = g4[k];
     }
+    if (threadIdx.x == 0) S.nfill = 0;
     // stream words this group reads: [bitpos(j0), bitpos(jend)) + lookahead
-    const uint64_t w_lo = idx[j0].bitpos >> 5;
-    const uint64_t bit_hi = jend < nchunks ? idx[jend].bitpos : sbytes * 8;
+    const uint64_t w_lo = rec_bitpos(j0) >> 5;
+    const uint64_t bit_hi = jend < nchunks ? rec_bitpos(jend) : sbytes * 8;
     const uint64_t w_hi = (bit_hi >> 5) + 3;
     const bool staged = w_hi - w_lo <= (uint64_t)kDecStageWords;
     const uint64_t sbase0 = staged ? w_lo * 32 : 0;
@@ -239,9 +260,9 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
 
     const bool active = j < jend;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const uint64_t C = 1ull << D.log2C;
     IndexRec r{};
-    if (active) r = idx[j];
+    if (active && j > 0) r = sidx[j - 1];
+    if (j == 0) r.last_lit = rsym; // initial decoder state (codec.cpp:587-590)
     uint64_t bp = r.bitpos;
     uint32_t run_left = r.run_left;
     const uint32_t *wsrc = staged ? S.sw : stream; // the window's word source ...
@@ -252,16 +273,27 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
     uint32_t last = r.last_lit;
     uint64_t ocur = r.ocur;
     double d1 = r.dprev, d2 = r.dprev2;
-    const uint64_t e0 = j << D.log2C;
+    const uint64_t e0 = j << log2Cp;
     const uint64_t e1 = active ? tmin<uint64_t>(e0 + C, D.L) : e0;
     double *out = D.out[pl];
     const uint64_t sbase = staged ? w_lo * 32 : 0;
     const uint64_t jw = j0 + (uint64_t)wid * 32; // first chunk of this warp
     double *row = S.sout[wid][lane];
+    uint32_t *skip = S.skip[wid];
 
     uint64_t i = e0;
     bool dead = !active;
-    for (uint64_t w0 = 0; w0 < C; w0 += kDecWin) {
+    uint64_t w0 = 0;
+    skip[lane] = 0;
+    while (true) {
+        // windows every lane has handed off (or finished) are skipped
+        uint64_t wnext = dead || i >= e1 ? C : (i - e0) & ~(uint64_t)(kDecWin - 1);
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t v = __shfl_xor_sync(0xffffffffu, wnext, o);
+            wnext = v < wnext ? v : wnext;
+        }
+        w0 = wnext > w0 ? wnext : w0;
+        if (w0 >= C) break;
         const uint64_t wb = e0 + w0;
         const uint64_t wend = tmin<uint64_t>(wb + kDecWin, e1);
         auto emit = [&](uint32_t s) {
@@ -281,12 +313,26 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
             d1 = v;
             ++i;
         };
-        while (!dead && i < wend) {
+        bool produced = false;
+        while (!dead && i >= wb && i < wend) {
             if (run_left > 0) {
                 // a run of a zero code with the previous-value predictor is a
                 // constant fill (d + 0.0 == d except -0.0, which emit() keeps)
                 if (pred_kind == 0 && last == (uint32_t)half && eb != 0.0 &&
                     bits_of(d1) != 0x8000000000000000ull && i > 0) {
+                    const uint64_t len = tmin<uint64_t>(run_left, e1 - i) & ~(uint64_t)(kDecWin - 1);
+                    if (i == wb && len >= (uint64_t)kDecFillMin) {
+                        // whole windows of the run: hand them to the block
+                        const uint32_t slot = atomicAdd(&S.nfill, 1u);
+                        if (slot < (uint32_t)kDecFills) {
+                            S.fill[slot] = DecFill{i, len, d1};
+                            run_left -= (uint32_t)len;
+                            i += len;
+                            d2 = d1;
+                            break; // this window produced nothing for this lane
+                        }
+                    }
+                    produced = true;
                     const uint64_t stop = tmin<uint64_t>(wend, i + run_left);
                     const double v = d1;
                     run_left -= (uint32_t)(stop - i);
@@ -294,6 +340,7 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
                     d2 = v;
                     continue;
                 }
+                produced = true;
                 emit(last);
                 --run_left;
                 continue;
@@ -346,19 +393,33 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
                     if (!staged) bw.init(wsrc, bp - wbase);
                 }
             } else {
+                produced = true;
                 emit(s);
                 last = s;
             }
         }
+        // a lane's row holds this window iff it decoded the window (a lane
+        // hands off only at a window start, before producing anything)
+        skip[lane] = produced ? 1u : 0u;
         __syncwarp();
         // the warp's 32 chunk windows, coalesced kDecWin-element rows
-        for (int q = lane; q < 32 * kDecWin; q += 32) {
-            const int rr = q / kDecWin, col = q % kDecWin;
+        for (int qq = lane; qq < 32 * kDecWin; qq += 32) {
+            const int rr = qq / kDecWin, col = qq % kDecWin;
             const uint64_t jr = jw + rr;
-            const uint64_t e = (jr << D.log2C) + w0 + col;
-            if (jr < jend && w0 + col < C && e < D.L) out[e] = S.sout[wid][rr][col];
+            const uint64_t e = (jr << log2Cp) + w0 + col;
+            if (jr < jend && skip[rr] && w0 + col < C && e < D.L) out[e] = S.sout[wid][rr][col];
         }
         __syncwarp();
+        w0 += kDecWin;
+    }
+    __syncthreads();
+    // deferred constant fills, coalesced by the whole block
+    const uint32_t nf = tmin<uint32_t>(S.nfill, (uint32_t)kDecFills);
+    for (uint32_t f = 0; f < nf; ++f) {
+        const DecFill F = S.fill[f];
+        double2 *o2 = reinterpret_cast<double2 *>(out + F.start); // window starts are 16-element aligned
+        const double2 v2 = make_double2(F.v, F.v);
+        for (uint64_t k = threadIdx.x; k < F.len / 2; k += kDecThreads) o2[k] = v2;
     }
 }
 

@@ -653,6 +653,7 @@ Engine::Engine(int n, const EngineConfig &cfg) : n_(n) {
     c.device = cfg.device;
     c.rank = cfg.rank;
     c.world = cfg.world;
+    c.wave_bytes = cfg.wave_bytes;
     check(qcsim_engine_create(&c, &h_));
     s_ = cfg.slice_bits < 0 ? default_slice_bits(n) : cfg.slice_bits;
 }
@@ -699,7 +700,26 @@ RunMetrics Engine::metrics() const {
     r.gates = m.gates;
     r.index_bytes = m.index_bytes;
     r.fallback_planes = m.fallback_planes;
+    const std::vector<GateMetrics> rows = gate_metrics();
+    for (size_t k = 1; k < rows.size(); ++k) r.per_gate_min_ratio.push_back(rows[k].min_ratio);
     return r;
+}
+
+std::vector<GateMetrics> Engine::gate_metrics() const {
+    uint64_t cnt = 0;
+    check(qcsim_engine_gate_metrics(h_, nullptr, 0, &cnt));
+    std::vector<qcsim_gate_metrics> raw(cnt);
+    check(qcsim_engine_gate_metrics(h_, raw.data(), raw.size(), &cnt));
+    std::vector<GateMetrics> out(cnt);
+    for (uint64_t k = 0; k < cnt; ++k) {
+        out[k].gate_index = (long long)k - 1;
+        out[k].min_ratio = raw[k].min_ratio;
+        out[k].mean_ratio = raw[k].mean_ratio;
+        out[k].seconds = raw[k].seconds;
+        out[k].compressed_bytes = raw[k].compressed_bytes;
+        out[k].index_bytes = raw[k].index_bytes;
+    }
+    return out;
 }
 
 StateVector Engine::gather_state(int guard) const {
@@ -735,6 +755,60 @@ std::pair<std::unique_ptr<Engine>, RunMetrics> run(const Circuit &c, const Engin
     eng->load(initial);
     RunMetrics m = eng->run(c);
     return {std::move(eng), m};
+}
+
+RunMetrics measure_overhead(const Circuit &c, const EngineConfig &cfg, const StateVector &initial) {
+    auto [on, m] = run(c, cfg, initial);
+    EngineConfig off_cfg = cfg;
+    off_cfg.compression_enabled = false;
+    auto [off, moff] = run(c, off_cfg, initial);
+    m.baseline_wall_seconds = moff.wall_seconds;
+    m.overhead_factor = moff.wall_seconds > 0.0 ? m.wall_seconds / moff.wall_seconds : 0.0;
+    return m;
+}
+
+namespace {
+std::string num(double v) {
+    if (!std::isfinite(v)) return "null";
+    char b[40];
+    std::snprintf(b, sizeof b, "%.17g", v);
+    return b;
+}
+} // namespace
+
+std::string metrics_json(const RunMetrics &m, const std::vector<GateMetrics> &rows) {
+    std::string o = "{";
+    o += "\"min_compression_ratio\": " + num(m.min_compression_ratio);
+    o += ", \"mean_compression_ratio\": " + num(m.mean_compression_ratio);
+    o += ", \"per_gate_min_ratio\": [";
+    for (size_t k = 0; k < m.per_gate_min_ratio.size(); ++k) o += (k ? ", " : "") + num(m.per_gate_min_ratio[k]);
+    o += "], \"wall_seconds\": " + num(m.wall_seconds);
+    o += ", \"baseline_wall_seconds\": " + (m.baseline_wall_seconds > 0 ? num(m.baseline_wall_seconds) : "null");
+    o += ", \"overhead_factor\": " + (m.overhead_factor > 0 ? num(m.overhead_factor) : "null");
+    o += ", \"peak_compressed_bytes\": " + std::to_string(m.peak_compressed_bytes);
+    o += ", \"dense_bytes\": " + std::to_string(m.dense_bytes);
+    o += ", \"final_norm\": " + num(m.final_norm);
+    o += ", \"compress_calls\": " + std::to_string(m.compress_calls);
+    o += ", \"gates\": " + std::to_string(m.gates);
+    o += ", \"index_bytes\": " + std::to_string(m.index_bytes);
+    o += ", \"fallback_planes\": " + std::to_string(m.fallback_planes);
+    o += ", \"per_gate\": [";
+    for (size_t k = 0; k < rows.size(); ++k) {
+        const GateMetrics &r = rows[k];
+        o += std::string(k ? ", " : "") + "{\"gate_index\": " + std::to_string(r.gate_index) +
+             ", \"min_ratio\": " + num(r.min_ratio) + ", \"mean_ratio\": " + num(r.mean_ratio) +
+             ", \"seconds\": " + num(r.seconds) + ", \"compressed_bytes\": " + std::to_string(r.compressed_bytes) +
+             ", \"index_bytes\": " + std::to_string(r.index_bytes) + "}";
+    }
+    o += "]}";
+    return o;
+}
+
+std::string metrics_csv(const std::vector<GateMetrics> &rows) {
+    std::string o = "gate_index,min_ratio,mean_ratio,seconds\n";
+    for (const GateMetrics &r : rows)
+        o += std::to_string(r.gate_index) + "," + num(r.min_ratio) + "," + num(r.mean_ratio) + "," + num(r.seconds) + "\n";
+    return o;
 }
 
 } // namespace qcsim

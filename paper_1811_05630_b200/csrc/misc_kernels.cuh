@@ -212,7 +212,9 @@ __global__ void __launch_bounds__(256) slot_scan_stats(const uint64_t *slot_byte
                                                        const uint64_t *bytes, const uint32_t *err,
                                                        const PlaneParams *params, int planes, uint64_t L,
                                                        unsigned long long gate, EngineDevStats *st,
-                                                       uint32_t *overflow) {
+                                                       uint32_t *overflow, GateRowDev *rows,
+                                                       unsigned long long row0, unsigned long long nrows,
+                                                       int log2C) {
     pdl_begin();
     if (threadIdx.x == 0) *overflow = 0u;
     using Scan = cub::BlockScan<unsigned long long, 256>;
@@ -238,9 +240,9 @@ __global__ void __launch_bounds__(256) slot_scan_stats(const uint64_t *slot_byte
     }
     if (tid == 0) slot_off[planes] = carry;
     const double in_bytes = (double)(8 * L);
-    unsigned long long tsum = 0, fb = 0;
+    unsigned long long tsum = 0, fb = 0, isum = 0;
     int bad = 0;
-    double rmin = 0.0, rsum = 0.0;
+    double rmin = 0.0, rsum = 0.0, pmin = INFINITY, psum = 0.0;
     if (tid == 0) {
         rmin = st->ratio_min;
         rsum = st->ratio_sum;
@@ -251,6 +253,7 @@ __global__ void __launch_bounds__(256) slot_scan_stats(const uint64_t *slot_byte
             const uint64_t b = bytes[base + k];
             ratio[k] = ddiv(in_bytes, (double)b);
             tsum += b;
+            isum += index_records(L, b, log2C) * sizeof(IndexRec);
             fb += (params[base + k].flags & kFlagFallback) ? 1 : 0;
             bad |= err[base + k] != 0;
         }
@@ -260,14 +263,19 @@ __global__ void __launch_bounds__(256) slot_scan_stats(const uint64_t *slot_byte
                 const double r = ratio[k];
                 if (r < rmin) rmin = r;
                 rsum = dadd(rsum, r);
+                if (r < pmin) pmin = r;
+                psum = dadd(psum, r);
             }
         __syncthreads();
     }
     tsum = Red(tmp.red).Sum(tsum);
     __syncthreads();
     fb = Red(tmp.red).Sum(fb);
+    __syncthreads();
+    isum = Red(tmp.red).Sum(isum);
     bad = __syncthreads_or(bad);
     if (tid == 0) {
+        write_gate_row(rows, row0, nrows, gate, pmin, psum, (unsigned long long)planes, tsum, isum);
         st->ratio_min = rmin;
         st->ratio_sum = rsum;
         st->calls += (unsigned long long)planes;

@@ -19,6 +19,21 @@ struct EngineDevStats {
     uint32_t status, pad;
 };
 
+// Per-gate row of a deferred run (index gate - row0 + 1; row 0 holds the
+// run's start stamp): this pass's min ratio, ratio sum in plane order, calls,
+// block bytes, decode-index bytes and a %globaltimer stamp taken when the
+// pass's metrics are settled.
+struct GateRowDev {
+    double min_ratio, ratio_sum;
+    unsigned long long calls, bytes, index_bytes, t_ns;
+};
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 struct NormArgs {
     int norm;              // run the normalization (norm_every)
     const double *tilesum; // [slice][ntiles] partial trees of the previous pass (nullptr: sq holds the norms)
@@ -39,26 +54,46 @@ struct NormArgs {
     const PlaneParams *params;
     int planes;
     uint64_t L;
+    int log2C;             // finest decode-index chunk (index bytes per plane, common.cuh)
     unsigned long long stats_gate;
+    GateRowDev *rows;      // per-gate rows of the run (nullptr: none)
+    unsigned long long row0;
+    unsigned long long nrows;
+    int stamp;             // first pass of a run: stamp rows[0]
 };
+
+__device__ __forceinline__ void write_gate_row(GateRowDev *rows, unsigned long long row0, unsigned long long nrows,
+                                               unsigned long long gate, double pmin, double psum,
+                                               unsigned long long calls, unsigned long long bytes,
+                                               unsigned long long ibytes) {
+    if (!rows || gate < row0 || gate - row0 >= nrows) return;
+    GateRowDev &r = rows[gate - row0 + 1];
+    r.min_ratio = pmin;
+    r.ratio_sum = psum;
+    r.calls = calls;
+    r.bytes = bytes;
+    r.index_bytes = ibytes;
+    r.t_ns = global_ns();
+}
 
 // Per encode pass: compression ratio min / sum in plane order (as the
 // host's record_sizes), current and peak bytes, fallback planes, latched
 // codec errors.  The whole block: ratios in parallel, the plane-order sum
 // by thread 0.
 __device__ void pass_stats(const uint64_t *bytes, const uint32_t *err, const PlaneParams *params, int planes,
-                           uint64_t L, unsigned long long gate, EngineDevStats *st) {
+                           uint64_t L, unsigned long long gate, EngineDevStats *st, const NormArgs &N) {
     __shared__ double s_r[256];
-    __shared__ unsigned long long s_tsum, s_fb;
+    __shared__ unsigned long long s_tsum, s_fb, s_isum;
     __shared__ int s_bad;
     const int tid = threadIdx.x, nt = min((int)blockDim.x, 256);
     const double in_bytes = (double)(8 * L);
     if (tid == 0) {
         s_tsum = 0;
         s_fb = 0;
+        s_isum = 0;
         s_bad = 0;
     }
-    double rmin = 0.0, rsum = 0.0;
+    double rmin = 0.0, rsum = 0.0, pmin = INFINITY, psum = 0.0;
     if (tid == 0) {
         rmin = st->ratio_min;
         rsum = st->ratio_sum;
@@ -70,6 +105,7 @@ __device__ void pass_stats(const uint64_t *bytes, const uint32_t *err, const Pla
             const uint64_t b = bytes[k];
             s_r[tid] = ddiv(in_bytes, (double)b);
             atomicAdd(&s_tsum, (unsigned long long)b);
+            atomicAdd(&s_isum, (unsigned long long)(index_records(L, b, N.log2C) * sizeof(IndexRec)));
             if (params[k].flags & kFlagFallback) atomicAdd(&s_fb, 1ull);
             if (err[k] != 0) s_bad = 1;
         }
@@ -79,10 +115,13 @@ __device__ void pass_stats(const uint64_t *bytes, const uint32_t *err, const Pla
                 const double r = s_r[j];
                 if (r < rmin) rmin = r;
                 rsum = dadd(rsum, r);
+                if (r < pmin) pmin = r;
+                psum = dadd(psum, r);
             }
         __syncthreads();
     }
     if (tid == 0) {
+        write_gate_row(N.rows, N.row0, N.nrows, gate, pmin, psum, (unsigned long long)planes, s_tsum, s_isum);
         st->ratio_min = rmin;
         st->ratio_sum = rsum;
         st->calls += (unsigned long long)planes;
@@ -98,7 +137,7 @@ __device__ void pass_stats(const uint64_t *bytes, const uint32_t *err, const Pla
 }
 __global__ void pass_stats_kernel(NormArgs N) {
     pdl_begin();
-    pass_stats(N.bytes, N.err, N.params, N.planes, N.L, N.stats_gate, N.st);
+    pass_stats(N.bytes, N.err, N.params, N.planes, N.L, N.stats_gate, N.st, N);
 }
 
 
@@ -118,7 +157,8 @@ __device__ void engine_norm_body(const NormArgs &N) {
     const uint32_t *overflow = N.overflow;
     EngineDevStats *st = N.st;
     const int tid = threadIdx.x, nt = blockDim.x;
-    if (N.stats) pass_stats(N.bytes, N.err, N.params, N.planes, N.L, N.stats_gate, st);
+    if (N.stats) pass_stats(N.bytes, N.err, N.params, N.planes, N.L, N.stats_gate, st, N);
+    if (N.stamp && N.rows && tid == 0) N.rows[0].t_ns = global_ns();
     if (!N.norm) return;
     // slice norms: one thread per slice over its (aligned power-of-two) tiles
     // (tilesum == nullptr: `sq` already holds them)

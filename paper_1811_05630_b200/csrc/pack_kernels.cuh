@@ -36,10 +36,12 @@ struct CodeBook {
     uint32_t *nsym;
     uint64_t *stream_bits;
     uint64_t *block_bytes;
-    uint64_t *slot_bytes;      // 16 + round_up(block_bytes, 16)
+    uint64_t *slot_bytes;      // 16 + round_up(block_bytes, 16) + decode index (common.cuh)
     uint32_t *err;             // nonzero: codec error code
     uint64_t cap;
     int qb;
+    uint64_t L;                // plane length
+    int log2C;                 // finest decode-index chunk (the slot keeps every 2^(chunk_log2 - log2C)-th)
     DecTables dec;             // optional: decode tables of the new blocks
     uint8_t *zero_arena = nullptr; // fixed slots (plane p at p * zero_W): zero the plane's slot for the packer
     uint64_t zero_W = 0;
@@ -439,9 +441,11 @@ __device__ __forceinline__ void codebook_plane(const CodeBook &B, int planes, in
         B.nsym[pl] = n;
         B.stream_bits[pl] = bits;
         B.block_bytes[pl] = bytes;
-        B.slot_bytes[pl] = 16 + ((bytes + 15) & ~15ull);
+        const uint64_t slotb =
+            16 + ((bytes + 15) & ~15ull) + ((index_records(B.L, bytes, B.log2C) * sizeof(IndexRec) + 15) & ~15ull);
+        B.slot_bytes[pl] = slotb;
         B.err[pl] = s_err;
-        s_slotb = 16 + ((bytes + 15) & ~15ull);
+        s_slotb = slotb;
     }
     __syncthreads();
     if (B.zero_arena) { // stream words are OR-combined at chunk seams
@@ -684,6 +688,19 @@ __device__ __forceinline__ void pack_write_item(const PackArgs &A, int planes, i
     const uint64_t nidx = (A.L >> A.log2C) + 1;
     const uint32_t nchunks_idx = (uint32_t)((A.L + (1ull << A.log2C) - 1) >> A.log2C);
     IndexRec *idx = A.index + pl * nidx;
+    // the slot keeps every `keep`-th fine record (chunk_log2, common.cuh)
+    const uint64_t bbytes = kHeaderBytes + 4 + 5ull * n + (bits + 7) / 8 + 16ull * nout;
+    const uint32_t keep_sh = (uint32_t)(chunk_log2(A.L, bbytes, A.log2C) - A.log2C);
+    IndexRec *sidx = reinterpret_cast<IndexRec *>(A.arena + index_offset(off, bbytes));
+    auto put_rec = [&](uint32_t j, uint64_t bitpos) {
+        idx[j].bitpos = bitpos;
+        if ((j & ((1u << keep_sh) - 1)) == 0) {
+            IndexRec r = idx[j];
+            r.bitpos = bitpos;
+            r.tok = 0;
+            sidx[(j >> keep_sh) - 1] = r;
+        }
+    };
 
     if (c == 0) {
         const uint64_t payload = 4 + 5ull * n + sbytes + 16ull * nout;
@@ -786,7 +803,7 @@ __device__ __forceinline__ void pack_write_item(const PackArgs &A, int planes, i
         for (uint32_t j = 1 + tid; j < nchunks_idx; j += 256) {
             const uint32_t tk = idx[j].tok;
             if (tk >= t0 && (last_chunk || tk < t0 + tn))
-                idx[j].bitpos = tk >= t0 + tn ? base_bit + tot : base_bit + toff[tk - t0];
+                put_rec(j, tk >= t0 + tn ? base_bit + tot : base_bit + toff[tk - t0]);
         }
         return;
     }
@@ -810,7 +827,7 @@ __device__ __forceinline__ void pack_write_item(const PackArgs &A, int planes, i
     __syncthreads();
     for (uint32_t j = s_jlo + tid; j < s_jhi; j += 256) {
         const uint32_t tk = idx[j].tok;
-        idx[j].bitpos = tk >= t0 + tn ? base_bit + tot : base_bit + toff[tk - t0];
+        put_rec(j, tk >= t0 + tn ? base_bit + tot : base_bit + toff[tk - t0]);
     }
 }
 

@@ -14,6 +14,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include <cub/device/device_scan.cuh>
@@ -63,6 +64,10 @@ template <class F> qcsim_status guarded(F &&f) {
     }
 }
 
+// Device bytes held by this library's buffers (peak: high-water mark since
+// the last qcsim_device_memory reset).
+uint64_t g_dev_cur = 0, g_dev_peak = 0;
+
 // Grow-only device buffer (contents are not preserved on growth).
 template <class T> struct DBuf {
     T *p = nullptr;
@@ -70,22 +75,29 @@ template <class T> struct DBuf {
     DBuf() = default;
     DBuf(const DBuf &) = delete;
     DBuf &operator=(const DBuf &) = delete;
-    ~DBuf() {
-        if (p) cudaFree(p);
+    ~DBuf() { release(); }
+    void release() {
+        if (p) {
+            cudaFree(p);
+            g_dev_cur -= cap * sizeof(T);
+        }
+        p = nullptr;
+        cap = 0;
     }
     // returns true when (re)allocated
     bool ensure(size_t n, bool zero = false) {
         if (n <= cap && p) return false;
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
+        release();
         size_t want = std::max<size_t>(n, 1);
         cudaError_t e = cudaMalloc(&p, want * sizeof(T));
         if (e != cudaSuccess) {
             cudaGetLastError();
+            p = nullptr;
             raise(QCSIM_NOMEM, "device allocation of " + std::to_string(want * sizeof(T)) + " bytes failed");
         }
         cap = want;
+        g_dev_cur += cap * sizeof(T);
+        g_dev_peak = std::max(g_dev_peak, g_dev_cur);
         if (zero) CK(cudaMemset(p, 0, want * sizeof(T)));
         return true;
     }
@@ -272,6 +284,9 @@ struct EncScratch {
     DBuf<unsigned long long> pack_lb;    // pack_write look-back slots [plane][chunk]
     uint32_t pack_lb_epoch = 0;
     unsigned long long stats_gate = 0;
+    uint64_t arena_base = 0;             // this batch's slots start here in the arena (earlier waves before it)
+    GateRowDev *rows_out = nullptr;      // deferred engine: per-gate rows (slot_scan_stats)
+    unsigned long long row0 = 0, nrows = 0;
 
     void ensure(uint64_t planes, uint64_t units, uint64_t L, int qb) {
         const uint64_t ntiles = (L + kTile - 1) / kTile;
@@ -399,8 +414,8 @@ void launch_plane_scan(cudaStream_t st, const int32_t *in, int32_t *out, int nti
 void launch_pack(cudaStream_t st, EncScratch &S, DBuf<uint8_t> &arena, bool count = true) {
     if (!arena.p) arena.ensure(1 << 20);
     PackArgs P = S.pack;
-    P.arena = arena.p;
-    P.arena_cap = arena.cap;
+    P.arena = arena.p + S.arena_base;
+    P.arena_cap = arena.cap > S.arena_base ? arena.cap - S.arena_base : 0;
     const int nck = (int)((P.L + 1 + kPackTok - 1) / kPackTok);
     // (plane, K) blocks looping over the plane's chunks (pack_count / pack_write)
     const int K = std::min(nck, 32);
@@ -421,7 +436,7 @@ void launch_pack(cudaStream_t st, EncScratch &S, DBuf<uint8_t> &arena, bool coun
         launch_plane_scan(st, S.t_cbits.p, S.t_coff.p, nck, (int)S.planes, kScanSumExcl);
     } else {
         PROF("arena_zero", st); // re-pack after an arena overflow
-        launch_k(arena_zero, 296, 256, 0, st, arena.p, arena.cap, S.slot_off.p + S.planes);
+        launch_k(arena_zero, 296, 256, 0, st, P.arena, P.arena_cap, S.slot_off.p + S.planes);
     }
     {
         PROF("pack_write", st);
@@ -749,6 +764,8 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     B.err = S.err.p;
     B.cap = cap;
     B.qb = qb;
+    B.L = L;
+    B.log2C = log2C;
     B.dec = S.dec_out;
     if (S.fixed_W) {
         if (S.fixed_planes != planes || S.fixed_at != S.fixed_W) {
@@ -795,7 +812,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     } else if (S.stats_out) {
         PROF("slot_scan_stats", st);
         launch_k(slot_scan_stats, 1, 256, 0, st, S.slot_bytes.p, S.slot_off.p, S.block_bytes.p, S.err.p, S.params.p,
-                                           (int)planes, L, S.stats_gate, S.stats_out, S.overflow.p);
+                 (int)planes, L, S.stats_gate, S.stats_out, S.overflow.p, S.rows_out, S.row0, S.nrows, log2C);
     } else {
         PROF("slot_scan", st);
         launch_k(slot_scan, 1, 256, 0, st, S.slot_bytes.p, S.slot_off.p, (int)planes, S.overflow.p);
@@ -850,8 +867,19 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     }
 }
 
-// After the stream has been synchronised: errors, arena overflow (grow and
-// re-pack; nothing was written), per-plane results.
+// Grows a buffer keeping its first `keep` bytes.
+void grow_keep(DBuf<uint8_t> &b, uint64_t want, uint64_t keep, cudaStream_t st) {
+    if (b.cap >= want) return;
+    DBuf<uint8_t> nb;
+    nb.ensure(want);
+    if (b.p && keep) CK(cudaMemcpyAsync(nb.p, b.p, keep, cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    b.swap(nb);
+}
+
+// After the stream has been synchronised: errors, arena overflow (grow,
+// keeping the earlier waves' slots, and re-pack; nothing was written),
+// per-plane results.
 EncodeResult encode_finish(cudaStream_t st, EncScratch &S, DBuf<uint8_t> &arena) {
     CK(cudaGetLastError());
     const uint64_t planes = S.planes;
@@ -860,7 +888,7 @@ EncodeResult encode_finish(cudaStream_t st, EncScratch &S, DBuf<uint8_t> &arena)
     EncodeResult R;
     R.total = S.h_misc.p[0];
     if ((uint32_t)S.h_misc.p[1]) {
-        arena.ensure(R.total + R.total / 2 + (1 << 20));
+        grow_keep(arena, S.arena_base + R.total + R.total / 2 + (1 << 20), S.arena_base, st);
         CK(cudaMemsetAsync(S.overflow.p, 0, sizeof(uint32_t), st));
         launch_pack(st, S, arena, false);
         CK(cudaMemcpyAsync(S.h_off.p, S.blk_off.p, planes * 8, cudaMemcpyDeviceToHost, st));
@@ -905,14 +933,13 @@ struct DecScratch {
 // prepare = false: the tables were written by the encoder that produced the
 // blocks (enc_codebook -> emit_dec_tables), no table-parsing pass needed.
 void decode_batch(cudaStream_t st, DecScratch &S, const uint8_t *arena, const uint64_t *blk_off,
-                  const IndexRec *index, double *const *out, int planes, uint64_t L, int log2C, int qb,
+                  double *const *out, int planes, uint64_t L, int log2C, int qb,
                   bool prepare = true, const NormArgs *norm = nullptr) {
     if (prepare) S.ensure(planes, L, qb);
     const DecTables T = S.tables();
     DecPlanes D;
     D.arena = arena;
     D.blk_off = blk_off;
-    D.index = index;
     D.out = out;
     D.L = L;
     D.log2C = log2C;
@@ -1037,38 +1064,53 @@ CodecCtx &codec_ctx() {
 } // namespace
 
 // =================================================================== engine
+// Per-gate run metrics (SPEC.md:309-314 per_gate_min_ratio; the CSV report's
+// gate_index, min_ratio, mean_ratio, seconds), plus the state's bytes after
+// the gate.
+struct GateRow {
+    double min_ratio, ratio_sum;
+    uint64_t calls, bytes, index_bytes;
+    double seconds;
+};
+
 struct qcsim_engine {
     qcsim_engine_config cfg{};
     int n = 0, s = 0;
     uint64_t S = 0, L = 0;       // slices (global), slice length
     uint64_t s0 = 0, ns = 0;     // this rank's slice range
+    uint64_t wave = 0;           // slices per batch (wave) of a gate pass; ns = one batch
     int log2C = 0;
     uint64_t nidx = 0;
     cudaStream_t st = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evg = nullptr;
     bool compressed = true;
     bool loaded = false;
-    // compressed state (ping-pong)
+    // compressed state (ping-pong); every block's slot also holds its
+    // decode index (common.cuh)
     DBuf<uint8_t> arena[2];
-    DBuf<uint64_t> blk_off[2];
-    DBuf<IndexRec> index[2];
+    DBuf<uint64_t> blk_off[2];         // device copy of the block offsets, plane order
     std::vector<uint64_t> blk_bytes_h; // current block sizes, plane order
+    std::vector<uint64_t> blk_off_h;   // current block offsets, plane order
+    DBuf<IndexRec> index;              // encoder scratch: fine decode-index records
     int cur = 0;
-    // dense state (compression off) and decoded old values, [slot][2][L]
+    // dense state (compression off); decoded old values of one batch,
+    // [slot][re|im][L] (slots: the batch's units, then imported partners)
     DBuf<double> dense[2];
     DBuf<double> old;
-    DBuf<int32_t> slot_of;
-    DBuf<uint64_t> unit_slice;
-    DBuf<double *> outptrs;
+    DBuf<double *> outptrs;            // plane k of the batch -> old + k L
+    uint64_t outptr_planes = 0;
+    const double *outptr_base = nullptr;
+    DBuf<uint64_t> wave_off;           // block offsets of one wave's planes
+    HBuf<uint64_t> h_wave_off;
     DBuf<double> slice_sq;
     HBuf<double> h_sq;
     DBuf<double *> imp_ptrs;
-    bool tables_ready = false, slot_local = true;
     // partner slices imported from other ranks: slice -> QCB1 bytes
     std::vector<std::pair<uint64_t, std::vector<uint8_t>>> imported;
     std::vector<double> sq_norm; // all S slices (global view)
     EncScratch enc;
-    DecScratch dec[2]; // decode tables of arena[0/1], written by the encoder
+    DecScratch dec[2]; // decode tables of arena[0/1], written by the encoder (single-batch passes)
+    DecScratch decw;   // decode tables parsed from the blocks (waves, compare, gather)
     ValScratch val;
     DBuf<uint8_t> imp_bytes;
     DBuf<uint64_t> imp_off;
@@ -1082,25 +1124,30 @@ struct qcsim_engine {
     DBuf<double> norm_buf[2], dev_scale;
     DBuf<EngineDevStats> dev_stats;
     HBuf<EngineDevStats> h_stats;
+    DBuf<GateRowDev> dev_rows; // deferred run: one row per gate pass
+    HBuf<GateRowDev> h_rows;
+    uint64_t row0 = 0, nrows = 0;
     // metrics
     double ratio_min = INFINITY, ratio_sum = 0.0;
     uint64_t calls = 0, gates = 0, peak = 0, current = 0, fallback = 0;
     double wall = 0.0;
     uint64_t launches0 = 0;
+    std::vector<GateRow> rows; // since the last load
 };
 
 namespace {
 
-uint64_t partner_slice(const qcsim_action &a, int s, uint64_t j) {
-    if (a.kind == QCSIM_ACTION_BUTTERFLY && a.target >= s) return j ^ (1ull << (a.target - s));
+uint64_t partner_mask(const qcsim_action &a, int s) {
+    if (a.kind == QCSIM_ACTION_BUTTERFLY && a.target >= s) return 1ull << (a.target - s);
     if (a.kind == QCSIM_ACTION_SWAP) {
         uint64_t hm = 0;
         if (a.a >= s) hm |= 1ull << (a.a - s);
         if (a.b >= s) hm |= 1ull << (a.b - s);
-        return j ^ hm;
+        return hm;
     }
-    return j;
+    return 0;
 }
+uint64_t partner_slice(const qcsim_action &a, int s, uint64_t j) { return j ^ partner_mask(a, s); }
 
 DevAction to_dev(const qcsim_action &a) {
     DevAction d{};
@@ -1122,17 +1169,32 @@ double tree_sum_host(const double *v, uint64_t len) {
     return a + b;
 }
 
-void record_sizes(qcsim_engine *e, const std::vector<uint64_t> &bytes) {
+uint64_t index_bytes_of(const qcsim_engine *e, const std::vector<uint64_t> &bytes) {
+    uint64_t t = 0;
+    for (uint64_t b : bytes) t += index_records(e->L, b, e->log2C) * sizeof(IndexRec);
+    return t;
+}
+
+// Run metrics of one encode pass over all local planes (plane order, as the
+// oracle): min / mean ratio, bytes, and the per-gate row.
+void record_sizes(qcsim_engine *e, const std::vector<uint64_t> &bytes, double seconds) {
     uint64_t tot = 0;
+    GateRow row{INFINITY, 0.0, 0, 0, 0, seconds};
     for (uint64_t b : bytes) {
         const double ratio = (double)(8 * e->L) / (double)b;
         if (ratio < e->ratio_min) e->ratio_min = ratio;
         e->ratio_sum += ratio;
         e->calls++;
+        if (ratio < row.min_ratio) row.min_ratio = ratio;
+        row.ratio_sum += ratio;
+        row.calls++;
         tot += b;
     }
     e->current = tot;
     e->peak = std::max(e->peak, tot);
+    row.bytes = tot;
+    row.index_bytes = index_bytes_of(e, bytes);
+    e->rows.push_back(row);
 }
 
 // Identity source over [slot][2][L] planes (initial loads).
@@ -1145,174 +1207,318 @@ struct PlanarSrc {
         o[1] = v[(uint64_t)unit * 2 * L + L + i];
     }
 };
-// Basis state |x> restricted to local slices starting at s0.
+// Basis state |x> on the batch's slices.
 struct BasisSrc {
-    uint64_t x, s0;
+    uint64_t x;
+    SliceMap map;
     int s;
     static constexpr bool kNorms = true;
     __device__ __forceinline__ void load(int unit, uint64_t i, double *o) const {
-        const uint64_t g = ((s0 + unit) << s) | i;
+        const uint64_t g = ((map.s0 + map.slice_rel((uint32_t)unit)) << s) | i;
         o[0] = g == x ? 1.0 : 0.0;
         o[1] = 0.0;
     }
 };
 
-template <class Src> void engine_store(qcsim_engine *e, const Src &src) {
-    const int units = (int)e->ns;
-    const int nxt = e->cur ^ 1;
-    const uint64_t ntiles = (e->L + kTile - 1) / kTile;
-    if (e->deferred) { // no host round trip (qcsim_engine_run settles the books)
-        e->index[nxt].ensure(2 * e->ns * e->nidx);
-        e->dec[nxt].ensure(2 * e->ns, e->L, e->cfg.codec.quant_code_bits);
-        e->enc.dec_out = e->dec[nxt].tables();
-        e->enc.stats_out = e->dev_stats.p;
-        e->enc.stats_gate = e->gates;
-        e->blk_off[nxt].ensure(2 * e->ns);
-        e->enc.blk_off_out = e->blk_off[nxt].p;
-        encode_launch<2, Src>(e->st, e->enc, src, units, e->L, e->cfg.codec, e->log2C, e->index[nxt].p,
-                              e->arena[nxt], false, false, /*host_results=*/false);
-        e->enc.dec_out = DecTables{};
-        e->enc.stats_out = nullptr;
-        e->enc.blk_off_out = nullptr;
-        e->defer_fresh = false; // slice norms: next pass's engine_norm, or engine_defer_end
-        (void)ntiles;
-        e->cur = nxt;
-        return;
+// Slices per wave: the largest power of two whose dense working set (old
+// planes, encoder scratch, decode tables, fine index) fits the budget
+// (cfg.wave_bytes, else 45% of the device's memory; QCSIM_WAVE_SLICES
+// overrides for tests).  Grouped waves need a whole partner group (<= 4).
+uint64_t choose_wave(const qcsim_engine *e) {
+    if (!e->compressed) return e->ns;
+    if (const char *v = std::getenv("QCSIM_WAVE_SLICES")) {
+        uint64_t w = std::strtoull(v, nullptr, 10);
+        uint64_t p = 1;
+        while (p * 2 <= w && p * 2 <= e->ns) p *= 2;
+        return std::max<uint64_t>(std::min<uint64_t>(4, e->ns), p);
     }
-    if (e->compressed) {
-        e->index[nxt].ensure(2 * e->ns * e->nidx);
+    uint64_t budget = e->cfg.wave_bytes;
+    if (!budget) {
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+            cudaGetLastError();
+            tot = 180ull << 30;
+        }
+        budget = (uint64_t)(0.45 * (double)tot);
+    }
+    const uint64_t L = e->L;
+    const uint64_t cap = std::min<uint64_t>(L + 1, (1ull << e->cfg.codec.quant_code_bits) + 1);
+    const uint64_t per_plane = L * 70 + cap * 70 + (L >> e->log2C) * sizeof(IndexRec) + (8u << 10);
+    const uint64_t per_slice = 2 * per_plane;
+    uint64_t w = 1;
+    while (w * 2 <= e->ns && (w * 2) * per_slice <= budget) w *= 2;
+    return std::max<uint64_t>(std::min<uint64_t>(4, e->ns), w);
+}
+
+// Decode-output pointer table for batches of up to `planes` planes of `old`.
+void ensure_outptrs(qcsim_engine *e, uint64_t planes) {
+    e->old.ensure(planes * e->L);
+    if (e->outptr_planes >= planes && e->outptr_base == e->old.p) return;
+    std::vector<double *> ptrs(planes);
+    for (uint64_t k = 0; k < planes; ++k) ptrs[k] = e->old.p + k * e->L;
+    e->outptrs.ensure(planes);
+    CK(cudaMemcpy(e->outptrs.p, ptrs.data(), planes * sizeof(double *), cudaMemcpyHostToDevice));
+    e->outptr_planes = planes;
+    e->outptr_base = e->old.p;
+}
+
+// Imported partner blocks (other ranks) of units [u0, u0 + cnt), decoded by
+// the validating decoder into planes old[first_plane + 2u + p].
+void decode_imports(qcsim_engine *e, const SliceMap &map, uint64_t u0, uint64_t cnt, uint64_t first_plane) {
+    if (!cnt) return;
+    std::unordered_map<uint64_t, size_t> where;
+    for (size_t m = 0; m < e->imported.size(); ++m) where[e->imported[m].first] = m;
+    std::vector<uint8_t> all;
+    std::vector<uint64_t> offs;
+    for (uint64_t u = u0; u < u0 + cnt; ++u) {
+        const uint64_t pj = (e->s0 + map.slice_rel((uint32_t)u)) ^ map.hm;
+        auto it = where.find(pj);
+        if (it == where.end())
+            raise(QCSIM_INVALID_ARGUMENT,
+                  "partner slice " + std::to_string(pj) + " not imported (multi-rank exchange missing)");
+        const std::vector<uint8_t> &b = e->imported[it->second].second;
+        uint64_t pos = 0;
+        for (int p = 0; p < 2; ++p) {
+            uint64_t used = 0;
+            parse_header(b.data() + pos, b.size() - pos, &used);
+            offs.push_back(all.size());
+            all.insert(all.end(), b.begin() + pos, b.begin() + pos + used);
+            pos += used;
+        }
+    }
+    e->imp_bytes.ensure(all.size() + 64);
+    e->imp_off.ensure(offs.size());
+    CK(cudaMemcpyAsync(e->imp_bytes.p, all.data(), all.size(), cudaMemcpyHostToDevice, e->st));
+    CK(cudaMemcpyAsync(e->imp_off.p, offs.data(), offs.size() * 8, cudaMemcpyHostToDevice, e->st));
+    std::vector<double *> ptrs(offs.size());
+    for (uint64_t k = 0; k < offs.size(); ++k) ptrs[k] = e->old.p + (first_plane + k) * e->L;
+    e->imp_ptrs.ensure(ptrs.size());
+    CK(cudaMemcpyAsync(e->imp_ptrs.p, ptrs.data(), ptrs.size() * sizeof(double *), cudaMemcpyHostToDevice, e->st));
+    const uint64_t vcap = std::min<uint64_t>(e->L + 1, (1ull << e->cfg.codec.quant_code_bits) + 1);
+    e->val.ensure(offs.size(), vcap);
+    ValArgs V;
+    V.blocks = e->imp_bytes.p;
+    V.blk_off = e->imp_off.p;
+    V.out = e->imp_ptrs.p;
+    V.err = e->val.err.p;
+    V.ssym = e->val.ssym.p;
+    V.slen = e->val.slen.p;
+    V.cap = vcap;
+    {
+        PROF("dec_validate", e->st);
+        launch_k(dec_validate, (unsigned)((offs.size() + 31) / 32), 32, 0, e->st, V, (int)offs.size());
+    }
+    std::vector<uint32_t> errs(offs.size());
+    CK(cudaMemcpyAsync(errs.data(), e->val.err.p, errs.size() * 4, cudaMemcpyDeviceToHost, e->st));
+    CK(cudaStreamSynchronize(e->st));
+    for (uint32_t x : errs)
+        if (x) raise(QCSIM_CODEC, dec_message(x));
+}
+
+// Decodes local slices [k0, k0 + cnt) (contiguous planes) into old slots
+// [0, cnt): block offsets from the device table, tables parsed from the
+// blocks.  Compare / gather.
+void decode_range(qcsim_engine *e, uint64_t k0, uint64_t cnt) {
+    ensure_outptrs(e, 2 * cnt);
+    decode_batch(e->st, e->decw, e->arena[e->cur].p, e->blk_off[e->cur].p + 2 * k0, e->outptrs.p, (int)(2 * cnt),
+                 e->L, e->log2C, e->cfg.codec.quant_code_bits, /*prepare=*/true);
+}
+
+// Plane values of local slices [k0, k0 + cnt) in [slot][re|im][L] layout on
+// the device (decoded into `old`, or the dense state itself).
+const double *state_range(qcsim_engine *e, uint64_t k0, uint64_t cnt) {
+    if (!e->compressed) return e->dense[e->cur].p + k0 * 2 * e->L;
+    decode_range(e, k0, cnt);
+    return e->old.p;
+}
+
+// One encode batch: `units` slices produced by `src` into arena[nxt] at
+// enc.arena_base; the slice norms of the batch into h_sq[0, units).
+template <class Src>
+EncodeResult encode_units(qcsim_engine *e, const Src &src, uint64_t units, int nxt, bool tables) {
+    e->index.ensure(2 * units * e->nidx);
+    if (tables) {
         // the encoder also writes the decode tables of the blocks it packs
-        e->dec[nxt].ensure(2 * e->ns, e->L, e->cfg.codec.quant_code_bits);
+        e->dec[nxt].ensure(2 * units, e->L, e->cfg.codec.quant_code_bits);
         e->enc.dec_out = e->dec[nxt].tables();
-        encode_launch<2, Src>(e->st, e->enc, src, units, e->L, e->cfg.codec, e->log2C, e->index[nxt].p,
-                              e->arena[nxt], false, false);
-        e->enc.dec_out = DecTables{};
-    } else {
-        e->dense[nxt].ensure(e->ns * 2 * e->L);
-        e->enc.tilesum.ensure(e->ns * ntiles);
-        PROF("dense_gate", e->st);
-        launch_k(dense_gate<Src>, (unsigned)(units * ntiles), 256, 0, e->st, src, units, e->L, e->dense[nxt].p,
-                                                                        e->enc.tilesum.p);
     }
-    // per-slice sq_norm from the tile partials
-    e->slice_sq.ensure(e->ns);
+    encode_launch<2, Src>(e->st, e->enc, src, (int)units, e->L, e->cfg.codec, e->log2C, e->index.p, e->arena[nxt],
+                          false, false);
+    e->enc.dec_out = DecTables{};
+    const uint64_t ntiles = (e->L + kTile - 1) / kTile;
+    e->slice_sq.ensure(units);
     {
         PROF("slice_norms", e->st);
         if (ntiles > 64 && ntiles <= 4096)
-            launch_k(slice_norms_block, (unsigned)units, 256, 0, e->st, e->enc.tilesum.p, (int)ntiles, units, e->slice_sq.p);
+            launch_k(slice_norms_block, (unsigned)units, 256, 0, e->st, e->enc.tilesum.p, (int)ntiles, (int)units,
+                     e->slice_sq.p);
         else
-            launch_k(slice_norms, (units + 127) / 128, 128, 0, e->st, e->enc.tilesum.p, (int)ntiles, units, e->slice_sq.p);
+            launch_k(slice_norms, (unsigned)((units + 127) / 128), 128, 0, e->st, e->enc.tilesum.p, (int)ntiles,
+                     (int)units, e->slice_sq.p);
     }
-    e->h_sq.ensure(e->ns);
-    CK(cudaMemcpyAsync(e->h_sq.p, e->slice_sq.p, e->ns * sizeof(double), cudaMemcpyDeviceToHost, e->st));
-    // the one host synchronisation of a gate pass
-    CK(cudaStreamSynchronize(e->st));
+    e->h_sq.ensure(units);
+    CK(cudaMemcpyAsync(e->h_sq.p, e->slice_sq.p, units * sizeof(double), cudaMemcpyDeviceToHost, e->st));
+    CK(cudaStreamSynchronize(e->st)); // the host synchronisation of a batch
     g_prof.flush();
-    CK(cudaGetLastError());
-    if (e->compressed) {
-        EncodeResult R = encode_finish(e->st, e->enc, e->arena[nxt]);
-        e->blk_off[nxt].ensure(2 * e->ns);
-        CK(cudaMemcpyAsync(e->blk_off[nxt].p, e->enc.blk_off.p, 2 * e->ns * sizeof(uint64_t),
-                           cudaMemcpyDeviceToDevice, e->st));
-        e->blk_bytes_h = std::move(R.block_bytes);
-        e->fallback += R.fallback;
-        record_sizes(e, e->blk_bytes_h);
+    return encode_finish(e->st, e->enc, e->arena[nxt]);
+}
+
+// A host-synchronous gate pass (or load) over the local slices in waves of
+// e->wave slices.  `hm`: partner mask of the gate (0 for loads and local
+// gates); `remote`: partners live on other ranks (imported); `decode`: the
+// pass reads the old state.  make_src(map, old) returns the encoder source
+// of a batch.  One wave (wave == ns) keeps the identity layout and the
+// encoder-written decode tables; more waves decode with tables parsed from
+// the blocks and group each wave under the partner mask.
+template <class MakeSrc>
+void engine_waves(qcsim_engine *e, uint64_t hm, bool remote, bool decode, MakeSrc make_src) {
+    const int nxt = e->cur ^ 1;
+    const uint64_t W = e->wave, nw = e->ns / W;
+    const bool single = nw == 1;
+    int gsh = 0;
+    for (uint64_t h = hm; h; h &= h - 1) ++gsh;
+    CK(cudaEventRecord(e->evg, e->st));
+    std::vector<uint64_t> nbytes(2 * e->ns), noff(2 * e->ns);
+    if (!single) { // pre-size the new arena from the current state (waves append)
+        uint64_t used = 0;
+        for (uint64_t b : e->blk_bytes_h) used += b + 16;
+        used += index_bytes_of(e, e->blk_bytes_h);
+        if (e->arena[nxt].cap < used + used / 4 + (16ull << 20)) {
+            e->arena[nxt].release();
+            e->arena[nxt].ensure(used + used / 4 + (16ull << 20));
+        }
     }
-    for (uint64_t k = 0; k < e->ns; ++k) e->sq_norm[e->s0 + k] = e->h_sq.p[k];
+    e->enc.arena_base = 0;
+    uint64_t fb = 0;
+    for (uint64_t w = 0; w < nw; ++w) {
+        SliceMap map;
+        map.s0 = e->s0;
+        map.nunits = (uint32_t)W;
+        if (remote) {
+            map.mode = 2;
+            map.hm = hm; // (global XOR: every partner is remote)
+            map.gbase = w * W;
+        } else if (single) {
+            map.mode = 0;
+            map.hm = hm;
+        } else {
+            map.mode = 1;
+            map.hm = hm;
+            map.gsh = (uint32_t)gsh;
+            map.gbase = w * (W >> gsh);
+        }
+        const uint64_t slots = W + (remote ? W : 0);
+        if (decode) {
+            ensure_outptrs(e, 2 * slots);
+            if (single) {
+                decode_batch(e->st, e->dec[e->cur], e->arena[e->cur].p, e->blk_off[e->cur].p, e->outptrs.p,
+                             (int)(2 * W), e->L, e->log2C, e->cfg.codec.quant_code_bits, /*prepare=*/false);
+            } else {
+                e->h_wave_off.ensure(2 * W);
+                for (uint64_t u = 0; u < W; ++u) {
+                    const uint64_t k = map.slice_rel((uint32_t)u);
+                    e->h_wave_off.p[2 * u] = e->blk_off_h[2 * k];
+                    e->h_wave_off.p[2 * u + 1] = e->blk_off_h[2 * k + 1];
+                }
+                e->wave_off.ensure(2 * W);
+                CK(cudaMemcpyAsync(e->wave_off.p, e->h_wave_off.p, 2 * W * 8, cudaMemcpyHostToDevice, e->st));
+                decode_batch(e->st, e->decw, e->arena[e->cur].p, e->wave_off.p, e->outptrs.p, (int)(2 * W), e->L,
+                             e->log2C, e->cfg.codec.quant_code_bits, /*prepare=*/true);
+            }
+            if (remote) decode_imports(e, map, 0, W, 2 * W);
+        }
+        const auto src = make_src(map);
+        EncodeResult R = encode_units(e, src, W, nxt, single);
+        fb += R.fallback;
+        for (uint64_t u = 0; u < W; ++u) {
+            const uint64_t k = map.slice_rel((uint32_t)u);
+            for (int p = 0; p < 2; ++p) {
+                nbytes[2 * k + p] = R.block_bytes[2 * u + p];
+                noff[2 * k + p] = e->enc.arena_base + R.blk_off[2 * u + p];
+            }
+            e->sq_norm[e->s0 + k] = e->h_sq.p[u];
+        }
+        e->enc.arena_base += R.total;
+    }
+    e->enc.arena_base = 0;
+    e->blk_off[nxt].ensure(2 * e->ns);
+    CK(cudaMemcpyAsync(e->blk_off[nxt].p, noff.data(), 2 * e->ns * 8, cudaMemcpyHostToDevice, e->st));
+    CK(cudaEventRecord(e->ev1, e->st));
+    CK(cudaEventSynchronize(e->ev1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e->evg, e->ev1));
+    e->blk_bytes_h = std::move(nbytes);
+    e->blk_off_h = std::move(noff);
+    e->fallback += fb;
+    record_sizes(e, e->blk_bytes_h, ms * 1e-3);
     e->cur = nxt;
     e->loaded = true;
 }
 
-// Static device tables of the local slices, uploaded once: decode output
-// pointers (slot k = local slice k), unit -> slice, slice -> slot.
-void engine_tables(qcsim_engine *e) {
-    if (e->tables_ready) return;
-    e->old.ensure(e->ns * 2 * e->L);
-    std::vector<double *> ptrs(2 * e->ns);
-    for (uint64_t k = 0; k < 2 * e->ns; ++k) ptrs[k] = e->old.p + k * e->L;
-    e->outptrs.ensure(2 * e->ns);
-    CK(cudaMemcpy(e->outptrs.p, ptrs.data(), ptrs.size() * sizeof(double *), cudaMemcpyHostToDevice));
-    std::vector<uint64_t> us(e->ns);
-    for (uint64_t k = 0; k < e->ns; ++k) us[k] = e->s0 + k;
-    e->unit_slice.ensure(e->ns);
-    CK(cudaMemcpy(e->unit_slice.p, us.data(), e->ns * sizeof(uint64_t), cudaMemcpyHostToDevice));
-    std::vector<int32_t> slot(e->S, -1);
-    for (uint64_t k = 0; k < e->ns; ++k) slot[e->s0 + k] = (int32_t)k;
-    e->slot_of.ensure(e->S);
-    CK(cudaMemcpy(e->slot_of.p, slot.data(), e->S * sizeof(int32_t), cudaMemcpyHostToDevice));
-    e->slot_local = true;
-    e->tables_ready = true;
+// Compression-off engine: one dense pass over all local slices.
+template <class Src> void engine_dense(qcsim_engine *e, const Src &src) {
+    const int nxt = e->cur ^ 1;
+    const uint64_t ntiles = (e->L + kTile - 1) / kTile;
+    CK(cudaEventRecord(e->evg, e->st));
+    e->dense[nxt].ensure(e->ns * 2 * e->L);
+    e->enc.tilesum.ensure(e->ns * ntiles);
+    {
+        PROF("dense_gate", e->st);
+        launch_k(dense_gate<Src>, (unsigned)(e->ns * ntiles), 256, 0, e->st, src, (int)e->ns, e->L, e->dense[nxt].p,
+                 e->enc.tilesum.p);
+    }
+    e->slice_sq.ensure(e->ns);
+    {
+        PROF("slice_norms", e->st);
+        if (ntiles > 64 && ntiles <= 4096)
+            launch_k(slice_norms_block, (unsigned)e->ns, 256, 0, e->st, e->enc.tilesum.p, (int)ntiles, (int)e->ns,
+                     e->slice_sq.p);
+        else
+            launch_k(slice_norms, (unsigned)((e->ns + 127) / 128), 128, 0, e->st, e->enc.tilesum.p, (int)ntiles,
+                     (int)e->ns, e->slice_sq.p);
+    }
+    e->h_sq.ensure(e->ns);
+    CK(cudaMemcpyAsync(e->h_sq.p, e->slice_sq.p, e->ns * sizeof(double), cudaMemcpyDeviceToHost, e->st));
+    CK(cudaEventRecord(e->ev1, e->st));
+    CK(cudaEventSynchronize(e->ev1));
+    g_prof.flush();
+    CK(cudaGetLastError());
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e->evg, e->ev1));
+    for (uint64_t k = 0; k < e->ns; ++k) e->sq_norm[e->s0 + k] = e->h_sq.p[k];
+    e->rows.push_back(GateRow{0.0, 0.0, 0, 16ull * e->ns * e->L, 0, ms * 1e-3});
+    e->cur = nxt;
+    e->loaded = true;
 }
 
-// Decodes the current state of the local slices (plus imported partner
-// slices) into e->old, slot k = local slice k, then imported ones.
-void engine_decode_old(qcsim_engine *e, bool need_imported) {
-    engine_tables(e);
-    const uint64_t extra = need_imported ? e->imported.size() : 0;
-    if (extra) {
-        // grow `old` for the imported slots (keeps pointers of local slots valid
-        // only if no reallocation: re-upload the tables when it happens)
-        if (e->old.cap < (e->ns + extra) * 2 * e->L) {
-            e->old.ensure((e->ns + extra) * 2 * e->L);
-            e->tables_ready = false;
-            engine_tables(e);
-        }
-    }
-    if (!e->compressed) {
-        if (e->norm.enabled) {
-            PROF("engine_norm", e->st);
-            launch_k(engine_norm, 1, 256, 0, e->st, e->norm);
-        }
-        CK(cudaMemcpyAsync(e->old.p, e->dense[e->cur].p, e->ns * 2 * e->L * sizeof(double),
-                           cudaMemcpyDeviceToDevice, e->st));
-    } else {
-        decode_batch(e->st, e->dec[e->cur], e->arena[e->cur].p, e->blk_off[e->cur].p, e->index[e->cur].p, e->outptrs.p,
-                     (int)(2 * e->ns), e->L, e->log2C, e->cfg.codec.quant_code_bits, /*prepare=*/false, &e->norm);
-    }
+// Deferred pass (single batch, identity layout, no host round trip): decode
+// (its extra block runs the normalization and the previous pass's metrics),
+// gate, encode with device-side run metrics.
+void engine_deferred_pass(qcsim_engine *e, const GateSrc &g0) {
+    const int nxt = e->cur ^ 1;
+    ensure_outptrs(e, 2 * e->ns);
+    decode_batch(e->st, e->dec[e->cur], e->arena[e->cur].p, e->blk_off[e->cur].p, e->outptrs.p, (int)(2 * e->ns),
+                 e->L, e->log2C, e->cfg.codec.quant_code_bits, /*prepare=*/false, &e->norm);
     e->norm.enabled = 0;
-    if (extra) {
-        // imported blocks: validating serial decode (they carry no index)
-        std::vector<uint8_t> all;
-        std::vector<uint64_t> offs;
-        for (auto &kv : e->imported) {
-            uint64_t pos = 0;
-            for (int p = 0; p < 2; ++p) {
-                uint64_t used = 0;
-                parse_header(kv.second.data() + pos, kv.second.size() - pos, &used);
-                offs.push_back(all.size());
-                all.insert(all.end(), kv.second.begin() + pos, kv.second.begin() + pos + used);
-                pos += used;
-            }
-        }
-        e->imp_bytes.ensure(all.size() + 64);
-        e->imp_off.ensure(offs.size());
-        CK(cudaMemcpyAsync(e->imp_bytes.p, all.data(), all.size(), cudaMemcpyHostToDevice, e->st));
-        CK(cudaMemcpyAsync(e->imp_off.p, offs.data(), offs.size() * 8, cudaMemcpyHostToDevice, e->st));
-        std::vector<double *> ptrs(offs.size());
-        for (uint64_t k = 0; k < offs.size(); ++k) ptrs[k] = e->old.p + (2 * e->ns + k) * e->L;
-        e->imp_ptrs.ensure(ptrs.size());
-        CK(cudaMemcpyAsync(e->imp_ptrs.p, ptrs.data(), ptrs.size() * sizeof(double *), cudaMemcpyHostToDevice,
-                           e->st));
-        const uint64_t vcap = std::min<uint64_t>(e->L + 1, (1ull << e->cfg.codec.quant_code_bits) + 1);
-        e->val.ensure(offs.size(), vcap);
-        ValArgs V;
-        V.blocks = e->imp_bytes.p;
-        V.blk_off = e->imp_off.p;
-        V.out = e->imp_ptrs.p;
-        V.err = e->val.err.p;
-        V.ssym = e->val.ssym.p;
-        V.slen = e->val.slen.p;
-        V.cap = vcap;
-        {
-            PROF("dec_validate", e->st);
-            launch_k(dec_validate, (unsigned)((offs.size() + 31) / 32), 32, 0, e->st, V, (int)offs.size());
-        }
-        std::vector<uint32_t> errs(offs.size());
-        CK(cudaMemcpyAsync(errs.data(), e->val.err.p, errs.size() * 4, cudaMemcpyDeviceToHost, e->st));
-        CK(cudaStreamSynchronize(e->st));
-        for (uint32_t x : errs)
-            if (x) raise(QCSIM_CODEC, dec_message(x));
-    }
+    GateSrc g = g0;
+    g.old = e->old.p;
+    e->index.ensure(2 * e->ns * e->nidx);
+    e->dec[nxt].ensure(2 * e->ns, e->L, e->cfg.codec.quant_code_bits);
+    e->enc.dec_out = e->dec[nxt].tables();
+    e->enc.stats_out = e->dev_stats.p;
+    e->enc.stats_gate = e->gates;
+    e->enc.rows_out = e->dev_rows.p;
+    e->enc.row0 = e->row0;
+    e->enc.nrows = e->nrows;
+    e->blk_off[nxt].ensure(2 * e->ns);
+    e->enc.blk_off_out = e->blk_off[nxt].p;
+    encode_launch<2, GateSrc>(e->st, e->enc, g, (int)e->ns, e->L, e->cfg.codec, e->log2C, e->index.p,
+                              e->arena[nxt], false, false, /*host_results=*/false);
+    e->enc.dec_out = DecTables{};
+    e->enc.stats_out = nullptr;
+    e->enc.blk_off_out = nullptr;
+    e->defer_fresh = false; // slice norms: next pass's engine_norm, or engine_defer_end
+    e->cur = nxt;
 }
 
 double g_host_t[4] = {0, 0, 0, 0}; // debug (QCSIM_ENQ_TIMING): gate prologue, decode, encode, total
@@ -1329,11 +1535,10 @@ void engine_gate(qcsim_engine *e, const qcsim_action &a) {
     double scale = 1.0;
     e->norm = NormArgs{};
     if (e->deferred) {
-        // run by the decoder grid's extra block (engine_decode_old):
-        // the previous pass's run metrics (none before the first pass), then
-        // the slice norms of the previous pass from its tile partials (or,
-        // for the first gate of a run, the norms uploaded by
-        // engine_defer_begin) and the scale
+        // run by the decoder grid's extra block: the previous pass's run
+        // metrics (none before the first pass), then the slice norms of the
+        // previous pass from its tile partials (or, for the first gate of a
+        // run, the norms uploaded by engine_defer_begin) and the scale
         NormArgs &N = e->norm;
         N.norm = apply ? 1 : 0;
         N.tilesum = e->defer_fresh ? nullptr : e->enc.tilesum.p;
@@ -1353,8 +1558,13 @@ void engine_gate(qcsim_engine *e, const qcsim_action &a) {
         N.params = e->enc.params.p;
         N.planes = (int)(2 * e->ns);
         N.L = e->L;
+        N.log2C = e->log2C;
         N.stats_gate = (unsigned long long)e->gates - 1;
-        N.enabled = N.norm || N.stats;
+        N.rows = e->dev_rows.p;
+        N.row0 = e->row0;
+        N.nrows = e->nrows;
+        N.stamp = e->defer_fresh ? 1 : 0;
+        N.enabled = N.norm || N.stats || N.stamp;
     } else if (apply) {
         const double G = tree_sum_host(e->sq_norm.data(), e->S);
         if (!std::isfinite(G) || std::fabs(G - 1.0) > 10.0 * e->cfg.norm_drift_tolerance) {
@@ -1365,103 +1575,71 @@ void engine_gate(qcsim_engine *e, const qcsim_action &a) {
         }
         scale = 1.0 / std::sqrt(G);
     }
-    // which old slices are needed: local + partners (imported if remote)
-    bool remote = false;
-    for (uint64_t k = 0; k < e->ns && !remote; ++k) {
-        const uint64_t pj = partner_slice(a, e->s, e->s0 + k);
-        if (pj < e->s0 || pj >= e->s0 + e->ns) remote = true;
-    }
-    const auto ht1 = std::chrono::steady_clock::now();
-    engine_decode_old(e, remote);
-    const auto ht2 = std::chrono::steady_clock::now();
-    if (remote) {
-        std::vector<int32_t> slot(e->S, -1);
-        for (uint64_t k = 0; k < e->ns; ++k) slot[e->s0 + k] = (int32_t)k;
-        for (uint64_t k = 0; k < e->ns; ++k) {
-            const uint64_t pj = partner_slice(a, e->s, e->s0 + k);
-            if (pj >= e->s0 && pj < e->s0 + e->ns) continue;
-            int found = -1;
-            for (size_t m = 0; m < e->imported.size(); ++m)
-                if (e->imported[m].first == pj) found = (int)m;
-            if (found < 0)
-                raise(QCSIM_INVALID_ARGUMENT,
-                      "partner slice " + std::to_string(pj) + " not imported (multi-rank exchange missing)");
-            slot[pj] = (int32_t)(e->ns + found);
-        }
-        CK(cudaMemcpy(e->slot_of.p, slot.data(), e->S * sizeof(int32_t), cudaMemcpyHostToDevice));
-        e->slot_local = false;
-    } else if (!e->slot_local) {
-        std::vector<int32_t> slot(e->S, -1);
-        for (uint64_t k = 0; k < e->ns; ++k) slot[e->s0 + k] = (int32_t)k;
-        CK(cudaMemcpy(e->slot_of.p, slot.data(), e->S * sizeof(int32_t), cudaMemcpyHostToDevice));
-        e->slot_local = true;
-    }
-    e->enc.ensure(2 * e->ns, e->ns, e->L, e->cfg.codec.quant_code_bits);
+    const uint64_t hm = partner_mask(a, e->s);
+    const bool remote = (hm & ~(e->ns - 1)) != 0; // partner slices on other ranks
     GateSrc g;
     g.old = e->old.p;
-    g.slot_of = e->slot_of.p;
-    g.unit_slice = e->unit_slice.p;
     g.scale = scale;
     g.scale_dev = e->deferred ? e->dev_scale.p : nullptr;
     g.apply_scale = apply ? 1 : 0;
     g.act = to_dev(a);
     g.s = e->s;
     g.L = e->L;
-    const auto ht3 = std::chrono::steady_clock::now();
-    engine_store(e, g);
-    const auto ht4 = std::chrono::steady_clock::now();
+    g.map.s0 = e->s0;
+    g.map.hm = hm;
+    g.map.nunits = (uint32_t)e->ns;
+    const auto ht1 = std::chrono::steady_clock::now();
+    if (e->deferred) {
+        engine_deferred_pass(e, g);
+    } else if (!e->compressed) {
+        if (remote) raise(QCSIM_INVALID_ARGUMENT, "compression-off engines do not exchange partner slices");
+        g.old = e->dense[e->cur].p;
+        engine_dense(e, g);
+    } else {
+        engine_waves(e, hm, remote, /*decode=*/true, [&](const SliceMap &map) {
+            GateSrc b = g;
+            b.old = e->old.p;
+            b.map = map;
+            return b;
+        });
+    }
+    const auto ht2 = std::chrono::steady_clock::now();
     g_host_t[0] += std::chrono::duration<double, std::micro>(ht1 - ht0).count();
-    g_host_t[1] += std::chrono::duration<double, std::micro>(ht2 - ht1).count();
-    g_host_t[2] += std::chrono::duration<double, std::micro>(ht4 - ht3).count();
-    g_host_t[3] += std::chrono::duration<double, std::micro>(ht4 - ht0).count();
+    g_host_t[2] += std::chrono::duration<double, std::micro>(ht2 - ht1).count();
+    g_host_t[3] += std::chrono::duration<double, std::micro>(ht2 - ht0).count();
     e->gates++;
     e->imported.clear();
 }
 
 // Worst-case arena bytes for one gate pass (every plane at qcsim_block_bound,
-// 16-byte slots): with arenas that large a pass cannot overflow, so the gate
-// loop needs no host round trip.
+// 16-byte slots, the largest decode index): with arenas that large a pass
+// cannot overflow, so the gate loop needs no host round trip.
 uint64_t fixed_slot_bytes(const qcsim_engine *e) {
     const uint64_t L = e->L;
     uint64_t nsym = (1ull << e->cfg.codec.quant_code_bits) + 1;
     if (nsym > L + 1) nsym = L + 1;
     const uint64_t bound = kHeaderBytes + 4 + 5 * nsym + (L * kMaxCodeLen + 7) / 8 + 16 + L * 16;
-    return (bound + 31) & ~15ull; // >= 16 + round_up(block bytes, 16): every slot_bytes fits
+    // >= 16 + round_up(block bytes, 16) + its decode index: every slot_bytes fits
+    return ((bound + 31) & ~15ull) + ((((L >> e->log2C) + 1) * sizeof(IndexRec) + 15) & ~15ull);
 }
-uint64_t arena_worst(const qcsim_engine *e) {
-    const uint64_t L = e->L;
-    uint64_t nsym = (1ull << e->cfg.codec.quant_code_bits) + 1;
-    if (nsym > L + 1) nsym = L + 1;
-    const uint64_t bound = kHeaderBytes + 4 + 5 * nsym + (L * kMaxCodeLen + 7) / 8 + 16 + L * 16;
-    return 2 * e->ns * ((bound + 31) & ~15ull) + (1 << 20);
-}
+uint64_t arena_worst(const qcsim_engine *e) { return 2 * e->ns * fixed_slot_bytes(e) + (1 << 20); }
 
-// Grows a buffer keeping its first `keep` bytes.
-void grow_keep(DBuf<uint8_t> &b, uint64_t want, uint64_t keep, cudaStream_t st) {
-    if (b.cap >= want) return;
-    DBuf<uint8_t> nb;
-    nb.ensure(want);
-    if (b.p && keep) CK(cudaMemcpyAsync(nb.p, b.p, keep, cudaMemcpyDeviceToDevice, st));
-    CK(cudaStreamSynchronize(st));
-    b.swap(nb);
-}
-
-// Deferred gate loop: single rank, compressed, worst-case arenas within the
-// budget (QCSIM_SYNC_GATES=1 forces the per-gate host round trip).
-bool engine_defer_begin(qcsim_engine *e) {
+// Deferred gate loop: single rank, compressed, one batch, worst-case arenas
+// within the budget (QCSIM_SYNC_GATES=1 forces the per-gate host round trip).
+bool engine_defer_begin(qcsim_engine *e, uint64_t count) {
     static const bool forced_sync = std::getenv("QCSIM_SYNC_GATES") != nullptr;
     constexpr uint64_t kBudget = 8ull << 30;
     const uint64_t worst = arena_worst(e);
-    if (forced_sync || e->cfg.world > 1 || !e->compressed || 2 * worst > kBudget || !e->imported.empty()) return false;
+    if (forced_sync || e->cfg.world > 1 || !e->compressed || e->wave != e->ns || 2 * worst > kBudget ||
+        !e->imported.empty())
+        return false;
     CK(cudaStreamSynchronize(e->st));
-    uint64_t used = 0;
-    for (uint64_t k = 0; k < e->blk_bytes_h.size(); ++k) used = std::max(used, e->blk_bytes_h[k]);
     {
         // current arena: keep its contents (up to the highest slot end)
-        std::vector<uint64_t> off(2 * e->ns);
-        CK(cudaMemcpy(off.data(), e->blk_off[e->cur].p, off.size() * 8, cudaMemcpyDeviceToHost));
         uint64_t hi = 0;
-        for (uint64_t k = 0; k < off.size(); ++k) hi = std::max(hi, off[k] + e->blk_bytes_h[k]);
+        for (uint64_t k = 0; k < e->blk_off_h.size(); ++k)
+            hi = std::max(hi, index_offset(e->blk_off_h[k], e->blk_bytes_h[k]) +
+                                  index_records(e->L, e->blk_bytes_h[k], e->log2C) * sizeof(IndexRec));
         grow_keep(e->arena[e->cur], worst, hi, e->st);
         grow_keep(e->arena[e->cur ^ 1], worst, 0, e->st);
     }
@@ -1473,6 +1651,11 @@ bool engine_defer_begin(qcsim_engine *e) {
     e->dev_stats.ensure(1);
     e->h_stats.ensure(1);
     e->h_sq.ensure(e->ns);
+    e->row0 = e->gates;
+    e->nrows = count;
+    e->dev_rows.ensure(count + 1);
+    e->h_rows.ensure(count + 1);
+    CK(cudaMemsetAsync(e->dev_rows.p, 0, (count + 1) * sizeof(GateRowDev), e->st));
     // the host view is authoritative between runs
     for (uint64_t k = 0; k < e->ns; ++k) e->h_sq.p[k] = e->sq_norm[e->s0 + k];
     CK(cudaMemcpyAsync(e->slice_sq.p, e->h_sq.p, e->ns * sizeof(double), cudaMemcpyHostToDevice, e->st));
@@ -1496,12 +1679,10 @@ bool engine_defer_begin(qcsim_engine *e) {
     return true;
 }
 
-// Settles a deferred run: metrics, norms and block sizes back to the host,
-// latched errors raised.
-void engine_defer_end(qcsim_engine *e, bool raise_errors) {
-    e->deferred = false;
+// The deferred run's last kernels (inside the timed region): the last
+// pass's run metrics and slice norms.
+void engine_defer_finish(qcsim_engine *e) {
     const bool fixed = e->enc.fixed_W != 0;
-    e->enc.fixed_W = 0;
     if (!e->defer_fresh && fixed) { // run metrics of the last pass (the others: the next pass's decoder grid)
         NormArgs N{};
         N.st = e->dev_stats.p;
@@ -1511,7 +1692,11 @@ void engine_defer_end(qcsim_engine *e, bool raise_errors) {
         N.params = e->enc.params.p;
         N.planes = (int)(2 * e->ns);
         N.L = e->L;
+        N.log2C = e->log2C;
         N.stats_gate = (unsigned long long)e->gates - 1;
+        N.rows = e->dev_rows.p;
+        N.row0 = e->row0;
+        N.nrows = e->nrows;
         PROF("pass_stats", e->st);
         launch_k(pass_stats_kernel, 1, 256, 0, e->st, N);
     }
@@ -1519,8 +1704,15 @@ void engine_defer_end(qcsim_engine *e, bool raise_errors) {
         const uint64_t ntiles = (e->L + kTile - 1) / kTile;
         PROF("slice_norms", e->st);
         launch_k(slice_norms, (unsigned)((e->ns + 127) / 128), 128, 0, e->st, e->enc.tilesum.p, (int)ntiles, (int)e->ns,
-                                                                         e->slice_sq.p);
+                 e->slice_sq.p);
     }
+}
+
+// Settles a deferred run: metrics, norms, block sizes and offsets back to
+// the host, latched errors raised.
+void engine_defer_end(qcsim_engine *e, bool raise_errors, uint64_t done) {
+    e->deferred = false;
+    e->enc.fixed_W = 0;
     uint32_t ovf = 0;
     if (!e->defer_fresh) CK(cudaMemcpyAsync(&ovf, e->enc.overflow.p, 4, cudaMemcpyDeviceToHost, e->st));
     CK(cudaStreamSynchronize(e->st));
@@ -1537,7 +1729,19 @@ void engine_defer_end(qcsim_engine *e, bool raise_errors) {
     e->fallback = h.fallback;
     for (uint64_t k = 0; k < e->ns; ++k) e->sq_norm[e->s0 + k] = e->h_sq.p[k];
     e->blk_bytes_h.resize(2 * e->ns);
+    e->blk_off_h.resize(2 * e->ns);
     CK(cudaMemcpy(e->blk_bytes_h.data(), e->enc.block_bytes.p, 2 * e->ns * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(e->blk_off_h.data(), e->blk_off[e->cur].p, 2 * e->ns * 8, cudaMemcpyDeviceToHost));
+    // per-gate rows (seconds from the passes' global-timer stamps)
+    if (done) {
+        CK(cudaMemcpy(e->h_rows.p, e->dev_rows.p, (done + 1) * sizeof(GateRowDev), cudaMemcpyDeviceToHost));
+        for (uint64_t k = 0; k < done; ++k) {
+            const GateRowDev &r = e->h_rows.p[k + 1];
+            const uint64_t t_prev = e->h_rows.p[k].t_ns;
+            e->rows.push_back(GateRow{r.min_ratio, r.ratio_sum, r.calls, r.bytes, r.index_bytes,
+                                      (t_prev && r.t_ns > t_prev) ? (double)(r.t_ns - t_prev) * 1e-9 : 0.0});
+        }
+    }
     if (!raise_errors) return;
     if (h.status == kEngNumeric) {
         // the gates queued after the failing one ran on an unnormalized
@@ -1552,6 +1756,14 @@ void engine_defer_end(qcsim_engine *e, bool raise_errors) {
     }
     if (h.status == kEngDepth) raise(QCSIM_CODEC, "prefix code depth out of range");
     if (h.status == kEngOverflow || ovf) raise(QCSIM_NOMEM, "compressed arena overflow");
+}
+
+// Decode-index bytes stored next to the current blocks (common.cuh).
+uint64_t engine_index_bytes(const qcsim_engine *e) {
+    if (!e->compressed) return 0;
+    uint64_t t = 0;
+    for (uint64_t b : e->blk_bytes_h) t += index_records(e->L, b, e->log2C) * sizeof(IndexRec);
+    return t;
 }
 
 } // namespace
@@ -1837,6 +2049,8 @@ qcsim_status qcsim_engine_create(const qcsim_engine_config *cfg, qcsim_engine **
         const int world = c.world > 0 ? c.world : 1;
         const uint64_t S = 1ull << (c.num_qubits - s);
         if (c.rank < 0 || c.rank >= world || S % (uint64_t)world) raise(QCSIM_INVALID_ARGUMENT, "bad rank/world for slice count");
+        if (((S / (uint64_t)world) & (S / (uint64_t)world - 1)) != 0)
+            raise(QCSIM_INVALID_ARGUMENT, "world size must be a power of two");
         ensure_device(c.device);
         auto *e = new qcsim_engine();
         e->cfg = c;
@@ -1851,6 +2065,7 @@ qcsim_status qcsim_engine_create(const qcsim_engine_config *cfg, qcsim_engine **
         e->log2C = c.checkpoint_bits > 0 ? c.checkpoint_bits : auto_log2C(e->L);
         e->nidx = (e->L >> e->log2C) + 1;
         e->compressed = c.compression_enabled != 0;
+        e->wave = choose_wave(e);
         e->sq_norm.assign(S, 0.0);
         e->launches0 = g_launches;
         cudaError_t err = cudaStreamCreateWithFlags(&e->st, cudaStreamNonBlocking);
@@ -1860,6 +2075,7 @@ qcsim_status qcsim_engine_create(const qcsim_engine_config *cfg, qcsim_engine **
         }
         CK(cudaEventCreate(&e->ev0));
         CK(cudaEventCreate(&e->ev1));
+        CK(cudaEventCreate(&e->evg));
         *out = e;
     });
 }
@@ -1870,6 +2086,7 @@ qcsim_status qcsim_engine_destroy(qcsim_engine *e) {
         if (e->st) cudaStreamSynchronize(e->st);
         if (e->ev0) cudaEventDestroy(e->ev0);
         if (e->ev1) cudaEventDestroy(e->ev1);
+        if (e->evg) cudaEventDestroy(e->evg);
         if (e->st) cudaStreamDestroy(e->st);
         delete e;
     });
@@ -1881,12 +2098,16 @@ qcsim_status qcsim_engine_load_basis(qcsim_engine *e, uint64_t x) {
         if (x >= (1ull << e->n)) raise(QCSIM_INVALID_ARGUMENT, "basis index out of range");
         CK(cudaSetDevice(e->cfg.device));
         std::fill(e->sq_norm.begin(), e->sq_norm.end(), 0.0);
+        e->rows.clear();
         const uint64_t xs = x >> e->s;
-        if (xs < e->s0 || xs >= e->s0 + e->ns) {
-            // remote ranks own |x>; the local slices are all zero
+        if (e->compressed) {
+            engine_waves(e, 0, false, /*decode=*/false, [&](const SliceMap &map) { return BasisSrc{x, map, e->s}; });
+        } else {
+            SliceMap id;
+            id.s0 = e->s0;
+            id.nunits = (uint32_t)e->ns;
+            engine_dense(e, BasisSrc{x, id, e->s});
         }
-        BasisSrc src{x, e->s0, e->s};
-        engine_store(e, src);
         // the owner knows the only nonzero norm; keep the global view exact
         e->sq_norm[xs] = 1.0;
     });
@@ -1897,17 +2118,29 @@ qcsim_status qcsim_engine_load_amplitudes(qcsim_engine *e, const double *amps, u
         if (!e || !amps) raise(QCSIM_INVALID_ARGUMENT, "null argument");
         if (count != (1ull << e->n)) raise(QCSIM_INVALID_ARGUMENT, "amplitude count must be 2^n");
         CK(cudaSetDevice(e->cfg.device));
-        std::vector<double> planar(e->ns * 2 * e->L);
-        for (uint64_t k = 0; k < e->ns; ++k)
-            for (uint64_t i = 0; i < e->L; ++i) {
-                const uint64_t g = ((e->s0 + k) << e->s) | i;
-                planar[k * 2 * e->L + i] = amps[2 * g];
-                planar[k * 2 * e->L + e->L + i] = amps[2 * g + 1];
-            }
-        engine_tables(e);
-        CK(cudaMemcpyAsync(e->old.p, planar.data(), planar.size() * sizeof(double), cudaMemcpyHostToDevice, e->st));
-        PlanarSrc src{e->old.p, e->L};
-        engine_store(e, src);
+        e->rows.clear();
+        // the planar [slot][re|im][L] layout of local slices [k0, k0 + cnt)
+        auto upload = [&](uint64_t k0, uint64_t cnt) {
+            std::vector<double> planar(cnt * 2 * e->L);
+            for (uint64_t k = 0; k < cnt; ++k)
+                for (uint64_t i = 0; i < e->L; ++i) {
+                    const uint64_t g = ((e->s0 + k0 + k) << e->s) | i;
+                    planar[k * 2 * e->L + i] = amps[2 * g];
+                    planar[k * 2 * e->L + e->L + i] = amps[2 * g + 1];
+                }
+            e->old.ensure(cnt * 2 * e->L);
+            CK(cudaMemcpyAsync(e->old.p, planar.data(), planar.size() * sizeof(double), cudaMemcpyHostToDevice, e->st));
+            CK(cudaStreamSynchronize(e->st));
+        };
+        if (e->compressed) {
+            engine_waves(e, 0, false, /*decode=*/false, [&](const SliceMap &map) {
+                upload(map.slice_rel(0), map.nunits);
+                return PlanarSrc{e->old.p, e->L};
+            });
+        } else {
+            upload(0, e->ns);
+            engine_dense(e, PlanarSrc{e->old.p, e->L});
+        }
     });
 }
 
@@ -1918,13 +2151,14 @@ qcsim_status qcsim_engine_run(qcsim_engine *e, const qcsim_action *actions, uint
         if (!e->loaded) raise(QCSIM_INVALID_ARGUMENT, "engine has no state (load_basis / load_amplitudes first)");
         CK(cudaSetDevice(e->cfg.device));
         if (count) {
-            const bool deferred = engine_defer_begin(e);
+            const bool deferred = engine_defer_begin(e, count);
             CK(cudaEventRecord(e->ev0, e->st));
             const auto h0 = std::chrono::steady_clock::now();
             try {
                 for (uint64_t k = 0; k < count; ++k) engine_gate(e, actions[k]);
+                if (deferred) engine_defer_finish(e);
             } catch (...) {
-                if (deferred) engine_defer_end(e, false);
+                if (deferred) engine_defer_end(e, false, 0);
                 throw;
             }
             const auto h1 = std::chrono::steady_clock::now();
@@ -1935,13 +2169,13 @@ qcsim_status qcsim_engine_run(qcsim_engine *e, const qcsim_action *actions, uint
             static const bool enq_timing = std::getenv("QCSIM_ENQ_TIMING") != nullptr; // debug
             if (enq_timing) {
                 std::fprintf(stderr, "engine_run: %llu gates, host enqueue %.3f ms, device %.3f ms | per gate us: "
-                             "prologue %.1f decode %.1f encode %.1f total %.1f\n",
+                             "prologue %.1f pass %.1f total %.1f\n",
                              (unsigned long long)count, std::chrono::duration<double, std::milli>(h1 - h0).count(), ms,
-                             g_host_t[0] / count, g_host_t[1] / count, g_host_t[2] / count, g_host_t[3] / count);
+                             g_host_t[0] / count, g_host_t[2] / count, g_host_t[3] / count);
                 for (double &v : g_host_t) v = 0;
             }
             e->wall += ms * 1e-3;
-            if (deferred) engine_defer_end(e, true);
+            if (deferred) engine_defer_end(e, true, count);
         }
         if (m) {
             std::memset(m, 0, sizeof *m);
@@ -1954,10 +2188,48 @@ qcsim_status qcsim_engine_run(qcsim_engine *e, const qcsim_action *actions, uint
             m->peak_compressed_bytes = e->peak;
             m->dense_bytes = 16ull << e->n;
             m->current_compressed_bytes = e->current;
-            m->index_bytes = e->compressed ? 2 * e->ns * e->nidx * sizeof(IndexRec) : 0;
+            m->index_bytes = engine_index_bytes(e);
             m->fallback_planes = e->fallback;
             m->kernel_launches = g_launches - e->launches0;
         }
+    });
+}
+
+qcsim_status qcsim_engine_gate_metrics(qcsim_engine *e, qcsim_gate_metrics *rows, uint64_t capacity,
+                                       uint64_t *count) {
+    return guarded([&] {
+        if (!e || !count) raise(QCSIM_INVALID_ARGUMENT, "null argument");
+        *count = e->rows.size();
+        if (!rows) return;
+        if (capacity < e->rows.size()) raise(QCSIM_INVALID_ARGUMENT, "output capacity too small");
+        for (size_t k = 0; k < e->rows.size(); ++k) {
+            const GateRow &r = e->rows[k];
+            qcsim_gate_metrics &o = rows[k];
+            o.min_ratio = r.calls ? r.min_ratio : 0.0;
+            o.mean_ratio = r.calls ? r.ratio_sum / (double)r.calls : 0.0;
+            o.seconds = r.seconds;
+            o.compressed_bytes = r.bytes;
+            o.index_bytes = r.index_bytes;
+            o.compress_calls = r.calls;
+        }
+    });
+}
+
+qcsim_status qcsim_engine_info(qcsim_engine *e, qcsim_engine_info_t *info) {
+    return guarded([&] {
+        if (!e || !info) raise(QCSIM_INVALID_ARGUMENT, "null argument");
+        info->local_slices = e->ns;
+        info->wave_slices = e->wave;
+        info->waves = e->ns / e->wave;
+        info->checkpoint_bits = e->log2C;
+    });
+}
+
+qcsim_status qcsim_device_memory(uint64_t *current, uint64_t *peak, int32_t reset_peak) {
+    return guarded([&] {
+        if (current) *current = g_dev_cur;
+        if (peak) *peak = g_dev_peak;
+        if (reset_peak) g_dev_peak = g_dev_cur;
     });
 }
 
@@ -1968,17 +2240,21 @@ qcsim_status qcsim_engine_gather(qcsim_engine *e, double *amps, uint64_t capacit
             raise(QCSIM_CAPACITY, "dense materialization of " + std::to_string(e->n) + " qubits exceeds the " +
                                       std::to_string(guard) + "-qubit guard");
         if (capacity < 2 * e->ns * e->L) raise(QCSIM_INVALID_ARGUMENT, "output capacity too small");
+        if (!e->loaded) raise(QCSIM_INVALID_ARGUMENT, "engine has no state");
         CK(cudaSetDevice(e->cfg.device));
-        engine_decode_old(e, false);
-        std::vector<double> planar(e->ns * 2 * e->L);
-        CK(cudaMemcpyAsync(planar.data(), e->old.p, planar.size() * sizeof(double), cudaMemcpyDeviceToHost, e->st));
-        CK(cudaStreamSynchronize(e->st));
-        CK(cudaGetLastError());
-        for (uint64_t k = 0; k < e->ns; ++k)
-            for (uint64_t i = 0; i < e->L; ++i) {
-                amps[2 * (k * e->L + i)] = planar[k * 2 * e->L + i];
-                amps[2 * (k * e->L + i) + 1] = planar[k * 2 * e->L + e->L + i];
-            }
+        const uint64_t W = e->wave;
+        std::vector<double> planar(W * 2 * e->L);
+        for (uint64_t k0 = 0; k0 < e->ns; k0 += W) {
+            const double *src = state_range(e, k0, W);
+            CK(cudaMemcpyAsync(planar.data(), src, planar.size() * sizeof(double), cudaMemcpyDeviceToHost, e->st));
+            CK(cudaStreamSynchronize(e->st));
+            CK(cudaGetLastError());
+            for (uint64_t k = 0; k < W; ++k)
+                for (uint64_t i = 0; i < e->L; ++i) {
+                    amps[2 * ((k0 + k) * e->L + i)] = planar[k * 2 * e->L + i];
+                    amps[2 * ((k0 + k) * e->L + i) + 1] = planar[k * 2 * e->L + e->L + i];
+                }
+        }
     });
 }
 
@@ -1989,22 +2265,26 @@ qcsim_status qcsim_engine_compare(qcsim_engine *a, qcsim_engine *b, qcsim_compar
             raise(QCSIM_INVALID_ARGUMENT, "engines differ in qubits, slice size, slice range or device");
         if (!a->loaded || !b->loaded) raise(QCSIM_INVALID_ARGUMENT, "engine has no state");
         CK(cudaSetDevice(a->cfg.device));
-        engine_decode_old(a, false);
-        engine_decode_old(b, false);
-        CK(cudaStreamSynchronize(b->st));
-        CK(cudaStreamSynchronize(a->st));
         const uint64_t ntiles = (a->L + kTile - 1) / kTile;
-        const uint64_t tiles = a->ns * ntiles;
+        const uint64_t W = std::min(a->wave, b->wave);
         DBuf<double> part;
-        part.ensure(5 * tiles);
-        {
-            PROF("state_compare", a->st);
-            launch_k(state_compare, (unsigned)tiles, 256, 0, a->st, a->old.p, b->old.p, a->L, (int)a->ns, part.p);
+        part.ensure(5 * W * ntiles);
+        std::vector<double> h(5 * a->ns * ntiles);
+        for (uint64_t k0 = 0; k0 < a->ns; k0 += W) {
+            const double *pa = state_range(a, k0, W);
+            CK(cudaStreamSynchronize(a->st));
+            const double *pb = state_range(b, k0, W);
+            CK(cudaStreamSynchronize(b->st));
+            {
+                PROF("state_compare", a->st);
+                launch_k(state_compare, (unsigned)(W * ntiles), 256, 0, a->st, pa, pb, a->L, (int)W, part.p);
+            }
+            CK(cudaMemcpyAsync(h.data() + 5 * k0 * ntiles, part.p, 5 * W * ntiles * sizeof(double),
+                               cudaMemcpyDeviceToHost, a->st));
+            CK(cudaStreamSynchronize(a->st));
+            CK(cudaGetLastError());
         }
-        std::vector<double> h(5 * tiles);
-        CK(cudaMemcpyAsync(h.data(), part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, a->st));
-        CK(cudaStreamSynchronize(a->st));
-        CK(cudaGetLastError());
+        const uint64_t tiles = a->ns * ntiles;
         std::vector<double> col(tiles);
         double r[4];
         for (int q = 0; q < 4; ++q) {

@@ -124,6 +124,9 @@ class ShardedEngine:
         m.wall_seconds = float(mx.item())
         return m
 
+    def slice_norms(self):
+        return self.eng.slice_norms()
+
     def export_local_blocks(self) -> bytes:
         return self.eng.export_blocks()[0]
 

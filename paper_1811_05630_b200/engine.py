@@ -39,11 +39,12 @@ class EngineConfig:
     rank: int = 0
     world: int = 1
     checkpoint_bits: int = 0
+    wave_bytes: int = 0  # dense working-set budget of a gate pass (0 = 45% of the device)
 
     def to_c(self) -> _native.EngineConfigC:
         return _native.EngineConfigC(self.num_qubits, self.slice_bits, self.codec.to_c(),
                                      int(self.compression_enabled), self.norm_every, self.norm_drift_tolerance,
-                                     self.device, self.rank, self.world, self.checkpoint_bits, 0)
+                                     self.device, self.rank, self.world, self.checkpoint_bits, self.wave_bytes)
 
 
 @dataclass
@@ -61,13 +62,26 @@ class RunMetrics:
     index_bytes: int
     fallback_planes: int
     kernel_launches: int
+    per_gate_min_ratio: list = field(default_factory=list)  # filled by Engine.metrics()/run()
+    baseline_wall_seconds: float | None = None             # measure_overhead
+    overhead_factor: float | None = None                   # measure_overhead: wall / baseline wall
 
     @classmethod
     def from_c(cls, m: _native.RunMetricsC):
         return cls(*[getattr(m, f) for f, _ in _native.RunMetricsC._fields_])
 
+    def to_json(self, rows=None) -> dict:
+        """Metrics report: every RunMetrics field plus the
+        per-gate rows."""
+        d = {f: getattr(self, f) for f in self.__dataclass_fields__}
+        if rows is not None:
+            d["per_gate"] = [dict(gate_index=k - 1, **r) for k, r in enumerate(rows)]
+        return d
+
 
 def _actions(actions):
+    if isinstance(actions, C.Array) and actions._type_ is _native.ActionC:
+        return actions, len(actions)  # already the C layout: no copy
     if isinstance(actions, Circuit):
         actions = lower(actions)
     arr = (_native.ActionC * max(1, len(actions)))()
@@ -116,6 +130,30 @@ class Engine:
         self._ck(self.L.qcsim_engine_run(self.h, arr, n, C.byref(m)))
         return RunMetrics.from_c(m)
 
+    def full_metrics(self) -> RunMetrics:
+        """metrics() plus per_gate_min_ratio (one entry per gate pass since
+        the load)."""
+        m = self.metrics()
+        m.per_gate_min_ratio = [r["min_ratio"] for r in self.gate_metrics()[1:]]
+        return m
+
+    def write_report(self, json_path=None, csv_path=None, metrics: RunMetrics | None = None) -> dict:
+        """JSON with every RunMetrics field plus the per-gate
+        rows; CSV of (gate_index, min_ratio, mean_ratio, seconds)."""
+        import json
+        rows = self.gate_metrics()
+        m = metrics or self.full_metrics()
+        d = m.to_json(rows)
+        if json_path:
+            with open(json_path, "w") as f:
+                json.dump(d, f, indent=1)
+        if csv_path:
+            with open(csv_path, "w") as f:
+                f.write("gate_index,min_ratio,mean_ratio,seconds\n")
+                for k, r in enumerate(rows):
+                    f.write(f"{k - 1},{r['min_ratio']!r},{r['mean_ratio']!r},{r['seconds']!r}\n")
+        return d
+
     def metrics(self) -> RunMetrics:
         return self.run(())
 
@@ -138,12 +176,38 @@ class Engine:
         return {"max_abs_diff": r.max_abs_diff, "inner": complex(r.inner_re, r.inner_im), "norm_a": r.norm_a,
                 "norm_b": r.norm_b, "fidelity": r.fidelity}
 
+    def gate_metrics(self) -> list:
+        """Per-pass rows since the last load (row 0: the initial
+        compression; row k: after gate k-1): min / mean ratio, device
+        seconds, compressed and decode-index bytes."""
+        cnt = C.c_uint64()
+        self._ck(self.L.qcsim_engine_gate_metrics(self.h, None, 0, C.byref(cnt)))
+        buf = (_native.GateMetricsC * max(1, cnt.value))()
+        self._ck(self.L.qcsim_engine_gate_metrics(self.h, buf, cnt.value, C.byref(cnt)))
+        return [{"min_ratio": r.min_ratio, "mean_ratio": r.mean_ratio, "seconds": r.seconds,
+                 "bytes": r.compressed_bytes, "index_bytes": r.index_bytes, "calls": r.compress_calls}
+                for r in buf[: cnt.value]]
+
+    def info(self) -> dict:
+        """Wave layout of a gate pass (qcsim_engine_info)."""
+        i = _native.EngineInfoC()
+        self._ck(self.L.qcsim_engine_info(self.h, C.byref(i)))
+        return {"local_slices": i.local_slices, "wave_slices": i.wave_slices, "waves": i.waves,
+                "checkpoint_bits": i.checkpoint_bits}
+
     def slice_norms(self) -> np.ndarray:
         out = np.empty(self.local_slices, dtype=np.float64)
         self._ck(self.L.qcsim_engine_slice_norms(self.h, out.ctypes.data_as(_native.dp), out.size))
         return out
 
     def export_blocks(self):
+        """QCB1 blocks of this rank's planes (slice-major, re then im) as
+        bytes, plus the plane offsets."""
+        out, offs = self.export_blocks_array()
+        return out.tobytes(), offs
+
+    def export_blocks_array(self):
+        """export_blocks without the bytes copy (a uint8 numpy array)."""
         ln = C.c_uint64()
         P = 2 * self.local_slices
         offs = (C.c_uint64 * (P + 1))()
@@ -151,7 +215,7 @@ class Engine:
         out = np.empty(ln.value, dtype=np.uint8)
         self._ck(self.L.qcsim_engine_export_blocks(self.h, out.ctypes.data_as(_native.u8p), out.size,
                                                    C.byref(ln), offs, P + 1))
-        return out.tobytes(), list(offs)
+        return out, list(offs)
 
     # ---- multi-rank hooks (paper_1811_05630_b200/distributed.py drives them)
     def partner_slices_needed(self, action) -> list:
@@ -177,6 +241,34 @@ class Engine:
     def set_global_norms(self, norms):
         v = np.ascontiguousarray(norms, dtype=np.float64)
         self._ck(self.L.qcsim_engine_set_global_norms(self.h, v.ctypes.data_as(_native.dp), v.size))
+
+
+def measure_overhead(actions, config: EngineConfig, basis: int = 0) -> RunMetrics:
+    """SPEC.md:353-361 (PAPER.md:127, Fig. 2: "24x, 21x and 19x"): the
+    circuit twice on the same device, compression on (`config`) and off;
+    returns the compressed run's metrics with baseline_wall_seconds and
+    overhead_factor = wall_on / wall_off filled (device time of the gate
+    passes)."""
+    import dataclasses
+    on = Engine(config)
+    on.load_basis(basis)
+    on.run(actions)
+    m = on.full_metrics()
+    off = Engine(dataclasses.replace(config, compression_enabled=False))
+    off.load_basis(basis)
+    moff = off.run(actions)
+    on.close()
+    off.close()
+    m.baseline_wall_seconds = moff.wall_seconds
+    m.overhead_factor = m.wall_seconds / moff.wall_seconds if moff.wall_seconds > 0 else None
+    return m
+
+
+def device_memory(reset_peak: bool = False) -> dict:
+    """Device bytes held by libqcsim_b200.so: current and high-water mark."""
+    cur, peak = C.c_uint64(), C.c_uint64()
+    raise_status(_native.lib().qcsim_device_memory(C.byref(cur), C.byref(peak), int(reset_peak)), _native.lib())
+    return {"current_bytes": cur.value, "peak_bytes": peak.value}
 
 
 def kernel_launches() -> int:

@@ -93,6 +93,20 @@ int main() {
     write_state_dump(out, dump);
     const StateVector rd = read_state_dump(dump, 6);
     REQUIRE(std::fabs(fidelity(rd, out) - global_sq_norm(out) * global_sq_norm(out)) < 1e-9);
-    std::printf("api_smoke ok: fidelity %.9f, min ratio %.3f\n", f, m.min_compression_ratio);
+    // per-gate metrics, overhead factor and the report
+    REQUIRE(m.per_gate_min_ratio.size() == qft.gate_count());
+    double pmin = 1e300;
+    for (double r : m.per_gate_min_ratio) pmin = std::min(pmin, r);
+    REQUIRE(pmin >= m.min_compression_ratio);
+    const auto rows = eng->gate_metrics();
+    REQUIRE(rows.size() == qft.gate_count() + 1 && rows[0].gate_index == -1);
+    REQUIRE(rows.back().compressed_bytes > 0);
+    const RunMetrics mo = measure_overhead(qft, ec, init_basis_state(n, k, 6));
+    REQUIRE(mo.baseline_wall_seconds > 0.0 && mo.overhead_factor > 0.0);
+    const std::string js = metrics_json(mo, rows), csv = metrics_csv(rows);
+    REQUIRE(js.find("\"overhead_factor\"") != std::string::npos && js.find("\"per_gate\"") != std::string::npos);
+    REQUIRE(csv.rfind("gate_index,min_ratio,mean_ratio,seconds\n", 0) == 0);
+    std::printf("api_smoke ok: fidelity %.9f, min ratio %.3f, overhead %.2fx\n", f, m.min_compression_ratio,
+                mo.overhead_factor);
     return 0;
 }
