@@ -266,6 +266,13 @@ qcsim_status qcsim_engine_partner_blocks_needed(qcsim_engine *eng,
 qcsim_status qcsim_engine_export_slice(qcsim_engine *eng, uint64_t slice,
                                        uint8_t *out, uint64_t capacity,
                                        uint64_t *len);
+/* Batched export_slice: the (re, im) blocks of `count` owned slices,
+ * concatenated in the given order (one device gather, one copy to host);
+ * offsets[k] = start of slice k, offsets[count] = total. */
+qcsim_status qcsim_engine_export_slices(qcsim_engine *eng, const uint64_t *slices,
+                                        uint64_t count, uint8_t *out,
+                                        uint64_t capacity, uint64_t *len,
+                                        uint64_t *offsets);
 qcsim_status qcsim_engine_import_partner(qcsim_engine *eng, uint64_t slice,
                                          const uint8_t *blocks, uint64_t len);
 /* Replace the norm source with an all-gathered table of every slice's

@@ -57,16 +57,31 @@ static_assert(sizeof(IndexRec) == 40, "IndexRec layout");
 // kIdxBlockBytesPerChunk block bytes, i.e. the index is <= 40/512 = 7.8% of
 // the block.  The QCB1 bytes themselves are untouched.
 constexpr uint64_t kIdxBlockBytesPerChunk = 512;
+// (QCSIM_IDX_BPC overrides it for experiments; set once per device before
+// any kernel runs -- encoder and decoder must agree)
+__device__ uint64_t d_idx_bpc = kIdxBlockBytesPerChunk;
+inline uint64_t h_idx_bpc = kIdxBlockBytesPerChunk;
+// chunks never exceed 2^(log2Cmin + shift) elements (decode work per thread)
+constexpr int kIdxMaxChunkShift = 30; // (no cap by default)
+__device__ int d_idx_cmax_shift = kIdxMaxChunkShift;
+inline int h_idx_cmax_shift = kIdxMaxChunkShift;
 __host__ __device__ __forceinline__ int ceil_log2_u64(uint64_t v) {
     int l = 0;
     while ((1ull << l) < v) ++l;
     return l;
 }
 __host__ __device__ __forceinline__ int chunk_log2(uint64_t n, uint64_t block_bytes, int log2Cmin) {
-    const uint64_t t = block_bytes / kIdxBlockBytesPerChunk; // target chunk count
+#ifdef __CUDA_ARCH__
+    const uint64_t t = block_bytes / d_idx_bpc; // target chunk count
+    const int cmax = log2Cmin + d_idx_cmax_shift;
+#else
+    const uint64_t t = block_bytes / h_idx_bpc;
+    const int cmax = log2Cmin + h_idx_cmax_shift;
+#endif
     int lt = 0;
     while (lt < 62 && (2ull << lt) <= t) ++lt;                // floor(log2(t)), 0 for t <= 1
-    const int c = ceil_log2_u64(n) - lt;
+    int c = ceil_log2_u64(n) - lt;
+    if (c > cmax) c = cmax;
     return c > log2Cmin ? c : log2Cmin;
 }
 __host__ __device__ __forceinline__ uint64_t index_records(uint64_t n, uint64_t block_bytes, int log2Cmin) {

@@ -163,22 +163,28 @@ struct BitWindow {
     }
 };
 
-constexpr int kDecThreads = 128;             // chunks per block
+constexpr int kDecThreads = 128;             // chunks per block (one per thread)
 constexpr int kDecStageWords = 4096;         // 16 KB of stream staged per block
-constexpr int kDecWin = 16;                  // output window per chunk (C is a multiple)
-constexpr int kDecFills = 64;                // deferred constant-run fills per block
-constexpr int kDecFillMin = 4 * kDecWin;     // shortest run worth deferring
+constexpr int kDecBatch = 8;                 // value runs per lane per batch
+constexpr int kDecFills = 64;                // block-wide fills per block
+constexpr uint32_t kDecBlockFill = 4096;     // runs at least this long are filled by the whole block
 struct DecFill {
     uint64_t start;
     uint64_t len;
     double v;
 };
+struct DecRun {          // elements [previous end, end) take `v`
+    uint32_t end;
+    uint32_t pad;
+    double v;
+};
 struct DecSmem {
     uint32_t lut[1 << kLutBits];
     uint32_t sw[kDecStageWords + 4];
-    double sout[kDecThreads / 32][32][kDecWin + 1]; // per warp: 32 chunks x one window
+    DecRun runs[kDecBatch][kDecThreads];          // entry-major: a warp's lanes write adjacent entries
     DecFill fill[kDecFills];
-    uint32_t skip[kDecThreads / 32][32];           // per lane: its row holds the current window
+    uint32_t pre[kDecThreads / 32][33];  // per warp: exclusive prefix of the lanes' batch lengths
+    uint32_t base[kDecThreads / 32][32]; // per warp: the lanes' batch start elements
     uint32_t nfill;
 };
 constexpr size_t kDecSmem = sizeof(DecSmem);
@@ -186,15 +192,22 @@ constexpr size_t kDecSmem = sizeof(DecSmem);
 // One block per (plane, group of kDecThreads index chunks).  The plane's
 // chunk size follows from its block size (chunk_log2), the records come
 // from the index stored after the block in its slot; blocks past the plane's
-// chunk count exit.  The plane's 11-bit LUT and the group's stream bytes are
-// staged in shared memory; each thread then resumes from its record and
-// reproduces codec.cpp:591-626 for its chunk, kDecWin elements at a time:
-// the warp parks its 32 chunks' windows in shared memory and stores them row
-// by row (coalesced rows instead of scattered 8-byte stores).  A zero-code
-// run with the previous-value predictor is a constant fill: a lane standing
-// at a window start inside such a run hands the whole windows it covers to
-// the block (shared fill list, written coalesced by all threads at the end)
-// and the warp skips windows every lane has handed off.
+// chunk count exit.  The plane's 11-bit LUT and the group's stream words
+// are staged in shared memory.
+//
+// Decoding reproduces codec.cpp:591-626 in two alternating phases per warp:
+//  1. every lane decodes its own chunk (token by token, from its record)
+//     into up to kDecBatch *value runs* (end, value) in shared memory: a
+//     literal is a run of one element (d = p + (2eb)m, or the outlier), a
+//     RUN token of a zero code with the previous-value predictor is ONE run
+//     of the constant d (d + 0.0 == d, the first element canonicalises -0.0);
+//     other RUN tokens (nonzero code, linear predictor) emit one element per
+//     step, as the reference's serial loop does.  The FP64 work is per
+//     token, in the reference's order;
+//  2. the warp writes the runs of each of its 32 chunks in turn, 32
+//     consecutive elements per store (coalesced), each lane walking the run
+//     list with a cursor.  Runs of >= kDecBlockFill elements go to a block
+//     list written by all threads at the end.
 // N.enabled: the grid's last block runs the engine's normalization for this
 // gate pass instead (it needs only the previous pass's norms; the gate kernel
 // that applies the scale runs after this grid).
@@ -253,21 +266,20 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
     const uint64_t bit_hi = jend < nchunks ? rec_bitpos(jend) : sbytes * 8;
     const uint64_t w_hi = (bit_hi >> 5) + 3;
     const bool staged = w_hi - w_lo <= (uint64_t)kDecStageWords;
-    const uint64_t sbase0 = staged ? w_lo * 32 : 0;
     if (staged)
         for (uint64_t w = w_lo + threadIdx.x; w < w_hi; w += kDecThreads) S.sw[w - w_lo] = __ldg(stream + w);
     __syncthreads();
 
     const bool active = j < jend;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     IndexRec r{};
     if (active && j > 0) r = sidx[j - 1];
     if (j == 0) r.last_lit = rsym; // initial decoder state (codec.cpp:587-590)
     uint64_t bp = r.bitpos;
     uint32_t run_left = r.run_left;
     const uint32_t *wsrc = staged ? S.sw : stream; // the window's word source ...
-    const uint64_t wbase = staged ? sbase0 : 0;     // ... and its first bit
-    // (unstaged groups only: staged words are cheap shared-memory peeks)
+    const uint64_t wbase = staged ? w_lo * 32 : 0;  // ... and its first bit
+    const uint64_t sbase = wbase;
     BitWindow bw;
     if (active && !staged) bw.init(wsrc, bp - wbase);
     uint32_t last = r.last_lit;
@@ -276,72 +288,60 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
     const uint64_t e0 = j << log2Cp;
     const uint64_t e1 = active ? tmin<uint64_t>(e0 + C, D.L) : e0;
     double *out = D.out[pl];
-    const uint64_t sbase = staged ? w_lo * 32 : 0;
-    const uint64_t jw = j0 + (uint64_t)wid * 32; // first chunk of this warp
-    double *row = S.sout[wid][lane];
-    uint32_t *skip = S.skip[wid];
+    const int wbase_t = threadIdx.x & ~31; // first thread of this warp
 
     uint64_t i = e0;
     bool dead = !active;
-    uint64_t w0 = 0;
-    skip[lane] = 0;
-    while (true) {
-        // windows every lane has handed off (or finished) are skipped
-        uint64_t wnext = dead || i >= e1 ? C : (i - e0) & ~(uint64_t)(kDecWin - 1);
-        for (int o = 16; o > 0; o >>= 1) {
-            const uint64_t v = __shfl_xor_sync(0xffffffffu, wnext, o);
-            wnext = v < wnext ? v : wnext;
+    // value of the element at i for symbol s (codec.cpp:605-611)
+    auto value_of = [&](uint32_t s) -> double {
+        if (s == kOutlierSym) {
+            const double v = __longlong_as_double((long long)load_le(orec + 16 * ocur + 8, 8));
+            ++ocur;
+            return v;
         }
-        w0 = wnext > w0 ? wnext : w0;
-        if (w0 >= C) break;
-        const uint64_t wb = e0 + w0;
-        const uint64_t wend = tmin<uint64_t>(wb + kDecWin, e1);
-        auto emit = [&](uint32_t s) {
-            double v;
-            if (s == kOutlierSym) {
-                v = __longlong_as_double((long long)load_le(orec + 16 * ocur + 8, 8));
-                ++ocur;
-            } else {
-                double pred;
-                if (pred_kind == 0) pred = i > 0 ? d1 : 0.0;
-                else pred = i == 0 ? 0.0 : (i == 1 ? d1 : predict_linear(d1, d2));
-                const long long m = (long long)s - half;
-                v = eb == 0.0 ? pred : dadd(pred, dmul(q, (double)m));
-            }
-            row[i - wb] = v;
-            d2 = d1;
-            d1 = v;
-            ++i;
-        };
-        bool produced = false;
-        while (!dead && i >= wb && i < wend) {
+        double pred;
+        if (pred_kind == 0) pred = i > 0 ? d1 : 0.0;
+        else pred = i == 0 ? 0.0 : (i == 1 ? d1 : predict_linear(d1, d2));
+        const long long m = (long long)s - half;
+        return eb == 0.0 ? pred : dadd(pred, dmul(q, (double)m));
+    };
+    const int wid = threadIdx.x >> 5;
+    while (__any_sync(0xffffffffu, !dead && i < e1)) {
+        // ---- phase 1: up to kDecBatch value runs of this lane's chunk; a
+        // run handed to the block list ends the batch (ranges stay contiguous)
+        const uint64_t a = i;
+        uint64_t bend = i;
+        int nr = 0;
+        while (!dead && i < e1 && nr < kDecBatch) {
             if (run_left > 0) {
-                // a run of a zero code with the previous-value predictor is a
-                // constant fill (d + 0.0 == d except -0.0, which emit() keeps)
-                if (pred_kind == 0 && last == (uint32_t)half && eb != 0.0 &&
-                    bits_of(d1) != 0x8000000000000000ull && i > 0) {
-                    const uint64_t len = tmin<uint64_t>(run_left, e1 - i) & ~(uint64_t)(kDecWin - 1);
-                    if (i == wb && len >= (uint64_t)kDecFillMin) {
-                        // whole windows of the run: hand them to the block
+                const double v = value_of(last);
+                if (pred_kind == 0 && bits_of(v) == bits_of(d1) && i > 0) {
+                    // a constant run: the rest of the RUN (within the chunk)
+                    const uint64_t take = tmin<uint64_t>(run_left, e1 - i);
+                    if (take >= kDecBlockFill) {
                         const uint32_t slot = atomicAdd(&S.nfill, 1u);
                         if (slot < (uint32_t)kDecFills) {
-                            S.fill[slot] = DecFill{i, len, d1};
-                            run_left -= (uint32_t)len;
-                            i += len;
-                            d2 = d1;
-                            break; // this window produced nothing for this lane
+                            S.fill[slot] = DecFill{i, take, v};
+                            i += take;
+                            run_left -= (uint32_t)take;
+                            d2 = v;
+                            break; // bend stays before the block-filled run
                         }
                     }
-                    produced = true;
-                    const uint64_t stop = tmin<uint64_t>(wend, i + run_left);
-                    const double v = d1;
-                    run_left -= (uint32_t)(stop - i);
-                    for (; i < stop; ++i) row[i - wb] = v;
+                    i += take;
+                    run_left -= (uint32_t)take;
+                    S.runs[nr++][threadIdx.x] = DecRun{(uint32_t)i, 0u, v};
+                    bend = i;
                     d2 = v;
                     continue;
                 }
-                produced = true;
-                emit(last);
+                // one element of the run (first element of a -0.0 run, a
+                // nonzero code, the linear predictor)
+                S.runs[nr++][threadIdx.x] = DecRun{(uint32_t)(i + 1), 0u, v};
+                d2 = d1;
+                d1 = v;
+                ++i;
+                bend = i;
                 --run_left;
                 continue;
             }
@@ -393,33 +393,62 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
                     if (!staged) bw.init(wsrc, bp - wbase);
                 }
             } else {
-                produced = true;
-                emit(s);
+                const double v = value_of(s);
+                S.runs[nr++][threadIdx.x] = DecRun{(uint32_t)(i + 1), 0u, v};
+                d2 = d1;
+                d1 = v;
+                ++i;
+                bend = i;
                 last = s;
             }
         }
-        // a lane's row holds this window iff it decoded the window (a lane
-        // hands off only at a window start, before producing anything)
-        skip[lane] = produced ? 1u : 0u;
+        // ---- phase 2: the warp writes the batch's elements of all 32 lanes
+        // as one concatenated index space (consecutive k -> consecutive
+        // addresses inside a lane's range: coalesced stores)
+        const uint32_t len = (uint32_t)(bend - a);
+        uint32_t incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        S.pre[wid][lane] = incl - len;
+        S.base[wid][lane] = (uint32_t)a;
         __syncwarp();
-        // the warp's 32 chunk windows, coalesced kDecWin-element rows
-        for (int qq = lane; qq < 32 * kDecWin; qq += 32) {
-            const int rr = qq / kDecWin, col = qq % kDecWin;
-            const uint64_t jr = jw + rr;
-            const uint64_t e = (jr << log2Cp) + w0 + col;
-            if (jr < jend && skip[rr] && w0 + col < C && e < D.L) out[e] = S.sout[wid][rr][col];
+        for (uint32_t k = lane; k < total; k += 32) {
+            int rr = 0; // last lane whose range starts at or before k
+#pragma unroll
+            for (int st = 16; st >= 1; st >>= 1)
+                if (S.pre[wid][rr + st] <= k) rr += st;
+            const uint32_t e = S.base[wid][rr] + (k - S.pre[wid][rr]);
+            const int col = wbase_t + rr;
+            int c = 0;
+            while (S.runs[c][col].end <= e) ++c;
+            out[e] = S.runs[c][col].v;
         }
         __syncwarp();
-        w0 += kDecWin;
     }
     __syncthreads();
-    // deferred constant fills, coalesced by the whole block
+    // long constant runs, coalesced by the whole block
     const uint32_t nf = tmin<uint32_t>(S.nfill, (uint32_t)kDecFills);
     for (uint32_t f = 0; f < nf; ++f) {
         const DecFill F = S.fill[f];
-        double2 *o2 = reinterpret_cast<double2 *>(out + F.start); // window starts are 16-element aligned
+        uint64_t st = F.start, len = F.len;
+        if (st & 1) { // 16-byte aligned vector stores after an odd head
+            if (threadIdx.x == 0) out[st] = F.v;
+            ++st;
+            --len;
+        }
+        double4 *o4 = reinterpret_cast<double4 *>(out + st);
+        const uint64_t n4 = (st & 3) ? 0 : len / 4; // 32-byte stores when aligned
+        const double4 v4 = make_double4(F.v, F.v, F.v, F.v);
+        for (uint64_t k = threadIdx.x; k < n4; k += kDecThreads) o4[k] = v4;
+        double2 *o2 = reinterpret_cast<double2 *>(out + st + 4 * n4);
+        const uint64_t rest = len - 4 * n4;
         const double2 v2 = make_double2(F.v, F.v);
-        for (uint64_t k = threadIdx.x; k < F.len / 2; k += kDecThreads) o2[k] = v2;
+        for (uint64_t k = threadIdx.x; k < rest / 2; k += kDecThreads) o2[k] = v2;
+        if ((rest & 1) && threadIdx.x == 0) out[st + 4 * n4 + rest - 1] = F.v;
     }
 }
 

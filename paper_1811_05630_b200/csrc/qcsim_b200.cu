@@ -121,6 +121,18 @@ void ensure_device(int dev) {
         CK(cudaGetDeviceProperties(&prop, dev));
         if (prop.major != 10) raise(QCSIM_CUDA, std::string("device is not sm_100 (Blackwell): ") + prop.name);
         g_device_checked = dev;
+        static uint64_t bpc_set = 0; // per-device bitmask
+        if (const char *v = std::getenv("QCSIM_IDX_BPC"); v && !(bpc_set & (1ull << dev))) {
+            h_idx_bpc = std::max<uint64_t>(1, std::strtoull(v, nullptr, 10));
+            CK(cudaMemcpyToSymbol(d_idx_bpc, &h_idx_bpc, sizeof h_idx_bpc));
+            bpc_set |= 1ull << dev;
+        }
+        static uint64_t cmax_set = 0;
+        if (const char *v = std::getenv("QCSIM_IDX_CMAX_SHIFT"); v && !(cmax_set & (1ull << dev))) {
+            h_idx_cmax_shift = std::atoi(v);
+            CK(cudaMemcpyToSymbol(d_idx_cmax_shift, &h_idx_cmax_shift, sizeof h_idx_cmax_shift));
+            cmax_set |= 1ull << dev;
+        }
     }
 }
 
@@ -341,14 +353,35 @@ struct EncScratch {
 // enc_chain_scan counters: [0] resolve points, [1] refuted chunks redone
 // serially, [4] chunks run serially because the maps did not fit
 constexpr uint64_t kScanChainMaxPlanes = 256; // more planes fill the GPU with serial warps
-uint32_t *chain_stats() {
-    static DBuf<uint32_t> buf;
-    if (!buf.p) {
-        buf.ensure(16);
-        CK(cudaMemset(buf.p, 0, 16 * sizeof(uint32_t)));
+constexpr int kMaxDevices = 64;
+int current_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        dev = 0;
     }
-    return buf.p;
+    if (dev < 0 || dev >= kMaxDevices) raise(QCSIM_CUDA, "device ordinal beyond the library's table");
+    return dev;
 }
+// per-device counters (the buffer lives on the device that uses it)
+uint32_t *chain_stats() {
+    static DBuf<uint32_t> buf[kMaxDevices];
+    DBuf<uint32_t> &b = buf[current_device()];
+    if (!b.p) {
+        b.ensure(16);
+        CK(cudaMemset(b.p, 0, 16 * sizeof(uint32_t)));
+    }
+    return b.p;
+}
+// kernels needing more than 48 KB of dynamic shared memory: the attribute
+// is per device, set once on each
+template <class K> void set_smem_once(K kernel, size_t bytes, uint64_t *done_mask, int bit) {
+    const int dev = current_device();
+    if (done_mask[dev] & (1ull << bit)) return;
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    done_mask[dev] |= 1ull << bit;
+}
+uint64_t g_smem_set[kMaxDevices] = {};
 
 
 // Every kernel launch goes through here: Programmatic Dependent Launch lets
@@ -611,12 +644,8 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     {
         // (chain_mode / scan: chosen before enc_lattice, see chain_choice)
         static const int chain_debug = std::getenv("QCSIM_CHAIN_DEBUG") ? 1 : 0;
-        static bool attr = false;
-        if (!attr) {
-            set_smem(enc_chain, kChainSmem);
-            set_smem(enc_chain_scan, kChainScanSmem);
-            attr = true;
-        }
+        set_smem_once(enc_chain, kChainSmem, g_smem_set, 0);
+        set_smem_once(enc_chain_scan, kChainScanSmem, g_smem_set, 1);
         const bool scan = chain_scan_selected(planes);
         const int chain_mode = chain_choice();
         if (chain_mode != 1 && scan) {
@@ -950,11 +979,7 @@ void decode_batch(cudaStream_t st, DecScratch &S, const uint8_t *arena, const ui
     const uint64_t nchunks = (L + (1ull << log2C) - 1) >> log2C;
     const uint64_t groups = (nchunks + kDecThreads - 1) / kDecThreads;
     {
-        static bool attr = false;
-        if (!attr) {
-            set_smem(dec_chunks, kDecSmem);
-            attr = true;
-        }
+        set_smem_once(dec_chunks, kDecSmem, g_smem_set, 2);
         PROF("dec_chunks", st);
         NormArgs N{};
         if (norm) N = *norm;
@@ -1045,20 +1070,18 @@ struct CodecCtx {
     DBuf<double *> optrs;
     DBuf<uint64_t> offs;
 };
-thread_local CodecCtx *t_codec = nullptr;
+// one context per (thread, device): streams and buffers belong to a device
+thread_local CodecCtx *t_codec[kMaxDevices] = {};
 CodecCtx &codec_ctx() {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) {
-        cudaGetLastError();
-        dev = 0;
-    }
+    const int dev = current_device();
     ensure_device(dev);
-    if (!t_codec) {
-        t_codec = new CodecCtx();
-        t_codec->dev = dev;
-        CK(cudaStreamCreateWithFlags(&t_codec->st, cudaStreamNonBlocking));
+    CodecCtx *&c = t_codec[dev];
+    if (!c) {
+        c = new CodecCtx();
+        c->dev = dev;
+        CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
     }
-    return *t_codec;
+    return *c;
 }
 
 } // namespace
@@ -2391,6 +2414,41 @@ qcsim_status qcsim_engine_export_slice(qcsim_engine *e, uint64_t slice, uint8_t 
         CK(cudaStreamSynchronize(e->st));
         CK(cudaMemcpyAsync(out, e->arena[e->cur].p + off[0], b0, cudaMemcpyDeviceToHost, e->st));
         CK(cudaMemcpyAsync(out + b0, e->arena[e->cur].p + off[1], b1, cudaMemcpyDeviceToHost, e->st));
+        CK(cudaStreamSynchronize(e->st));
+    });
+}
+
+qcsim_status qcsim_engine_export_slices(qcsim_engine *e, const uint64_t *slices, uint64_t count, uint8_t *out,
+                                        uint64_t capacity, uint64_t *len, uint64_t *offsets) {
+    return guarded([&] {
+        if (!e || !len || (count && !slices)) raise(QCSIM_INVALID_ARGUMENT, "null argument");
+        if (!e->compressed) raise(QCSIM_INVALID_ARGUMENT, "engine is not compressed");
+        uint64_t tot = 0;
+        std::vector<uint64_t> meta(3 * 2 * count);
+        const uint64_t P = 2 * count;
+        for (uint64_t k = 0; k < count; ++k) {
+            if (slices[k] < e->s0 || slices[k] >= e->s0 + e->ns) raise(QCSIM_INVALID_ARGUMENT, "slice not owned by this rank");
+            if (offsets) offsets[k] = tot;
+            const uint64_t j = slices[k] - e->s0;
+            for (int p = 0; p < 2; ++p) {
+                meta[2 * k + p] = e->blk_off_h[2 * j + p];
+                meta[P + 2 * k + p] = tot;
+                meta[2 * P + 2 * k + p] = e->blk_bytes_h[2 * j + p];
+                tot += e->blk_bytes_h[2 * j + p];
+            }
+        }
+        if (offsets) offsets[count] = tot;
+        *len = tot;
+        if (!out || !count) return;
+        if (capacity < tot) raise(QCSIM_INVALID_ARGUMENT, "output capacity too small");
+        CK(cudaSetDevice(e->cfg.device));
+        // one gather on the device, one device->host copy
+        e->exp_meta.ensure(3 * P);
+        e->exp_buf.ensure(tot + 16);
+        CK(cudaMemcpyAsync(e->exp_meta.p, meta.data(), meta.size() * 8, cudaMemcpyHostToDevice, e->st));
+        launch_k(gather_blocks, (unsigned)P, 256, 0, e->st, (const uint8_t *)e->arena[e->cur].p,
+                 (const uint64_t *)e->exp_meta.p, (int)P, e->exp_buf.p);
+        CK(cudaMemcpyAsync(out, e->exp_buf.p, tot, cudaMemcpyDeviceToHost, e->st));
         CK(cudaStreamSynchronize(e->st));
     });
 }

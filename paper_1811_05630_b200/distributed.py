@@ -77,13 +77,23 @@ class ShardedEngine:
         if rbits == 0:
             return
         peer = self.rank ^ rbits
-        blobs = [self.eng.export_slice(self.s0 + k) for k in range(self.ns)]
-        lens = torch.tensor([len(b) for b in blobs], dtype=torch.int64, device=self.dev)
+        # the peer's partners are exactly my slices (XOR with a rank bit maps
+        # its range onto mine): one device gather + one copy for all of them
+        mine = [self.s0 + k for k in range(self.ns)]
+        if hasattr(self.eng, "export_slices"):
+            buf, offs = self.eng.export_slices(mine)
+            blob = np.asarray(buf, dtype=np.uint8)
+            lens_l = [offs[k + 1] - offs[k] for k in range(self.ns)]
+        else:  # oracle engine (CPU tests)
+            blobs = [self.eng.export_slice(j) for j in mine]
+            blob = np.frombuffer(b"".join(blobs), dtype=np.uint8)
+            lens_l = [len(b) for b in blobs]
+        lens = torch.tensor(lens_l, dtype=torch.int64, device=self.dev)
         rlens = torch.empty_like(lens)
         ops = [dist.P2POp(dist.isend, lens, peer, self.group), dist.P2POp(dist.irecv, rlens, peer, self.group)]
         for r in dist.batch_isend_irecv(ops):
             r.wait()
-        payload = torch.from_numpy(np.frombuffer(b"".join(blobs), dtype=np.uint8).copy()).to(self.dev)
+        payload = torch.from_numpy(blob.copy()).to(self.dev)
         rbuf = torch.empty(int(rlens.sum().item()), dtype=torch.uint8, device=self.dev)
         ops = [dist.P2POp(dist.isend, payload, peer, self.group), dist.P2POp(dist.irecv, rbuf, peer, self.group)]
         for r in dist.batch_isend_irecv(ops):
@@ -106,8 +116,16 @@ class ShardedEngine:
     # ------------------------------------------------------------ metrics
     def metrics(self):
         m = self.eng.run([]) if not hasattr(self.eng, "metrics") else self.eng.metrics()
+        peak = m.peak_compressed_bytes
+        if hasattr(self.eng, "gate_metrics"):
+            # global peak = max over passes of the SUM over ranks (every rank
+            # runs the same passes since its load)
+            per = torch.tensor([float(r["bytes"]) for r in self.eng.gate_metrics()], dtype=torch.float64,
+                               device=self.dev)
+            dist.all_reduce(per, op=dist.ReduceOp.SUM, group=self.group)
+            peak = int(per.max().item()) if per.numel() else 0
         t = torch.tensor([m.min_compression_ratio, m.mean_compression_ratio * m.compress_calls, m.compress_calls,
-                          m.current_compressed_bytes, m.peak_compressed_bytes, m.wall_seconds],
+                          m.current_compressed_bytes, 0.0, m.wall_seconds],
                          dtype=torch.float64, device=self.dev)
         mn = t[0:1].clone()
         dist.all_reduce(mn, op=dist.ReduceOp.MIN, group=self.group)
@@ -120,7 +138,7 @@ class ShardedEngine:
         m.mean_compression_ratio = float(sm[0].item()) / calls if calls else 0.0
         m.compress_calls = int(calls)
         m.current_compressed_bytes = int(sm[2].item())
-        m.peak_compressed_bytes = int(sm[3].item())
+        m.peak_compressed_bytes = peak if hasattr(self.eng, "gate_metrics") else int(m.peak_compressed_bytes)
         m.wall_seconds = float(mx.item())
         return m
 

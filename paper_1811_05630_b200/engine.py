@@ -234,6 +234,18 @@ class Engine:
                                                   C.byref(ln)))
         return out.tobytes()
 
+    def export_slices(self, slices) -> tuple:
+        """Blocks of several owned slices in one device gather + one copy:
+        (bytes, offsets) with offsets[k] the start of slices[k]."""
+        arr = (C.c_uint64 * max(1, len(slices)))(*slices)
+        ln = C.c_uint64()
+        offs = (C.c_uint64 * (len(slices) + 1))()
+        self._ck(self.L.qcsim_engine_export_slices(self.h, arr, len(slices), None, 0, C.byref(ln), offs))
+        out = np.empty(ln.value, dtype=np.uint8)
+        self._ck(self.L.qcsim_engine_export_slices(self.h, arr, len(slices), out.ctypes.data_as(_native.u8p),
+                                                   out.size, C.byref(ln), offs))
+        return out, list(offs)
+
     def import_partner(self, slice_index: int, data: bytes):
         b = np.frombuffer(data, dtype=np.uint8).copy()
         self._ck(self.L.qcsim_engine_import_partner(self.h, slice_index, b.ctypes.data_as(_native.u8p), b.size))

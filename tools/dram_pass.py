@@ -26,6 +26,10 @@ for (_, n), m in k.items():
                             "dram_write_bytes": m["dram__bytes_write.sum"], "gbs": round(b / d / 1e3, 1),
                             "frac_hbm": round(b / d / 1e3 / peak, 3),
                             "sm_pct": m.get("sm__throughput.avg.pct_of_peak_sustained_elapsed")})
+passes = float(sys.argv[5]) if len(sys.argv) > 5 else 1.0  # gate passes in the capture
+res["passes"] = passes
+res["dram_bytes_per_pass"] = sum(ln["dram_read_bytes"] + ln["dram_write_bytes"] for ln in res["launches"]) / passes
+res["duration_us_per_pass"] = sum(ln["duration_us"] for ln in res["launches"]) / passes
 json.dump(res, open(out, "w"), indent=1)
 tot = 0.0
 for ln in res["launches"]:
