@@ -268,6 +268,7 @@ def run_ours(args, wl, rank, world, dist):
     if world == 1 and wl["n"] <= 32 and not args.no_accuracy:
         dense = None
         try:
+            eng.trim()  # the FP64 replica needs the gate-pass scratch's room
             dense = q.Engine(q.EngineConfig(num_qubits=wl["n"], slice_bits=wl["s"], compression_enabled=False,
                                             device=dev, norm_every=wl["norm_every"]))
             dense.load_basis(wl["basis"])

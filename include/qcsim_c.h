@@ -218,6 +218,10 @@ qcsim_status qcsim_engine_gate_metrics(qcsim_engine *eng, qcsim_gate_metrics *ro
 /* Wave layout of the engine (see qcsim_engine_info_t). */
 qcsim_status qcsim_engine_info(qcsim_engine *eng, qcsim_engine_info_t *info);
 
+/* Releases the engine's gate-pass scratch (encoder buffers, decoded planes,
+ * the idle arena); the compressed state stays.  The next pass re-allocates. */
+qcsim_status qcsim_engine_trim(qcsim_engine *eng);
+
 /* Device bytes held by the library's buffers: current and the high-water
  * mark (reset to the current value when reset_peak != 0). */
 qcsim_status qcsim_device_memory(uint64_t *current, uint64_t *peak,

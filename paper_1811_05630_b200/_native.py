@@ -91,6 +91,7 @@ SIGNATURES = [
     ("qcsim_engine_gate_metrics", C.c_int, [C.c_void_p, P(GateMetricsC), C.c_uint64, u64p]),
     ("qcsim_engine_info", C.c_int, [C.c_void_p, P(EngineInfoC)]),
     ("qcsim_device_memory", C.c_int, [u64p, u64p, C.c_int32]),
+    ("qcsim_engine_trim", C.c_int, [C.c_void_p]),
 ]
 EXTRA = [("qcsim_kernel_launches", C.c_uint64, [])]
 

@@ -1245,8 +1245,9 @@ struct BasisSrc {
 
 // Slices per wave: the largest power of two whose dense working set (old
 // planes, encoder scratch, decode tables, fine index) fits the budget
-// (cfg.wave_bytes, else 45% of the device's memory; QCSIM_WAVE_SLICES
-// overrides for tests).  Grouped waves need a whole partner group (<= 4).
+// (cfg.wave_bytes, else 85% of the device memory free at creation;
+// QCSIM_WAVE_SLICES overrides for tests).  Grouped waves need a whole
+// partner group (<= 4).
 uint64_t choose_wave(const qcsim_engine *e) {
     if (!e->compressed) return e->ns;
     if (const char *v = std::getenv("QCSIM_WAVE_SLICES")) {
@@ -1256,13 +1257,13 @@ uint64_t choose_wave(const qcsim_engine *e) {
         return std::max<uint64_t>(std::min<uint64_t>(4, e->ns), p);
     }
     uint64_t budget = e->cfg.wave_bytes;
-    if (!budget) {
+    if (!budget) { // 85% of the device memory free when the engine is created
         size_t fr = 0, tot = 0;
         if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
             cudaGetLastError();
-            tot = 180ull << 30;
+            fr = 160ull << 30;
         }
-        budget = (uint64_t)(0.45 * (double)tot);
+        budget = (uint64_t)(0.85 * (double)fr);
     }
     const uint64_t L = e->L;
     const uint64_t cap = std::min<uint64_t>(L + 1, (1ull << e->cfg.codec.quant_code_bits) + 1);
@@ -1402,13 +1403,16 @@ void engine_waves(qcsim_engine *e, uint64_t hm, bool remote, bool decode, MakeSr
     for (uint64_t h = hm; h; h &= h - 1) ++gsh;
     CK(cudaEventRecord(e->evg, e->st));
     std::vector<uint64_t> nbytes(2 * e->ns), noff(2 * e->ns);
-    if (!single) { // pre-size the new arena from the current state (waves append)
+    {
+        // pre-size the new arena from the current state: a gate can grow the
+        // state (an overflow costs a grow-and-copy plus a re-pack)
         uint64_t used = 0;
-        for (uint64_t b : e->blk_bytes_h) used += b + 16;
+        for (uint64_t b : e->blk_bytes_h) used += b + 32;
         used += index_bytes_of(e, e->blk_bytes_h);
-        if (e->arena[nxt].cap < used + used / 4 + (16ull << 20)) {
+        const uint64_t want = 2 * used + (64ull << 20);
+        if (e->arena[nxt].cap < want) {
             e->arena[nxt].release();
-            e->arena[nxt].ensure(used + used / 4 + (16ull << 20));
+            e->arena[nxt].ensure(want);
         }
     }
     e->enc.arena_base = 0;
@@ -2248,6 +2252,24 @@ qcsim_status qcsim_engine_info(qcsim_engine *e, qcsim_engine_info_t *info) {
     });
 }
 
+qcsim_status qcsim_engine_trim(qcsim_engine *e) {
+    return guarded([&] {
+        if (!e) raise(QCSIM_INVALID_ARGUMENT, "null engine");
+        CK(cudaSetDevice(e->cfg.device));
+        CK(cudaStreamSynchronize(e->st));
+        e->enc.~EncScratch();
+        new (&e->enc) EncScratch();
+        e->decw.~DecScratch();
+        new (&e->decw) DecScratch();
+        e->old.release();
+        e->outptr_planes = 0;
+        e->index.release();
+        e->arena[e->cur ^ 1].release();
+        e->dec[e->cur ^ 1].~DecScratch();
+        new (&e->dec[e->cur ^ 1]) DecScratch();
+    });
+}
+
 qcsim_status qcsim_device_memory(uint64_t *current, uint64_t *peak, int32_t reset_peak) {
     return guarded([&] {
         if (current) *current = g_dev_cur;
@@ -2265,7 +2287,7 @@ qcsim_status qcsim_engine_gather(qcsim_engine *e, double *amps, uint64_t capacit
         if (capacity < 2 * e->ns * e->L) raise(QCSIM_INVALID_ARGUMENT, "output capacity too small");
         if (!e->loaded) raise(QCSIM_INVALID_ARGUMENT, "engine has no state");
         CK(cudaSetDevice(e->cfg.device));
-        const uint64_t W = e->wave;
+        const uint64_t W = std::min<uint64_t>(e->wave, std::max<uint64_t>(1, (1ull << 30) / (16 * e->L)));
         std::vector<double> planar(W * 2 * e->L);
         for (uint64_t k0 = 0; k0 < e->ns; k0 += W) {
             const double *src = state_range(e, k0, W);
@@ -2289,7 +2311,8 @@ qcsim_status qcsim_engine_compare(qcsim_engine *a, qcsim_engine *b, qcsim_compar
         if (!a->loaded || !b->loaded) raise(QCSIM_INVALID_ARGUMENT, "engine has no state");
         CK(cudaSetDevice(a->cfg.device));
         const uint64_t ntiles = (a->L + kTile - 1) / kTile;
-        const uint64_t W = std::min(a->wave, b->wave);
+        // bounded steps: the decoded planes of a step live in `old`
+        const uint64_t W = std::min<uint64_t>(std::min(a->wave, b->wave), std::max<uint64_t>(1, (1ull << 30) / (16 * a->L)));
         DBuf<double> part;
         part.ensure(5 * W * ntiles);
         std::vector<double> h(5 * a->ns * ntiles);

@@ -188,6 +188,10 @@ class Engine:
                  "bytes": r.compressed_bytes, "index_bytes": r.index_bytes, "calls": r.compress_calls}
                 for r in buf[: cnt.value]]
 
+    def trim(self):
+        """Release the gate-pass scratch (the compressed state stays)."""
+        self._ck(self.L.qcsim_engine_trim(self.h))
+
     def info(self) -> dict:
         """Wave layout of a gate pass (qcsim_engine_info)."""
         i = _native.EngineInfoC()
