@@ -49,44 +49,39 @@ struct IndexRec {
 static_assert(sizeof(IndexRec) == 40, "IndexRec layout");
 
 // Decode index stored next to its block: the block's arena
-// slot is [QCB1 block | pad to 16 | IndexRec x (chunks - 1)], the record of
-// chunk j >= 1 at position j - 1 (chunk 0 starts from the initial decoder
-// state).  The chunk size is a power of two >= 2^log2Cmin chosen from the
+// slot is [QCB1 block | pad to 16 | IndexRec x nrec].  Record k (k >= 1,
+// stored at k - 1) is the encoder's decoder state at the first fine
+// checkpoint (a multiple of 2^log2Cmin elements) whose stream position is at
+// least k * B bits, with its element index in `tok`; chunk k of the decoder
+// runs from record k to record k + 1 (chunk 0 from the initial state).  So
+// every chunk carries about B bits of tokens -- decode work is balanced by
+// tokens, not by elements, and long constant runs cost nothing.  B = 4096
+// bits, doubled until nrec fits the fine checkpoints; nrec follows from the
 // block size alone, so the encoder (which knows the exact block size before
-// packing) and any decoder agree without extra metadata: one chunk per
-// kIdxBlockBytesPerChunk block bytes, i.e. the index is <= 40/512 = 7.8% of
-// the block.  The QCB1 bytes themselves are untouched.
+// packing) and any decoder agree without extra metadata, and the index is
+// <= 40 B per 512 block bytes = 7.8% of the block.  Records past the end of
+// the stream are end markers (empty chunks).  The QCB1 bytes are untouched.
 constexpr uint64_t kIdxBlockBytesPerChunk = 512;
 // (QCSIM_IDX_BPC overrides it for experiments; set once per device before
 // any kernel runs -- encoder and decoder must agree)
 __device__ uint64_t d_idx_bpc = kIdxBlockBytesPerChunk;
 inline uint64_t h_idx_bpc = kIdxBlockBytesPerChunk;
-// chunks never exceed 2^(log2Cmin + shift) elements (decode work per thread)
-constexpr int kIdxMaxChunkShift = 30; // (no cap by default)
-__device__ int d_idx_cmax_shift = kIdxMaxChunkShift;
-inline int h_idx_cmax_shift = kIdxMaxChunkShift;
-__host__ __device__ __forceinline__ int ceil_log2_u64(uint64_t v) {
-    int l = 0;
-    while ((1ull << l) < v) ++l;
-    return l;
-}
-__host__ __device__ __forceinline__ int chunk_log2(uint64_t n, uint64_t block_bytes, int log2Cmin) {
+// log2 of the record spacing in bytes of block (record k sits at k * 8 *
+// 2^shift bits of stream)
+__host__ __device__ __forceinline__ int index_shift(uint64_t n, uint64_t block_bytes, int log2Cmin) {
 #ifdef __CUDA_ARCH__
-    const uint64_t t = block_bytes / d_idx_bpc; // target chunk count
-    const int cmax = log2Cmin + d_idx_cmax_shift;
+    const uint64_t bpc = d_idx_bpc;
 #else
-    const uint64_t t = block_bytes / h_idx_bpc;
-    const int cmax = log2Cmin + h_idx_cmax_shift;
+    const uint64_t bpc = h_idx_bpc;
 #endif
-    int lt = 0;
-    while (lt < 62 && (2ull << lt) <= t) ++lt;                // floor(log2(t)), 0 for t <= 1
-    int c = ceil_log2_u64(n) - lt;
-    if (c > cmax) c = cmax;
-    return c > log2Cmin ? c : log2Cmin;
+    const uint64_t fine = (n + (1ull << log2Cmin) - 1) >> log2Cmin; // fine checkpoints (incl. element 0)
+    int sh = 0;
+    while ((1ull << sh) < bpc) ++sh;
+    while (sh < 62 && (block_bytes >> sh) > fine - 1) ++sh;
+    return sh;
 }
 __host__ __device__ __forceinline__ uint64_t index_records(uint64_t n, uint64_t block_bytes, int log2Cmin) {
-    const int lc = chunk_log2(n, block_bytes, log2Cmin);
-    return ((n + (1ull << lc) - 1) >> lc) - 1;
+    return block_bytes >> index_shift(n, block_bytes, log2Cmin);
 }
 // byte offset of the index records of the block at `blk_off` (slot-relative
 // arithmetic: slots start 16-byte aligned)

@@ -33,7 +33,7 @@ struct DecPlanes {
     const uint64_t *blk_off;   // [plane] block start in the arena (its decode index follows it)
     double *const *out;        // [plane] output plane
     uint64_t L;
-    int log2C;                 // finest index chunk (chunk_log2, common.cuh)
+    int log2C;                 // fine checkpoint spacing (index_records, common.cuh)
 };
 
 __device__ __forceinline__ uint64_t load_le(const uint8_t *p, int bytes) {
@@ -168,6 +168,7 @@ constexpr int kDecStageWords = 4096;         // 16 KB of stream staged per block
 constexpr int kDecBatch = 8;                 // value runs per lane per batch
 constexpr int kDecFills = 64;                // block-wide fills per block
 constexpr uint32_t kDecBlockFill = 4096;     // runs at least this long are filled by the whole block
+constexpr uint32_t kDecWarpRun = 32;         // runs at least this long are written by the whole warp
 struct DecFill {
     uint64_t start;
     uint64_t len;
@@ -183,14 +184,12 @@ struct DecSmem {
     uint32_t sw[kDecStageWords + 4];
     DecRun runs[kDecBatch][kDecThreads];          // entry-major: a warp's lanes write adjacent entries
     DecFill fill[kDecFills];
-    uint32_t pre[kDecThreads / 32][33];  // per warp: exclusive prefix of the lanes' batch lengths
-    uint32_t base[kDecThreads / 32][32]; // per warp: the lanes' batch start elements
     uint32_t nfill;
 };
 constexpr size_t kDecSmem = sizeof(DecSmem);
 
 // One block per (plane, group of kDecThreads index chunks).  The plane's
-// chunk size follows from its block size (chunk_log2), the records come
+// chunk count follows from its block size (index_records), the records come
 // from the index stored after the block in its slot; blocks past the plane's
 // chunk count exit.  The plane's 11-bit LUT and the group's stream words
 // are staged in shared memory.
@@ -219,16 +218,14 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
     }
     extern __shared__ __align__(16) unsigned char dec_raw[];
     DecSmem &S = *reinterpret_cast<DecSmem *>(dec_raw);
-    const uint64_t nchunks_max = (D.L + (1ull << D.log2C) - 1) >> D.log2C;
+    const uint64_t nchunks_max = (D.L + (1ull << D.log2C) - 1) >> D.log2C; // >= records + 1
     const uint32_t groups = (uint32_t)((nchunks_max + kDecThreads - 1) / kDecThreads);
     const int pl = (int)(blockIdx.x / groups);
     if (pl >= planes) return;
     const uint8_t *blk = D.arena + D.blk_off[pl];
     const uint64_t payload = load_le(blk + 32, 8);
     const uint64_t bbytes = kHeaderBytes + payload;
-    const int log2Cp = chunk_log2(D.L, bbytes, D.log2C);
-    const uint64_t C = 1ull << log2Cp;
-    const uint64_t nchunks = (D.L + C - 1) >> log2Cp;
+    const uint64_t nchunks = index_records(D.L, bbytes, D.log2C) + 1;
     const uint64_t j0 = (uint64_t)(blockIdx.x % groups) * kDecThreads;
     if (j0 >= nchunks) return;
     const uint64_t j = j0 + threadIdx.x;
@@ -280,13 +277,16 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
     const uint32_t *wsrc = staged ? S.sw : stream; // the window's word source ...
     const uint64_t wbase = staged ? w_lo * 32 : 0;  // ... and its first bit
     const uint64_t sbase = wbase;
+    // the lane's next bits in a register window (refilled one 32-bit word at
+    // a time from the staged words or the stream): one LUT probe per token
     BitWindow bw;
-    if (active && !staged) bw.init(wsrc, bp - wbase);
+    if (active) bw.init(wsrc, bp - wbase);
     uint32_t last = r.last_lit;
     uint64_t ocur = r.ocur;
     double d1 = r.dprev, d2 = r.dprev2;
-    const uint64_t e0 = j << log2Cp;
-    const uint64_t e1 = active ? tmin<uint64_t>(e0 + C, D.L) : e0;
+    // chunk j: from record j to record j + 1 (element indices in `tok`)
+    const uint64_t e0 = j == 0 ? 0 : (uint64_t)r.tok;
+    const uint64_t e1 = !active ? e0 : (j + 1 < nchunks ? (uint64_t)sidx[j].tok : D.L);
     double *out = D.out[pl];
     const int wbase_t = threadIdx.x & ~31; // first thread of this warp
 
@@ -305,12 +305,10 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
         const long long m = (long long)s - half;
         return eb == 0.0 ? pred : dadd(pred, dmul(q, (double)m));
     };
-    const int wid = threadIdx.x >> 5;
     while (__any_sync(0xffffffffu, !dead && i < e1)) {
         // ---- phase 1: up to kDecBatch value runs of this lane's chunk; a
         // run handed to the block list ends the batch (ranges stay contiguous)
         const uint64_t a = i;
-        uint64_t bend = i;
         int nr = 0;
         while (!dead && i < e1 && nr < kDecBatch) {
             if (run_left > 0) {
@@ -325,13 +323,12 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
                             i += take;
                             run_left -= (uint32_t)take;
                             d2 = v;
-                            break; // bend stays before the block-filled run
+                            break; // the batch ends before the block-filled run
                         }
                     }
                     i += take;
                     run_left -= (uint32_t)take;
                     S.runs[nr++][threadIdx.x] = DecRun{(uint32_t)i, 0u, v};
-                    bend = i;
                     d2 = v;
                     continue;
                 }
@@ -341,22 +338,21 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
                 d2 = d1;
                 d1 = v;
                 ++i;
-                bend = i;
                 --run_left;
                 continue;
             }
-            const uint64_t wtop = staged ? peek64<true>(S.sw, bp - sbase) : bw.acc;
+            const uint64_t wtop = bw.acc;
             const uint32_t le = S.lut[wtop >> (64 - kLutBits)];
             uint32_t s, l;
             if (le & 63) {
                 l = le & 63;
                 s = le >> 6;
-                if (!staged) bw.skip((int)l);
+                bw.skip((int)l);
             } else {
                 // a code longer than the LUT: from the window when it holds
-                // maxlen bits, else from the stream (then the window restarts)
-                const bool inwin = staged || (int)maxlen <= bw.n;
-                const uint64_t w = inwin ? wtop : peek64<false>(stream, bp);
+                // maxlen bits, else from the words (then the window restarts)
+                const bool inwin = (int)maxlen <= bw.n;
+                const uint64_t w = inwin ? wtop : (staged ? peek64<true>(S.sw, bp - sbase) : peek64<false>(stream, bp));
                 s = 0;
                 l = 0;
                 for (uint32_t ll = kLutBits + 1; ll <= maxlen; ++ll) {
@@ -372,16 +368,14 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
                     dead = true;
                     break;
                 }
-                if (!staged) {
-                    if (inwin) bw.skip((int)l);
-                    else bw.init(wsrc, bp + l - wbase);
-                }
+                if (inwin) bw.skip((int)l);
+                else bw.init(wsrc, bp + l - wbase);
             }
             bp += l;
             if (s == rsym) {
                 // Elias gamma: z zeros, then the value in z + 1 bits
-                const int z = staged ? 64 : __clzll((long long)bw.acc);
-                if (!staged && 2 * z + 1 <= bw.n) {
+                const int z = __clzll((long long)bw.acc);
+                if (2 * z + 1 <= bw.n) {
                     run_left = (uint32_t)(bw.acc >> (64 - (2 * z + 1)));
                     bw.skip(2 * z + 1);
                     bp += 2 * z + 1;
@@ -390,7 +384,7 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
                     const int zz = __clzll((long long)g);
                     run_left = (uint32_t)(g >> (64 - (2 * zz + 1)));
                     bp += 2 * zz + 1;
-                    if (!staged) bw.init(wsrc, bp - wbase);
+                    bw.init(wsrc, bp - wbase);
                 }
             } else {
                 const double v = value_of(s);
@@ -398,34 +392,41 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
                 d2 = d1;
                 d1 = v;
                 ++i;
-                bend = i;
                 last = s;
             }
         }
-        // ---- phase 2: the warp writes the batch's elements of all 32 lanes
-        // as one concatenated index space (consecutive k -> consecutive
-        // addresses inside a lane's range: coalesced stores)
-        const uint32_t len = (uint32_t)(bend - a);
-        uint32_t incl = len;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
+        // ---- phase 2: runs shorter than kDecWarpRun elements are written by
+        // their own lane (a few contiguous stores); longer ones by the whole
+        // warp, 32 consecutive elements per store (coalesced)
+        uint32_t longmask = 0; // this lane's runs of >= kDecWarpRun elements
+        {
+            uint64_t p0 = a;
+            for (int c = 0; c < nr; ++c) {
+                const DecRun R = S.runs[c][threadIdx.x];
+                const uint64_t p1 = R.end;
+                if (p1 - p0 >= kDecWarpRun) {
+                    longmask |= 1u << c;
+                } else {
+                    for (uint64_t e = p0; e < p1; ++e) out[e] = R.v;
+                }
+                p0 = p1;
+            }
         }
-        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        S.pre[wid][lane] = incl - len;
-        S.base[wid][lane] = (uint32_t)a;
-        __syncwarp();
-        for (uint32_t k = lane; k < total; k += 32) {
-            int rr = 0; // last lane whose range starts at or before k
-#pragma unroll
-            for (int st = 16; st >= 1; st >>= 1)
-                if (S.pre[wid][rr + st] <= k) rr += st;
-            const uint32_t e = S.base[wid][rr] + (k - S.pre[wid][rr]);
+        unsigned lanes = __ballot_sync(0xffffffffu, longmask != 0);
+        while (lanes) {
+            const int rr = __ffs(lanes) - 1;
+            lanes &= lanes - 1;
+            uint32_t lm = __shfl_sync(0xffffffffu, longmask, rr);
+            const uint64_t ra = __shfl_sync(0xffffffffu, a, rr);
             const int col = wbase_t + rr;
-            int c = 0;
-            while (S.runs[c][col].end <= e) ++c;
-            out[e] = S.runs[c][col].v;
+            while (lm) {
+                const int c = __ffs(lm) - 1;
+                lm &= lm - 1;
+                const uint64_t p0 = c ? S.runs[c - 1][col].end : ra;
+                const uint64_t p1 = S.runs[c][col].end;
+                const double v = S.runs[c][col].v;
+                for (uint64_t e = p0 + (uint64_t)lane; e < p1; e += 32) out[e] = v;
+            }
         }
         __syncwarp();
     }

@@ -41,7 +41,7 @@ struct CodeBook {
     uint64_t cap;
     int qb;
     uint64_t L;                // plane length
-    int log2C;                 // finest decode-index chunk (the slot keeps every 2^(chunk_log2 - log2C)-th)
+    int log2C;                 // fine checkpoint spacing (the slot keeps a subset, index_select)
     DecTables dec;             // optional: decode tables of the new blocks
     uint8_t *zero_arena = nullptr; // fixed slots (plane p at p * zero_W): zero the plane's slot for the packer
     uint64_t zero_W = 0;
@@ -688,19 +688,7 @@ __device__ __forceinline__ void pack_write_item(const PackArgs &A, int planes, i
     const uint64_t nidx = (A.L >> A.log2C) + 1;
     const uint32_t nchunks_idx = (uint32_t)((A.L + (1ull << A.log2C) - 1) >> A.log2C);
     IndexRec *idx = A.index + pl * nidx;
-    // the slot keeps every `keep`-th fine record (chunk_log2, common.cuh)
-    const uint64_t bbytes = kHeaderBytes + 4 + 5ull * n + (bits + 7) / 8 + 16ull * nout;
-    const uint32_t keep_sh = (uint32_t)(chunk_log2(A.L, bbytes, A.log2C) - A.log2C);
-    IndexRec *sidx = reinterpret_cast<IndexRec *>(A.arena + index_offset(off, bbytes));
-    auto put_rec = [&](uint32_t j, uint64_t bitpos) {
-        idx[j].bitpos = bitpos;
-        if ((j & ((1u << keep_sh) - 1)) == 0) {
-            IndexRec r = idx[j];
-            r.bitpos = bitpos;
-            r.tok = 0;
-            sidx[(j >> keep_sh) - 1] = r;
-        }
-    };
+    auto put_rec = [&](uint32_t j, uint64_t bitpos) { idx[j].bitpos = bitpos; };
 
     if (c == 0) {
         const uint64_t payload = 4 + 5ull * n + sbytes + 16ull * nout;
@@ -857,6 +845,51 @@ __global__ void __launch_bounds__(256) pack_count(PackArgs A, int planes, int nc
         __syncthreads();
     }
 }
+// The slot's decode index (common.cuh): record k = the first fine
+// checkpoint at or past k * B stream bits.  One thread per fine checkpoint j
+// writes the records k with bitpos(j - 1) < k * B <= bitpos(j); the last one
+// also writes the end markers.  After pack_write (bit positions final).
+__global__ void __launch_bounds__(256) index_select(PackArgs A, int planes) {
+    pdl_begin();
+    const uint64_t nfine = (A.L + (1ull << A.log2C) - 1) >> A.log2C;
+    const uint32_t per = (uint32_t)((nfine + 255) / 256);
+    const int pl = blockIdx.x / per;
+    if (pl >= planes) return;
+    const uint64_t j = (uint64_t)(blockIdx.x % per) * 256 + threadIdx.x;
+    if (j >= nfine) return;
+    if (A.slot_off[A.planes_total] + 64 > A.arena_cap) return; // arena overflow: nothing was packed
+    const uint32_t n = A.nsym[pl];
+    const uint64_t bits = A.stream_bits[pl];
+    const uint64_t nout = A.ocount[pl];
+    const uint64_t bbytes = kHeaderBytes + 4 + 5ull * n + (bits + 7) / 8 + 16ull * nout;
+    const int sh = index_shift(A.L, bbytes, A.log2C);
+    const uint64_t nrec = bbytes >> sh;
+    if (!nrec) return;
+    const uint64_t B = 8ull << sh; // bits per record
+    const uint64_t nidx = (A.L >> A.log2C) + 1;
+    const IndexRec *fine = A.index + (uint64_t)pl * nidx;
+    const uint64_t pre = kHeaderBytes + 4 + 5ull * n;
+    const uint64_t off = A.slot_off[pl] + ((16 - (pre & 15)) & 15);
+    IndexRec *sidx = reinterpret_cast<IndexRec *>(A.arena + index_offset(off, bbytes));
+    const uint64_t bj = j == 0 ? 0 : fine[j].bitpos;
+    const uint64_t bprev = j == 0 ? 0 : (j == 1 ? 0 : fine[j - 1].bitpos);
+    // k in (bprev / B, bj / B]  (j = 0: k = 0 only, not stored)
+    uint64_t k0 = j == 0 ? 1 : bprev / B + 1, k1 = j == 0 ? 0 : bj / B;
+    if (j > 0 && bprev == bj) k1 = k0 - 1; // no new multiple crossed
+    if (k1 > nrec) k1 = nrec;
+    if (j > 0) {
+        IndexRec r = fine[j];
+        r.tok = (uint32_t)(j << A.log2C);
+        for (uint64_t k = k0; k <= k1; ++k) sidx[k - 1] = r;
+    }
+    if (j == nfine - 1) { // records past the last checkpoint: end markers
+        IndexRec e{};
+        e.bitpos = bits;
+        e.tok = (uint32_t)A.L;
+        for (uint64_t k = (j == 0 ? 1 : tmax<uint64_t>(k1 + 1, k0)); k <= nrec; ++k) sidx[k - 1] = e;
+    }
+}
+
 __global__ void __launch_bounds__(256) pack_write(PackArgs A, int planes, int nck, int K, const int32_t *coff,
                                                   const int32_t *cbits) {
     pdl_begin();

@@ -127,12 +127,7 @@ void ensure_device(int dev) {
             CK(cudaMemcpyToSymbol(d_idx_bpc, &h_idx_bpc, sizeof h_idx_bpc));
             bpc_set |= 1ull << dev;
         }
-        static uint64_t cmax_set = 0;
-        if (const char *v = std::getenv("QCSIM_IDX_CMAX_SHIFT"); v && !(cmax_set & (1ull << dev))) {
-            h_idx_cmax_shift = std::atoi(v);
-            CK(cudaMemcpyToSymbol(d_idx_cmax_shift, &h_idx_cmax_shift, sizeof h_idx_cmax_shift));
-            cmax_set |= 1ull << dev;
-        }
+
     }
 }
 
@@ -474,6 +469,11 @@ void launch_pack(cudaStream_t st, EncScratch &S, DBuf<uint8_t> &arena, bool coun
     {
         PROF("pack_write", st);
         launch_k(pack_write, grid, 256, 0, st, P, (int)S.planes, nck, K, S.t_coff.p, S.t_cbits.p);
+    }
+    if (P.index) {
+        const uint64_t nfine = (P.L + (1ull << P.log2C) - 1) >> P.log2C;
+        PROF("index_select", st);
+        launch_k(index_select, (unsigned)(S.planes * ((nfine + 255) / 256)), 256, 0, st, P, (int)S.planes);
     }
 }
 

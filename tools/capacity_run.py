@@ -2,7 +2,7 @@
 VERDICT r1 item 3): a state far larger than the dense working set the
 engine holds, processed in waves of slices.
 
-    python tools/capacity_run.py qft32 [GATES]      # 2^32 amplitudes, 64 GiB dense
+    python tools/capacity_run.py qft32 [GATES] [EB]  # 2^32 amplitudes, 64 GiB dense
     python tools/capacity_run.py grover38 [GATES]   # 2^38 amplitudes, 4 TiB dense
 
 Prints one JSON line: geometry, waves, per-gate device seconds, peak device
@@ -24,7 +24,7 @@ import paper_1811_05630_b200 as q  # noqa: E402
 
 name = sys.argv[1]
 ngates = sys.argv[2] if len(sys.argv) > 2 else "4"
-wl = bench.workload(name)
+wl = bench.workload(name, 0, float(sys.argv[3]) if len(sys.argv) > 3 else None)
 n, s = wl["n"], wl["s"]
 acts = wl["setup"] + [a for k in range(wl["nsteps"]) for a in wl["steps"](k)]
 if ngates != "all":
