@@ -277,6 +277,23 @@ qcsim_status qcsim_engine_export_slices(qcsim_engine *eng, const uint64_t *slice
                                         uint64_t count, uint8_t *out,
                                         uint64_t capacity, uint64_t *len,
                                         uint64_t *offsets);
+/* Device-direct exchange (NCCL/P2P on device buffers, no host staging):
+ * export_slices_device gathers the (re, im) blocks of owned slices into a
+ * caller-owned DEVICE buffer (out = NULL: query `*len`); plane_offsets (host,
+ * 2*count+1 entries) receives each plane's start.  import_partners_device
+ * registers partner slices held in a device buffer (same layout) for the
+ * next run(); the buffer must stay valid until run() returns.  Imported
+ * blocks are validated on the device (from_bytes + decoder checks). */
+qcsim_status qcsim_engine_export_slices_device(qcsim_engine *eng,
+                                               const uint64_t *slices,
+                                               uint64_t count, void *out,
+                                               uint64_t capacity, uint64_t *len,
+                                               uint64_t *plane_offsets);
+qcsim_status qcsim_engine_import_partners_device(qcsim_engine *eng,
+                                                 const uint64_t *slices,
+                                                 uint64_t count,
+                                                 const void *blocks,
+                                                 const uint64_t *plane_offsets);
 qcsim_status qcsim_engine_import_partner(qcsim_engine *eng, uint64_t slice,
                                          const uint8_t *blocks, uint64_t len);
 /* Replace the norm source with an all-gathered table of every slice's

@@ -87,6 +87,9 @@ SIGNATURES = [
     ("qcsim_engine_export_slice", C.c_int, [C.c_void_p, C.c_uint64, u8p, C.c_uint64, u64p]),
     ("qcsim_engine_import_partner", C.c_int, [C.c_void_p, C.c_uint64, u8p, C.c_uint64]),
     ("qcsim_engine_export_slices", C.c_int, [C.c_void_p, u64p, C.c_uint64, u8p, C.c_uint64, u64p, u64p]),
+    ("qcsim_engine_export_slices_device", C.c_int, [C.c_void_p, u64p, C.c_uint64, C.c_void_p, C.c_uint64, u64p,
+                                                    u64p]),
+    ("qcsim_engine_import_partners_device", C.c_int, [C.c_void_p, u64p, C.c_uint64, C.c_void_p, u64p]),
     ("qcsim_engine_set_global_norms", C.c_int, [C.c_void_p, dp, C.c_uint64]),
     ("qcsim_engine_gate_metrics", C.c_int, [C.c_void_p, P(GateMetricsC), C.c_uint64, u64p]),
     ("qcsim_engine_info", C.c_int, [C.c_void_p, P(EngineInfoC)]),

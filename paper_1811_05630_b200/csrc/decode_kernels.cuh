@@ -474,6 +474,19 @@ enum DecErr : uint32_t {
     kDecOutUnused,        // "unused trailing outliers"
     kDecStreamLen,        // "code stream length mismatch"
     kDecNoMem,            // scratch too small
+    // header checks (from_bytes, codec.cpp:366-408) for device-resident
+    // blocks whose headers the host never saw (engine partner imports)
+    kDecHdrTrunc,         // "block header truncated"
+    kDecMagic,            // "bad block magic"
+    kDecVersion,          // "unsupported block version"
+    kDecModeByte,         // "bad codec mode byte"
+    kDecPredByte,         // "bad predictor byte"
+    kDecQbRange,          // "quant_code_bits out of range"
+    kDecCount0,           // "element_count must be at least 1"
+    kDecOutCount,         // "outlier_count exceeds element_count"
+    kDecEbBad,            // "bad effective_abs_bound"
+    kDecPayTrunc,         // "block payload truncated"
+    kDecWrongLen,         // element_count differs from the destination plane
 };
 
 struct ValArgs {
@@ -485,6 +498,8 @@ struct ValArgs {
     uint32_t *ssym;            // [plane][cap]
     uint8_t *slen;             // [plane][cap]
     uint64_t cap;
+    const uint64_t *avail = nullptr; // [plane] bytes available: check the header on the device
+    uint64_t n_expected = 0;         // != 0: element_count must equal it
 };
 
 struct ByteBits {
@@ -506,6 +521,23 @@ __global__ void dec_validate(ValArgs A, int planes) {
     const int pl = blockIdx.x * blockDim.x + threadIdx.x;
     if (pl >= planes) return;
     const uint8_t *blk = A.blocks + A.blk_off[pl];
+    auto fail = [&](uint32_t e) { A.err[pl] = e; };
+    if (A.avail) { // CompressedBlock::from_bytes checks, in the reference's order
+        const uint64_t len = A.avail[pl];
+        if (len < kHeaderBytes) return fail(kDecHdrTrunc);
+        if (blk[0] != 'Q' || blk[1] != 'C' || blk[2] != 'B' || blk[3] != '1') return fail(kDecMagic);
+        if (blk[4] != 1) return fail(kDecVersion);
+        if (blk[5] > 2) return fail(kDecModeByte);
+        if (blk[6] > 1) return fail(kDecPredByte);
+        if (blk[7] < 4 || blk[7] > 24) return fail(kDecQbRange);
+        const uint64_t hn = load_le(blk + 8, 8), ho = load_le(blk + 24, 8), hp = load_le(blk + 32, 8);
+        const double heb = __longlong_as_double((long long)load_le(blk + 16, 8));
+        if (hn == 0) return fail(kDecCount0);
+        if (ho > hn) return fail(kDecOutCount);
+        if (!(heb >= 0.0) || !isfinite(heb)) return fail(kDecEbBad);
+        if (hp > len - kHeaderBytes) return fail(kDecPayTrunc);
+        if (A.n_expected && hn != A.n_expected) return fail(kDecWrongLen);
+    }
     const uint8_t pred_kind = blk[6];
     const int qb = blk[7];
     const uint64_t n = load_le(blk + 8, 8);
@@ -517,7 +549,6 @@ __global__ void dec_validate(ValArgs A, int planes) {
     const uint32_t rsym = 1u << qb;
     const uint8_t *pl_ = blk + kHeaderBytes;
     double *out = A.out[pl];
-    auto fail = [&](uint32_t e) { A.err[pl] = e; };
     if (plen < 4) return fail(kDecPayloadSmall);
     const uint32_t tc = (uint32_t)load_le(pl_, 4);
     const uint64_t table_bytes = 4 + (uint64_t)tc * 5;

@@ -6,6 +6,7 @@
 // fallback: every compute path below launches the kernels in *_kernels.cuh;
 // without a CUDA device every entry point fails with QCSIM_CUDA.
 #include <algorithm>
+#include <array>
 #include <cfloat>
 #include <cmath>
 #include <chrono>
@@ -1042,6 +1043,17 @@ const char *dec_message(uint32_t e) {
     case kDecOutPos: return "outlier position mismatch";
     case kDecOutUnused: return "unused trailing outliers";
     case kDecStreamLen: return "code stream length mismatch";
+    case kDecHdrTrunc: return "block header truncated";
+    case kDecMagic: return "bad block magic";
+    case kDecVersion: return "unsupported block version";
+    case kDecModeByte: return "bad codec mode byte";
+    case kDecPredByte: return "bad predictor byte";
+    case kDecQbRange: return "quant_code_bits out of range";
+    case kDecCount0: return "element_count must be at least 1";
+    case kDecOutCount: return "outlier_count exceeds element_count";
+    case kDecEbBad: return "bad effective_abs_bound";
+    case kDecPayTrunc: return "block payload truncated";
+    case kDecWrongLen: return "partner block length does not match the slice";
     default: return "decoder scratch exhausted";
     }
 }
@@ -1130,6 +1142,11 @@ struct qcsim_engine {
     DBuf<double *> imp_ptrs;
     // partner slices imported from other ranks: slice -> QCB1 bytes
     std::vector<std::pair<uint64_t, std::vector<uint8_t>>> imported;
+    // ... or resident in a caller-owned device buffer (import_partners_device):
+    // slice -> (re offset, im offset, re length, im length)
+    const uint8_t *dev_imp = nullptr;
+    std::unordered_map<uint64_t, std::array<uint64_t, 4>> dev_imp_at;
+    DBuf<uint64_t> dev_imp_meta; // [plane offsets | available lengths] of a batch
     std::vector<double> sq_norm; // all S slices (global view)
     EncScratch enc;
     DecScratch dec[2]; // decode tables of arena[0/1], written by the encoder (single-batch passes)
@@ -1290,6 +1307,51 @@ void ensure_outptrs(qcsim_engine *e, uint64_t planes) {
 // the validating decoder into planes old[first_plane + 2u + p].
 void decode_imports(qcsim_engine *e, const SliceMap &map, uint64_t u0, uint64_t cnt, uint64_t first_plane) {
     if (!cnt) return;
+    if (e->dev_imp) {
+        // device-resident partner blocks: no host staging; from_bytes checks
+        // run on the device with the validating decoder
+        std::vector<uint64_t> meta(4 * cnt);
+        for (uint64_t u = u0; u < u0 + cnt; ++u) {
+            const uint64_t pj = (e->s0 + map.slice_rel((uint32_t)u)) ^ map.hm;
+            auto it = e->dev_imp_at.find(pj);
+            if (it == e->dev_imp_at.end())
+                raise(QCSIM_INVALID_ARGUMENT,
+                      "partner slice " + std::to_string(pj) + " not imported (multi-rank exchange missing)");
+            const uint64_t k = u - u0;
+            meta[2 * k] = it->second[0];
+            meta[2 * k + 1] = it->second[1];
+            meta[2 * cnt + 2 * k] = it->second[2];
+            meta[2 * cnt + 2 * k + 1] = it->second[3];
+        }
+        e->dev_imp_meta.ensure(4 * cnt);
+        CK(cudaMemcpyAsync(e->dev_imp_meta.p, meta.data(), meta.size() * 8, cudaMemcpyHostToDevice, e->st));
+        std::vector<double *> ptrs(2 * cnt);
+        for (uint64_t k = 0; k < 2 * cnt; ++k) ptrs[k] = e->old.p + (first_plane + k) * e->L;
+        e->imp_ptrs.ensure(ptrs.size());
+        CK(cudaMemcpyAsync(e->imp_ptrs.p, ptrs.data(), ptrs.size() * sizeof(double *), cudaMemcpyHostToDevice, e->st));
+        const uint64_t vcap = std::min<uint64_t>(e->L + 1, (1ull << e->cfg.codec.quant_code_bits) + 1);
+        e->val.ensure(2 * cnt, vcap);
+        ValArgs V;
+        V.blocks = e->dev_imp;
+        V.blk_off = e->dev_imp_meta.p;
+        V.avail = e->dev_imp_meta.p + 2 * cnt;
+        V.n_expected = e->L;
+        V.out = e->imp_ptrs.p;
+        V.err = e->val.err.p;
+        V.ssym = e->val.ssym.p;
+        V.slen = e->val.slen.p;
+        V.cap = vcap;
+        {
+            PROF("dec_validate", e->st);
+            launch_k(dec_validate, (unsigned)((2 * cnt + 31) / 32), 32, 0, e->st, V, (int)(2 * cnt));
+        }
+        std::vector<uint32_t> errs(2 * cnt);
+        CK(cudaMemcpyAsync(errs.data(), e->val.err.p, errs.size() * 4, cudaMemcpyDeviceToHost, e->st));
+        CK(cudaStreamSynchronize(e->st));
+        for (uint32_t x : errs)
+            if (x) raise(QCSIM_CODEC, dec_message(x));
+        return;
+    }
     std::unordered_map<uint64_t, size_t> where;
     for (size_t m = 0; m < e->imported.size(); ++m) where[e->imported[m].first] = m;
     std::vector<uint8_t> all;
@@ -1409,7 +1471,7 @@ void engine_waves(qcsim_engine *e, uint64_t hm, bool remote, bool decode, MakeSr
         uint64_t used = 0;
         for (uint64_t b : e->blk_bytes_h) used += b + 32;
         used += index_bytes_of(e, e->blk_bytes_h);
-        const uint64_t want = 2 * used + (64ull << 20);
+        const uint64_t want = used + used / 4 + (64ull << 20);
         if (e->arena[nxt].cap < want) {
             e->arena[nxt].release();
             e->arena[nxt].ensure(want);
@@ -1548,6 +1610,21 @@ void engine_deferred_pass(qcsim_engine *e, const GateSrc &g0) {
     e->cur = nxt;
 }
 
+// Frees the gate-pass scratch (encoder buffers, parsed decode tables,
+// decoded planes, fine index, idle arena); the compressed state stays.
+void engine_release_scratch(qcsim_engine *e) {
+    e->enc.~EncScratch();
+    new (&e->enc) EncScratch();
+    e->decw.~DecScratch();
+    new (&e->decw) DecScratch();
+    e->old.release();
+    e->outptr_planes = 0;
+    e->index.release();
+    e->arena[e->cur ^ 1].release();
+    e->dec[e->cur ^ 1].~DecScratch();
+    new (&e->dec[e->cur ^ 1]) DecScratch();
+}
+
 double g_host_t[4] = {0, 0, 0, 0}; // debug (QCSIM_ENQ_TIMING): gate prologue, decode, encode, total
 void engine_gate(qcsim_engine *e, const qcsim_action &a) {
     const auto ht0 = std::chrono::steady_clock::now();
@@ -1623,12 +1700,25 @@ void engine_gate(qcsim_engine *e, const qcsim_action &a) {
         g.old = e->dense[e->cur].p;
         engine_dense(e, g);
     } else {
-        engine_waves(e, hm, remote, /*decode=*/true, [&](const SliceMap &map) {
-            GateSrc b = g;
-            b.old = e->old.p;
-            b.map = map;
-            return b;
-        });
+        for (;;) {
+            try {
+                engine_waves(e, hm, remote, /*decode=*/true, [&](const SliceMap &map) {
+                    GateSrc b = g;
+                    b.old = e->old.p;
+                    b.map = map;
+                    return b;
+                });
+                break;
+            } catch (const Fail &f) {
+                // the compressed state grew into the scratch's room: smaller
+                // waves, then the pass again (it only read arena[cur])
+                if (f.st != QCSIM_NOMEM || e->wave <= std::min<uint64_t>(4, e->ns)) throw;
+                CK(cudaStreamSynchronize(e->st));
+                cudaGetLastError();
+                engine_release_scratch(e);
+                e->wave /= 2;
+            }
+        }
     }
     const auto ht2 = std::chrono::steady_clock::now();
     g_host_t[0] += std::chrono::duration<double, std::micro>(ht1 - ht0).count();
@@ -1636,6 +1726,8 @@ void engine_gate(qcsim_engine *e, const qcsim_action &a) {
     g_host_t[3] += std::chrono::duration<double, std::micro>(ht2 - ht0).count();
     e->gates++;
     e->imported.clear();
+    e->dev_imp = nullptr;
+    e->dev_imp_at.clear();
 }
 
 // Worst-case arena bytes for one gate pass (every plane at qcsim_block_bound,
@@ -1658,7 +1750,7 @@ bool engine_defer_begin(qcsim_engine *e, uint64_t count) {
     constexpr uint64_t kBudget = 8ull << 30;
     const uint64_t worst = arena_worst(e);
     if (forced_sync || e->cfg.world > 1 || !e->compressed || e->wave != e->ns || 2 * worst > kBudget ||
-        !e->imported.empty())
+        !e->imported.empty() || e->dev_imp)
         return false;
     CK(cudaStreamSynchronize(e->st));
     {
@@ -2257,16 +2349,7 @@ qcsim_status qcsim_engine_trim(qcsim_engine *e) {
         if (!e) raise(QCSIM_INVALID_ARGUMENT, "null engine");
         CK(cudaSetDevice(e->cfg.device));
         CK(cudaStreamSynchronize(e->st));
-        e->enc.~EncScratch();
-        new (&e->enc) EncScratch();
-        e->decw.~DecScratch();
-        new (&e->decw) DecScratch();
-        e->old.release();
-        e->outptr_planes = 0;
-        e->index.release();
-        e->arena[e->cur ^ 1].release();
-        e->dec[e->cur ^ 1].~DecScratch();
-        new (&e->dec[e->cur ^ 1]) DecScratch();
+        engine_release_scratch(e);
     });
 }
 
@@ -2473,6 +2556,52 @@ qcsim_status qcsim_engine_export_slices(qcsim_engine *e, const uint64_t *slices,
                  (const uint64_t *)e->exp_meta.p, (int)P, e->exp_buf.p);
         CK(cudaMemcpyAsync(out, e->exp_buf.p, tot, cudaMemcpyDeviceToHost, e->st));
         CK(cudaStreamSynchronize(e->st));
+    });
+}
+
+qcsim_status qcsim_engine_export_slices_device(qcsim_engine *e, const uint64_t *slices, uint64_t count, void *out,
+                                               uint64_t capacity, uint64_t *len, uint64_t *plane_offsets) {
+    return guarded([&] {
+        if (!e || !len || !plane_offsets || (count && !slices)) raise(QCSIM_INVALID_ARGUMENT, "null argument");
+        if (!e->compressed) raise(QCSIM_INVALID_ARGUMENT, "engine is not compressed");
+        const uint64_t P = 2 * count;
+        std::vector<uint64_t> meta(3 * P);
+        uint64_t tot = 0;
+        for (uint64_t k = 0; k < count; ++k) {
+            if (slices[k] < e->s0 || slices[k] >= e->s0 + e->ns) raise(QCSIM_INVALID_ARGUMENT, "slice not owned by this rank");
+            const uint64_t j = slices[k] - e->s0;
+            for (int p = 0; p < 2; ++p) {
+                plane_offsets[2 * k + p] = tot;
+                meta[2 * k + p] = e->blk_off_h[2 * j + p];
+                meta[P + 2 * k + p] = tot;
+                meta[2 * P + 2 * k + p] = e->blk_bytes_h[2 * j + p];
+                tot += e->blk_bytes_h[2 * j + p];
+            }
+        }
+        plane_offsets[P] = tot;
+        *len = tot;
+        if (!out || !count) return;
+        if (capacity < tot) raise(QCSIM_INVALID_ARGUMENT, "output capacity too small");
+        CK(cudaSetDevice(e->cfg.device));
+        e->exp_meta.ensure(3 * P);
+        CK(cudaMemcpyAsync(e->exp_meta.p, meta.data(), meta.size() * 8, cudaMemcpyHostToDevice, e->st));
+        launch_k(gather_blocks, (unsigned)P, 256, 0, e->st, (const uint8_t *)e->arena[e->cur].p,
+                 (const uint64_t *)e->exp_meta.p, (int)P, (uint8_t *)out);
+        CK(cudaStreamSynchronize(e->st));
+    });
+}
+
+qcsim_status qcsim_engine_import_partners_device(qcsim_engine *e, const uint64_t *slices, uint64_t count,
+                                                 const void *blocks, const uint64_t *plane_offsets) {
+    return guarded([&] {
+        if (!e || (count && (!slices || !blocks || !plane_offsets))) raise(QCSIM_INVALID_ARGUMENT, "null argument");
+        e->dev_imp = (const uint8_t *)blocks;
+        for (uint64_t k = 0; k < count; ++k) {
+            if (slices[k] >= e->S) raise(QCSIM_INVALID_ARGUMENT, "slice out of range");
+            const uint64_t a = plane_offsets[2 * k], b = plane_offsets[2 * k + 1], c = plane_offsets[2 * k + 2];
+            if (b < a || c < b) raise(QCSIM_INVALID_ARGUMENT, "plane offsets must be non-decreasing");
+            e->dev_imp_at[slices[k]] = {a, b, b - a, c - b};
+        }
     });
 }
 

@@ -78,8 +78,11 @@ class ShardedEngine:
             return
         peer = self.rank ^ rbits
         # the peer's partners are exactly my slices (XOR with a rank bit maps
-        # its range onto mine): one device gather + one copy for all of them
+        # its range onto mine)
         mine = [self.s0 + k for k in range(self.ns)]
+        if self.dev.type == "cuda" and hasattr(self.eng, "export_slices_device"):
+            self._exchange_device(mine, peer)
+            return
         if hasattr(self.eng, "export_slices"):
             buf, offs = self.eng.export_slices(mine)
             blob = np.asarray(buf, dtype=np.uint8)
@@ -105,6 +108,28 @@ class ShardedEngine:
         for k, ln in enumerate(rlens.cpu().tolist()):
             self.eng.import_partner(p0 + k, data[off:off + ln])
             off += ln
+
+    def _exchange_device(self, mine, peer):
+        """X1 without host staging: the engine gathers my slices' blocks into
+        a device tensor, NCCL ships it to the peer, the peer's engine decodes
+        straight from the received device buffer."""
+        total, offs = self.eng.export_slices_device(mine)
+        buf = torch.empty(max(1, total), dtype=torch.uint8, device=self.dev)
+        self.eng.export_slices_device(mine, buf.data_ptr(), buf.numel())
+        meta = torch.tensor(offs, dtype=torch.int64, device=self.dev)
+        rmeta = torch.empty_like(meta)
+        ops = [dist.P2POp(dist.isend, meta, peer, self.group), dist.P2POp(dist.irecv, rmeta, peer, self.group)]
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+        roffs = rmeta.cpu().tolist()
+        rbuf = torch.empty(max(1, roffs[-1]), dtype=torch.uint8, device=self.dev)
+        ops = [dist.P2POp(dist.isend, buf, peer, self.group), dist.P2POp(dist.irecv, rbuf, peer, self.group)]
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+        torch.cuda.current_stream(self.dev).synchronize()  # the engine's stream reads rbuf next
+        self.exchanged_bytes += total
+        self.eng.import_partners_device([peer * self.ns + k for k in range(self.ns)], rbuf.data_ptr(), roffs)
+        self._keep = rbuf  # alive until the gate has run
 
     def run(self, actions=()):
         for a in actions:

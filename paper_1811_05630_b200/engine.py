@@ -250,6 +250,24 @@ class Engine:
                                                    out.size, C.byref(ln), offs))
         return out, list(offs)
 
+    def export_slices_device(self, slices, out_ptr=None, capacity=0):
+        """Device-direct export: gathers the slices' blocks into the device
+        buffer at `out_ptr` (None: size query).  Returns (total bytes,
+        per-plane offsets)."""
+        arr = (C.c_uint64 * max(1, len(slices)))(*slices)
+        ln = C.c_uint64()
+        offs = (C.c_uint64 * (2 * len(slices) + 1))()
+        self._ck(self.L.qcsim_engine_export_slices_device(self.h, arr, len(slices), out_ptr, capacity, C.byref(ln),
+                                                          offs))
+        return ln.value, list(offs)
+
+    def import_partners_device(self, slices, ptr, plane_offsets):
+        """Registers partner slices whose blocks sit in a device buffer
+        (kept alive by the caller until the next run returns)."""
+        arr = (C.c_uint64 * max(1, len(slices)))(*slices)
+        offs = (C.c_uint64 * max(1, len(plane_offsets)))(*plane_offsets)
+        self._ck(self.L.qcsim_engine_import_partners_device(self.h, arr, len(slices), ptr, offs))
+
     def import_partner(self, slice_index: int, data: bytes):
         b = np.frombuffer(data, dtype=np.uint8).copy()
         self._ck(self.L.qcsim_engine_import_partner(self.h, slice_index, b.ctypes.data_as(_native.u8p), b.size))

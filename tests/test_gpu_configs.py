@@ -294,12 +294,25 @@ class _InProcessRanks:
             e.load_basis(x)
         self._norms()
 
-    def run(self, acts):
+    def run(self, acts, device=False):
+        import torch
         ns = self.engs[0].local_slices
         for a in acts:
+            keep = []
             for e in self.engs:
-                for pj in e.partner_slices_needed(a):
-                    e.import_partner(pj, self.engs[pj // ns].export_slice(pj))
+                need = e.partner_slices_needed(a)
+                if not need:
+                    continue
+                if device:  # device-direct: peer gathers into a device buffer, e decodes from it
+                    owner = self.engs[need[0] // ns]
+                    total, offs = owner.export_slices_device(need)
+                    buf = torch.empty(max(1, total), dtype=torch.uint8, device="cuda")
+                    owner.export_slices_device(need, buf.data_ptr(), buf.numel())
+                    e.import_partners_device(need, buf.data_ptr(), offs)
+                    keep.append(buf)
+                else:
+                    for pj in need:
+                        e.import_partner(pj, self.engs[pj // ns].export_slice(pj))
             for e in self.engs:
                 e.run([a])
             self._norms()
@@ -308,12 +321,15 @@ class _InProcessRanks:
         return b"".join(e.export_blocks()[0] for e in self.engs)
 
 
+@pytest.mark.parametrize("device", [False, True])
 @pytest.mark.parametrize("world", [2, 4])
-def test_ranks_on_one_gpu_vs_single(q, world):
-    """The multi-rank CUDA path (export_slice / import_partner / validating
-    decode of imported partners / set_global_norms / remote slot layout) with
-    `world` engines as logical ranks on one GPU: byte-identical to one
-    engine, including butterflies and swaps on the rank bits."""
+def test_ranks_on_one_gpu_vs_single(q, world, device):
+    """The multi-rank CUDA path (export_slice / import_partner, or the
+    device-direct export_slices_device / import_partners_device; validating
+    decode of imported partners with on-device header checks;
+    set_global_norms; remote slot layout) with `world` engines as logical
+    ranks on one GPU: byte-identical to one engine, including butterflies and
+    swaps on the rank bits."""
     n, s = 12, 6
     G = q.Gate
     gates = [G.h(k) for k in range(n)] + [G.cnot(11, 2), G.swap(3, 11), G.swap(10, 11), G.swap(7, 10), G.y(11),
@@ -325,7 +341,7 @@ def test_ranks_on_one_gpu_vs_single(q, world):
     one.run(acts)
     ranks = _InProcessRanks(q, kw, world)
     ranks.load_basis(1234)
-    ranks.run(acts)
+    ranks.run(acts, device=device)
     assert ranks.blocks() == one.export_blocks()[0]
     m1 = one.metrics()
     assert sum(e.metrics().compress_calls for e in ranks.engs) == m1.compress_calls
@@ -350,3 +366,23 @@ def test_measure_overhead_and_report(q, tmp_path):
     assert len(d["per_gate"]) == len(acts) + 1 and d["per_gate"][0]["gate_index"] == -1
     lines = (tmp_path / "m.csv").read_text().splitlines()
     assert lines[0] == "gate_index,min_ratio,mean_ratio,seconds" and len(lines) == len(acts) + 2
+
+
+def test_device_import_rejects_corrupt(q):
+    """A corrupt device-resident partner block fails with the reference's
+    from_bytes message (header checks on the device)."""
+    import torch
+    kw = dict(num_qubits=8, slice_bits=4, codec=q.CodecConfig(q.CodecMode.Absolute, 1e-5))
+    a = q.Engine(q.EngineConfig(rank=0, world=2, **kw))
+    b = q.Engine(q.EngineConfig(rank=1, world=2, **kw))
+    for e in (a, b):
+        e.load_basis(3)
+    act = q.to_action_c(q.gate_action(q.Gate.h(7)))
+    need = a.partner_slices_needed(act)
+    total, offs = b.export_slices_device(need)
+    buf = torch.empty(total, dtype=torch.uint8, device="cuda")
+    b.export_slices_device(need, buf.data_ptr(), total)
+    buf[0] = ord("X")  # first block's magic
+    a.import_partners_device(need, buf.data_ptr(), offs)
+    with pytest.raises(q.CodecError, match="bad block magic"):
+        a.run([act])
