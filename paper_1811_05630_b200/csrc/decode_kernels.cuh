@@ -34,6 +34,11 @@ struct DecPlanes {
     double *const *out;        // [plane] output plane
     uint64_t L;
     int log2C;                 // fine checkpoint spacing (index_records, common.cuh)
+    // foreign blocks (no index in a slot): records built by fd_scan
+    const IndexRec *ext_index = nullptr; // [plane][ext_stride]
+    const uint32_t *ext_nrec = nullptr;  // [plane]
+    uint64_t ext_stride = 0;
+    const uint32_t *skip = nullptr;      // [plane] != 0: not decoded (a codec error was found)
 };
 
 __device__ __forceinline__ uint64_t load_le(const uint8_t *p, int bytes) {
@@ -46,6 +51,7 @@ __global__ void __launch_bounds__(256) dec_prepare(DecPlanes D, DecTables T, int
     pdl_begin();
     const int pl = blockIdx.x;
     if (pl >= planes) return;
+    if (D.skip && D.skip[pl]) return; // invalid table: never parsed
     const int tid = threadIdx.x;
     __shared__ uint32_t cnt[kMaxCodeLen + 1];
     __shared__ uint64_t first[kMaxCodeLen + 1];
@@ -218,14 +224,15 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
     }
     extern __shared__ __align__(16) unsigned char dec_raw[];
     DecSmem &S = *reinterpret_cast<DecSmem *>(dec_raw);
-    const uint64_t nchunks_max = (D.L + (1ull << D.log2C) - 1) >> D.log2C; // >= records + 1
+    const uint64_t nchunks_max = D.ext_index ? D.ext_stride + 1 : ((D.L + (1ull << D.log2C) - 1) >> D.log2C);
     const uint32_t groups = (uint32_t)((nchunks_max + kDecThreads - 1) / kDecThreads);
     const int pl = (int)(blockIdx.x / groups);
     if (pl >= planes) return;
+    if (D.skip && D.skip[pl]) return;
     const uint8_t *blk = D.arena + D.blk_off[pl];
     const uint64_t payload = load_le(blk + 32, 8);
     const uint64_t bbytes = kHeaderBytes + payload;
-    const uint64_t nchunks = index_records(D.L, bbytes, D.log2C) + 1;
+    const uint64_t nchunks = (D.ext_index ? D.ext_nrec[pl] : index_records(D.L, bbytes, D.log2C)) + 1;
     const uint64_t j0 = (uint64_t)(blockIdx.x % groups) * kDecThreads;
     if (j0 >= nchunks) return;
     const uint64_t j = j0 + threadIdx.x;
@@ -248,7 +255,8 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
     const uint32_t *count = T.count + (uint64_t)pl * (kMaxCodeLen + 1);
     const uint32_t *basei = T.basei + (uint64_t)pl * (kMaxCodeLen + 1);
     const uint32_t *sorted = T.sorted + (uint64_t)pl * T.cap;
-    const IndexRec *sidx = reinterpret_cast<const IndexRec *>(D.arena + index_offset(D.blk_off[pl], bbytes));
+    const IndexRec *sidx = D.ext_index ? D.ext_index + (uint64_t)pl * D.ext_stride
+                                       : reinterpret_cast<const IndexRec *>(D.arena + index_offset(D.blk_off[pl], bbytes));
     auto rec_bitpos = [&](uint64_t jj) -> uint64_t { return jj == 0 ? 0ull : sidx[jj - 1].bitpos; };
 
     {
@@ -673,6 +681,217 @@ __global__ void dec_validate(ValArgs A, int planes) {
     if (ocur != nout) return fail(kDecOutUnused);
     if (br.byte + (br.bit != 0) != sbytes) return fail(kDecStreamLen);
     A.err[pl] = kDecOk;
+}
+
+
+// ------------------------------------------------------- foreign blocks
+// QCB1 blocks that carry no decode index (decompress_plane, partner
+// imports): fd_head validates header and code table (codec.cpp:366-408,
+// 535-583, the reference's order), dec_prepare builds the tables, fd_scan
+// walks every token once -- one thread per plane, every check of
+// codec.cpp:585-632 in order, no element stores -- and leaves a decode
+// record (the decoder state at a token boundary) every kFdBits stream bits;
+// dec_chunks then writes the elements chunk-parallel from those records.
+constexpr uint64_t kFdBits = 4096;
+
+struct FdArgs {
+    const uint8_t *arena;      // staged blocks (code streams 16-byte aligned, padded)
+    const uint64_t *blk_off;   // [plane]
+    const uint64_t *avail;     // [plane] bytes available (header checks)
+    uint32_t *err;             // [plane] out: first error (kDec*), 0 = ok
+    uint64_t n_expected;       // element_count every block must have
+    uint64_t cap;              // code-table capacity of the decode tables
+    IndexRec *rec;             // [plane][stride] out
+    uint32_t *nrec;            // [plane] out
+    uint64_t stride;
+};
+
+__global__ void fd_head(FdArgs A, int planes) {
+    pdl_begin();
+    const int pl = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pl >= planes) return;
+    const uint8_t *blk = A.arena + A.blk_off[pl];
+    auto fail = [&](uint32_t e) { A.err[pl] = e; };
+    A.err[pl] = kDecOk;
+    const uint64_t len = A.avail[pl];
+    if (len < kHeaderBytes) return fail(kDecHdrTrunc);
+    if (blk[0] != 'Q' || blk[1] != 'C' || blk[2] != 'B' || blk[3] != '1') return fail(kDecMagic);
+    if (blk[4] != 1) return fail(kDecVersion);
+    if (blk[5] > 2) return fail(kDecModeByte);
+    if (blk[6] > 1) return fail(kDecPredByte);
+    if (blk[7] < 4 || blk[7] > 24) return fail(kDecQbRange);
+    const uint64_t n = load_le(blk + 8, 8), nout = load_le(blk + 24, 8), plen = load_le(blk + 32, 8);
+    const double heb = __longlong_as_double((long long)load_le(blk + 16, 8));
+    if (n == 0) return fail(kDecCount0);
+    if (nout > n) return fail(kDecOutCount);
+    if (!(heb >= 0.0) || !isfinite(heb)) return fail(kDecEbBad);
+    if (plen > len - kHeaderBytes) return fail(kDecPayTrunc);
+    if (A.n_expected && n != A.n_expected) return fail(kDecWrongLen);
+    const uint32_t rsym = 1u << blk[7];
+    const uint8_t *pl_ = blk + kHeaderBytes;
+    if (plen < 4) return fail(kDecPayloadSmall);
+    const uint32_t tc = (uint32_t)load_le(pl_, 4);
+    const uint64_t table_bytes = 4 + (uint64_t)tc * 5;
+    if (tc == 0) return fail(kDecTableEmpty);
+    if (plen < table_bytes) return fail(kDecTableTrunc);
+    if (tc > A.cap) return fail(kDecNoMem);
+    uint32_t cnt[kMaxCodeLen + 1];
+    for (int l = 0; l <= kMaxCodeLen; ++l) cnt[l] = 0;
+    uint32_t prev = 0;
+    for (uint32_t i = 0; i < tc; ++i) {
+        const uint32_t sy = (uint32_t)load_le(pl_ + 4 + 5ull * i, 4);
+        const uint8_t l = pl_[4 + 5ull * i + 4];
+        if (i > 0 && sy <= prev) return fail(kDecSymOrder);
+        if (sy > rsym) return fail(kDecSymRange);
+        if (l < 1 || l > kMaxCodeLen) return fail(kDecLenRange);
+        ++cnt[l];
+        prev = sy;
+    }
+    double kraft = 0.0;
+    for (int l = 1; l <= kMaxCodeLen; ++l) {
+        const double term = ldexp(1.0, -l);
+        for (uint32_t k = 0; k < cnt[l]; ++k) kraft = dadd(kraft, term);
+    }
+    if (kraft > 1.0 + 1e-9) return fail(kDecOverfull);
+    if (plen < table_bytes + nout * 16) return fail(kDecLenMismatch);
+}
+
+__global__ void fd_scan(FdArgs A, DecTables T, int planes) {
+    pdl_begin();
+    const int pl = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pl >= planes || A.err[pl]) return;
+    const uint8_t *blk = A.arena + A.blk_off[pl];
+    auto fail = [&](uint32_t e) { A.err[pl] = e; };
+    const uint8_t pred_kind = blk[6];
+    const int qb = blk[7];
+    const uint64_t n = load_le(blk + 8, 8);
+    const double eb = __longlong_as_double((long long)load_le(blk + 16, 8));
+    const double q = dmul(2.0, eb);
+    const uint64_t nout = load_le(blk + 24, 8);
+    const uint64_t plen = load_le(blk + 32, 8);
+    const long long half = 1ll << (qb - 1);
+    const uint32_t rsym = 1u << qb;
+    const uint32_t tc = (uint32_t)load_le(blk + kHeaderBytes, 4);
+    const uint64_t table_bytes = 4 + 5ull * tc;
+    const uint64_t sbytes = plen - table_bytes - 16 * nout;
+    const uint64_t sbits = sbytes * 8;
+    const uint32_t *stream = reinterpret_cast<const uint32_t *>(blk + kHeaderBytes + table_bytes);
+    const uint8_t *orec = blk + kHeaderBytes + table_bytes + sbytes;
+    const uint32_t *lut = T.lut + (uint64_t)pl * (1u << kLutBits);
+    const uint64_t *first = T.first + (uint64_t)pl * (kMaxCodeLen + 1);
+    const uint32_t *count = T.count + (uint64_t)pl * (kMaxCodeLen + 1);
+    const uint32_t *basei = T.basei + (uint64_t)pl * (kMaxCodeLen + 1);
+    const uint32_t *sorted = T.sorted + (uint64_t)pl * T.cap;
+    const uint32_t maxlen = T.meta[4 * pl];
+    IndexRec *rec = A.rec + (uint64_t)pl * A.stride;
+    uint32_t nr = 0;
+    uint64_t next_mark = kFdBits;
+    BitWindow bw;
+    bw.init(stream, 0);
+    uint64_t bp = 0, i = 0, ocur = 0;
+    uint32_t last = rsym;
+    double d1 = 0.0, d2 = 0.0;
+    // the reference's value of element i for symbol es (codec.cpp:605-611)
+    auto value = [&](uint32_t es) -> double {
+        double pred;
+        if (pred_kind == 0) pred = i > 0 ? d1 : 0.0;
+        else pred = i == 0 ? 0.0 : (i == 1 ? d1 : predict_linear(d1, d2));
+        const long long m = (long long)es - half;
+        return eb == 0.0 ? pred : dadd(pred, dmul(q, (double)m));
+    };
+    while (i < n) {
+        if (bp >= next_mark) { // a record at this token boundary
+            if (nr < A.stride) rec[nr++] = IndexRec{d1, d2, bp, 0u, (uint32_t)ocur, last, (uint32_t)i};
+            next_mark = (bp / kFdBits + 1) * kFdBits;
+        }
+        // prefix code (PrefixDecoder, codec.cpp:251-286): LUT, then long codes
+        const uint64_t remain = sbits - bp;
+        const uint32_t le = lut[bw.acc >> (64 - kLutBits)];
+        uint32_t s = 0, l = le & 63;
+        if (l) {
+            s = le >> 6;
+        } else {
+            const uint64_t w = (int)maxlen <= bw.n ? bw.acc : peek64<false>(stream, bp);
+            for (uint32_t ll = kLutBits + 1; ll <= maxlen; ++ll) {
+                if (!count[ll]) continue;
+                const uint64_t c = w >> (64 - ll);
+                if (c >= first[ll] && c - first[ll] < count[ll]) {
+                    s = sorted[basei[ll] + (uint32_t)(c - first[ll])];
+                    l = ll;
+                    break;
+                }
+            }
+        }
+        if (l == 0) return fail(remain < maxlen ? kDecStreamTrunc : kDecInvalidCode);
+        if (l > remain) return fail(kDecStreamTrunc);
+        if ((int)l <= bw.n) bw.skip((int)l);
+        else bw.init(stream, bp + l);
+        bp += l;
+        if (s == rsym) {
+            if (last == rsym || last == kOutlierSym) return fail(kDecRunNoCode);
+            // Elias gamma: zeros, a one, then the value's low bits
+            const uint64_t g = peek64<false>(stream, bp);
+            int zeros = g ? __clzll((long long)g) : 64;
+            if (zeros > 63 || (g == 0 && sbits - bp > 64)) { // more than 63 zeros before the terminating one
+                if (sbits - bp <= 63) return fail(kDecStreamTrunc);
+                return fail(kDecRunRange);
+            }
+            if ((uint64_t)zeros + 1 > sbits - bp) return fail(kDecStreamTrunc);
+            uint64_t v;
+            if (zeros == 0) {
+                v = 1;
+            } else {
+                const uint64_t vb = bp + zeros; // the value: the one + `zeros` bits
+                if (vb + zeros + 1 > sbits) return fail(kDecStreamTrunc);
+                const uint64_t h = peek64<false>(stream, vb);
+                v = h >> (63 - zeros);
+            }
+            bp += 2 * (uint64_t)zeros + 1;
+            bw.init(stream, bp);
+            if (v > n - i) return fail(kDecRunOverflow);
+            // v repeats of `last`: a constant run needs no per-element work
+            if (pred_kind == 0) {
+                uint64_t k = 0;
+                while (k < v) {
+                    const double x = value(last);
+                    if (bits_of(x) == bits_of(d1) && i > 0) { // constant from here on
+                        d2 = d1;
+                        i += v - k;
+                        k = v;
+                        break;
+                    }
+                    d2 = d1;
+                    d1 = x;
+                    ++i;
+                    ++k;
+                }
+            } else {
+                for (uint64_t k = 0; k < v; ++k) {
+                    const double x = value(last);
+                    d2 = d1;
+                    d1 = x;
+                    ++i;
+                }
+            }
+            continue;
+        }
+        last = s;
+        double x;
+        if (s == kOutlierSym) {
+            if (ocur >= nout) return fail(kDecOutExhausted);
+            if (load_le(orec + 16 * ocur, 8) != i) return fail(kDecOutPos);
+            x = __longlong_as_double((long long)load_le(orec + 16 * ocur + 8, 8));
+            ++ocur;
+        } else {
+            x = value(s);
+        }
+        d2 = d1;
+        d1 = x;
+        ++i;
+    }
+    if (ocur != nout) return fail(kDecOutUnused);
+    if ((bp + 7) / 8 != sbytes) return fail(kDecStreamLen);
+    A.nrec[pl] = nr;
 }
 
 } // namespace qcb

@@ -938,8 +938,9 @@ struct DecScratch {
     DBuf<uint32_t> lut, count, basei, sorted, meta;
     DBuf<uint64_t> first;
     uint64_t cap = 0;
-    void ensure(uint64_t planes, uint64_t L, int qb) {
-        cap = std::min<uint64_t>(L + 1, (1ull << qb) + 1);
+    void ensure(uint64_t planes, uint64_t L, int qb) { ensure_cap(planes, std::min<uint64_t>(L + 1, (1ull << qb) + 1)); }
+    void ensure_cap(uint64_t planes, uint64_t c) {
+        cap = c;
         lut.ensure(planes << kLutBits);
         first.ensure(planes * (kMaxCodeLen + 1));
         count.ensure(planes * (kMaxCodeLen + 1));
@@ -1068,6 +1069,114 @@ struct ValScratch {
     }
 };
 
+// Foreign-block decoding (no index next to the blocks): stage the blocks
+// with 16-byte aligned code streams, validate header + table (fd_head),
+// parse the tables, one validating token walk per plane leaving a record
+// every kFdBits stream bits (fd_scan), then the chunk-parallel decoder.
+struct ForeignScratch {
+    DBuf<uint8_t> arena;
+    HBuf<uint8_t> h_arena;
+    DBuf<uint64_t> meta; // [offsets | lengths]
+    DBuf<uint32_t> err, nrec;
+    DBuf<IndexRec> rec;
+    DBuf<double *> outs;
+    DecScratch tables;
+    std::vector<uint32_t> h_err;
+};
+struct ForeignBlock {
+    const uint8_t *src; // host or device bytes
+    uint64_t len;       // bytes available at src
+    uint32_t table_count;
+    uint64_t payload;
+    double *out;        // device plane
+};
+
+// Decodes blocks of one element count `n` into their device planes; returns
+// the first failing block's error code (plane order) or 0.
+uint32_t foreign_decode(cudaStream_t st, ForeignScratch &F, const std::vector<ForeignBlock> &B, bool src_device,
+                        uint64_t n, int qb) {
+    const uint64_t P = B.size();
+    if (!P) return 0;
+    std::vector<uint64_t> meta(2 * P);
+    uint64_t end = 0, maxtc = 1, stride = 1;
+    for (uint64_t k = 0; k < P; ++k) {
+        const uint64_t pre = kHeaderBytes + 4 + 5ull * B[k].table_count;
+        const uint64_t off = ((end + 15) & ~15ull) + ((16 - (pre & 15)) & 15); // stream 16-byte aligned
+        meta[k] = off;
+        meta[P + k] = B[k].len;
+        end = off + B[k].len + 64; // padding: the bit window reads ahead
+        maxtc = std::max<uint64_t>(maxtc, B[k].table_count);
+        stride = std::max<uint64_t>(stride, (B[k].payload * 8) / kFdBits + 2);
+    }
+    F.arena.ensure(end + 64);
+    if (src_device) {
+        for (uint64_t k = 0; k < P; ++k)
+            CK(cudaMemcpyAsync(F.arena.p + meta[k], B[k].src, B[k].len, cudaMemcpyDeviceToDevice, st));
+    } else {
+        F.h_arena.ensure(end + 64);
+        for (uint64_t k = 0; k < P; ++k) std::memcpy(F.h_arena.p + meta[k], B[k].src, B[k].len);
+        CK(cudaMemcpyAsync(F.arena.p, F.h_arena.p, end, cudaMemcpyHostToDevice, st));
+    }
+    F.meta.ensure(2 * P);
+    CK(cudaMemcpyAsync(F.meta.p, meta.data(), 2 * P * 8, cudaMemcpyHostToDevice, st));
+    std::vector<double *> outs(P);
+    for (uint64_t k = 0; k < P; ++k) outs[k] = B[k].out;
+    F.outs.ensure(P);
+    CK(cudaMemcpyAsync(F.outs.p, outs.data(), P * sizeof(double *), cudaMemcpyHostToDevice, st));
+    F.err.ensure(P);
+    F.nrec.ensure(P);
+    F.rec.ensure(P * stride);
+    const uint64_t cap = std::min<uint64_t>(std::max<uint64_t>(maxtc, 1), 1ull << 25);
+    (void)qb;
+    F.tables.ensure_cap(P, cap);
+    FdArgs A;
+    A.arena = F.arena.p;
+    A.blk_off = F.meta.p;
+    A.avail = F.meta.p + P;
+    A.err = F.err.p;
+    A.n_expected = n;
+    A.cap = F.tables.cap;
+    A.rec = F.rec.p;
+    A.nrec = F.nrec.p;
+    A.stride = stride;
+    {
+        PROF("fd_head", st);
+        launch_k(fd_head, (unsigned)((P + 31) / 32), 32, 0, st, A, (int)P);
+    }
+    DecPlanes D;
+    D.arena = F.arena.p;
+    D.blk_off = F.meta.p;
+    D.out = F.outs.p;
+    D.L = n;
+    D.log2C = 10;
+    D.skip = F.err.p;
+    const DecTables T = F.tables.tables();
+    {
+        PROF("dec_prepare", st);
+        launch_k(dec_prepare, (unsigned)P, 256, 0, st, D, T, (int)P);
+    }
+    {
+        PROF("fd_scan", st);
+        launch_k(fd_scan, (unsigned)((P + 31) / 32), 32, 0, st, A, T, (int)P);
+    }
+    D.ext_index = F.rec.p;
+    D.ext_nrec = F.nrec.p;
+    D.ext_stride = stride;
+    {
+        set_smem_once(dec_chunks, kDecSmem, g_smem_set, 2);
+        PROF("dec_chunks", st);
+        const uint64_t groups = (stride + 1 + kDecThreads - 1) / kDecThreads;
+        launch_k(dec_chunks, (unsigned)(groups * P), kDecThreads, kDecSmem, st, D, T, (int)P, NormArgs{});
+    }
+    F.h_err.resize(P);
+    CK(cudaMemcpyAsync(F.h_err.data(), F.err.p, P * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    for (uint64_t k = 0; k < P; ++k)
+        if (F.h_err[k]) return F.h_err[k];
+    return 0;
+}
+
 // ------------------------------------------------------------- context
 // Per-thread codec context for the single-plane / batched codec API.
 struct CodecCtx {
@@ -1075,6 +1184,7 @@ struct CodecCtx {
     cudaStream_t st = nullptr;
     EncScratch enc;
     ValScratch val;
+    ForeignScratch fore;
     DBuf<uint8_t> arena, bytes;
     DBuf<double> vals;
     DBuf<IndexRec> index;
@@ -1152,6 +1262,7 @@ struct qcsim_engine {
     DecScratch dec[2]; // decode tables of arena[0/1], written by the encoder (single-batch passes)
     DecScratch decw;   // decode tables parsed from the blocks (waves, compare, gather)
     ValScratch val;
+    ForeignScratch fore; // partner blocks imported from host bytes
     DBuf<uint8_t> imp_bytes;
     DBuf<uint64_t> imp_off;
     // deferred gate loop (no host round trip per gate): device scale,
@@ -1354,8 +1465,7 @@ void decode_imports(qcsim_engine *e, const SliceMap &map, uint64_t u0, uint64_t 
     }
     std::unordered_map<uint64_t, size_t> where;
     for (size_t m = 0; m < e->imported.size(); ++m) where[e->imported[m].first] = m;
-    std::vector<uint8_t> all;
-    std::vector<uint64_t> offs;
+    std::vector<ForeignBlock> fb;
     for (uint64_t u = u0; u < u0 + cnt; ++u) {
         const uint64_t pj = (e->s0 + map.slice_rel((uint32_t)u)) ^ map.hm;
         auto it = where.find(pj);
@@ -1366,39 +1476,18 @@ void decode_imports(qcsim_engine *e, const SliceMap &map, uint64_t u0, uint64_t 
         uint64_t pos = 0;
         for (int p = 0; p < 2; ++p) {
             uint64_t used = 0;
-            parse_header(b.data() + pos, b.size() - pos, &used);
-            offs.push_back(all.size());
-            all.insert(all.end(), b.begin() + pos, b.begin() + pos + used);
+            const Header h = parse_header(b.data() + pos, b.size() - pos, &used);
+            if (h.n != e->L) raise(QCSIM_CODEC, "partner block length does not match the slice");
+            const uint32_t tc = h.payload >= 4 ? (uint32_t)(b[pos + 40] | (b[pos + 41] << 8) | (b[pos + 42] << 16) |
+                                                            ((uint32_t)b[pos + 43] << 24))
+                                               : 0;
+            fb.push_back(ForeignBlock{b.data() + pos, used, tc, h.payload,
+                                      e->old.p + (first_plane + 2 * (u - u0) + p) * e->L});
             pos += used;
         }
     }
-    e->imp_bytes.ensure(all.size() + 64);
-    e->imp_off.ensure(offs.size());
-    CK(cudaMemcpyAsync(e->imp_bytes.p, all.data(), all.size(), cudaMemcpyHostToDevice, e->st));
-    CK(cudaMemcpyAsync(e->imp_off.p, offs.data(), offs.size() * 8, cudaMemcpyHostToDevice, e->st));
-    std::vector<double *> ptrs(offs.size());
-    for (uint64_t k = 0; k < offs.size(); ++k) ptrs[k] = e->old.p + (first_plane + k) * e->L;
-    e->imp_ptrs.ensure(ptrs.size());
-    CK(cudaMemcpyAsync(e->imp_ptrs.p, ptrs.data(), ptrs.size() * sizeof(double *), cudaMemcpyHostToDevice, e->st));
-    const uint64_t vcap = std::min<uint64_t>(e->L + 1, (1ull << e->cfg.codec.quant_code_bits) + 1);
-    e->val.ensure(offs.size(), vcap);
-    ValArgs V;
-    V.blocks = e->imp_bytes.p;
-    V.blk_off = e->imp_off.p;
-    V.out = e->imp_ptrs.p;
-    V.err = e->val.err.p;
-    V.ssym = e->val.ssym.p;
-    V.slen = e->val.slen.p;
-    V.cap = vcap;
-    {
-        PROF("dec_validate", e->st);
-        launch_k(dec_validate, (unsigned)((offs.size() + 31) / 32), 32, 0, e->st, V, (int)offs.size());
-    }
-    std::vector<uint32_t> errs(offs.size());
-    CK(cudaMemcpyAsync(errs.data(), e->val.err.p, errs.size() * 4, cudaMemcpyDeviceToHost, e->st));
-    CK(cudaStreamSynchronize(e->st));
-    for (uint32_t x : errs)
-        if (x) raise(QCSIM_CODEC, dec_message(x));
+    const uint32_t err = foreign_decode(e->st, e->fore, fb, false, e->L, e->cfg.codec.quant_code_bits);
+    if (err) raise(QCSIM_CODEC, dec_message(err));
 }
 
 // Decodes local slices [k0, k0 + cnt) (contiguous planes) into old slots
@@ -2025,34 +2114,12 @@ qcsim_status qcsim_decompress_plane(const uint8_t *block, uint64_t len, double *
         if (!out) return;
         if (h.n > capacity) raise(QCSIM_INVALID_ARGUMENT, "output capacity too small");
         CodecCtx &C = codec_ctx();
-        C.bytes.ensure(used + 64);
-        CK(cudaMemcpyAsync(C.bytes.p, block, used, cudaMemcpyHostToDevice, C.st));
         C.vals.ensure(h.n);
-        C.optrs.ensure(1);
-        double *op = C.vals.p;
-        CK(cudaMemcpyAsync(C.optrs.p, &op, sizeof op, cudaMemcpyHostToDevice, C.st));
-        C.offs.ensure(1);
-        CK(cudaMemsetAsync(C.offs.p, 0, 8, C.st));
         uint32_t tc = 0;
         if (h.payload >= 4) tc = (uint32_t)(block[40] | (block[41] << 8) | (block[42] << 16) | ((uint32_t)block[43] << 24));
-        const uint64_t cap = std::max<uint64_t>(1, std::min<uint64_t>(tc, (1ull << 25)));
-        C.val.ensure(1, cap);
-        ValArgs V;
-        V.blocks = C.bytes.p;
-        V.blk_off = C.offs.p;
-        V.out = C.optrs.p;
-        V.err = C.val.err.p;
-        V.ssym = C.val.ssym.p;
-        V.slen = C.val.slen.p;
-        V.cap = cap;
-        {
-            PROF("dec_validate", C.st);
-            launch_k(dec_validate, 1, 32, 0, C.st, V, 1);
-        }
-        uint32_t e = 0;
-        CK(cudaMemcpyAsync(&e, C.val.err.p, 4, cudaMemcpyDeviceToHost, C.st));
-        CK(cudaStreamSynchronize(C.st));
-        CK(cudaGetLastError());
+        // validating token walk + chunk-parallel decode (foreign_decode)
+        const uint32_t e = foreign_decode(C.st, C.fore, {ForeignBlock{block, used, tc, h.payload, C.vals.p}}, false, h.n,
+                                          h.qb);
         if (e) raise(QCSIM_CODEC, dec_message(e));
         CK(cudaMemcpyAsync(out, C.vals.p, h.n * sizeof(double), cudaMemcpyDeviceToHost, C.st));
         CK(cudaStreamSynchronize(C.st));
@@ -2113,42 +2180,32 @@ qcsim_status qcsim_decompress_planes_device(const uint8_t *blocks, const uint64_
         if (planes == 0) return;
         CodecCtx &C = codec_ctx();
         cudaStream_t st = stream ? (cudaStream_t)stream : C.st;
-        // header checks on the host copy of each header
-        uint64_t maxtc = 1;
+        // header checks on the host copy of each header (from_bytes order)
+        std::vector<ForeignBlock> fb(planes);
+        std::vector<uint64_t> ns(planes);
+        std::vector<int> qbs(planes);
         for (uint32_t p = 0; p < planes; ++p) {
-            uint8_t hdr[44];
+            uint8_t hdr[44] = {};
             const uint64_t avail = offsets_host[p + 1] - offsets_host[p];
             CK(cudaMemcpy(hdr, blocks + offsets_host[p], std::min<uint64_t>(44, avail), cudaMemcpyDeviceToHost));
-            Header h = parse_header(hdr, avail, nullptr);
+            uint64_t used = 0;
+            Header h = parse_header(hdr, avail, &used);
             if (h.n > capacity[p]) raise(QCSIM_INVALID_ARGUMENT, "output capacity too small");
-            if (h.payload >= 4)
-                maxtc = std::max<uint64_t>(maxtc, hdr[40] | (hdr[41] << 8) | (hdr[42] << 16) | ((uint64_t)hdr[43] << 24));
+            const uint32_t tc = h.payload >= 4 ? (uint32_t)(hdr[40] | (hdr[41] << 8) | (hdr[42] << 16) | ((uint32_t)hdr[43] << 24)) : 0;
+            fb[p] = ForeignBlock{blocks + offsets_host[p], used, tc, h.payload, out[p]};
+            ns[p] = h.n;
+            qbs[p] = h.qb;
         }
-        maxtc = std::min<uint64_t>(maxtc, 1ull << 25);
-        C.offs.ensure(planes);
-        CK(cudaMemcpyAsync(C.offs.p, offsets_host, planes * 8, cudaMemcpyHostToDevice, st));
-        C.optrs.ensure(planes);
-        CK(cudaMemcpyAsync(C.optrs.p, out, planes * sizeof(double *), cudaMemcpyHostToDevice, st));
-        C.val.ensure(planes, maxtc);
-        ValArgs V;
-        V.blocks = blocks;
-        V.blk_off = C.offs.p;
-        V.out = C.optrs.p;
-        V.err = C.val.err.p;
-        V.ssym = C.val.ssym.p;
-        V.slen = C.val.slen.p;
-        V.cap = maxtc;
-        {
-            PROF("dec_validate", st);
-            launch_k(dec_validate, (planes + 31) / 32, 32, 0, st, V, (int)planes);
+        // one foreign_decode per run of planes with the same element count
+        for (uint32_t p0 = 0; p0 < planes;) {
+            uint32_t p1 = p0 + 1;
+            while (p1 < planes && ns[p1] == ns[p0]) ++p1;
+            std::vector<ForeignBlock> part(fb.begin() + p0, fb.begin() + p1);
+            const uint32_t e = foreign_decode(st, C.fore, part, true, ns[p0], qbs[p0]);
+            if (e) raise(QCSIM_CODEC, dec_message(e));
+            p0 = p1;
         }
-        std::vector<uint32_t> errs(planes);
-        CK(cudaMemcpyAsync(errs.data(), C.val.err.p, planes * 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-    g_prof.flush();
-        CK(cudaGetLastError());
-        for (uint32_t x : errs)
-            if (x) raise(QCSIM_CODEC, dec_message(x));
+        g_prof.flush();
     });
 }
 
