@@ -704,6 +704,7 @@ struct FdArgs {
     IndexRec *rec;             // [plane][stride] out
     uint32_t *nrec;            // [plane] out
     uint64_t stride;
+    const uint32_t *only = nullptr; // fd_scan: [plane] != 0 selects the planes to walk
 };
 
 __global__ void fd_head(FdArgs A, int planes) {
@@ -759,7 +760,7 @@ __global__ void fd_head(FdArgs A, int planes) {
 __global__ void fd_scan(FdArgs A, DecTables T, int planes) {
     pdl_begin();
     const int pl = blockIdx.x * blockDim.x + threadIdx.x;
-    if (pl >= planes || A.err[pl]) return;
+    if (pl >= planes || A.err[pl] || (A.only && !A.only[pl])) return;
     const uint8_t *blk = A.arena + A.blk_off[pl];
     auto fail = [&](uint32_t e) { A.err[pl] = e; };
     const uint8_t pred_kind = blk[6];

@@ -24,6 +24,7 @@
 #include "../../include/qcsim_c.h"
 #include "common.cuh"
 #include "decode_kernels.cuh"
+#include "foreign_kernels.cuh"
 #include "enc_tiles.cuh"
 #include "sources.cuh"
 #include "misc_kernels.cuh"
@@ -1077,9 +1078,14 @@ struct ForeignScratch {
     DBuf<uint8_t> arena;
     HBuf<uint8_t> h_arena;
     DBuf<uint64_t> meta; // [offsets | lengths]
-    DBuf<uint32_t> err, nrec;
+    DBuf<uint32_t> err, nrec, slow, nseg;
     DBuf<IndexRec> rec;
     DBuf<double *> outs;
+    DBuf<FpBound> bnd;
+    DBuf<FpSeg> seg;
+    DBuf<FpEntry> ent;
+    DBuf<double> ev;
+    DBuf<uint8_t> evk;
     DecScratch tables;
     std::vector<uint32_t> h_err;
 };
@@ -1093,8 +1099,21 @@ struct ForeignBlock {
 
 // Decodes blocks of one element count `n` into their device planes; returns
 // the first failing block's error code (plane order) or 0.
+uint32_t foreign_decode_batch(cudaStream_t st, ForeignScratch &F, const std::vector<ForeignBlock> &B,
+                              bool src_device, uint64_t n, int qb);
 uint32_t foreign_decode(cudaStream_t st, ForeignScratch &F, const std::vector<ForeignBlock> &B, bool src_device,
                         uint64_t n, int qb) {
+    // sub-batches bound the event lists (8 B + 1 B per element)
+    const uint64_t per = std::max<uint64_t>(1, (1ull << 27) / std::max<uint64_t>(n, 1));
+    for (uint64_t k0 = 0; k0 < B.size(); k0 += per) {
+        std::vector<ForeignBlock> part(B.begin() + k0, B.begin() + std::min<uint64_t>(B.size(), k0 + per));
+        const uint32_t e = foreign_decode_batch(st, F, part, src_device, n, qb);
+        if (e) return e;
+    }
+    return 0;
+}
+uint32_t foreign_decode_batch(cudaStream_t st, ForeignScratch &F, const std::vector<ForeignBlock> &B,
+                              bool src_device, uint64_t n, int qb) {
     const uint64_t P = B.size();
     if (!P) return 0;
     std::vector<uint64_t> meta(2 * P);
@@ -1155,6 +1174,61 @@ uint32_t foreign_decode(cudaStream_t st, ForeignScratch &F, const std::vector<Fo
         PROF("dec_prepare", st);
         launch_k(dec_prepare, (unsigned)P, 256, 0, st, D, T, (int)P);
     }
+    // the parallel path (foreign_kernels.cuh); planes it declines: fd_scan
+    static const bool serial_only = std::getenv("QCSIM_FOREIGN_SERIAL") != nullptr; // (debug)
+    F.slow.ensure(P);
+    if (serial_only) {
+        CK(cudaMemsetAsync(F.slow.p, 0xFF, P * 4, st));
+    } else {
+        FpArgs G;
+        G.arena = F.arena.p;
+        G.blk_off = F.meta.p;
+        G.err = F.err.p;
+        G.slow = F.slow.p;
+        G.stride = stride;
+        F.bnd.ensure(P * stride * kFpM);
+        F.seg.ensure(P * stride);
+        F.ent.ensure(P * stride);
+        F.nseg.ensure(P);
+        F.ev.ensure(P * n);
+        F.evk.ensure(P * n);
+        G.bnd = F.bnd.p;
+        G.seg = F.seg.p;
+        G.ent = F.ent.p;
+        G.nseg = F.nseg.p;
+        G.ev = F.ev.p;
+        G.evk = F.evk.p;
+        G.rec = F.rec.p;
+        G.nrec = F.nrec.p;
+        G.rec_stride = stride;
+        G.n = n;
+        const unsigned segs = (unsigned)((P * stride + 127) / 128);
+        {
+            PROF("fp_spec", st);
+            launch_k(fp_spec, segs, 128, 0, st, G, T, (int)P);
+        }
+        {
+            PROF("fp_resolve", st);
+            launch_k(fp_resolve, (unsigned)((P + 31) / 32), 32, 0, st, G, T, (int)P);
+        }
+        {
+            PROF("fp_count", st);
+            launch_k(fp_count, segs, 128, 0, st, G, T, (int)P);
+        }
+        {
+            PROF("fp_evscan", st);
+            launch_k(fp_evscan, (unsigned)((P + 31) / 32), 32, 0, st, G, (int)P);
+        }
+        {
+            PROF("fp_events", st);
+            launch_k(fp_events, segs, 128, 0, st, G, T, (int)P);
+        }
+        {
+            PROF("fp_chain", st);
+            launch_k(fp_chain, (unsigned)P, 32, 0, st, G, (int)P);
+        }
+    }
+    A.only = F.slow.p;
     {
         PROF("fd_scan", st);
         launch_k(fd_scan, (unsigned)((P + 31) / 32), 32, 0, st, A, T, (int)P);
