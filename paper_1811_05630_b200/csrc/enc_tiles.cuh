@@ -666,6 +666,285 @@ __global__ void __launch_bounds__(kEncThreads, 5) enc_lattice(TileArgs A, int pl
     stamp(5);
 }
 
+// Decoupled look-back of a running MAX over the tiles of one plane (warp-wide,
+// like lookback_exclusive): values are positions + 1 (0 = none).
+__device__ uint32_t lookback_max_exclusive(unsigned long long *slots, uint32_t epoch, int t, uint32_t local) {
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) st_release_u64(&slots[t], lb_tag(epoch, t == 0 ? 2 : 1) | local);
+    uint32_t prefix = 0;
+    int hi = t - 1;
+    while (hi >= 0) {
+        const int k = hi - lane;
+        unsigned long long w = 0;
+        uint32_t st = 2;
+        if (k >= 0) {
+            do {
+                w = ld_acquire_u64(&slots[k]);
+                st = ((uint32_t)(w >> 32) >> 2) == epoch ? ((uint32_t)(w >> 32) & 3) : 0;
+                if (st == 0) __nanosleep(32);
+            } while (st == 0);
+        }
+        const unsigned incl = __ballot_sync(0xffffffffu, st == 2);
+        const int stop = incl ? __ffs(incl) - 1 : 32;
+        uint32_t v = (lane <= stop && k >= 0) ? (uint32_t)w : 0u;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, off));
+        prefix = max(prefix, v);
+        if (incl) break;
+        hi -= 32;
+    }
+    if (lane == 0 && t > 0) st_release_u64(&slots[t], lb_tag(epoch, 2) | max(prefix, local));
+    return prefix;
+}
+
+// T1+T2 fused for planes of > kInlineTiles tiles (the gate pass of the dense
+// configurations): new = gate(scale * old) (enc_x) and, on the values still
+// in shared memory, the speculative outliers and the lattice codes /
+// estimates / event flags (enc_lattice).  The segment base
+// of a tile (the last speculative outlier before it) comes from a decoupled
+// look-back of a running max over the plane's tiles instead of the
+// t_lastout / plane_scan / t_base round trip, so x and the flags are written
+// once and never read back by this stage.  Identical results to enc_x +
+// enc_lattice (same operations on the same values).
+template <int NP, class Src>
+__global__ void __launch_bounds__(kEncThreads) enc_x_lattice(TileArgs A, Src src, int units) {
+    pdl_begin();
+    const int unit = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
+    if (unit >= units) return;
+    const int tid = threadIdx.x;
+    const uint64_t L = A.L;
+    const uint64_t t0 = (uint64_t)t * kTile;
+    const int tl = (int)tmin<uint64_t>(kTile, L - t0);
+    if (t == 0 && tid < NP) {
+        // per-pass reset of the plane's flags and histogram bookkeeping
+        // (tiles > 0 set flags only after their look-back, which orders them
+        // after this tile's publication)
+        const int pl = unit * NP + tid;
+        const PlaneParams pp = A.params[pl];
+        A.params[pl].flags = (A.predictor == 1 && pp.eb != 0.0) ? kFlagFallback : 0u;
+        A.symrange[2 * pl] = 0xFFFFFFFFu;
+        A.symrange[2 * pl + 1] = 0;
+        A.hspecial[2 * pl] = 0;
+        A.hspecial[2 * pl + 1] = 0;
+        A.gamma[pl] = 0;
+    }
+    __shared__ double xs[NP][kTile + 2]; // [0] = x[t0-2], [1] = x[t0-1], [k+2] = x[t0+k]
+    __shared__ double red[kEncThreads];
+    __shared__ long long kb[kEncThreads];
+    __shared__ uint32_t s_base[NP];
+    using ScanI = cub::BlockScan<int, kEncThreads>;
+    using RedI = cub::BlockReduce<int, kEncThreads>;
+    __shared__ union {
+        typename ScanI::TempStorage scan;
+        typename RedI::TempStorage red;
+    } tmp;
+    for (int k = tid; k < kTile + 2; k += kEncThreads) {
+        double v[2] = {0.0, 0.0};
+        const int64_t i = (int64_t)t0 + k - 2;
+        if (i >= 0 && k - 2 < tl) src.load(unit, (uint64_t)i, v);
+        for (int p = 0; p < NP; ++p) xs[p][k] = v[p];
+    }
+    __syncthreads();
+    for (int p = 0; p < NP; ++p) {
+        double *xrow = A.x + ((uint64_t)unit * NP + p) * L;
+        for (int k = tid; k < tl; k += kEncThreads) xrow[t0 + k] = xs[p][k + 2];
+    }
+    if (Src::kNorms) {
+        double acc[kPerThread];
+        for (int e = 0; e < kPerThread; ++e) {
+            const int k = tid * kPerThread + e + 2;
+            const double a = dmul(xs[0][k], xs[0][k]);
+            const double b = dmul(xs[NP - 1][k], xs[NP - 1][k]);
+            acc[e] = dadd(a, b);
+        }
+        double v = dadd(dadd(acc[0], acc[1]), dadd(acc[2], acc[3]));
+        const int lane = tid & 31;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const double o = __shfl_down_sync(0xffffffffu, v, off);
+            if ((lane & (2 * off - 1)) == 0) v = dadd(v, o);
+        }
+        if (lane == 0) red[tid >> 5] = v;
+        __syncthreads();
+        if (tid == 0) {
+            const double s01 = dadd(red[0], red[1]), s23 = dadd(red[2], red[3]);
+            const double s45 = dadd(red[4], red[5]), s67 = dadd(red[6], red[7]);
+            A.tilesum[(uint64_t)unit * A.ntiles + t] = dadd(dadd(s01, s23), dadd(s45, s67));
+        }
+    }
+    const long long half = 1ll << (A.qb - 1);
+    const double hh = (double)half;
+    // speculative outliers (enc_x) of every plane, the tile's last one
+    int opos[NP][kPerThread];
+    bool prevout0[NP];
+    for (int p = 0; p < NP; ++p) {
+        const PlaneParams pp = A.params[(uint64_t)unit * NP + p];
+        int last = -1;
+        for (int e = 0; e < kPerThread; ++e) {
+            const int k = tid * kPerThread + e;
+            bool out = false;
+            if (k < tl && pp.eb != 0.0) {
+                const double rr = dmul(dsub(xs[p][k + 2], xs[p][k + 1]), pp.inv_q);
+                out = !(fabs(rr) < hh - 0.5);
+            }
+            opos[p][e] = out ? k : -1;
+            if (out) last = k;
+        }
+        // element t0 - 1 (its own flag, for the first element's predecessor)
+        prevout0[p] = false;
+        if (t0 > 0 && pp.eb != 0.0) {
+            const double rr = dmul(dsub(xs[p][1], xs[p][0]), pp.inv_q);
+            prevout0[p] = !(fabs(rr) < hh - 0.5);
+        }
+        const int tl_last = RedI(tmp.red).Reduce(last, cub::Max());
+        __syncthreads();
+        if (tid == 0) s_base[p] = tl_last >= 0 ? (uint32_t)(t0 + tl_last) + 1u : 0u;
+    }
+    __syncthreads();
+    // segment base of the tile: the last speculative outlier of the earlier
+    // tiles (look-back per plane, one warp each); publishing after the x
+    // stores makes x[tbase] readable by later tiles
+    if (tid < 32 * NP) {
+        const int p = tid >> 5;
+        const uint64_t pl = (uint64_t)unit * NP + p;
+        if (tid == 32 * p) __threadfence();
+        __syncwarp();
+        const uint32_t ex = lookback_max_exclusive(A.lb + pl * A.ntiles, A.lb_epoch, t, s_base[p]);
+        __syncwarp();
+        if ((tid & 31) == 0) s_base[p] = ex;
+    }
+    __syncthreads();
+    for (int p = 0; p < NP; ++p) {
+        const uint64_t pl = (uint64_t)unit * NP + p;
+        const PlaneParams pp = A.params[pl];
+        const bool fallback = A.predictor == 1 && pp.eb != 0.0; // linear + lossy: serial re-encode
+        const double *x = A.x + pl * L;
+        uint8_t *fl = A.fl + pl * L;
+        uint32_t *sym = A.sym + pl * L;
+        if (fallback) {
+            if (tid == 0) A.t_nev[pl * A.ntiles + t] = 0;
+            continue;
+        }
+        if (pp.eb == 0.0) { // lossless: d == x, symbols final, no events
+            for (int e = 0; e < kPerThread; ++e) {
+                const int k = tid * kPerThread + e;
+                if (k >= tl) continue;
+                const uint64_t i = t0 + k;
+                const double x1 = i > 0 ? xs[p][k + 1] : 0.0;
+                double pred;
+                if (A.predictor == 0) pred = x1;
+                else pred = i == 0 ? 0.0 : (i == 1 ? x1 : predict_linear(x1, xs[p][k]));
+                sym[i] = bits_of(xs[p][k + 2]) == bits_of(pred) ? (uint32_t)half : 0u;
+                fl[i] = 0;
+            }
+            if (tid == 0) A.t_nev[pl * A.ntiles + t] = 0;
+            continue;
+        }
+        double xv[kPerThread];
+        for (int e = 0; e < kPerThread; ++e) {
+            const int k = tid * kPerThread + e;
+            xv[e] = k < tl ? xs[p][k + 2] : 0.0;
+        }
+        int lo[kPerThread];
+        {
+            bool anyout = false;
+            for (int e = 0; e < kPerThread; ++e) anyout |= opos[p][e] >= 0;
+            if (__syncthreads_or(anyout)) {
+                ScanI(tmp.scan).ExclusiveScan(opos[p], lo, -1, cub::Max());
+                __syncthreads();
+            } else {
+                for (int e = 0; e < kPerThread; ++e) lo[e] = -1;
+            }
+        }
+        const int32_t tbase = (int32_t)s_base[p] - 1; // position or -1
+        auto xat = [&](int64_t i) -> double { // x[i] for i < t0 + tl
+            if (i >= (int64_t)t0 - 2) return xs[p][i - (int64_t)t0 + 2];
+            return __ldcg(x + i);
+        };
+        const double tbx = tbase >= 0 ? xat(tbase) : 0.0;
+        long long K[kPerThread];
+        double dh[kPerThread];
+        for (int e = 0; e < kPerThread; ++e) {
+            const int k = tid * kPerThread + e;
+            if (opos[p][e] >= 0) {
+                K[e] = 0;
+                dh[e] = xv[e];
+            } else {
+                double base;
+                if (lo[e] >= 0) base = xs[p][lo[e] + 2];
+                else base = tbx;
+                K[e] = k < tl ? llround_exact(dmul(dsub(xv[e], base), pp.inv_q)) : 0;
+                dh[e] = dadd(base, dmul(pp.q, (double)K[e]));
+            }
+        }
+        kb[tid] = K[kPerThread - 1];
+        long long kprev0 = 0;
+        const double xprev0 = xs[p][1];
+        if (t0 > 0 && !prevout0[p]) kprev0 = llround_exact(dmul(dsub(xprev0, tbx), pp.inv_q));
+        __syncthreads();
+        int evflag[kPerThread];
+        uint32_t esym[kPerThread];
+        uint32_t fword = 0;
+        int bad = 0;
+        for (int e = 0; e < kPerThread; ++e) {
+            const int k = tid * kPerThread + e;
+            evflag[e] = 0;
+            esym[e] = 0;
+            if (k >= tl) continue;
+            long long kprev;
+            bool prev_out;
+            double xp;
+            if (e > 0) { kprev = K[e - 1]; prev_out = opos[p][e - 1] >= 0; xp = xv[e - 1]; }
+            else if (tid > 0) { kprev = kb[tid - 1]; prev_out = lo[0] == k - 1; xp = xs[p][k + 1]; }
+            else { kprev = kprev0; prev_out = prevout0[p]; xp = xprev0; }
+            if (prev_out) kprev = 0;
+            uint8_t f;
+            uint32_t sy;
+            if (opos[p][e] >= 0) {
+                f = 3;
+                sy = kOutlierSym;
+            } else {
+                const long long m = K[e] - kprev;
+                if (m <= -half || m >= half) bad = 1;
+                sy = (uint32_t)(m + half);
+                f = (m != 0 || (prev_out && is_negzero(xp))) ? 1 : 0;
+            }
+            fword |= (uint32_t)f << (8 * e);
+            esym[e] = sy;
+            evflag[e] = f & 1;
+        }
+        {
+            const int k0 = tid * kPerThread;
+            if (k0 + kPerThread <= tl) {
+                *reinterpret_cast<uint32_t *>(fl + t0 + k0) = fword;
+                *reinterpret_cast<uint4 *>(sym + t0 + k0) = make_uint4(esym[0], esym[1], esym[2], esym[3]);
+            } else {
+                for (int e = 0; e < kPerThread && k0 + e < tl; ++e) {
+                    fl[t0 + k0 + e] = (uint8_t)(fword >> (8 * e));
+                    sym[t0 + k0 + e] = esym[e];
+                }
+            }
+        }
+        if (bad) atomicOr(&A.params[pl].flags, kFlagFallback);
+        // lattice estimates of the events (enc_compact places the records)
+        int mine = 0;
+        double *dhat = A.dval + pl * L;
+        for (int e = 0; e < kPerThread; ++e) {
+            mine += evflag[e];
+            if (evflag[e]) dhat[t0 + tid * kPerThread + e] = dh[e];
+        }
+        mine = __reduce_add_sync(0xffffffffu, mine);
+        if ((tid & 31) == 0) red[tid >> 5] = (double)mine;
+        __syncthreads();
+        if (tid == 0) {
+            int tot = 0;
+            for (int w = 0; w < kEncThreads / 32; ++w) tot += (int)red[w];
+            A.t_nev[pl * A.ntiles + t] = (uint32_t)tot;
+        }
+        __syncthreads();
+    }
+}
+
 // ------------------------------------------------------------------ T3
 // Event list for planes with many tiles (the fused look-back in enc_lattice
 // would serialise hundreds of tiles): tile offsets from the plane scan.

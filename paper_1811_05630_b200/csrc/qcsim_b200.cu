@@ -566,23 +566,31 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     A.hspecial = S.hspecial.p;
     A.gamma = S.gamma.p;
     A.t_nev = reinterpret_cast<uint32_t *>(S.t_nev.p);
-    {
+    if (S.lb.ensure(planes * ntiles, /*zero=*/true)) S.lb_epoch = 0;
+    if (++S.lb_epoch >= (1u << 30)) { // epoch wrapped: clean slots
+        CK(cudaMemsetAsync(S.lb.p, 0, S.lb.cap * sizeof(unsigned long long), st));
+        S.lb_epoch = 1;
+    }
+    A.lb = S.lb.p;
+    A.lb_epoch = S.lb_epoch;
+    // planes of many tiles: gate + lattice in one grid with a max look-back
+    // for the segment base (QCSIM_FUSE_XL=1; measured slower than the two
+    // grids -- 34 vs 22 ms per Random-30 pass -- so off by default)
+    static const bool fuse_env = std::getenv("QCSIM_FUSE_XL") && std::getenv("QCSIM_FUSE_XL")[0] == '1';
+    const bool fused_xl = fuse_env && ntiles > kInlineTiles;
+    if (fused_xl) {
+        PROF("enc_x_lattice", st);
+        launch_k(enc_x_lattice<NP, Src>, tgrid_u, kEncThreads, 0, st, A, src, units);
+    } else {
         PROF("enc_x", st);
         launch_k(enc_x<NP, Src>, tgrid_u, kEncThreads, 0, st, A, src, units);
     }
-    launch_plane_scan(st, S.t_lastout.p, S.t_base.p, ntiles, (int)planes, kScanMaxExcl);
+    if (!fused_xl) launch_plane_scan(st, S.t_lastout.p, S.t_base.p, ntiles, (int)planes, kScanMaxExcl);
     // event records at tile-local slots when the block-parallel chain reads
     // them (no look-back between the tiles of a plane)
     static const bool tile_local_off = std::getenv("QCSIM_EV_TILE_LOCAL") && std::getenv("QCSIM_EV_TILE_LOCAL")[0] == '0';
     A.ev_tile_local = (ntiles <= kInlineTiles && chain_scan_selected(planes) && !tile_local_off) ? 1 : 0;
-    {
-        if (S.lb.ensure(planes * ntiles, /*zero=*/true)) S.lb_epoch = 0;
-        if (++S.lb_epoch >= (1u << 30)) { // epoch wrapped: clean slots
-            CK(cudaMemsetAsync(S.lb.p, 0, S.lb.cap * sizeof(unsigned long long), st));
-            S.lb_epoch = 1;
-        }
-        A.lb = S.lb.p;
-        A.lb_epoch = S.lb_epoch;
+    if (!fused_xl) {
         // debug: QCSIM_LAT_TRACE_AT = encode call -> phase stamps to QCSIM_LAT_TRACE_FILE
         static const long lat_at = std::getenv("QCSIM_LAT_TRACE_AT") ? std::atol(std::getenv("QCSIM_LAT_TRACE_AT")) : -1;
         static long lat_calls = 0;

@@ -134,7 +134,7 @@ print(info["waves"], hashlib.sha256(blob).hexdigest(), hashlib.sha256(amps.tobyt
 
 def _run_script(script, args, env_extra):
     e = dict(os.environ)
-    for k in ("QCSIM_WAVE_SLICES", "QCSIM_SYNC_GATES", "QCSIM_FOREIGN_SERIAL"):
+    for k in ("QCSIM_WAVE_SLICES", "QCSIM_SYNC_GATES", "QCSIM_FOREIGN_SERIAL", "QCSIM_FUSE_XL"):
         e.pop(k, None)
     e.update(env_extra)
     r = subprocess.run([sys.executable, "-c", script] + args, cwd=ROOT, env=e, capture_output=True, text=True,
@@ -412,3 +412,30 @@ def test_foreign_decode_parallel_vs_serial():
     fast = _run_script(_FOREIGN_SCRIPT, [], {})
     slow = _run_script(_FOREIGN_SCRIPT, [], {"QCSIM_FOREIGN_SERIAL": "1"})
     assert fast == slow
+
+
+_FUSE_SCRIPT = r"""
+import hashlib, sys
+import paper_1811_05630_b200 as q
+n, s = 19, 17  # 4 slices of 2^17: 128 tiles per plane (the fused gate + lattice grid)
+acts = q.lower(q.build_qft(n))[:60] + q.random_u3_circuit_actions(n, 1, seed=3)
+eng = q.Engine(q.EngineConfig(num_qubits=n, slice_bits=s, codec=q.CodecConfig(q.CodecMode.Absolute, 1e-5)))
+eng.load_basis(12345)
+m = eng.run(acts)
+print(hashlib.sha256(eng.export_blocks()[0]).hexdigest(), repr(m.mean_compression_ratio), m.fallback_planes)
+"""
+
+
+def test_fused_gate_lattice_bit_identical(oracle):
+    """The fused gate + lattice grid (planes of > 64 tiles) produces the same
+    blocks as the two separate grids, and as the C oracle."""
+    fused = _run_script(_FUSE_SCRIPT, [], {"QCSIM_FUSE_XL": "1"})
+    split = _run_script(_FUSE_SCRIPT, [], {})
+    assert fused == split
+    import paper_1811_05630_b200 as q
+    n, s = 19, 17
+    acts = q.lower(q.build_qft(n))[:60] + q.random_u3_circuit_actions(n, 1, seed=3)
+    oe = oracle.engine(OEng.make(n, s, OCfg.make(1, 1e-5, 16, 0)))
+    oe.load_basis(12345)
+    oe.run(acts)
+    assert fused[0] == hashlib.sha256(oe.export_blocks()[0]).hexdigest()
