@@ -75,6 +75,11 @@ class Engine {
     std::vector<GateMetrics> gate_metrics() const;
     StateVector gather_state(int guard_qubits = 28) const; // dense StateVector
     std::vector<CompressedPlanes> compressed_slices() const; // checkpoint
+    std::vector<double> slice_norms() const;                 // cached sq_norm per slice (statevec.hpp:72)
+    // Resume from a checkpoint: the slices' QCB1 planes, their cached sq_norm
+    // and the number of gates already applied (qcsim_engine_load_blocks).
+    void resume(const std::vector<CompressedPlanes> &slices, const std::vector<double> &sq_norms,
+                uint64_t gates_done = 0);
 
     int num_qubits() const { return n_; }
     int slice_bits() const { return s_; }

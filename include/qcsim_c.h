@@ -257,6 +257,25 @@ qcsim_status qcsim_engine_export_blocks(qcsim_engine *eng, uint8_t *out,
                                         uint64_t capacity, uint64_t *len,
                                         uint64_t *offsets, uint64_t offsets_cap);
 
+/* Resume from a checkpoint (CompressedBlock::from_bytes,
+ * codec.cpp:366-408): `blocks` holds this rank's 2 * local_slices QCB1 blocks
+ * in export_blocks order (host bytes), offsets[planes + 1] their starts;
+ * `sq_norms` is the table of EVERY slice's cached sq_norm (2^(n-s) doubles,
+ * statevec.hpp:72) and `gates_done` the number of gates already applied (it
+ * continues the gate numbering of norm_every and the drift message).  Every
+ * block goes through the from_bytes / decompress_plane checks (CodecError
+ * with the reference's message) and must match the engine's codec (mode,
+ * predictor, quant_code_bits, element count).  The state is rebuilt wave by
+ * wave on the device (decode -> the engine's own encoder, which reproduces
+ * the block bytes and adds the decode index); a block that does not
+ * re-encode to its own size is rejected (QCSIM_CODEC).  Absolute and
+ * Lossless bounds only (a RangeRelative bound depends on the pre-compression
+ * range, which a block does not carry). */
+qcsim_status qcsim_engine_load_blocks(qcsim_engine *eng, const uint8_t *blocks,
+                                      uint64_t len, const uint64_t *offsets,
+                                      uint64_t planes, const double *sq_norms,
+                                      uint64_t norm_count, uint64_t gates_done);
+
 /* Multi-rank hooks (slice sharding).  A gate whose
  * butterfly/swap partner slice lives on another rank needs that slice's
  * compressed planes: `exchange_plan` lists (local slice, remote slice)

@@ -78,6 +78,7 @@ SIGNATURES = [
     ("qcsim_engine_destroy", C.c_int, [C.c_void_p]),
     ("qcsim_engine_load_basis", C.c_int, [C.c_void_p, C.c_uint64]),
     ("qcsim_engine_load_amplitudes", C.c_int, [C.c_void_p, dp, C.c_uint64]),
+    ("qcsim_engine_load_blocks", C.c_int, [C.c_void_p, u8p, C.c_uint64, u64p, C.c_uint64, dp, C.c_uint64, C.c_uint64]),
     ("qcsim_engine_run", C.c_int, [C.c_void_p, P(ActionC), C.c_uint64, P(RunMetricsC)]),
     ("qcsim_engine_gather", C.c_int, [C.c_void_p, dp, C.c_uint64, C.c_int32]),
     ("qcsim_engine_slice_norms", C.c_int, [C.c_void_p, dp, C.c_uint64]),

@@ -27,6 +27,8 @@ constexpr uint32_t kHeaderBytes = 40;
 
 // Encoder tiling.
 constexpr int kTile = 1024;          // elements per encoder tile
+constexpr int kTileLog2 = 10;
+static_assert((1 << kTileLog2) == kTile, "tile size");
 constexpr int kEncThreads = 256;     // threads per encoder block
 constexpr int kPerThread = kTile / kEncThreads;
 // Symbol window histogrammed in shared memory: m in [-kWin/2, kWin/2).

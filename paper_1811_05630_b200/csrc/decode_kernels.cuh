@@ -8,9 +8,9 @@
 // D2 dec_chunks   one thread per (plane, checkpoint chunk): resumes from the
 //                 encoder's IndexRec and reproduces codec.cpp:591-626 for
 //                 C elements -- chunk-parallel and bit-exact.
-// DV dec_validate one thread per plane, byte-serial, every check and error
-//                 of codec.cpp:535-633 in the reference's order: the path for
-//                 foreign blocks (host API), no index needed.
+// FD fd_head / fd_scan (below) + foreign_kernels.cuh: blocks without a decode
+//                 index (host API, partner imports), every check and error of
+//                 codec.cpp:535-633 in the reference's order.
 #pragma once
 
 #include "common.cuh"
@@ -39,6 +39,13 @@ struct DecPlanes {
     const uint32_t *ext_nrec = nullptr;  // [plane]
     uint64_t ext_stride = 0;
     const uint32_t *skip = nullptr;      // [plane] != 0: not decoded (a codec error was found)
+    // Zero-tile flags (run-aware gate pass, SURVEY.md §7 H1 "run-aware
+    // shortcut"): an encoder tile (kTile elements) that lies inside one long
+    // run of +0.0 is not written at all; zflag[plane * ztiles + tile] = 1
+    // tells the gate kernel that the tile's values are +0.0.  The flags are
+    // cleared before the grid runs.  nullptr: every element is written.
+    uint8_t *zflag = nullptr;
+    uint32_t ztiles = 0;
 };
 
 __device__ __forceinline__ uint64_t load_le(const uint8_t *p, int bytes) {
@@ -441,23 +448,38 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
     __syncthreads();
     // long constant runs, coalesced by the whole block
     const uint32_t nf = tmin<uint32_t>(S.nfill, (uint32_t)kDecFills);
-    for (uint32_t f = 0; f < nf; ++f) {
-        const DecFill F = S.fill[f];
-        uint64_t st = F.start, len = F.len;
+    auto fill_range = [&](uint64_t st, uint64_t len, double v) {
+        if (len == 0) return;
         if (st & 1) { // 16-byte aligned vector stores after an odd head
-            if (threadIdx.x == 0) out[st] = F.v;
+            if (threadIdx.x == 0) out[st] = v;
             ++st;
             --len;
         }
         double4 *o4 = reinterpret_cast<double4 *>(out + st);
         const uint64_t n4 = (st & 3) ? 0 : len / 4; // 32-byte stores when aligned
-        const double4 v4 = make_double4(F.v, F.v, F.v, F.v);
+        const double4 v4 = make_double4(v, v, v, v);
         for (uint64_t k = threadIdx.x; k < n4; k += kDecThreads) o4[k] = v4;
         double2 *o2 = reinterpret_cast<double2 *>(out + st + 4 * n4);
         const uint64_t rest = len - 4 * n4;
-        const double2 v2 = make_double2(F.v, F.v);
+        const double2 v2 = make_double2(v, v);
         for (uint64_t k = threadIdx.x; k < rest / 2; k += kDecThreads) o2[k] = v2;
-        if ((rest & 1) && threadIdx.x == 0) out[st + 4 * n4 + rest - 1] = F.v;
+        if ((rest & 1) && threadIdx.x == 0) out[st + 4 * n4 + rest - 1] = v;
+    };
+    for (uint32_t f = 0; f < nf; ++f) {
+        const DecFill F = S.fill[f];
+        if (D.zflag && bits_of(F.v) == 0ull) {
+            // whole tiles of +0.0: flagged, not written (the gate kernel
+            // reads the flag); the ragged head and tail are written
+            const uint64_t t_lo = (F.start + kTile - 1) >> kTileLog2, t_hi = (F.start + F.len) >> kTileLog2;
+            if (t_hi > t_lo) {
+                uint8_t *zf = D.zflag + (uint64_t)pl * D.ztiles;
+                for (uint64_t t = t_lo + threadIdx.x; t < t_hi; t += kDecThreads) zf[t] = 1;
+                fill_range(F.start, (t_lo << kTileLog2) - F.start, F.v);
+                fill_range(t_hi << kTileLog2, F.start + F.len - (t_hi << kTileLog2), F.v);
+                continue;
+            }
+        }
+        fill_range(F.start, F.len, F.v);
     }
 }
 
@@ -496,192 +518,6 @@ enum DecErr : uint32_t {
     kDecPayTrunc,         // "block payload truncated"
     kDecWrongLen,         // element_count differs from the destination plane
 };
-
-struct ValArgs {
-    const uint8_t *blocks;     // device bytes
-    const uint64_t *blk_off;   // [plane]
-    double *const *out;        // [plane]
-    uint32_t *err;             // [plane]
-    // scratch per plane for the (len, sym) sort
-    uint32_t *ssym;            // [plane][cap]
-    uint8_t *slen;             // [plane][cap]
-    uint64_t cap;
-    const uint64_t *avail = nullptr; // [plane] bytes available: check the header on the device
-    uint64_t n_expected = 0;         // != 0: element_count must equal it
-};
-
-struct ByteBits {
-    const uint8_t *p;
-    uint64_t n, byte;
-    int bit;
-    __device__ __forceinline__ int get(bool &trunc) {
-        if (byte >= n) { trunc = true; return 0; }
-        const int b = (p[byte] >> (7 - bit)) & 1;
-        if (++bit == 8) { bit = 0; ++byte; }
-        return b;
-    }
-};
-
-// Header (from_bytes) checks are done by the caller; this is
-// decompress_plane's payload part.  One thread per plane.
-__global__ void dec_validate(ValArgs A, int planes) {
-    pdl_begin();
-    const int pl = blockIdx.x * blockDim.x + threadIdx.x;
-    if (pl >= planes) return;
-    const uint8_t *blk = A.blocks + A.blk_off[pl];
-    auto fail = [&](uint32_t e) { A.err[pl] = e; };
-    if (A.avail) { // CompressedBlock::from_bytes checks, in the reference's order
-        const uint64_t len = A.avail[pl];
-        if (len < kHeaderBytes) return fail(kDecHdrTrunc);
-        if (blk[0] != 'Q' || blk[1] != 'C' || blk[2] != 'B' || blk[3] != '1') return fail(kDecMagic);
-        if (blk[4] != 1) return fail(kDecVersion);
-        if (blk[5] > 2) return fail(kDecModeByte);
-        if (blk[6] > 1) return fail(kDecPredByte);
-        if (blk[7] < 4 || blk[7] > 24) return fail(kDecQbRange);
-        const uint64_t hn = load_le(blk + 8, 8), ho = load_le(blk + 24, 8), hp = load_le(blk + 32, 8);
-        const double heb = __longlong_as_double((long long)load_le(blk + 16, 8));
-        if (hn == 0) return fail(kDecCount0);
-        if (ho > hn) return fail(kDecOutCount);
-        if (!(heb >= 0.0) || !isfinite(heb)) return fail(kDecEbBad);
-        if (hp > len - kHeaderBytes) return fail(kDecPayTrunc);
-        if (A.n_expected && hn != A.n_expected) return fail(kDecWrongLen);
-    }
-    const uint8_t pred_kind = blk[6];
-    const int qb = blk[7];
-    const uint64_t n = load_le(blk + 8, 8);
-    const double eb = __longlong_as_double((long long)load_le(blk + 16, 8));
-    const double q = dmul(2.0, eb);
-    const uint64_t nout = load_le(blk + 24, 8);
-    const uint64_t plen = load_le(blk + 32, 8);
-    const long long half = 1ll << (qb - 1);
-    const uint32_t rsym = 1u << qb;
-    const uint8_t *pl_ = blk + kHeaderBytes;
-    double *out = A.out[pl];
-    if (plen < 4) return fail(kDecPayloadSmall);
-    const uint32_t tc = (uint32_t)load_le(pl_, 4);
-    const uint64_t table_bytes = 4 + (uint64_t)tc * 5;
-    if (tc == 0) return fail(kDecTableEmpty);
-    if (plen < table_bytes) return fail(kDecTableTrunc);
-    if (tc > A.cap) return fail(kDecNoMem);
-    uint32_t cnt[kMaxCodeLen + 1];
-    for (int l = 0; l <= kMaxCodeLen; ++l) cnt[l] = 0;
-    uint32_t prev = 0;
-    for (uint32_t i = 0; i < tc; ++i) {
-        const uint32_t s = (uint32_t)load_le(pl_ + 4 + 5ull * i, 4);
-        const uint8_t l = pl_[4 + 5ull * i + 4];
-        if (i > 0 && s <= prev) return fail(kDecSymOrder);
-        if (s > rsym) return fail(kDecSymRange);
-        if (l < 1 || l > kMaxCodeLen) return fail(kDecLenRange);
-        ++cnt[l];
-        prev = s;
-    }
-    // PrefixDecoder: canonical codes, kraft in (len, sym) order
-    uint64_t first[kMaxCodeLen + 1];
-    uint32_t basei[kMaxCodeLen + 1];
-    {
-        uint64_t c = 0;
-        int prevl = -1;
-        uint32_t b = 0;
-        double kraft = 0.0;
-        for (int l = 1; l <= kMaxCodeLen; ++l) {
-            first[l] = 0;
-            basei[l] = b;
-            if (!cnt[l]) continue;
-            if (prevl >= 0) c <<= (l - prevl);
-            first[l] = c;
-            c += cnt[l];
-            b += cnt[l];
-            prevl = l;
-            const double term = ldexp(1.0, -l);
-            for (uint32_t k = 0; k < cnt[l]; ++k) kraft = dadd(kraft, term);
-        }
-        if (kraft > 1.0 + 1e-9) return fail(kDecOverfull);
-    }
-    int maxlen = 0;
-    for (int l = 1; l <= kMaxCodeLen; ++l)
-        if (cnt[l]) maxlen = l;
-    uint32_t *sorted = A.ssym + (uint64_t)pl * A.cap;
-    {
-        uint32_t next[kMaxCodeLen + 1];
-        for (int l = 0; l <= kMaxCodeLen; ++l) next[l] = basei[l];
-        for (uint32_t i = 0; i < tc; ++i) {
-            const uint8_t l = pl_[4 + 5ull * i + 4];
-            sorted[next[l]++] = (uint32_t)load_le(pl_ + 4 + 5ull * i, 4);
-        }
-    }
-    const uint64_t obytes = nout * 16;
-    if (plen < table_bytes + obytes) return fail(kDecLenMismatch);
-    const uint64_t sbytes = plen - table_bytes - obytes;
-    ByteBits br{pl_ + table_bytes, sbytes, 0, 0};
-    const uint8_t *oreg = pl_ + table_bytes + sbytes;
-    uint64_t ocur = 0, i = 0;
-    uint32_t last = rsym;
-    double d1 = 0.0, d2 = 0.0;
-    bool trunc = false;
-    while (i < n) {
-        uint64_t acc = 0;
-        uint32_t s = 0;
-        bool found = false;
-        for (int l = 1; l <= maxlen; ++l) {
-            acc = (acc << 1) | (uint64_t)br.get(trunc);
-            if (trunc) return fail(kDecStreamTrunc);
-            if (cnt[l] != 0) {
-                const uint64_t off = acc - first[l];
-                if (acc >= first[l] && off < cnt[l]) {
-                    s = sorted[basei[l] + (uint32_t)off];
-                    found = true;
-                    break;
-                }
-            }
-        }
-        if (!found) return fail(kDecInvalidCode);
-        uint64_t reps = 1;
-        uint32_t es = s;
-        if (s == rsym) {
-            if (last == rsym || last == kOutlierSym) return fail(kDecRunNoCode);
-            int zeros = 0;
-            for (;;) {
-                const int b = br.get(trunc);
-                if (trunc) return fail(kDecStreamTrunc);
-                if (b) break;
-                if (++zeros > 63) return fail(kDecRunRange);
-            }
-            uint64_t v = 1;
-            for (int k = 0; k < zeros; ++k) {
-                v = (v << 1) | (uint64_t)br.get(trunc);
-                if (trunc) return fail(kDecStreamTrunc);
-            }
-            if (v > n - i) return fail(kDecRunOverflow);
-            reps = v;
-            es = last;
-        } else {
-            last = s;
-        }
-        for (uint64_t k = 0; k < reps; ++k) {
-            double pred;
-            if (pred_kind == 0) pred = i > 0 ? d1 : 0.0;
-            else pred = i == 0 ? 0.0 : (i == 1 ? d1 : predict_linear(d1, d2));
-            double v;
-            if (es == kOutlierSym) {
-                if (ocur >= nout) return fail(kDecOutExhausted);
-                const uint64_t pos = load_le(oreg + 16 * ocur, 8);
-                if (pos != i) return fail(kDecOutPos);
-                v = __longlong_as_double((long long)load_le(oreg + 16 * ocur + 8, 8));
-                ++ocur;
-            } else {
-                const long long m = (long long)es - half;
-                v = eb == 0.0 ? pred : dadd(pred, dmul(q, (double)m));
-            }
-            out[i] = v;
-            d2 = d1;
-            d1 = v;
-            ++i;
-        }
-    }
-    if (ocur != nout) return fail(kDecOutUnused);
-    if (br.byte + (br.bit != 0) != sbytes) return fail(kDecStreamLen);
-    A.err[pl] = kDecOk;
-}
 
 
 // ------------------------------------------------------- foreign blocks

@@ -23,6 +23,8 @@
 //   TC tok_emit      tokens, outlier records, decode-index token state
 #pragma once
 
+#include <type_traits>
+
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
@@ -44,6 +46,15 @@ struct TileArgs {
     unsigned long long *lb; // [plane][ntiles] event-offset look-back slots (epoch-tagged)
     uint32_t lb_epoch;
     unsigned long long *trace; // debug: enc_lattice phase stamps, 8 per block
+    // Run-aware shortcuts for planes of many tiles (nullptr: off).
+    //   zx[plane][tile]    = 1: the tile's new values are all +-0.0 (enc_x);
+    //   ztriv[plane][tile] = 1: the tile's final symbols are all the zero
+    //                        code, continuing a run that began before the
+    //                        tile, no outliers (enc_verify) -- the tokenizer
+    //                        treats it as flat without loading its symbols.
+    uint8_t *zx, *ztriv;
+    int want_evD;          // the block-parallel chain reads the lattice estimates (evD);
+                           // the serial warp chain does not: they are not written
     int ev_tile_local;     // event records at tile-local slots (tile * kTile + rank), no
                            // plane-wide offsets: the chain-scan kernel maps ordinals
     // run statistics of the final symbols (tokenizer input, codec.cpp:468-482),
@@ -286,8 +297,9 @@ __device__ __forceinline__ int32_t carry_of(const int32_t *scanned, int scanned_
 }
 
 // ------------------------------------------------------------------ T1
-template <int NP, class Src>
-__global__ void __launch_bounds__(kEncThreads) enc_x(TileArgs A, Src src, int units) {
+// kVec: element pairs through Src::load2 (16-byte loads) instead of load().
+template <int NP, class Src, bool kVec>
+__global__ void __launch_bounds__(kEncThreads, 5) enc_x(TileArgs A, Src src, int units) {
     pdl_begin();
     const int unit = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
     if (unit >= units) return;
@@ -310,17 +322,57 @@ __global__ void __launch_bounds__(kEncThreads) enc_x(TileArgs A, Src src, int un
     __shared__ double red[kEncThreads];
     using RedI = cub::BlockReduce<int, kEncThreads>;
     __shared__ typename RedI::TempStorage red_tmp;
-    // striped load/compute (coalesced), element t0-1 as xs[.][0]
-    for (int k = tid; k <= kTile; k += kEncThreads) {
-        double v[2] = {0.0, 0.0};
-        const int64_t i = (int64_t)t0 + k - 1;
-        if (k == 0 ? t0 > 0 : k - 1 < tl) src.load(unit, (uint64_t)i, v);
-        for (int p = 0; p < NP; ++p) xs[p][k] = v[p];
-    }
+    // Element pairs, striped over the block (coalesced; 16-byte loads where
+    // the source has them); element t0-1 as xs[.][0].  Blocks none of whose
+    // source tiles carries a decoder zero flag read without looking at flags.
+    static_assert(kTile % 2 == 0, "pairs");
+    __shared__ int s_flagged;
+    if (tid == 0) s_flagged = src.flagged_sources(unit, (uint32_t)t) ? 1 : 0;
     __syncthreads();
-    for (int p = 0; p < NP; ++p) {
-        double *xrow = A.x + ((uint64_t)unit * NP + p) * L;
-        for (int k = tid; k < tl; k += kEncThreads) xrow[t0 + k] = xs[p][k + 1];
+    const bool flagged = s_flagged != 0;
+    int nonzero[NP];
+    for (int p = 0; p < NP; ++p) nonzero[p] = 0;
+    auto load_tile = [&](auto kF) {
+        constexpr bool kFlags = decltype(kF)::value;
+#pragma unroll 2
+        for (int k2 = tid; k2 < kTile / 2; k2 += kEncThreads) {
+            double a[2] = {0.0, 0.0}, b[2] = {0.0, 0.0};
+            const int k = 2 * k2;
+            if (kVec && k + 1 < tl) src.template load2f<kFlags>(unit, t0 + k, a, b);
+            else {
+                if (k < tl) src.template loadf<kFlags>(unit, t0 + k, a);
+                if (k + 1 < tl) src.template loadf<kFlags>(unit, t0 + k + 1, b);
+            }
+            for (int p = 0; p < NP; ++p) {
+                xs[p][k + 1] = a[p];
+                xs[p][k + 2] = b[p];
+                nonzero[p] |= (a[p] != 0.0) | (b[p] != 0.0); // (NaN counts as nonzero)
+            }
+            // the new values go out as they arrive (one 16-byte store per plane)
+            for (int p = 0; p < NP; ++p) {
+                double *xrow = A.x + ((uint64_t)unit * NP + p) * L + t0 + k;
+                if (k + 1 < tl && (L & 1) == 0) *reinterpret_cast<double2 *>(xrow) = make_double2(a[p], b[p]);
+                else {
+                    if (k < tl) xrow[0] = a[p];
+                    if (k + 1 < tl) xrow[1] = b[p];
+                }
+            }
+        }
+        if (tid == 0) {
+            double v[2] = {0.0, 0.0};
+            if (t0 > 0) src.template loadf<kFlags>(unit, t0 - 1, v);
+            for (int p = 0; p < NP; ++p) xs[p][0] = v[p];
+        }
+    };
+    if (flagged) load_tile(std::true_type{});
+    else load_tile(std::false_type{});
+    if (A.zx) { // all-zero tiles are flagged for the later grids
+        for (int p = 0; p < NP; ++p) {
+            const int any = __syncthreads_or(nonzero[p]);
+            if (tid == 0) A.zx[((uint64_t)unit * NP + p) * A.ntiles + t] = any ? 0 : 1;
+        }
+    } else {
+        __syncthreads();
     }
     if (Src::kNorms) {
         double acc[kPerThread];
@@ -511,6 +563,35 @@ __global__ void __launch_bounds__(kEncThreads, 5) enc_lattice(TileArgs A, int pl
         }
         return;
     }
+    if (A.zx && A.ntiles > kInlineTiles && tl == kTile && A.zx[(uint64_t)pl * A.ntiles + t]) {
+        // Every value of the tile is +-0.0 (enc_x), so K is the same for all
+        // its elements and only the first one can carry a code: when it does
+        // not (and is no speculative outlier), the tile is the zero code
+        // throughout -- no value loads, no scans.  Same operations as the
+        // general path below for these inputs (block-uniform decision).
+        bool trivial = !(fl[t0] & 2);
+        if (trivial) {
+            const int32_t tb = A.t_base[(uint64_t)pl * A.ntiles + t]; // last outlier before the tile or -1
+            const double base = tb >= 0 ? x[tb] : 0.0;
+            const long long Kz = llround_exact(dmul(dsub(0.0, base), pp.inv_q));
+            long long kprev = 0;
+            bool prev_out = false;
+            double xp = 0.0;
+            if (t0 > 0) {
+                xp = x[t0 - 1];
+                prev_out = (fl[t0 - 1] & 2) != 0;
+                if (!prev_out) kprev = llround_exact(dmul(dsub(xp, base), pp.inv_q));
+            }
+            trivial = Kz - kprev == 0 && !(prev_out && is_negzero(xp));
+        }
+        if (trivial) {
+            const uint32_t hs = (uint32_t)half;
+            *reinterpret_cast<uint4 *>(sym + t0 + tid * kPerThread) = make_uint4(hs, hs, hs, hs);
+            // (the flags enc_x wrote are already 0: no speculative outliers)
+            if (tid == 0) A.t_nev[(uint64_t)pl * A.ntiles + t] = 0;
+            return;
+        }
+    }
     // speculative outliers of this tile and the element before it
     int opos[kPerThread];
     double xv[kPerThread];
@@ -629,9 +710,11 @@ __global__ void __launch_bounds__(kEncThreads, 5) enc_lattice(TileArgs A, int pl
     if (!fused) {
         // lattice estimates of the events only (enc_compact reads them there;
         // dval is scratch until the chain overwrites it)
-        double *dhat = A.dval + (uint64_t)pl * L;
-        for (int e = 0; e < kPerThread; ++e)
-            if (evflag[e]) dhat[t0 + tid * kPerThread + e] = dh[e];
+        if (A.want_evD) {
+            double *dhat = A.dval + (uint64_t)pl * L;
+            for (int e = 0; e < kPerThread; ++e)
+                if (evflag[e]) dhat[t0 + tid * kPerThread + e] = dh[e];
+        }
         if (tid == 0) A.t_nev[(uint64_t)pl * A.ntiles + t] = (uint32_t)tot;
         return;
     }
@@ -661,7 +744,7 @@ __global__ void __launch_bounds__(kEncThreads, 5) enc_lattice(TileArgs A, int pl
         // addend q*m^ (or the outlier value), lattice estimate of d
         ev[o] = i | (out ? 0x80000000u : 0u);
         evc[o] = out ? xv[e] : dmul(pp.q, (double)((long long)esym[e] - half));
-        evD[o] = dh[e];
+        if (A.want_evD) evD[o] = dh[e];
     }
     stamp(5);
 }
@@ -931,7 +1014,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_x_lattice(TileArgs A, Src src
         double *dhat = A.dval + pl * L;
         for (int e = 0; e < kPerThread; ++e) {
             mine += evflag[e];
-            if (evflag[e]) dhat[t0 + tid * kPerThread + e] = dh[e];
+            if (evflag[e] && A.want_evD) dhat[t0 + tid * kPerThread + e] = dh[e];
         }
         mine = __reduce_add_sync(0xffffffffu, mine);
         if ((tid & 31) == 0) red[tid >> 5] = (double)mine;
@@ -980,7 +1063,7 @@ __device__ __forceinline__ void compact_tile(const TileArgs &A, int pl, int t) {
         // and the element index with bit 31 = outlier
         ev[base + pos[e]] = (uint32_t)i | (out ? 0x80000000u : 0u);
         evc[base + pos[e]] = out ? x[i] : dmul(q, (double)((long long)sym[i] - half));
-        evD[base + pos[e]] = dhat[i];
+        if (A.want_evD) evD[base + pos[e]] = dhat[i];
     }
 }
 // Grid of (plane, K) blocks; block (p, y) takes the plane's tiles y, y + K,
@@ -1205,14 +1288,48 @@ __device__ __forceinline__ void verify_tile(const TileArgs &A, int planes, const
         tile_stats(sv);
         return;
     }
+    const long long half = 1ll << (A.qb - 1);
+    const double *dv = A.dval + (uint64_t)pl * L;
+    if (A.zx && A.ntiles > kInlineTiles && tl == kTile && A.zx[(uint64_t)pl * A.ntiles + t] &&
+        A.t_nev[(uint64_t)pl * A.ntiles + t] == 0) {
+        // All values +-0.0 and no event in the tile (every code is the zero
+        // code, no speculative outlier): every element sees the same exact
+        // prediction -- the chain value of the last event before the tile --
+        // and the same decision (codec.cpp:440-451 with x = 0), so one
+        // evaluation stands for the tile.  Anything but "zero code accepted"
+        // falls through to the general path.  Block-uniform.
+        const int32_t *eo = reinterpret_cast<const int32_t *>(A.t_evoff) + (uint64_t)pl * (A.ntiles + 1);
+        const uint32_t evbase = (uint32_t)eo[t], nev_plane = (uint32_t)eo[A.ntiles];
+        if (evbase <= nev_plane && nev_plane <= L) {
+            const double pred = evbase > 0 ? (chain_done ? __ldcg(dv + evbase - 1) : __ldg(dv + evbase - 1)) : 0.0;
+            const double r0 = dmul(dsub(0.0, pred), pp.inv_q);
+            const double rr = dadd(pred, dmul(pp.q, 0.0));
+            // (-0.0 values give the same: only |x - rr| and |r0| enter)
+            if (fabs(r0) < 0.49 && isfinite(rr) && fabs(dsub(0.0, rr)) <= pp.eb && bits_of(rr) == bits_of(pred)) {
+                for (uint64_t i = t0 + (uint64_t)tid * C; i < t0 + kTile; i += (uint64_t)kEncThreads * C) {
+                    if (i & (C - 1)) continue; // (checkpoints wider than a tile)
+                    idx[i >> A.log2C].dprev = pred;
+                    idx[i >> A.log2C].dprev2 = 0.0;
+                }
+                if (tid == 0) {
+                    // run statistics: the only possible run start is the first element
+                    const uint32_t prev = t0 > 0 ? fsym[t0 - 1] : 0u;
+                    const bool starts = t0 == 0 || prev != (uint32_t)half;
+                    A.t_firstb[(uint64_t)pl * A.ntiles + t] = starts ? (int32_t)t0 : 0x7FFFFFFF;
+                    A.t_lastb[(uint64_t)pl * A.ntiles + t] = starts ? (int32_t)t0 : -1;
+                    A.t_nout[(uint64_t)pl * A.ntiles + t] = 0;
+                    A.ztriv[(uint64_t)pl * A.ntiles + t] = starts ? 0 : 1;
+                }
+                return;
+            }
+        }
+    }
     using ScanI = cub::BlockScan<int, kEncThreads>;
     __shared__ typename ScanI::TempStorage scan_tmp;
     __shared__ int s_bad;
     if (tid == 0) s_bad = 0;
-    const long long half = 1ll << (A.qb - 1);
     const uint8_t *fl = A.fl + (uint64_t)pl * L;
     uint32_t *sym = A.sym + (uint64_t)pl * L;
-    const double *dv = A.dval + (uint64_t)pl * L;
     int f[kPerThread], rank[kPerThread];
     double xv[kPerThread];
     uint32_t symv[kPerThread];
@@ -1372,6 +1489,7 @@ __device__ __forceinline__ void serial_plane(const TileArgs &A, int pl) {
             A.t_firstb[(uint64_t)pl * A.ntiles + t] = fb;
             A.t_lastb[(uint64_t)pl * A.ntiles + t] = lb;
             A.t_nout[(uint64_t)pl * A.ntiles + t] = no;
+            if (A.ztriv) A.ztriv[(uint64_t)pl * A.ntiles + t] = 0; // (the symbols were rewritten)
             fb = 0x7FFFFFFF;
             lb = -1;
             no = 0;
@@ -1414,6 +1532,7 @@ struct TokArgs {
     int32_t *t_prevb;            // scanned: last run start strictly before the tile
     int32_t *t_nextb;            // scanned: first run start strictly after the tile
     int32_t *t_ntok, *t_tokoff;  // tokens per tile, scanned (+1)
+    const uint8_t *ztriv;        // [plane][tile] flat zero-code tiles (TileArgs::ztriv) or nullptr
     uint64_t L;
     int ntiles, log2C, qb;
 };
@@ -1583,6 +1702,10 @@ __global__ void __launch_bounds__(kEncThreads) tok_count(TokArgs A, int planes, 
     const int tl = (int)tmin<uint64_t>(kTile, L - t0);
     const uint32_t *sym = A.sym + (uint64_t)pl * L;
     uint32_t sv[kPerThread + 1];
+    if (A.ztriv && A.ztriv[(uint64_t)pl * A.ntiles + t]) { // known flat (enc_verify): nothing to load
+        if (tid == 0) A.t_ntok[(uint64_t)pl * A.ntiles + t] = 0;
+        return;
+    }
     {
         uint32_t fs;
         if (tile_is_flat(sym, t0, tl, sv, fs)) { // inside one long run: no tokens, no counts
@@ -1685,11 +1808,12 @@ __device__ __forceinline__ void tok_emit_tile(const TokArgs &A, int planes, int 
     IndexRec *idx = A.index + (uint64_t)pl * nidx;
     uint32_t sv[kPerThread + 1];
     int32_t carries[4];
-    tile_load_syms(sym, t0, tl, sv); // in flight while warp 0 gathers the carries
+    const bool known_flat = A.ztriv && A.ztriv[(uint64_t)pl * A.ntiles + t]; // (enc_verify: the zero code throughout)
+    if (!known_flat) tile_load_syms(sym, t0, tl, sv); // in flight while warp 0 gathers the carries
     tile_carries(A, pl, t, carries);
     {
-        uint32_t fs;
-        if (tile_flat(sym, t0, tl, sv, fs)) {
+        uint32_t fs = 1u << (A.qb - 1);
+        if (known_flat || tile_flat(sym, t0, tl, sv, fs)) {
             // inside one long run: no tokens or outliers; the index records
             // resume after the run's literal + RUN tokens
             const int32_t nextb = carries[1], tokb = carries[2], ob = carries[3];

@@ -746,6 +746,27 @@ std::vector<CompressedPlanes> Engine::compressed_slices() const {
     return out;
 }
 
+std::vector<double> Engine::slice_norms() const {
+    std::vector<double> v(uint64_t{1} << (n_ - s_));
+    check(qcsim_engine_slice_norms(h_, v.data(), v.size()));
+    return v;
+}
+
+void Engine::resume(const std::vector<CompressedPlanes> &slices, const std::vector<double> &sq_norms,
+                    uint64_t gates_done) {
+    std::vector<uint8_t> bytes;
+    std::vector<uint64_t> offs;
+    for (const CompressedPlanes &cp : slices) {
+        offs.push_back(bytes.size());
+        cp.re.append_bytes(bytes);
+        offs.push_back(bytes.size());
+        cp.im.append_bytes(bytes);
+    }
+    offs.push_back(bytes.size());
+    check(qcsim_engine_load_blocks(h_, bytes.data(), bytes.size(), offs.data(), offs.size() - 1, sq_norms.data(),
+                                   sq_norms.size(), gates_done));
+}
+
 std::pair<std::unique_ptr<Engine>, RunMetrics> run(const Circuit &c, const EngineConfig &cfg,
                                                    const StateVector &initial) {
     if (initial.num_qubits() != c.num_qubits) throw std::invalid_argument("circuit/state width mismatch");

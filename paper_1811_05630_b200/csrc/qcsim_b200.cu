@@ -258,6 +258,7 @@ struct EncScratch {
     DBuf<double> x, dval, evc, oval, tilesum;
     DBuf<uint32_t> sym, evlist, opos, ocount, ntok, tsym, trep, hist, hspecial, symrange, nsym, err, nonfinite;
     DBuf<uint8_t> fl, cb_len, cub_tmp;
+    DBuf<uint8_t> zx, ztriv; // run-aware tile flags (TileArgs), planes of many tiles
     DBuf<int32_t> t_lastout, t_base, t_nev, t_evoff, t_firstb, t_lastb, t_nout, t_ooff, t_prevb, t_nextb, t_ntok,
         t_tokoff, t_cbits, t_coff;
     DBuf<unsigned long long> gamma;
@@ -306,7 +307,6 @@ struct EncScratch {
         dval.ensure(planes * L);
         evc.ensure(planes * L + 8);       // TMA chunks round up to 16 bytes
         evlist.ensure(planes * L + 8);
-        evD.ensure(planes * L + 8);
         sym.ensure(planes * L);
         fl.ensure(planes * L);
         opos.ensure(planes * L);
@@ -548,7 +548,6 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     A.evlist = S.evlist.p;
     A.evc = S.evc.p;
     A.dval = S.dval.p;
-    A.evD = S.evD.p;
     A.t_firstb = S.t_firstb.p;
     A.t_lastb = S.t_lastb.p;
     A.t_nout = S.t_nout.p;
@@ -573,6 +572,21 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     }
     A.lb = S.lb.p;
     A.lb_epoch = S.lb_epoch;
+    {
+        // run-aware tile flags (QCSIM_ZERO_TILES=0: off)
+        static const bool zoff = std::getenv("QCSIM_ZERO_TILES") && std::getenv("QCSIM_ZERO_TILES")[0] == '0';
+        A.zx = A.ztriv = nullptr;
+        if (!zoff && ntiles > kInlineTiles && cfg.predictor == 0) {
+            S.zx.ensure(planes * ntiles);
+            S.ztriv.ensure(planes * ntiles);
+            A.zx = S.zx.p;
+            A.ztriv = S.ztriv.p;
+            CK(cudaMemsetAsync(S.ztriv.p, 0, planes * ntiles, st)); // (enc_verify's general path leaves 0)
+        }
+    }
+    A.want_evD = chain_scan_selected(planes) ? 1 : 0;
+    if (A.want_evD) S.evD.ensure(planes * L + 8); // (the serial warp chain needs no estimates)
+    A.evD = S.evD.p;
     // planes of many tiles: gate + lattice in one grid with a max look-back
     // for the segment base (QCSIM_FUSE_XL=1; measured slower than the two
     // grids -- 34 vs 22 ms per Random-30 pass -- so off by default)
@@ -583,7 +597,9 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
         launch_k(enc_x_lattice<NP, Src>, tgrid_u, kEncThreads, 0, st, A, src, units);
     } else {
         PROF("enc_x", st);
-        launch_k(enc_x<NP, Src>, tgrid_u, kEncThreads, 0, st, A, src, units);
+        static const bool vec_off = std::getenv("QCSIM_ENCX_VEC") && std::getenv("QCSIM_ENCX_VEC")[0] == '0';
+        if (vec_off) launch_k(enc_x<NP, Src, false>, tgrid_u, kEncThreads, 0, st, A, src, units);
+        else launch_k(enc_x<NP, Src, true>, tgrid_u, kEncThreads, 0, st, A, src, units);
     }
     if (!fused_xl) launch_plane_scan(st, S.t_lastout.p, S.t_base.p, ntiles, (int)planes, kScanMaxExcl);
     // event records at tile-local slots when the block-parallel chain reads
@@ -634,7 +650,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
             std::vector<PlaneParams> h_pp(planes);
             CK(cudaMemcpy(h_ev.data(), S.evlist.p, nel * 4, cudaMemcpyDeviceToHost));
             CK(cudaMemcpy(h_c.data(), S.evc.p, nel * 8, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(h_d.data(), S.evD.p, nel * 8, cudaMemcpyDeviceToHost));
+            if (A.want_evD) CK(cudaMemcpy(h_d.data(), S.evD.p, nel * 8, cudaMemcpyDeviceToHost));
             CK(cudaMemcpy(h_nev.data(), S.t_nev.p, planes * ntiles * 4, cudaMemcpyDeviceToHost));
             CK(cudaMemcpy(h_pp.data(), S.params.p, planes * sizeof(PlaneParams), cudaMemcpyDeviceToHost));
             if (FILE *f = std::fopen(std::getenv("QCSIM_CHAIN_DUMP_FILE"), "wb")) {
@@ -768,6 +784,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     T.t_nextb = S.t_nextb.p;
     T.t_ntok = S.t_ntok.p;
     T.t_tokoff = S.t_tokoff.p;
+    T.ztriv = A.ztriv;
     T.L = L;
     T.ntiles = ntiles;
     T.log2C = log2C;
@@ -782,6 +799,21 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
                  (const uint32_t *)(flow ? S.ser_done.p : nullptr), flow_epoch);
     }
     launch_plane_scan(st, S.t_ntok.p, S.t_tokoff.p, ntiles, (int)planes, kScanSumExcl);
+    {
+        // debug: QCSIM_ZT_STATS=1 prints how many tiles took the run-aware paths
+        static const bool zt_stats = std::getenv("QCSIM_ZT_STATS") != nullptr;
+        if (zt_stats && A.zx) {
+            std::vector<uint8_t> hx(planes * ntiles), ht(planes * ntiles);
+            CK(cudaMemcpyAsync(hx.data(), S.zx.p, hx.size(), cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(ht.data(), S.ztriv.p, ht.size(), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            uint64_t nx = 0, nt = 0;
+            for (uint8_t v : hx) nx += v != 0;
+            for (uint8_t v : ht) nt += v != 0;
+            std::fprintf(stderr, "zero tiles: %llu of %llu zero-valued, %llu flat zero-code\n", (unsigned long long)nx,
+                         (unsigned long long)hx.size(), (unsigned long long)nt);
+        }
+    }
 
     CodeBook B;
     B.hist = S.hist.p;
@@ -974,7 +1006,8 @@ struct DecScratch {
 // blocks (enc_codebook -> emit_dec_tables), no table-parsing pass needed.
 void decode_batch(cudaStream_t st, DecScratch &S, const uint8_t *arena, const uint64_t *blk_off,
                   double *const *out, int planes, uint64_t L, int log2C, int qb,
-                  bool prepare = true, const NormArgs *norm = nullptr) {
+                  bool prepare = true, const NormArgs *norm = nullptr, uint8_t *zflag = nullptr,
+                  uint64_t zflag_planes = 0) {
     if (prepare) S.ensure(planes, L, qb);
     const DecTables T = S.tables();
     DecPlanes D;
@@ -983,6 +1016,11 @@ void decode_batch(cudaStream_t st, DecScratch &S, const uint8_t *arena, const ui
     D.out = out;
     D.L = L;
     D.log2C = log2C;
+    if (zflag) { // zero-tile flags of the batch's slots (imported partner slots stay 0)
+        D.zflag = zflag;
+        D.ztiles = (uint32_t)((L + kTile - 1) / kTile);
+        CK(cudaMemsetAsync(zflag, 0, zflag_planes * D.ztiles, st));
+    }
     if (prepare) {
         PROF("dec_prepare", st);
         launch_k(dec_prepare, planes, 256, 0, st, D, T, planes);
@@ -1067,16 +1105,6 @@ const char *dec_message(uint32_t e) {
     default: return "decoder scratch exhausted";
     }
 }
-
-struct ValScratch {
-    DBuf<uint32_t> ssym, err;
-    DBuf<uint8_t> slen;
-    void ensure(uint64_t planes, uint64_t cap) {
-        ssym.ensure(planes * cap);
-        slen.ensure(planes * cap);
-        err.ensure(planes);
-    }
-};
 
 // Foreign-block decoding (no index next to the blocks): stage the blocks
 // with 16-byte aligned code streams, validate header + table (fd_head),
@@ -1265,7 +1293,6 @@ struct CodecCtx {
     int dev = -1;
     cudaStream_t st = nullptr;
     EncScratch enc;
-    ValScratch val;
     ForeignScratch fore;
     DBuf<uint8_t> arena, bytes;
     DBuf<double> vals;
@@ -1324,6 +1351,7 @@ struct qcsim_engine {
     // [slot][re|im][L] (slots: the batch's units, then imported partners)
     DBuf<double> dense[2];
     DBuf<double> old;
+    DBuf<uint8_t> zold;                // zero-tile flags of `old`, [plane][ntiles] (big planes only)
     DBuf<double *> outptrs;            // plane k of the batch -> old + k L
     uint64_t outptr_planes = 0;
     const double *outptr_base = nullptr;
@@ -1343,7 +1371,6 @@ struct qcsim_engine {
     EncScratch enc;
     DecScratch dec[2]; // decode tables of arena[0/1], written by the encoder (single-batch passes)
     DecScratch decw;   // decode tables parsed from the blocks (waves, compare, gather)
-    ValScratch val;
     ForeignScratch fore; // partner blocks imported from host bytes
     DBuf<uint8_t> imp_bytes;
     DBuf<uint64_t> imp_off;
@@ -1439,6 +1466,16 @@ struct PlanarSrc {
         o[0] = v[(uint64_t)unit * 2 * L + i];
         o[1] = v[(uint64_t)unit * 2 * L + L + i];
     }
+    __device__ __forceinline__ void load2(int unit, uint64_t i, double *a, double *b) const { // i even, L even
+        const double2 r = *reinterpret_cast<const double2 *>(v + (uint64_t)unit * 2 * L + i);
+        const double2 m = *reinterpret_cast<const double2 *>(v + (uint64_t)unit * 2 * L + L + i);
+        a[0] = r.x; a[1] = m.x; b[0] = r.y; b[1] = m.y;
+    }
+    template <bool> __device__ __forceinline__ void loadf(int unit, uint64_t i, double *o) const { load(unit, i, o); }
+    template <bool> __device__ __forceinline__ void load2f(int unit, uint64_t i, double *a, double *b) const {
+        load2(unit, i, a, b);
+    }
+    __device__ __forceinline__ bool flagged_sources(int, uint32_t) const { return false; }
 };
 // Basis state |x> on the batch's slices.
 struct BasisSrc {
@@ -1451,6 +1488,15 @@ struct BasisSrc {
         o[0] = g == x ? 1.0 : 0.0;
         o[1] = 0.0;
     }
+    __device__ __forceinline__ void load2(int unit, uint64_t i, double *a, double *b) const {
+        load(unit, i, a);
+        load(unit, i + 1, b);
+    }
+    template <bool> __device__ __forceinline__ void loadf(int unit, uint64_t i, double *o) const { load(unit, i, o); }
+    template <bool> __device__ __forceinline__ void load2f(int unit, uint64_t i, double *a, double *b) const {
+        load2(unit, i, a, b);
+    }
+    __device__ __forceinline__ bool flagged_sources(int, uint32_t) const { return false; }
 };
 
 // Slices per wave: the largest power of two whose dense working set (old
@@ -1503,7 +1549,11 @@ void decode_imports(qcsim_engine *e, const SliceMap &map, uint64_t u0, uint64_t 
     if (e->dev_imp) {
         // device-resident partner blocks: no host staging; from_bytes checks
         // run on the device with the validating decoder
-        std::vector<uint64_t> meta(4 * cnt);
+        // (headers gathered by one kernel + one copy; from_bytes checks on
+        // the host copy, then the parallel foreign decoder reads the blocks
+        // where they lie)
+        const uint64_t P = 2 * cnt;
+        std::vector<uint64_t> src_off(P), avail(P), meta(3 * P);
         for (uint64_t u = u0; u < u0 + cnt; ++u) {
             const uint64_t pj = (e->s0 + map.slice_rel((uint32_t)u)) ^ map.hm;
             auto it = e->dev_imp_at.find(pj);
@@ -1511,38 +1561,40 @@ void decode_imports(qcsim_engine *e, const SliceMap &map, uint64_t u0, uint64_t 
                 raise(QCSIM_INVALID_ARGUMENT,
                       "partner slice " + std::to_string(pj) + " not imported (multi-rank exchange missing)");
             const uint64_t k = u - u0;
-            meta[2 * k] = it->second[0];
-            meta[2 * k + 1] = it->second[1];
-            meta[2 * cnt + 2 * k] = it->second[2];
-            meta[2 * cnt + 2 * k + 1] = it->second[3];
+            for (int p = 0; p < 2; ++p) {
+                src_off[2 * k + p] = it->second[p];
+                avail[2 * k + p] = it->second[2 + p];
+            }
         }
-        e->dev_imp_meta.ensure(4 * cnt);
+        constexpr uint64_t kHead = 48; // header + table count, padded
+        for (uint64_t k = 0; k < P; ++k) {
+            meta[k] = src_off[k];
+            meta[P + k] = k * kHead;
+            meta[2 * P + k] = std::min<uint64_t>(44, avail[k]);
+        }
+        e->dev_imp_meta.ensure(3 * P);
+        e->exp_buf.ensure(P * kHead + 16);
         CK(cudaMemcpyAsync(e->dev_imp_meta.p, meta.data(), meta.size() * 8, cudaMemcpyHostToDevice, e->st));
-        std::vector<double *> ptrs(2 * cnt);
-        for (uint64_t k = 0; k < 2 * cnt; ++k) ptrs[k] = e->old.p + (first_plane + k) * e->L;
-        e->imp_ptrs.ensure(ptrs.size());
-        CK(cudaMemcpyAsync(e->imp_ptrs.p, ptrs.data(), ptrs.size() * sizeof(double *), cudaMemcpyHostToDevice, e->st));
-        const uint64_t vcap = std::min<uint64_t>(e->L + 1, (1ull << e->cfg.codec.quant_code_bits) + 1);
-        e->val.ensure(2 * cnt, vcap);
-        ValArgs V;
-        V.blocks = e->dev_imp;
-        V.blk_off = e->dev_imp_meta.p;
-        V.avail = e->dev_imp_meta.p + 2 * cnt;
-        V.n_expected = e->L;
-        V.out = e->imp_ptrs.p;
-        V.err = e->val.err.p;
-        V.ssym = e->val.ssym.p;
-        V.slen = e->val.slen.p;
-        V.cap = vcap;
         {
-            PROF("dec_validate", e->st);
-            launch_k(dec_validate, (unsigned)((2 * cnt + 31) / 32), 32, 0, e->st, V, (int)(2 * cnt));
+            PROF("gather_heads", e->st);
+            launch_k(gather_blocks, (unsigned)P, 64, 0, e->st, e->dev_imp, (const uint64_t *)e->dev_imp_meta.p, (int)P,
+                     e->exp_buf.p);
         }
-        std::vector<uint32_t> errs(2 * cnt);
-        CK(cudaMemcpyAsync(errs.data(), e->val.err.p, errs.size() * 4, cudaMemcpyDeviceToHost, e->st));
+        std::vector<uint8_t> heads(P * kHead, 0);
+        CK(cudaMemcpyAsync(heads.data(), e->exp_buf.p, P * kHead, cudaMemcpyDeviceToHost, e->st));
         CK(cudaStreamSynchronize(e->st));
-        for (uint32_t x : errs)
-            if (x) raise(QCSIM_CODEC, dec_message(x));
+        std::vector<ForeignBlock> fb(P);
+        for (uint64_t k = 0; k < P; ++k) {
+            uint8_t *h = heads.data() + k * kHead;
+            if (avail[k] < 44) std::memset(h + avail[k], 0, 44 - avail[k]);
+            uint64_t used = 0;
+            const Header hd = parse_header(h, avail[k], &used);
+            if (hd.n != e->L) raise(QCSIM_CODEC, "partner block length does not match the slice");
+            const uint32_t tc = hd.payload >= 4 ? (uint32_t)(h[40] | (h[41] << 8) | (h[42] << 16) | ((uint32_t)h[43] << 24)) : 0;
+            fb[k] = ForeignBlock{e->dev_imp + src_off[k], used, tc, hd.payload, e->old.p + (first_plane + k) * e->L};
+        }
+        const uint32_t err = foreign_decode(e->st, e->fore, fb, true, e->L, e->cfg.codec.quant_code_bits);
+        if (err) raise(QCSIM_CODEC, dec_message(err));
         return;
     }
     std::unordered_map<uint64_t, size_t> where;
@@ -1587,6 +1639,15 @@ const double *state_range(qcsim_engine *e, uint64_t k0, uint64_t cnt) {
     if (!e->compressed) return e->dense[e->cur].p + k0 * 2 * e->L;
     decode_range(e, k0, cnt);
     return e->old.p;
+}
+
+// Run-aware gate pass for planes of many tiles (QCSIM_ZERO_TILES=0 turns it
+// off): the decoder flags tiles of +0.0, the gate / lattice / verify /
+// tokenizer grids take an O(1) path through tiles they know to be trivial.
+bool zero_tiles_enabled(const qcsim_engine *e) {
+    static const bool off = std::getenv("QCSIM_ZERO_TILES") && std::getenv("QCSIM_ZERO_TILES")[0] == '0';
+    return !off && e->compressed && (e->L + kTile - 1) / kTile > (uint64_t)kInlineTiles &&
+           e->cfg.codec.mode != QCSIM_MODE_LOSSLESS && e->cfg.codec.predictor == 0;
 }
 
 // One encode batch: `units` slices produced by `src` into arena[nxt] at
@@ -1670,9 +1731,17 @@ void engine_waves(qcsim_engine *e, uint64_t hm, bool remote, bool decode, MakeSr
         const uint64_t slots = W + (remote ? W : 0);
         if (decode) {
             ensure_outptrs(e, 2 * slots);
+            // zero-tile flags (planes of many tiles): long runs of +0.0 are
+            // flagged instead of written, the gate kernel skips them
+            uint8_t *zf = nullptr;
+            if (zero_tiles_enabled(e)) {
+                e->zold.ensure(2 * slots * ((e->L + kTile - 1) / kTile));
+                zf = e->zold.p;
+            }
             if (single) {
                 decode_batch(e->st, e->dec[e->cur], e->arena[e->cur].p, e->blk_off[e->cur].p, e->outptrs.p,
-                             (int)(2 * W), e->L, e->log2C, e->cfg.codec.quant_code_bits, /*prepare=*/false);
+                             (int)(2 * W), e->L, e->log2C, e->cfg.codec.quant_code_bits, /*prepare=*/false, nullptr, zf,
+                             2 * slots);
             } else {
                 e->h_wave_off.ensure(2 * W);
                 for (uint64_t u = 0; u < W; ++u) {
@@ -1683,7 +1752,7 @@ void engine_waves(qcsim_engine *e, uint64_t hm, bool remote, bool decode, MakeSr
                 e->wave_off.ensure(2 * W);
                 CK(cudaMemcpyAsync(e->wave_off.p, e->h_wave_off.p, 2 * W * 8, cudaMemcpyHostToDevice, e->st));
                 decode_batch(e->st, e->decw, e->arena[e->cur].p, e->wave_off.p, e->outptrs.p, (int)(2 * W), e->L,
-                             e->log2C, e->cfg.codec.quant_code_bits, /*prepare=*/true);
+                             e->log2C, e->cfg.codec.quant_code_bits, /*prepare=*/true, nullptr, zf, 2 * slots);
             }
             if (remote) decode_imports(e, map, 0, W, 2 * W);
         }
@@ -1877,6 +1946,8 @@ void engine_gate(qcsim_engine *e, const qcsim_action &a) {
                     GateSrc b = g;
                     b.old = e->old.p;
                     b.map = map;
+                    b.zold = zero_tiles_enabled(e) ? e->zold.p : nullptr;
+                    b.ztiles = (uint32_t)((e->L + kTile - 1) / kTile);
                     return b;
                 });
                 break;
@@ -2399,6 +2470,64 @@ qcsim_status qcsim_engine_load_amplitudes(qcsim_engine *e, const double *amps, u
             upload(0, e->ns);
             engine_dense(e, PlanarSrc{e->old.p, e->L});
         }
+    });
+}
+
+qcsim_status qcsim_engine_load_blocks(qcsim_engine *e, const uint8_t *blocks, uint64_t len, const uint64_t *offsets,
+                                      uint64_t planes, const double *sq_norms, uint64_t norm_count,
+                                      uint64_t gates_done) {
+    return guarded([&] {
+        if (!e || !blocks || !offsets || !sq_norms) raise(QCSIM_INVALID_ARGUMENT, "null argument");
+        if (!e->compressed) raise(QCSIM_INVALID_ARGUMENT, "engine is not compressed");
+        if (e->cfg.codec.mode == QCSIM_MODE_RANGE_RELATIVE)
+            raise(QCSIM_INVALID_ARGUMENT, "resume needs an absolute or lossless bound");
+        if (planes != 2 * e->ns) raise(QCSIM_INVALID_ARGUMENT, "block count must be 2 * local slices");
+        if (norm_count != e->S) raise(QCSIM_INVALID_ARGUMENT, "norm table must hold every slice");
+        for (uint64_t k = 0; k < planes; ++k)
+            if (offsets[k + 1] < offsets[k] || offsets[k + 1] > len)
+                raise(QCSIM_INVALID_ARGUMENT, "block offsets must be non-decreasing and inside the buffer");
+        CK(cudaSetDevice(e->cfg.device));
+        // from_bytes checks of every block first (nothing is replaced on failure)
+        std::vector<Header> hd(planes);
+        std::vector<uint64_t> used(planes);
+        for (uint64_t k = 0; k < planes; ++k) {
+            hd[k] = parse_header(blocks + offsets[k], offsets[k + 1] - offsets[k], &used[k]);
+            const Header &h = hd[k];
+            if (h.n != e->L) raise(QCSIM_INVALID_ARGUMENT, "block element count does not match the slice");
+            if (h.mode != e->cfg.codec.mode || h.pred != e->cfg.codec.predictor || h.qb != e->cfg.codec.quant_code_bits)
+                raise(QCSIM_INVALID_ARGUMENT, "block codec (mode, predictor, quant_code_bits) differs from the engine's");
+        }
+        e->rows.clear();
+        e->loaded = false;
+        engine_waves(e, 0, false, /*decode=*/false, [&](const SliceMap &map) {
+            // this wave's slices, decoded by the validating foreign decoder
+            const uint64_t W = map.nunits;
+            e->old.ensure(2 * W * e->L);
+            std::vector<ForeignBlock> fb(2 * W);
+            for (uint64_t u = 0; u < W; ++u) {
+                const uint64_t k = map.slice_rel((uint32_t)u);
+                for (int p = 0; p < 2; ++p) {
+                    const uint64_t b = 2 * k + p;
+                    const uint8_t *src = blocks + offsets[b];
+                    const uint32_t tc = hd[b].payload >= 4 ? (uint32_t)(src[40] | (src[41] << 8) | (src[42] << 16) |
+                                                                        ((uint32_t)src[43] << 24))
+                                                           : 0;
+                    fb[2 * u + p] = ForeignBlock{src, used[b], tc, hd[b].payload, e->old.p + (2 * u + p) * e->L};
+                }
+            }
+            const uint32_t err = foreign_decode(e->st, e->fore, fb, false, e->L, e->cfg.codec.quant_code_bits);
+            if (err) raise(QCSIM_CODEC, dec_message(err));
+            return PlanarSrc{e->old.p, e->L};
+        });
+        for (uint64_t k = 0; k < planes; ++k)
+            if (e->blk_bytes_h[k] != used[k]) {
+                e->loaded = false;
+                raise(QCSIM_CODEC, "block " + std::to_string(k) + " does not re-encode to itself (" +
+                                       std::to_string(used[k]) + " -> " + std::to_string(e->blk_bytes_h[k]) + " bytes)");
+            }
+        // the cached norms are those of the pre-compression values
+        std::memcpy(e->sq_norm.data(), sq_norms, e->S * sizeof(double));
+        e->gates = gates_done;
     });
 }
 

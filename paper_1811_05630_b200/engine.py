@@ -124,6 +124,17 @@ class Engine:
         a = np.ascontiguousarray(a, dtype=np.float64)
         self._ck(self.L.qcsim_engine_load_amplitudes(self.h, a.ctypes.data_as(_native.dp), a.size // 2))
 
+    def load_blocks(self, blocks, offsets, sq_norms, gates_done: int = 0):
+        """Resume from a checkpoint: this rank's QCB1 blocks in
+        export_blocks order, their offsets, and the global per-slice sq_norm
+        table (qcsim_engine_load_blocks)."""
+        b = np.frombuffer(bytes(blocks), dtype=np.uint8) if not isinstance(blocks, np.ndarray) else blocks
+        b = np.ascontiguousarray(b, dtype=np.uint8)
+        offs = (C.c_uint64 * len(offsets))(*offsets)
+        v = np.ascontiguousarray(sq_norms, dtype=np.float64)
+        self._ck(self.L.qcsim_engine_load_blocks(self.h, b.ctypes.data_as(_native.u8p), b.size, offs,
+                                                 len(offsets) - 1, v.ctypes.data_as(_native.dp), v.size, gates_done))
+
     def run(self, actions=()) -> RunMetrics:
         arr, n = _actions(actions)
         m = _native.RunMetricsC()

@@ -106,6 +106,22 @@ int main() {
     const std::string js = metrics_json(mo, rows), csv = metrics_csv(rows);
     REQUIRE(js.find("\"overhead_factor\"") != std::string::npos && js.find("\"per_gate\"") != std::string::npos);
     REQUIRE(csv.rfind("gate_index,min_ratio,mean_ratio,seconds\n", 0) == 0);
+    // checkpoint -> resume: the resumed engine holds the same
+    // blocks and continues identically
+    {
+        Engine again(n, ec);
+        again.resume(slices, eng->slice_norms(), qft.gate_count());
+        const auto s2 = again.compressed_slices();
+        REQUIRE(s2.size() == slices.size());
+        for (size_t j = 0; j < slices.size(); ++j)
+            REQUIRE(s2[j].re.to_bytes() == slices[j].re.to_bytes() && s2[j].im.to_bytes() == slices[j].im.to_bytes());
+        const std::vector<GateAction> more{gate_action(Gate::h(3)), gate_action(Gate::h(9))};
+        again.run(more);
+        eng->run(more);
+        const auto a1 = eng->compressed_slices(), a2 = again.compressed_slices();
+        for (size_t j = 0; j < a1.size(); ++j)
+            REQUIRE(a1[j].re.to_bytes() == a2[j].re.to_bytes() && a1[j].im.to_bytes() == a2[j].im.to_bytes());
+    }
     std::printf("api_smoke ok: fidelity %.9f, min ratio %.3f, overhead %.2fx\n", f, m.min_compression_ratio,
                 mo.overhead_factor);
     return 0;

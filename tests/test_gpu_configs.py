@@ -439,3 +439,53 @@ def test_fused_gate_lattice_bit_identical(oracle):
     oe.load_basis(12345)
     oe.run(acts)
     assert fused[0] == hashlib.sha256(oe.export_blocks()[0]).hexdigest()
+
+
+_RESUME_SCRIPT = r"""
+import sys
+import numpy as np
+import paper_1811_05630_b200 as q
+n, s = 14, 8
+acts = q.lower(q.build_qft(n))
+cut = 60
+cfg = q.EngineConfig(num_qubits=n, slice_bits=s, codec=q.CodecConfig(q.CodecMode.Absolute, 1e-5))
+a = q.Engine(cfg)
+a.load_basis(777)
+a.run(acts[:cut])
+blob, offs = a.export_blocks()
+norms = a.slice_norms()
+b = q.Engine(cfg)
+b.load_blocks(blob, offs, norms, gates_done=cut)
+same_ckpt = b.export_blocks()[0] == blob
+mb = b.run(acts[cut:])
+ma = a.run(acts[cut:])
+ok = same_ckpt and b.export_blocks()[0] == a.export_blocks()[0] and np.array_equal(a.slice_norms(), b.slice_norms())
+ok = ok and ma.final_norm == mb.final_norm and mb.gates == len(acts)
+bad = bytearray(blob)
+bad[offs[3] + 1] ^= 0xFF                     # magic of block 3
+try:
+    q.Engine(cfg).load_blocks(bytes(bad), offs, norms)
+    ok = False
+except q.CodecError as e:
+    ok = ok and "bad block magic" in str(e)
+sys.stdout.write(str(b.info()["waves"]) + " " + str(ok) + " " + a.export_blocks()[0].hex() + "\n")
+"""
+
+
+@pytest.mark.parametrize("wave", [None, "4"])
+def test_resume_from_checkpoint(oracle, q, wave):
+    """Checkpoint / resume: QCB1 blocks + the sq_norm table
+    exported after 60 gates of QFT-14 are loaded into a fresh engine
+    (qcsim_engine_load_blocks: from_bytes + decoder checks, decode and
+    re-encode on the device), which then holds byte-identical blocks and
+    finishes the circuit exactly like the uninterrupted engine and the
+    oracle.  A corrupt checkpoint fails with the reference's message."""
+    env = {"QCSIM_WAVE_SLICES": wave} if wave else {}
+    waves, rest = _run_script(_RESUME_SCRIPT, [], env)
+    ok, hexblob = rest.split(" ", 1)
+    assert int(waves) == (16 if wave else 1)
+    assert ok == "True"
+    oe = oracle.engine(OEng.make(14, 8, OCfg.make(1, 1e-5, 16, 0)))
+    oe.load_basis(777)
+    oe.run(q.lower(q.build_qft(14)))
+    assert bytes.fromhex(hexblob) == oe.export_blocks()[0]
