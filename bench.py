@@ -235,11 +235,13 @@ def run_ours(args, wl, rank, world, dist):
     clocks = ClockSampler()
     clocks.start()
     dev_s, wall, gates = 0.0, 0.0, 0
+    step_ms = []
     for k in range(W, W + K):
         m0 = eng.metrics().wall_seconds
         m, dt = timed(k, lambda k: eng.run(wl["steps"](k)))
         wall += dt
         dev_s += m.wall_seconds - m0
+        step_ms.append(round(1e3 * (m.wall_seconds - m0), 3))
         gates += len(wl["steps"](k))
     clk = clocks.stop()
     launches = lib.qcsim_kernel_launches() - launches0
@@ -307,7 +309,7 @@ def run_ours(args, wl, rank, world, dist):
         d2h += ho
     mem = q.device_memory() if hasattr(q, "device_memory") else None
     return dict(gates=gates, dev_s=dev_s, wall=wall, clocks=clk, launches=launches, m_w=m_w, m_t=m_t, m_p=m_p,
-                gates0=gates0, rows=rows, kprof=kprof, pgates=pgates, chain=chain, accuracy=accuracy, sha=sha,
+                gates0=gates0, rows=rows, kprof=kprof, step_ms=step_ms, pgates=pgates, chain=chain, accuracy=accuracy, sha=sha,
                 e2e_t=e2e_t, h2d=h2d // K, d2h=d2h // K, mem=mem)
 
 
@@ -473,7 +475,8 @@ def main():
                             "dense_bytes": m.dense_bytes, "fallback_planes": m.fallback_planes},
             "device_memory": res["mem"],
             "accuracy": res["accuracy"],
-            "wall_ms_per_step": 1e3 * wall / args.steps, "device_ms_per_step": 1e3 * dev_s / args.steps}
+            "wall_ms_per_step": 1e3 * wall / args.steps, "device_ms_per_step": 1e3 * dev_s / args.steps,
+            "device_ms_steps": res["step_ms"]}
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

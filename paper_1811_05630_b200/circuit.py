@@ -6,8 +6,8 @@ basis index; CPhase(theta) multiplies |11> by exp(i*theta).
 
 Lowering (gate_action, circuit.cpp:392-427) is bit-identical to the
 reference: same 1/sqrt(2) literal, same std::cos/std::sin (glibc via
-math.cos/math.sin) -- tests/test_host_api.py pins it against the compiled
-reference.  Extension: U3 enters as a pre-lowered
+math.cos/math.sin) -- tests/test_oracle_golden.py::
+test_python_lowering_matches_reference pins it against the compiled reference.  Extension: U3 enters as a pre-lowered
 ButterflyOp; its matrix convention is stated in ``u3_matrix``.
 """
 from __future__ import annotations

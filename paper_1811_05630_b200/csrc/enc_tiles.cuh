@@ -1290,22 +1290,37 @@ __device__ __forceinline__ void verify_tile(const TileArgs &A, int planes, const
     }
     const long long half = 1ll << (A.qb - 1);
     const double *dv = A.dval + (uint64_t)pl * L;
-    if (A.zx && A.ntiles > kInlineTiles && tl == kTile && A.zx[(uint64_t)pl * A.ntiles + t] &&
-        A.t_nev[(uint64_t)pl * A.ntiles + t] == 0) {
-        // All values +-0.0 and no event in the tile (every code is the zero
-        // code, no speculative outlier): every element sees the same exact
-        // prediction -- the chain value of the last event before the tile --
-        // and the same decision (codec.cpp:440-451 with x = 0), so one
-        // evaluation stands for the tile.  Anything but "zero code accepted"
-        // falls through to the general path.  Block-uniform.
+    if (A.zx && A.ntiles > kInlineTiles && tl == kTile && A.t_nev[(uint64_t)pl * A.ntiles + t] == 0) {
+        // No event in the tile: every code is the zero code, no speculative
+        // outlier, so every element sees the same exact prediction -- the
+        // chain value of the last event before the tile -- and the reference
+        // decision (codec.cpp:440-451) reduces to "m = 0 accepted":
+        // |r| < 0.49 (m = 0 for certain), rec = pred + q*0 finite and equal
+        // to pred, |x - rec| <= eb.  A tile of +-0.0 values (enc_x's flag)
+        // evaluates that once; other tiles per element from x alone (no
+        // flag / symbol loads, no rank scan, no chain gathers).  Anything
+        // else falls through to the general path.  Block-uniform.
         const int32_t *eo = reinterpret_cast<const int32_t *>(A.t_evoff) + (uint64_t)pl * (A.ntiles + 1);
         const uint32_t evbase = (uint32_t)eo[t], nev_plane = (uint32_t)eo[A.ntiles];
         if (evbase <= nev_plane && nev_plane <= L) {
             const double pred = evbase > 0 ? (chain_done ? __ldcg(dv + evbase - 1) : __ldg(dv + evbase - 1)) : 0.0;
-            const double r0 = dmul(dsub(0.0, pred), pp.inv_q);
             const double rr = dadd(pred, dmul(pp.q, 0.0));
-            // (-0.0 values give the same: only |x - rr| and |r0| enter)
-            if (fabs(r0) < 0.49 && isfinite(rr) && fabs(dsub(0.0, rr)) <= pp.eb && bits_of(rr) == bits_of(pred)) {
+            bool ok = isfinite(rr) && bits_of(rr) == bits_of(pred);
+            if (A.zx[(uint64_t)pl * A.ntiles + t]) {
+                // (-0.0 values give the same: only |x - rr| and |r0| enter)
+                const double r0 = dmul(dsub(0.0, pred), pp.inv_q);
+                ok = ok && fabs(r0) < 0.49 && fabs(dsub(0.0, rr)) <= pp.eb;
+            } else {
+                double xv4[kPerThread];
+                load4(x + t0, tid * kPerThread, tl, xv4);
+#pragma unroll
+                for (int e = 0; e < kPerThread; ++e) {
+                    const double r0 = dmul(dsub(xv4[e], pred), pp.inv_q);
+                    ok = ok && fabs(r0) < 0.49 && fabs(dsub(xv4[e], rr)) <= pp.eb;
+                }
+                ok = __syncthreads_and(ok);
+            }
+            if (ok) {
                 for (uint64_t i = t0 + (uint64_t)tid * C; i < t0 + kTile; i += (uint64_t)kEncThreads * C) {
                     if (i & (C - 1)) continue; // (checkpoints wider than a tile)
                     idx[i >> A.log2C].dprev = pred;

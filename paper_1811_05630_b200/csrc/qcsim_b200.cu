@@ -1703,10 +1703,12 @@ void engine_waves(qcsim_engine *e, uint64_t hm, bool remote, bool decode, MakeSr
         uint64_t used = 0;
         for (uint64_t b : e->blk_bytes_h) used += b + 32;
         used += index_bytes_of(e, e->blk_bytes_h);
-        const uint64_t want = used + used / 4 + (64ull << 20);
+        // (a butterfly on a fresh qubit can double a sparse state: room for
+        // 2x up to 4 GB of growth; a larger jump re-packs after growing)
+        const uint64_t want = used + std::min<uint64_t>(used, 4ull << 30) + (256ull << 20);
         if (e->arena[nxt].cap < want) {
             e->arena[nxt].release();
-            e->arena[nxt].ensure(want);
+            e->arena[nxt].ensure(want + std::min<uint64_t>(want / 2, 1ull << 30)); // (fewer reallocations as it grows)
         }
     }
     e->enc.arena_base = 0;

@@ -113,6 +113,28 @@ def test_lowering_matches_reference(oracle, reflib):
             assert bytes(a) == bytes(b), (kind, qs, theta)
 
 
+def test_python_lowering_matches_reference(oracle, reflib):
+    """The Python mirror's gate_action / to_action_c (paper_1811_05630_b200/
+    circuit.py) produces the same flattened actions as the compiled reference
+    (circuit.cpp:392-427) and the C restatement, byte for byte -- including
+    the Phase / CPhase factors from libm's cos / sin."""
+    import math
+    from paper_1811_05630_b200 import circuit as pc
+    cases = [(0, [3]), (1, [0]), (2, [5]), (3, [1]), (4, [2]), (5, [7]), (6, [4]), (7, [1, 6]), (8, [2, 0]),
+             (9, [0, 3]), (10, [1, 9]), (11, [0, 2, 5])]
+    for kind, qs in cases:
+        for theta in (0.0, 0.3, -2.0 * math.pi / 3, 2.0 * math.pi / (1 << 20)):
+            mine = bytes(pc.to_action_c(pc.gate_action(pc.Gate(pc.GateKind(kind), theta, list(qs)))))
+            assert mine == bytes(reflib.gate_action(kind, qs, theta)), (kind, qs, theta)
+            assert mine == bytes(oracle.gate_action(kind, qs, theta)), (kind, qs, theta)
+    # the QFT / Grover builders emit the reference's gate lists (circuit.cpp:88-168)
+    for n in (5, 12):
+        ref = reflib.circuit("qft", n, 1)
+        assert [bytes(a) for a in pc.lower(pc.build_qft(n))] == [bytes(a) for a in ref]
+    ref = reflib.circuit("grover", 6, 37, 3)
+    assert [bytes(a) for a in pc.lower(pc.build_grover(6, 37, 3))] == [bytes(a) for a in ref]
+
+
 def test_codec_errors(oracle):
     with pytest.raises(OracleError, match="cannot compress an empty plane"):
         oracle.compress(np.zeros(0), CodecConfig.make())
