@@ -53,6 +53,7 @@ struct TileArgs {
     //                        tile, no outliers (enc_verify) -- the tokenizer
     //                        treats it as flat without loading its symbols.
     uint8_t *zx, *ztriv;
+    uint32_t *lat_bad;     // [plane] enc_gate_lattice met a code outside (-H, H) (zeroed per pass)
     int want_evD;          // the block-parallel chain reads the lattice estimates (evD);
                            // the serial warp chain does not: they are not written
     int ev_tile_local;     // event records at tile-local slots (tile * kTile + rank), no
@@ -70,6 +71,7 @@ struct TileArgs {
     double *tilesum;       // [unit][ntiles]
     uint64_t L;
     int ntiles;
+    int tile_sh;           // log2(ntiles) when ntiles is a power of two, else -1 (split_block)
     int log2C;
     int qb;
     int predictor;
@@ -79,6 +81,18 @@ struct TileArgs {
     unsigned long long *gamma;       // [plane]
 };
 
+// (plane or unit, tile) of a block: a shift when the tile count is a power of
+// two (engine planes), else the division.
+__device__ __forceinline__ void split_block(uint32_t b, int ntiles, int sh, int &pl, int &t) {
+    if (sh >= 0) {
+        pl = (int)(b >> sh);
+        t = (int)(b & (uint32_t)(ntiles - 1));
+    } else {
+        pl = (int)(b / (uint32_t)ntiles);
+        t = (int)(b % (uint32_t)ntiles);
+    }
+}
+
 __device__ __forceinline__ bool is_negzero(double v) { return bits_of(v) == 0x8000000000000000ull; }
 
 // Plane parameters as ONE consistent snapshot per block.  Other blocks of
@@ -86,11 +100,12 @@ __device__ __forceinline__ bool is_negzero(double v) { return bits_of(v) == 0x80
 // read could let some threads of a block return early while the rest enter
 // a barrier or a block-wide scan.  All threads must call this.
 __device__ __forceinline__ PlaneParams block_params(const PlaneParams *params, int pl) {
-    __shared__ PlaneParams s_pp;
-    if (threadIdx.x == 0) s_pp = params[pl];
-    __syncthreads();
-    const PlaneParams pp = s_pp;
-    __syncthreads();
+    // bounds are fixed while the tile grids run (every lane loads the same
+    // words: one transaction per warp); only the fallback flag can change
+    // under the block, so the block agrees on it with one voting barrier
+    PlaneParams pp = params[pl];
+    const int fb = __syncthreads_or((int)(__ldcg(&params[pl].flags) & kFlagFallback));
+    pp.flags = (pp.flags & ~(uint32_t)kFlagFallback) | (fb ? (uint32_t)kFlagFallback : 0u);
     return pp;
 }
 
@@ -301,7 +316,8 @@ __device__ __forceinline__ int32_t carry_of(const int32_t *scanned, int scanned_
 template <int NP, class Src, bool kVec>
 __global__ void __launch_bounds__(kEncThreads, 5) enc_x(TileArgs A, Src src, int units) {
     pdl_begin();
-    const int unit = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
+    int unit, t;
+    split_block(blockIdx.x, A.ntiles, A.tile_sh, unit, t);
     if (unit >= units) return;
     const int tid = threadIdx.x;
     const uint64_t L = A.L;
@@ -512,10 +528,7 @@ __device__ uint32_t lookback_exclusive(unsigned long long *slots, uint32_t epoch
 // ------------------------------------------------------------------ T2
 // Lattice codes, flags and the plane's event list (the compaction is fused:
 // the tile's event offset comes from the look-back above).
-__global__ void __launch_bounds__(kEncThreads, 5) enc_lattice(TileArgs A, int planes) {
-    pdl_begin();
-    const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
-    if (pl >= planes) return;
+__device__ __forceinline__ void lattice_tile(const TileArgs &A, int pl, int t) {
     auto stamp = [&](int k) {
         if (A.trace && threadIdx.x == 0) {
             unsigned long long tt;
@@ -592,25 +605,26 @@ __global__ void __launch_bounds__(kEncThreads, 5) enc_lattice(TileArgs A, int pl
             return;
         }
     }
-    // speculative outliers of this tile and the element before it
+    // speculative outliers of this tile and the element before it (enc_x
+    // recorded whether the tile has any: most have none, and then neither
+    // the flags nor a scan are needed -- every element's segment base comes
+    // from the carry)
+    const bool tile_out = A.t_lastout[(uint64_t)pl * A.ntiles + t] >= 0; // block-uniform
     int opos[kPerThread];
     double xv[kPerThread];
-    for (int e = 0; e < kPerThread; ++e) {
-        const int k = tid * kPerThread + e;
-        opos[e] = (k < tl && (fl[t0 + k] & 2)) ? k : -1;
-        xv[e] = k < tl ? x[t0 + k] : 0.0;
+    if (tile_out) {
+        uint32_t fv[kPerThread];
+        load4(fl + t0, tid * kPerThread, tl, fv);
+        for (int e = 0; e < kPerThread; ++e) opos[e] = (tid * kPerThread + e < tl && (fv[e] & 2)) ? tid * kPerThread + e : -1;
+    } else {
+        for (int e = 0; e < kPerThread; ++e) opos[e] = -1;
     }
+    load4(x + t0, tid * kPerThread, tl, xv);
     int lo[kPerThread];
-    {
-        // (no speculative outlier in the tile: every element's segment base
-        // comes from the carry)
-        bool anyout = false;
-        for (int e = 0; e < kPerThread; ++e) anyout |= opos[e] >= 0;
-        if (__syncthreads_or(anyout)) {
-            ScanI(scan_tmp).ExclusiveScan(opos, lo, -1, cub::Max());
-        } else {
-            for (int e = 0; e < kPerThread; ++e) lo[e] = -1;
-        }
+    if (tile_out) {
+        ScanI(scan_tmp).ExclusiveScan(opos, lo, -1, cub::Max());
+    } else {
+        for (int e = 0; e < kPerThread; ++e) lo[e] = -1;
     }
     stamp(1);
     const int32_t tbase = carry_of(A.t_base, A.ntiles, A.t_lastout, pl, t, A.ntiles, kScanMaxExcl); // position or -1
@@ -748,283 +762,201 @@ __global__ void __launch_bounds__(kEncThreads, 5) enc_lattice(TileArgs A, int pl
     }
     stamp(5);
 }
-
-// Decoupled look-back of a running MAX over the tiles of one plane (warp-wide,
-// like lookback_exclusive): values are positions + 1 (0 = none).
-__device__ uint32_t lookback_max_exclusive(unsigned long long *slots, uint32_t epoch, int t, uint32_t local) {
-    const int lane = threadIdx.x & 31;
-    if (lane == 0) st_release_u64(&slots[t], lb_tag(epoch, t == 0 ? 2 : 1) | local);
-    uint32_t prefix = 0;
-    int hi = t - 1;
-    while (hi >= 0) {
-        const int k = hi - lane;
-        unsigned long long w = 0;
-        uint32_t st = 2;
-        if (k >= 0) {
-            do {
-                w = ld_acquire_u64(&slots[k]);
-                st = ((uint32_t)(w >> 32) >> 2) == epoch ? ((uint32_t)(w >> 32) & 3) : 0;
-                if (st == 0) __nanosleep(32);
-            } while (st == 0);
-        }
-        const unsigned incl = __ballot_sync(0xffffffffu, st == 2);
-        const int stop = incl ? __ffs(incl) - 1 : 32;
-        uint32_t v = (lane <= stop && k >= 0) ? (uint32_t)w : 0u;
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, off));
-        prefix = max(prefix, v);
-        if (incl) break;
-        hi -= 32;
+// redo == nullptr: one block per (plane, tile).  Otherwise the planes listed
+// in redo[1 .. redo[0]] only (enc_gate_lattice's planes with a speculative
+// outlier), on a grid of rmax * ntiles blocks.
+__global__ void __launch_bounds__(kEncThreads, 5) enc_lattice(TileArgs A, int planes, const uint32_t *redo, int rmax) {
+    pdl_begin();
+    int r, t;
+    split_block(blockIdx.x, A.ntiles, A.tile_sh, r, t);
+    if (!redo) {
+        if (r < planes) lattice_tile(A, r, t);
+        return;
     }
-    if (lane == 0 && t > 0) st_release_u64(&slots[t], lb_tag(epoch, 2) | max(prefix, local));
-    return prefix;
+    const uint32_t cnt = redo[0];
+    for (; (uint32_t)r < cnt; r += rmax) {
+        lattice_tile(A, (int)redo[1 + r], t);
+        __syncthreads();
+    }
 }
 
-// T1+T2 fused for planes of > kInlineTiles tiles (the gate pass of the dense
-// configurations): new = gate(scale * old) (enc_x) and, on the values still
-// in shared memory, the speculative outliers and the lattice codes /
-// estimates / event flags (enc_lattice).  The segment base
-// of a tile (the last speculative outlier before it) comes from a decoupled
-// look-back of a running max over the plane's tiles instead of the
-// t_lastout / plane_scan / t_base round trip, so x and the flags are written
-// once and never read back by this stage.  Identical results to enc_x +
-// enc_lattice (same operations on the same values).
-template <int NP, class Src>
-__global__ void __launch_bounds__(kEncThreads) enc_x_lattice(TileArgs A, Src src, int units) {
+// Planes with a speculative outlier anywhere (t_lastout / its exclusive max
+// scan t_base), listed for enc_lattice's redo grid.  One block.
+__global__ void __launch_bounds__(256) lattice_redo_list(TileArgs A, int planes, uint32_t *redo) {
     pdl_begin();
-    const int unit = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
+    __shared__ uint32_t s_cnt;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    for (int pl = threadIdx.x; pl < planes; pl += blockDim.x) {
+        const uint64_t last = (uint64_t)pl * A.ntiles + (A.ntiles - 1);
+        if (A.t_base[last] >= 0 || A.t_lastout[last] >= 0) redo[1 + atomicAdd(&s_cnt, 1u)] = (uint32_t)pl;
+        else if (A.lat_bad[pl]) atomicOr(&A.params[pl].flags, kFlagFallback); // serial re-encode
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) redo[0] = s_cnt;
+}
+
+// T1+T2 for planes of many whole tiles with a lossy absolute bound and the
+// previous-value predictor: new = gate(scale * old) AND its lattice codes in
+// one grid, each thread keeping its 4 consecutive elements of every plane in
+// registers (no shared-memory staging; 16-byte loads and stores).  The
+// segment base is taken as "no speculative outlier before this element"
+// (base 0.0) -- true for every element of a plane without speculative
+// outliers, which is almost every plane; the few planes that have one
+// (t_lastout) are listed by lattice_redo_list and redone by enc_lattice from
+// the x and flags written here.  Same operations on the same values as
+// enc_x + enc_lattice for the planes it finishes.
+template <int NP, class Src>
+__global__ void __launch_bounds__(kEncThreads, 4) enc_gate_lattice(TileArgs A, Src src, int units) {
+    pdl_begin();
+    int unit, t;
+    split_block(blockIdx.x, A.ntiles, A.tile_sh, unit, t);
     if (unit >= units) return;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint64_t L = A.L;
-    const uint64_t t0 = (uint64_t)t * kTile;
-    const int tl = (int)tmin<uint64_t>(kTile, L - t0);
+    const uint64_t t0 = (uint64_t)t * kTile; // (whole tiles: L is a multiple of kTile)
     if (t == 0 && tid < NP) {
         // per-pass reset of the plane's flags and histogram bookkeeping
-        // (tiles > 0 set flags only after their look-back, which orders them
-        // after this tile's publication)
         const int pl = unit * NP + tid;
-        const PlaneParams pp = A.params[pl];
-        A.params[pl].flags = (A.predictor == 1 && pp.eb != 0.0) ? kFlagFallback : 0u;
+        A.params[pl].flags = 0u;
         A.symrange[2 * pl] = 0xFFFFFFFFu;
         A.symrange[2 * pl + 1] = 0;
         A.hspecial[2 * pl] = 0;
         A.hspecial[2 * pl + 1] = 0;
         A.gamma[pl] = 0;
     }
-    __shared__ double xs[NP][kTile + 2]; // [0] = x[t0-2], [1] = x[t0-1], [k+2] = x[t0+k]
-    __shared__ double red[kEncThreads];
-    __shared__ long long kb[kEncThreads];
-    __shared__ uint32_t s_base[NP];
-    using ScanI = cub::BlockScan<int, kEncThreads>;
-    using RedI = cub::BlockReduce<int, kEncThreads>;
-    __shared__ union {
-        typename ScanI::TempStorage scan;
-        typename RedI::TempStorage red;
-    } tmp;
-    for (int k = tid; k < kTile + 2; k += kEncThreads) {
-        double v[2] = {0.0, 0.0};
-        const int64_t i = (int64_t)t0 + k - 2;
-        if (i >= 0 && k - 2 < tl) src.load(unit, (uint64_t)i, v);
-        for (int p = 0; p < NP; ++p) xs[p][k] = v[p];
+    __shared__ int s_flagged;
+    __shared__ double s_last[NP][kEncThreads / 32]; // each warp's last element
+    __shared__ double s_halo[NP];                   // element t0 - 1
+    __shared__ double red[kEncThreads / 32];
+    __shared__ int s_nev[NP], s_lastout[NP];
+    if (tid == 0) s_flagged = src.flagged_sources(unit, (uint32_t)t) ? 1 : 0;
+    if (tid < NP) {
+        s_nev[tid] = 0;
+        s_lastout[tid] = -1;
     }
     __syncthreads();
+    const bool flagged = s_flagged != 0;
+    const int k0 = tid * kPerThread;
+    double xv[NP][kPerThread];
+    auto load_mine = [&](auto kF) {
+        constexpr bool kFlags = decltype(kF)::value;
+#pragma unroll
+        for (int h = 0; h < kPerThread; h += 2) {
+            double a[2] = {0.0, 0.0}, b[2] = {0.0, 0.0};
+            src.template load2f<kFlags>(unit, t0 + k0 + h, a, b);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                xv[p][h] = a[p];
+                xv[p][h + 1] = b[p];
+            }
+        }
+        if (tid == kEncThreads - 1) { // (the last thread: its own loads are issued first)
+            double v[2] = {0.0, 0.0};
+            if (t0 > 0) src.template loadf<kFlags>(unit, t0 - 1, v);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) s_halo[p] = v[p];
+        }
+    };
+    if (flagged) load_mine(std::true_type{});
+    else load_mine(std::false_type{});
+    int nonzero[NP];
+#pragma unroll
     for (int p = 0; p < NP; ++p) {
-        double *xrow = A.x + ((uint64_t)unit * NP + p) * L;
-        for (int k = tid; k < tl; k += kEncThreads) xrow[t0 + k] = xs[p][k + 2];
+        double *xrow = A.x + ((uint64_t)unit * NP + p) * L + t0 + k0;
+        *reinterpret_cast<double2 *>(xrow) = make_double2(xv[p][0], xv[p][1]);
+        *reinterpret_cast<double2 *>(xrow + 2) = make_double2(xv[p][2], xv[p][3]);
+        nonzero[p] = (xv[p][0] != 0.0) | (xv[p][1] != 0.0) | (xv[p][2] != 0.0) | (xv[p][3] != 0.0);
+        if (lane == 31) s_last[p][wid] = xv[p][kPerThread - 1];
     }
+    double nv = 0.0;
     if (Src::kNorms) {
         double acc[kPerThread];
-        for (int e = 0; e < kPerThread; ++e) {
-            const int k = tid * kPerThread + e + 2;
-            const double a = dmul(xs[0][k], xs[0][k]);
-            const double b = dmul(xs[NP - 1][k], xs[NP - 1][k]);
-            acc[e] = dadd(a, b);
-        }
-        double v = dadd(dadd(acc[0], acc[1]), dadd(acc[2], acc[3]));
-        const int lane = tid & 31;
+#pragma unroll
+        for (int e = 0; e < kPerThread; ++e)
+            acc[e] = dadd(dmul(xv[0][e], xv[0][e]), dmul(xv[NP - 1][e], xv[NP - 1][e]));
+        // the tile's adjacent-pair tree (as enc_x)
+        nv = dadd(dadd(acc[0], acc[1]), dadd(acc[2], acc[3]));
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
-            const double o = __shfl_down_sync(0xffffffffu, v, off);
-            if ((lane & (2 * off - 1)) == 0) v = dadd(v, o);
+            const double o = __shfl_down_sync(0xffffffffu, nv, off);
+            if ((lane & (2 * off - 1)) == 0) nv = dadd(nv, o);
         }
-        if (lane == 0) red[tid >> 5] = v;
-        __syncthreads();
-        if (tid == 0) {
-            const double s01 = dadd(red[0], red[1]), s23 = dadd(red[2], red[3]);
-            const double s45 = dadd(red[4], red[5]), s67 = dadd(red[6], red[7]);
-            A.tilesum[(uint64_t)unit * A.ntiles + t] = dadd(dadd(s01, s23), dadd(s45, s67));
-        }
+        if (lane == 0) red[wid] = nv;
+    }
+    // all-zero tiles are flagged for the later grids (also the barrier that
+    // publishes s_last / s_halo / red)
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        const int any = __syncthreads_or(nonzero[p]);
+        if (tid == 0 && A.zx) A.zx[((uint64_t)unit * NP + p) * A.ntiles + t] = any ? 0 : 1;
+    }
+    if (Src::kNorms && tid == 0) {
+        static_assert(kEncThreads == 256, "8 warp sums");
+        const double s01 = dadd(red[0], red[1]), s23 = dadd(red[2], red[3]);
+        const double s45 = dadd(red[4], red[5]), s67 = dadd(red[6], red[7]);
+        A.tilesum[(uint64_t)unit * A.ntiles + t] = dadd(dadd(s01, s23), dadd(s45, s67));
     }
     const long long half = 1ll << (A.qb - 1);
     const double hh = (double)half;
-    // speculative outliers (enc_x) of every plane, the tile's last one
-    int opos[NP][kPerThread];
-    bool prevout0[NP];
-    for (int p = 0; p < NP; ++p) {
-        const PlaneParams pp = A.params[(uint64_t)unit * NP + p];
-        int last = -1;
-        for (int e = 0; e < kPerThread; ++e) {
-            const int k = tid * kPerThread + e;
-            bool out = false;
-            if (k < tl && pp.eb != 0.0) {
-                const double rr = dmul(dsub(xs[p][k + 2], xs[p][k + 1]), pp.inv_q);
-                out = !(fabs(rr) < hh - 0.5);
-            }
-            opos[p][e] = out ? k : -1;
-            if (out) last = k;
-        }
-        // element t0 - 1 (its own flag, for the first element's predecessor)
-        prevout0[p] = false;
-        if (t0 > 0 && pp.eb != 0.0) {
-            const double rr = dmul(dsub(xs[p][1], xs[p][0]), pp.inv_q);
-            prevout0[p] = !(fabs(rr) < hh - 0.5);
-        }
-        const int tl_last = RedI(tmp.red).Reduce(last, cub::Max());
-        __syncthreads();
-        if (tid == 0) s_base[p] = tl_last >= 0 ? (uint32_t)(t0 + tl_last) + 1u : 0u;
-    }
-    __syncthreads();
-    // segment base of the tile: the last speculative outlier of the earlier
-    // tiles (look-back per plane, one warp each); publishing after the x
-    // stores makes x[tbase] readable by later tiles
-    if (tid < 32 * NP) {
-        const int p = tid >> 5;
-        const uint64_t pl = (uint64_t)unit * NP + p;
-        if (tid == 32 * p) __threadfence();
-        __syncwarp();
-        const uint32_t ex = lookback_max_exclusive(A.lb + pl * A.ntiles, A.lb_epoch, t, s_base[p]);
-        __syncwarp();
-        if ((tid & 31) == 0) s_base[p] = ex;
-    }
-    __syncthreads();
+#pragma unroll
     for (int p = 0; p < NP; ++p) {
         const uint64_t pl = (uint64_t)unit * NP + p;
-        const PlaneParams pp = A.params[pl];
-        const bool fallback = A.predictor == 1 && pp.eb != 0.0; // linear + lossy: serial re-encode
-        const double *x = A.x + pl * L;
-        uint8_t *fl = A.fl + pl * L;
-        uint32_t *sym = A.sym + pl * L;
-        if (fallback) {
-            if (tid == 0) A.t_nev[pl * A.ntiles + t] = 0;
-            continue;
-        }
-        if (pp.eb == 0.0) { // lossless: d == x, symbols final, no events
-            for (int e = 0; e < kPerThread; ++e) {
-                const int k = tid * kPerThread + e;
-                if (k >= tl) continue;
-                const uint64_t i = t0 + k;
-                const double x1 = i > 0 ? xs[p][k + 1] : 0.0;
-                double pred;
-                if (A.predictor == 0) pred = x1;
-                else pred = i == 0 ? 0.0 : (i == 1 ? x1 : predict_linear(x1, xs[p][k]));
-                sym[i] = bits_of(xs[p][k + 2]) == bits_of(pred) ? (uint32_t)half : 0u;
-                fl[i] = 0;
-            }
-            if (tid == 0) A.t_nev[pl * A.ntiles + t] = 0;
-            continue;
-        }
-        double xv[kPerThread];
-        for (int e = 0; e < kPerThread; ++e) {
-            const int k = tid * kPerThread + e;
-            xv[e] = k < tl ? xs[p][k + 2] : 0.0;
-        }
-        int lo[kPerThread];
-        {
-            bool anyout = false;
-            for (int e = 0; e < kPerThread; ++e) anyout |= opos[p][e] >= 0;
-            if (__syncthreads_or(anyout)) {
-                ScanI(tmp.scan).ExclusiveScan(opos[p], lo, -1, cub::Max());
-                __syncthreads();
-            } else {
-                for (int e = 0; e < kPerThread; ++e) lo[e] = -1;
-            }
-        }
-        const int32_t tbase = (int32_t)s_base[p] - 1; // position or -1
-        auto xat = [&](int64_t i) -> double { // x[i] for i < t0 + tl
-            if (i >= (int64_t)t0 - 2) return xs[p][i - (int64_t)t0 + 2];
-            return __ldcg(x + i);
-        };
-        const double tbx = tbase >= 0 ? xat(tbase) : 0.0;
-        long long K[kPerThread];
+        const PlaneParams pp = A.params[pl]; // (eb, q, inv_q: fixed while this grid runs)
+        // the element before this thread's first one
+        double xp = __shfl_up_sync(0xffffffffu, xv[p][kPerThread - 1], 1);
+        if (lane == 0) xp = wid > 0 ? s_last[p][wid - 1] : s_halo[p];
+        // K of that element against base 0.0 (dsub(x, 0.0) == x bitwise)
+        long long kprev = llround_exact(dmul(dsub(xp, 0.0), pp.inv_q));
+        uint32_t esym[kPerThread], fword = 0;
+        int nev = 0, last = -1, bad = 0;
         double dh[kPerThread];
+#pragma unroll
         for (int e = 0; e < kPerThread; ++e) {
-            const int k = tid * kPerThread + e;
-            if (opos[p][e] >= 0) {
-                K[e] = 0;
-                dh[e] = xv[e];
-            } else {
-                double base;
-                if (lo[e] >= 0) base = xs[p][lo[e] + 2];
-                else base = tbx;
-                K[e] = k < tl ? llround_exact(dmul(dsub(xv[e], base), pp.inv_q)) : 0;
-                dh[e] = dadd(base, dmul(pp.q, (double)K[e]));
+            const double xi = xv[p][e];
+            // speculative outlier (enc_x): the jump from the previous value
+            const double rr = dmul(dsub(xi, xp), pp.inv_q);
+            const bool out = !(fabs(rr) < hh - 0.5);
+            const long long K = llround_exact(dmul(dsub(xi, 0.0), pp.inv_q));
+            const long long m = K - kprev;
+            if (m <= -half || m >= half) bad = 1;
+            uint32_t f = m != 0 ? 1u : 0u;
+            esym[e] = (uint32_t)(m + half);
+            if (out) { // (the plane is redone by enc_lattice: only the flag matters)
+                f = 3u;
+                esym[e] = kOutlierSym;
+                last = k0 + e;
+                bad = 0;
             }
+            dh[e] = dadd(0.0, dmul(pp.q, (double)K));
+            fword |= f << (8 * e);
+            nev += (int)(f & 1u);
+            kprev = K;
+            xp = xi;
         }
-        kb[tid] = K[kPerThread - 1];
-        long long kprev0 = 0;
-        const double xprev0 = xs[p][1];
-        if (t0 > 0 && !prevout0[p]) kprev0 = llround_exact(dmul(dsub(xprev0, tbx), pp.inv_q));
-        __syncthreads();
-        int evflag[kPerThread];
-        uint32_t esym[kPerThread];
-        uint32_t fword = 0;
-        int bad = 0;
-        for (int e = 0; e < kPerThread; ++e) {
-            const int k = tid * kPerThread + e;
-            evflag[e] = 0;
-            esym[e] = 0;
-            if (k >= tl) continue;
-            long long kprev;
-            bool prev_out;
-            double xp;
-            if (e > 0) { kprev = K[e - 1]; prev_out = opos[p][e - 1] >= 0; xp = xv[e - 1]; }
-            else if (tid > 0) { kprev = kb[tid - 1]; prev_out = lo[0] == k - 1; xp = xs[p][k + 1]; }
-            else { kprev = kprev0; prev_out = prevout0[p]; xp = xprev0; }
-            if (prev_out) kprev = 0;
-            uint8_t f;
-            uint32_t sy;
-            if (opos[p][e] >= 0) {
-                f = 3;
-                sy = kOutlierSym;
-            } else {
-                const long long m = K[e] - kprev;
-                if (m <= -half || m >= half) bad = 1;
-                sy = (uint32_t)(m + half);
-                f = (m != 0 || (prev_out && is_negzero(xp))) ? 1 : 0;
-            }
-            fword |= (uint32_t)f << (8 * e);
-            esym[e] = sy;
-            evflag[e] = f & 1;
+        *reinterpret_cast<uint32_t *>(A.fl + pl * L + t0 + k0) = fword;
+        *reinterpret_cast<uint4 *>(A.sym + pl * L + t0 + k0) = make_uint4(esym[0], esym[1], esym[2], esym[3]);
+        if (A.want_evD && nev) {
+            double *dhat = A.dval + pl * L + t0 + k0;
+#pragma unroll
+            for (int e = 0; e < kPerThread; ++e)
+                if ((fword >> (8 * e)) & 1u) dhat[e] = dh[e];
         }
-        {
-            const int k0 = tid * kPerThread;
-            if (k0 + kPerThread <= tl) {
-                *reinterpret_cast<uint32_t *>(fl + t0 + k0) = fword;
-                *reinterpret_cast<uint4 *>(sym + t0 + k0) = make_uint4(esym[0], esym[1], esym[2], esym[3]);
-            } else {
-                for (int e = 0; e < kPerThread && k0 + e < tl; ++e) {
-                    fl[t0 + k0 + e] = (uint8_t)(fword >> (8 * e));
-                    sym[t0 + k0 + e] = esym[e];
-                }
-            }
+        // (decided per plane by lattice_redo_list: a plane that is redone
+        // ignores it)
+        if (bad) atomicOr(&A.lat_bad[pl], 1u);
+        nev = __reduce_add_sync(0xffffffffu, nev);
+        last = __reduce_max_sync(0xffffffffu, last);
+        if (lane == 0) {
+            if (nev) atomicAdd(&s_nev[p], nev);
+            if (last >= 0) atomicMax(&s_lastout[p], last);
         }
-        if (bad) atomicOr(&A.params[pl].flags, kFlagFallback);
-        // lattice estimates of the events (enc_compact places the records)
-        int mine = 0;
-        double *dhat = A.dval + pl * L;
-        for (int e = 0; e < kPerThread; ++e) {
-            mine += evflag[e];
-            if (evflag[e] && A.want_evD) dhat[t0 + tid * kPerThread + e] = dh[e];
-        }
-        mine = __reduce_add_sync(0xffffffffu, mine);
-        if ((tid & 31) == 0) red[tid >> 5] = (double)mine;
-        __syncthreads();
-        if (tid == 0) {
-            int tot = 0;
-            for (int w = 0; w < kEncThreads / 32; ++w) tot += (int)red[w];
-            A.t_nev[pl * A.ntiles + t] = (uint32_t)tot;
-        }
-        __syncthreads();
+    }
+    __syncthreads();
+    if (tid < NP) {
+        const uint64_t pl = (uint64_t)unit * NP + tid;
+        A.t_nev[pl * A.ntiles + t] = (uint32_t)s_nev[tid];
+        A.t_lastout[pl * A.ntiles + t] = s_lastout[tid] >= 0 ? (int32_t)(t0 + s_lastout[tid]) : -1;
     }
 }
 
@@ -1217,7 +1149,8 @@ __global__ void __launch_bounds__(32) enc_chain(TileArgs A, int planes, int nbuf
 // reads the chain values from L2.
 __device__ __forceinline__ void verify_tile(const TileArgs &A, int planes, const uint32_t *chain_done,
                                             uint32_t epoch) {
-    const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
+    int pl, t;
+    split_block(blockIdx.x, A.ntiles, A.tile_sh, pl, t);
     if (pl >= planes) return;
     const PlaneParams pp = block_params(A.params, pl);
     if (pp.flags & kFlagFallback) return;
@@ -1549,7 +1482,7 @@ struct TokArgs {
     int32_t *t_ntok, *t_tokoff;  // tokens per tile, scanned (+1)
     const uint8_t *ztriv;        // [plane][tile] flat zero-code tiles (TileArgs::ztriv) or nullptr
     uint64_t L;
-    int ntiles, log2C, qb;
+    int ntiles, tile_sh, log2C, qb;
 };
 
 struct RunInfo {
@@ -1705,7 +1638,8 @@ __global__ void __launch_bounds__(kEncThreads) tok_count(TokArgs A, int planes, 
                                                          uint32_t epoch) {
     if (ser_done) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     else pdl_begin();
-    const int pl = blockIdx.x / A.ntiles, t = blockIdx.x % A.ntiles;
+    int pl, t;
+    split_block(blockIdx.x, A.ntiles, A.tile_sh, pl, t);
     if (pl >= planes) return;
     if (ser_done) {
         if (threadIdx.x == 0) flow_wait(ser_done, pl, epoch);
@@ -1804,7 +1738,8 @@ __global__ void __launch_bounds__(kEncThreads) tok_count(TokArgs A, int planes, 
 }
 
 __device__ __forceinline__ void tok_emit_tile(const TokArgs &A, int planes, int blk) {
-    const int pl = blk / A.ntiles, t = blk % A.ntiles;
+    int pl, t;
+    split_block((uint32_t)blk, A.ntiles, A.tile_sh, pl, t);
     if (pl >= planes) return;
     const int tid = threadIdx.x;
     const uint64_t L = A.L;

@@ -259,6 +259,7 @@ struct EncScratch {
     DBuf<uint32_t> sym, evlist, opos, ocount, ntok, tsym, trep, hist, hspecial, symrange, nsym, err, nonfinite;
     DBuf<uint8_t> fl, cb_len, cub_tmp;
     DBuf<uint8_t> zx, ztriv; // run-aware tile flags (TileArgs), planes of many tiles
+    DBuf<uint32_t> lat_bad, lat_redo; // enc_gate_lattice: per-plane range flag, planes for enc_lattice to redo
     DBuf<int32_t> t_lastout, t_base, t_nev, t_evoff, t_firstb, t_lastb, t_nout, t_ooff, t_prevb, t_nextb, t_ntok,
         t_tokoff, t_cbits, t_coff;
     DBuf<unsigned long long> gamma;
@@ -558,6 +559,10 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     A.tilesum = S.tilesum.p;
     A.L = L;
     A.ntiles = ntiles;
+    A.tile_sh = -1;
+    if ((ntiles & (ntiles - 1)) == 0)
+        for (int sh = 0; sh < 31; ++sh)
+            if ((1 << sh) == ntiles) A.tile_sh = sh;
     A.log2C = log2C;
     A.qb = qb;
     A.predictor = cfg.predictor;
@@ -587,38 +592,55 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     A.want_evD = chain_scan_selected(planes) ? 1 : 0;
     if (A.want_evD) S.evD.ensure(planes * L + 8); // (the serial warp chain needs no estimates)
     A.evD = S.evD.p;
-    // planes of many tiles: gate + lattice in one grid with a max look-back
-    // for the segment base (QCSIM_FUSE_XL=1; measured slower than the two
-    // grids -- 34 vs 22 ms per Random-30 pass -- so off by default)
-    static const bool fuse_env = std::getenv("QCSIM_FUSE_XL") && std::getenv("QCSIM_FUSE_XL")[0] == '1';
-    const bool fused_xl = fuse_env && ntiles > kInlineTiles;
-    if (fused_xl) {
-        PROF("enc_x_lattice", st);
-        launch_k(enc_x_lattice<NP, Src>, tgrid_u, kEncThreads, 0, st, A, src, units);
-    } else {
-        PROF("enc_x", st);
-        static const bool vec_off = std::getenv("QCSIM_ENCX_VEC") && std::getenv("QCSIM_ENCX_VEC")[0] == '0';
-        if (vec_off) launch_k(enc_x<NP, Src, false>, tgrid_u, kEncThreads, 0, st, A, src, units);
-        else launch_k(enc_x<NP, Src, true>, tgrid_u, kEncThreads, 0, st, A, src, units);
-    }
-    if (!fused_xl) launch_plane_scan(st, S.t_lastout.p, S.t_base.p, ntiles, (int)planes, kScanMaxExcl);
+    // Planes of many whole tiles, lossy absolute bound, previous-value
+    // predictor: gate + lattice in ONE grid (enc_gate_lattice, base 0.0), then
+    // enc_lattice again only for the planes that hold a speculative outlier
+    // (QCSIM_FUSE_GL=0: the two separate grids).
+    static const bool fuse_gl_off = std::getenv("QCSIM_FUSE_GL") && std::getenv("QCSIM_FUSE_GL")[0] == '0';
+    const bool fused_gl = !fuse_gl_off && ntiles > kInlineTiles && L % kTile == 0 && cfg.mode == QCSIM_MODE_ABSOLUTE &&
+                          cfg.predictor == 0;
     // event records at tile-local slots when the block-parallel chain reads
     // them (no look-back between the tiles of a plane)
     static const bool tile_local_off = std::getenv("QCSIM_EV_TILE_LOCAL") && std::getenv("QCSIM_EV_TILE_LOCAL")[0] == '0';
     A.ev_tile_local = (ntiles <= kInlineTiles && chain_scan_selected(planes) && !tile_local_off) ? 1 : 0;
-    if (!fused_xl) {
+    A.trace = nullptr;
+    A.lat_bad = nullptr;
+    if (fused_gl) {
+        S.lat_bad.ensure(planes);
+        S.lat_redo.ensure(planes + 1);
+        A.lat_bad = S.lat_bad.p;
+        CK(cudaMemsetAsync(S.lat_bad.p, 0, planes * sizeof(uint32_t), st));
+        {
+            PROF("enc_gate_lattice", st);
+            launch_k(enc_gate_lattice<NP, Src>, tgrid_u, kEncThreads, 0, st, A, src, units);
+        }
+        launch_plane_scan(st, S.t_lastout.p, S.t_base.p, ntiles, (int)planes, kScanMaxExcl);
+        {
+            PROF("lattice_redo", st);
+            launch_k(lattice_redo_list, 1, 256, 0, st, A, (int)planes, S.lat_redo.p);
+            const int rmax = (int)std::min<uint64_t>(planes, 16);
+            launch_k(enc_lattice, (unsigned)(rmax * ntiles), kEncThreads, 0, st, A, (int)planes,
+                     (const uint32_t *)S.lat_redo.p, rmax);
+        }
+    } else {
+        {
+            PROF("enc_x", st);
+            static const bool vec_off = std::getenv("QCSIM_ENCX_VEC") && std::getenv("QCSIM_ENCX_VEC")[0] == '0';
+            if (vec_off) launch_k(enc_x<NP, Src, false>, tgrid_u, kEncThreads, 0, st, A, src, units);
+            else launch_k(enc_x<NP, Src, true>, tgrid_u, kEncThreads, 0, st, A, src, units);
+        }
+        launch_plane_scan(st, S.t_lastout.p, S.t_base.p, ntiles, (int)planes, kScanMaxExcl);
         // debug: QCSIM_LAT_TRACE_AT = encode call -> phase stamps to QCSIM_LAT_TRACE_FILE
         static const long lat_at = std::getenv("QCSIM_LAT_TRACE_AT") ? std::atol(std::getenv("QCSIM_LAT_TRACE_AT")) : -1;
         static long lat_calls = 0;
         static DBuf<unsigned long long> lat_trace;
-        A.trace = nullptr;
         if (lat_at >= 0 && lat_calls++ == lat_at) {
             lat_trace.ensure(8 * (uint64_t)tgrid_p);
             CK(cudaMemsetAsync(lat_trace.p, 0, 8 * (uint64_t)tgrid_p * 8, st));
             A.trace = lat_trace.p;
         }
         PROF("enc_lattice", st);
-        launch_k(enc_lattice, tgrid_p, kEncThreads, 0, st, A, (int)planes);
+        launch_k(enc_lattice, tgrid_p, kEncThreads, 0, st, A, (int)planes, (const uint32_t *)nullptr, 0);
         if (A.trace) {
             std::vector<unsigned long long> h(8 * (uint64_t)tgrid_p);
             CK(cudaMemcpyAsync(h.data(), A.trace, h.size() * 8, cudaMemcpyDeviceToHost, st));
@@ -787,6 +809,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     T.ztriv = A.ztriv;
     T.L = L;
     T.ntiles = ntiles;
+    T.tile_sh = A.tile_sh;
     T.log2C = log2C;
     T.qb = qb;
     // (tile run statistics: written by enc_verify / enc_serial_x)
