@@ -178,7 +178,8 @@ struct BitWindow {
 
 constexpr int kDecThreads = 128;             // chunks per block (one per thread)
 constexpr int kDecStageWords = 4096;         // 16 KB of stream staged per block
-constexpr int kDecBatch = 8;                 // value runs per lane per batch
+constexpr int kDecBatch = 8;                 // listed (long) runs per lane per batch
+constexpr int kDecTokBatch = 64;             // tokens per lane per batch
 constexpr int kDecFills = 64;                // block-wide fills per block
 constexpr uint32_t kDecBlockFill = 4096;     // runs at least this long are filled by the whole block
 constexpr uint32_t kDecWarpRun = 32;         // runs at least this long are written by the whole warp
@@ -187,9 +188,9 @@ struct DecFill {
     uint64_t len;
     double v;
 };
-struct DecRun {          // elements [previous end, end) take `v`
+struct DecRun {          // elements [start, end) take `v`
+    uint32_t start;
     uint32_t end;
-    uint32_t pad;
     double v;
 };
 struct DecSmem {
@@ -321,35 +322,39 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
         return eb == 0.0 ? pred : dadd(pred, dmul(q, (double)m));
     };
     while (__any_sync(0xffffffffu, !dead && i < e1)) {
-        // ---- phase 1: up to kDecBatch value runs of this lane's chunk; a
-        // run handed to the block list ends the batch (ranges stay contiguous)
-        const uint64_t a = i;
-        int nr = 0;
-        while (!dead && i < e1 && nr < kDecBatch) {
+        // ---- phase 1: up to kDecTokBatch tokens of this lane's chunk.
+        // Literals and constant runs shorter than kDecWarpRun elements are
+        // written at once by their own lane; longer runs go to the lane's
+        // run list (whole warp, phase 2) or the block list (>= kDecBlockFill)
+        int nr = 0, ntok = 0;
+        while (!dead && i < e1 && nr < kDecBatch && ntok < kDecTokBatch) {
+            ++ntok;
             if (run_left > 0) {
                 const double v = value_of(last);
                 if (pred_kind == 0 && bits_of(v) == bits_of(d1) && i > 0) {
                     // a constant run: the rest of the RUN (within the chunk)
                     const uint64_t take = tmin<uint64_t>(run_left, e1 - i);
+                    bool placed = false;
                     if (take >= kDecBlockFill) {
                         const uint32_t slot = atomicAdd(&S.nfill, 1u);
                         if (slot < (uint32_t)kDecFills) {
                             S.fill[slot] = DecFill{i, take, v};
-                            i += take;
-                            run_left -= (uint32_t)take;
-                            d2 = v;
-                            break; // the batch ends before the block-filled run
+                            placed = true;
                         }
+                    }
+                    if (!placed) {
+                        if (take >= kDecWarpRun) S.runs[nr++][threadIdx.x] = DecRun{(uint32_t)i, (uint32_t)(i + take), v};
+                        else
+                            for (uint64_t e = i; e < i + take; ++e) out[e] = v;
                     }
                     i += take;
                     run_left -= (uint32_t)take;
-                    S.runs[nr++][threadIdx.x] = DecRun{(uint32_t)i, 0u, v};
                     d2 = v;
                     continue;
                 }
                 // one element of the run (first element of a -0.0 run, a
                 // nonzero code, the linear predictor)
-                S.runs[nr++][threadIdx.x] = DecRun{(uint32_t)(i + 1), 0u, v};
+                out[i] = v;
                 d2 = d1;
                 d1 = v;
                 ++i;
@@ -403,44 +408,25 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
                 }
             } else {
                 const double v = value_of(s);
-                S.runs[nr++][threadIdx.x] = DecRun{(uint32_t)(i + 1), 0u, v};
+                out[i] = v;
                 d2 = d1;
                 d1 = v;
                 ++i;
                 last = s;
             }
         }
-        // ---- phase 2: runs shorter than kDecWarpRun elements are written by
-        // their own lane (a few contiguous stores); longer ones by the whole
-        // warp, 32 consecutive elements per store (coalesced)
-        uint32_t longmask = 0; // this lane's runs of >= kDecWarpRun elements
-        {
-            uint64_t p0 = a;
-            for (int c = 0; c < nr; ++c) {
-                const DecRun R = S.runs[c][threadIdx.x];
-                const uint64_t p1 = R.end;
-                if (p1 - p0 >= kDecWarpRun) {
-                    longmask |= 1u << c;
-                } else {
-                    for (uint64_t e = p0; e < p1; ++e) out[e] = R.v;
-                }
-                p0 = p1;
-            }
-        }
-        unsigned lanes = __ballot_sync(0xffffffffu, longmask != 0);
+        // ---- phase 2: the listed runs (>= kDecWarpRun elements), each by the
+        // whole warp, 32 consecutive elements per store (coalesced)
+        __syncwarp();
+        unsigned lanes = __ballot_sync(0xffffffffu, nr > 0);
         while (lanes) {
             const int rr = __ffs(lanes) - 1;
             lanes &= lanes - 1;
-            uint32_t lm = __shfl_sync(0xffffffffu, longmask, rr);
-            const uint64_t ra = __shfl_sync(0xffffffffu, a, rr);
+            const int n = __shfl_sync(0xffffffffu, nr, rr);
             const int col = wbase_t + rr;
-            while (lm) {
-                const int c = __ffs(lm) - 1;
-                lm &= lm - 1;
-                const uint64_t p0 = c ? S.runs[c - 1][col].end : ra;
-                const uint64_t p1 = S.runs[c][col].end;
-                const double v = S.runs[c][col].v;
-                for (uint64_t e = p0 + (uint64_t)lane; e < p1; e += 32) out[e] = v;
+            for (int c = 0; c < n; ++c) {
+                const DecRun R = S.runs[c][col];
+                for (uint64_t e = (uint64_t)R.start + (uint64_t)lane; e < (uint64_t)R.end; e += 32) out[e] = R.v;
             }
         }
         __syncwarp();

@@ -53,6 +53,9 @@ struct TileArgs {
     //                        tile, no outliers (enc_verify) -- the tokenizer
     //                        treats it as flat without loading its symbols.
     uint8_t *zx, *ztriv;
+    uint32_t *chain_prog;  // [plane] events whose chain value enc_chain has published (zeroed per
+                           // pass); non-null: enc_verify runs alongside the chain, tile-major,
+                           // each tile waiting for its own plane's chain front
     uint32_t *lat_bad;     // [plane] enc_gate_lattice met a code outside (-H, H) (zeroed per pass)
     int want_evD;          // the block-parallel chain reads the lattice estimates (evD);
                            // the serial warp chain does not: they are not written
@@ -1139,6 +1142,11 @@ __global__ void __launch_bounds__(32) enc_chain(TileArgs A, int planes, int nbuf
             if (lane < (int)cnt) dv[(uint64_t)ch * kChainChunk + base + lane] = mine;
         }
         __syncwarp();
+        if (A.chain_prog && lane == 0) { // the chain front: enc_verify's tiles wait for it
+            __threadfence();
+            const uint32_t upto = tmin<uint32_t>((ch + 1) * kChainChunk, nev);
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(A.chain_prog + pl), "r"(upto) : "memory");
+        }
         if (lane == 0 && ch + nbufs < nchunks) issue(ch + nbufs);
     }
 }
@@ -1150,11 +1158,39 @@ __global__ void __launch_bounds__(32) enc_chain(TileArgs A, int planes, int nbuf
 __device__ __forceinline__ void verify_tile(const TileArgs &A, int planes, const uint32_t *chain_done,
                                             uint32_t epoch) {
     int pl, t;
-    split_block(blockIdx.x, A.ntiles, A.tile_sh, pl, t);
+    if (A.chain_prog) { // tile-major: the chain fronts of all planes advance together
+        t = (int)(blockIdx.x / (uint32_t)planes);
+        pl = (int)(blockIdx.x - (uint32_t)t * (uint32_t)planes);
+    } else {
+        split_block(blockIdx.x, A.ntiles, A.tile_sh, pl, t);
+    }
     if (pl >= planes) return;
     const PlaneParams pp = block_params(A.params, pl);
     if (pp.flags & kFlagFallback) return;
-    if (chain_done && pp.eb != 0.0) {
+    if (A.chain_prog && pp.eb != 0.0) {
+        // the chain values of every event up to the end of this tile
+        const uint32_t need = (uint32_t)(reinterpret_cast<const int32_t *>(A.t_evoff) + (uint64_t)pl * (A.ntiles + 1))[t + 1];
+        __shared__ int s_gave_up;
+        if (threadIdx.x == 0) {
+            s_gave_up = 0;
+            uint32_t v = need, spins = 0;
+            if (need) do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(A.chain_prog + pl) : "memory");
+                if (v < need) {
+                    __nanosleep(128);
+                    if (++spins > (1u << 23)) { // (> 1 s: never in a healthy run) -> serial re-encode
+                        atomicOr(&A.params[pl].flags, kFlagFallback);
+                        s_gave_up = 1;
+                        break;
+                    }
+                }
+            } while (v < need);
+        }
+        __syncthreads();
+        if (s_gave_up) return;
+    }
+    if (A.chain_prog) chain_done = A.chain_prog; // (chain values through L2 from here on)
+    if (chain_done && !A.chain_prog && pp.eb != 0.0) {
         if (threadIdx.x == 0) {
             uint32_t v;
             do {
@@ -1364,7 +1400,7 @@ __device__ __forceinline__ void verify_tile(const TileArgs &A, int planes, const
 // when the plane was not refuted (enc_serial_x releases the refuted ones).
 __global__ void __launch_bounds__(kEncThreads, 6) enc_verify(TileArgs A, int planes, const uint32_t *chain_done,
                                                           uint32_t epoch, PlaneFlow flow, uint32_t *ser_done) {
-    if (chain_done) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (chain_done || A.chain_prog) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     else pdl_begin();
     verify_tile(A, planes, chain_done, epoch);
     if (!flow.cnt) return;

@@ -259,6 +259,7 @@ struct EncScratch {
     DBuf<uint32_t> sym, evlist, opos, ocount, ntok, tsym, trep, hist, hspecial, symrange, nsym, err, nonfinite;
     DBuf<uint8_t> fl, cb_len, cub_tmp;
     DBuf<uint8_t> zx, ztriv; // run-aware tile flags (TileArgs), planes of many tiles
+    DBuf<uint32_t> chain_prog; // enc_chain's per-plane front (enc_verify follows it)
     DBuf<uint32_t> lat_bad, lat_redo; // enc_gate_lattice: per-plane range flag, planes for enc_lattice to redo
     DBuf<int32_t> t_lastout, t_base, t_nev, t_evoff, t_firstb, t_lastb, t_nout, t_ooff, t_prevb, t_nextb, t_ntok,
         t_tokoff, t_cbits, t_coff;
@@ -605,6 +606,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     A.ev_tile_local = (ntiles <= kInlineTiles && chain_scan_selected(planes) && !tile_local_off) ? 1 : 0;
     A.trace = nullptr;
     A.lat_bad = nullptr;
+    A.chain_prog = nullptr;
     if (fused_gl) {
         S.lat_bad.ensure(planes);
         S.lat_redo.ensure(planes + 1);
@@ -750,6 +752,14 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
                 }
             }
         } else if (chain_mode != 1) {
+            // planes of many tiles: enc_verify is launched alongside the serial
+            // chain and follows each plane's chain front (QCSIM_CHAIN_PIPE=0: off)
+            static const bool pipe_off = std::getenv("QCSIM_CHAIN_PIPE") && std::getenv("QCSIM_CHAIN_PIPE")[0] == '0';
+            if (!pipe_off && ntiles > kInlineTiles) {
+                S.chain_prog.ensure(planes);
+                CK(cudaMemsetAsync(S.chain_prog.p, 0, planes * sizeof(uint32_t), st));
+                A.chain_prog = S.chain_prog.p;
+            }
             PROF("enc_chain", st);
             const int nbufs = planes > 2 * 148 ? 2 : kChainBufs; // latency hidden by other warps
             launch_k(enc_chain, (unsigned)planes, 32, chain_smem_bytes(nbufs), st, A, (int)planes, nbufs);
