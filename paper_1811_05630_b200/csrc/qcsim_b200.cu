@@ -452,7 +452,13 @@ void launch_pack(cudaStream_t st, EncScratch &S, DBuf<uint8_t> &arena, bool coun
     // (plane, K) blocks looping over the plane's chunks (pack_count / pack_write)
     const int K = std::min(nck, 32);
     const unsigned grid = (unsigned)(S.planes * K);
-    if (S.fixed_W && count) { // slots zeroed by the codebook; chunk offsets by look-back
+    // Chunk bit offsets by decoupled look-back inside pack_write (no counting
+    // pass); the slots must be zero (stream words are OR-combined at chunk
+    // seams): fixed slots are zeroed by the codebook grid, packed slots by
+    // arena_zero over the batch's range.  QCSIM_PACK_COUNT=1: the counting
+    // pass + plane scan instead.
+    static const bool count_pass = std::getenv("QCSIM_PACK_COUNT") && std::getenv("QCSIM_PACK_COUNT")[0] == '1';
+    if (S.fixed_W || !count_pass) {
         if (S.pack_lb.ensure(S.planes * nck, /*zero=*/true)) S.pack_lb_epoch = 0;
         if (++S.pack_lb_epoch >= (1u << 29)) {
             CK(cudaMemsetAsync(S.pack_lb.p, 0, S.pack_lb.cap * sizeof(unsigned long long), st));
@@ -460,6 +466,10 @@ void launch_pack(cudaStream_t st, EncScratch &S, DBuf<uint8_t> &arena, bool coun
         }
         P.lb = S.pack_lb.p;
         P.lb_epoch = S.pack_lb_epoch;
+        if (!S.fixed_W || !count) {
+            PROF("arena_zero", st);
+            launch_k(arena_zero, 296, 256, 0, st, P.arena, P.arena_cap, S.slot_off.p + S.planes);
+        }
     } else if (count) {
         {
             PROF("pack_count", st); // also zeroes the plane slots
@@ -572,7 +582,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     A.gamma = S.gamma.p;
     A.t_nev = reinterpret_cast<uint32_t *>(S.t_nev.p);
     if (S.lb.ensure(planes * ntiles, /*zero=*/true)) S.lb_epoch = 0;
-    if (++S.lb_epoch >= (1u << 30)) { // epoch wrapped: clean slots
+    if (++S.lb_epoch >= (1u << 30) - 4) { // epoch wrapped: clean slots
         CK(cudaMemsetAsync(S.lb.p, 0, S.lb.cap * sizeof(unsigned long long), st));
         S.lb_epoch = 1;
     }
@@ -826,12 +836,24 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     launch_plane_scan(st, S.t_lastb.p, S.t_prevb.p, ntiles, (int)planes, kScanMaxExcl);
     launch_plane_scan(st, S.t_firstb.p, S.t_nextb.p, ntiles, (int)planes, kScanMinExclRev);
     launch_plane_scan(st, S.t_nout.p, S.t_ooff.p, ntiles, (int)planes, kScanSumExcl);
-    {
+    // planes of many tiles: tokens counted, histogrammed and emitted in ONE
+    // grid (tok_fused, token offsets by look-back); QCSIM_FUSE_TOK=0: the
+    // counting grid + plane scan + emission grid
+    static const bool fuse_tok_off = std::getenv("QCSIM_FUSE_TOK") && std::getenv("QCSIM_FUSE_TOK")[0] == '0';
+    const bool fused_tok = !fuse_tok_off && ntiles > kInlineTiles && !flow;
+    T.lb = nullptr;
+    T.lb_epoch = 0;
+    if (fused_tok) {
+        T.lb = S.lb.p; // (the lattice's look-back slots are idle for planes of many tiles)
+        T.lb_epoch = ++S.lb_epoch;
+        PROF("tok_fused", st);
+        launch_k(tok_fused, tgrid_p, kEncThreads, 0, st, T, (int)planes);
+    } else {
         PROF("tok_count", st);
         launch_k(tok_count, tgrid_p, kEncThreads, 0, st, T, (int)planes,
                  (const uint32_t *)(flow ? S.ser_done.p : nullptr), flow_epoch);
     }
-    launch_plane_scan(st, S.t_ntok.p, S.t_tokoff.p, ntiles, (int)planes, kScanSumExcl);
+    if (!fused_tok) launch_plane_scan(st, S.t_ntok.p, S.t_tokoff.p, ntiles, (int)planes, kScanSumExcl);
     {
         // debug: QCSIM_ZT_STATS=1 prints how many tiles took the run-aware paths
         static const bool zt_stats = std::getenv("QCSIM_ZT_STATS") != nullptr;
@@ -898,7 +920,8 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     {
         // tokens and codebooks in one grid (both only consume tok_count)
         PROF("tok_emit_codebook", st);
-        launch_k(tok_emit_codebook, (unsigned)planes + tgrid_p, 256, 0, st, T, B, (int)planes);
+        // (after tok_fused only the codebook blocks remain)
+        launch_k(tok_emit_codebook, (unsigned)planes + (fused_tok ? 0u : tgrid_p), 256, 0, st, T, B, (int)planes);
     }
     if (cb_tracing) {
         std::vector<unsigned long long> h(16 * planes);
