@@ -1517,8 +1517,6 @@ struct TokArgs {
     int32_t *t_nextb;            // scanned: first run start strictly after the tile
     int32_t *t_ntok, *t_tokoff;  // tokens per tile, scanned (+1)
     const uint8_t *ztriv;        // [plane][tile] flat zero-code tiles (TileArgs::ztriv) or nullptr
-    unsigned long long *lb;      // tok_fused: token-offset look-back slots [plane][ntiles] (epoch-tagged)
-    uint32_t lb_epoch;
     uint64_t L;
     int ntiles, tile_sh, log2C, qb;
 };
@@ -1896,192 +1894,6 @@ __device__ __forceinline__ void tok_emit_tile(const TokArgs &A, int planes, int 
 __global__ void __launch_bounds__(kEncThreads) tok_emit(TokArgs A, int planes) {
     pdl_begin();
     tok_emit_tile(A, planes, blockIdx.x);
-}
-
-// TB + TC in one grid for planes of many tiles: the tile's runs are found
-// once; tokens are counted, histogrammed (codec.cpp:484-488) and emitted
-// (codec.cpp:460-482) in the same block, the tile's token offset coming from a
-// decoupled look-back over the plane's earlier tiles instead of a counting
-// pass + plane scan.  Same tokens, counts and index records as tok_count +
-// tok_emit.  (Blocks of a plane are dispatched in tile order.)
-__global__ void __launch_bounds__(kEncThreads) tok_fused(TokArgs A, int planes) {
-    pdl_begin();
-    int pl, t;
-    split_block(blockIdx.x, A.ntiles, A.tile_sh, pl, t);
-    if (pl >= planes) return;
-    const int tid = threadIdx.x;
-    const uint64_t L = A.L;
-    const uint64_t t0 = (uint64_t)t * kTile;
-    const int tl = (int)tmin<uint64_t>(kTile, L - t0);
-    const uint32_t *sym = A.sym + (uint64_t)pl * L;
-    const double *x = A.x + (uint64_t)pl * L;
-    const uint32_t rsym = 1u << A.qb;
-    const uint64_t C = 1ull << A.log2C;
-    const uint64_t nidx = (L >> A.log2C) + 1;
-    uint32_t *tsym = A.tsym + (uint64_t)pl * (L + 1);
-    uint32_t *trep = A.trep + (uint64_t)pl * (L + 1);
-    IndexRec *idx = A.index + (uint64_t)pl * nidx;
-    unsigned long long *lbs = A.lb + (uint64_t)pl * A.ntiles;
-    __shared__ uint32_t s_tokbase;
-    uint32_t sv[kPerThread + 1];
-    const bool known_flat = A.ztriv && A.ztriv[(uint64_t)pl * A.ntiles + t];
-    if (!known_flat) tile_load_syms(sym, t0, tl, sv);
-    // prevb, nextb and the outlier base from the plane scans (enc_verify's
-    // tile statistics); the token base from the look-back below
-    int32_t prevb, nextb, obase_i;
-    {
-        const uint64_t o = (uint64_t)pl * A.ntiles + t;
-        prevb = A.t_prevb[o];
-        nextb = A.t_nextb[o];
-        obase_i = A.t_ooff[(uint64_t)pl * (A.ntiles + 1) + t];
-    }
-    {
-        uint32_t fs = 1u << (A.qb - 1);
-        if (known_flat || tile_flat(sym, t0, tl, sv, fs)) {
-            // inside one long run: no tokens, counts or outliers; the index
-            // records resume after the run's literal + RUN tokens
-            if (tid < 32) {
-                const uint32_t b = lookback_exclusive(lbs, A.lb_epoch, t, 0u);
-                if (tid == 0) s_tokbase = b;
-            }
-            __syncthreads();
-            const uint32_t tokb = s_tokbase;
-            const uint64_t end = nextb == 0x7FFFFFFF ? L : (uint64_t)nextb;
-            for (uint64_t i = ((t0 + C - 1) & ~(C - 1)) + (uint64_t)tid * C; i < t0 + tl; i += (uint64_t)kEncThreads * C) {
-                IndexRec *r = idx + (i >> A.log2C);
-                r->last_lit = fs;
-                r->ocur = (uint32_t)obase_i;
-                r->tok = tokb;
-                r->run_left = (uint32_t)(end - i);
-            }
-            if (t == A.ntiles - 1 && tid == 0) {
-                A.ntok[pl] = tokb;
-                A.ocount[pl] = (uint32_t)obase_i;
-            }
-            return;
-        }
-    }
-    using ScanI = cub::BlockScan<int, kEncThreads>;
-    __shared__ typename ScanI::TempStorage tmp;
-    __shared__ int s_next[kTile];
-    __shared__ __align__(16) uint32_t hist[kWin];
-    __shared__ uint16_t touched[kTile + 1]; // window bins this tile hit (first-touch list)
-    __shared__ uint32_t ntouched;
-    __shared__ uint32_t h0, hrun, smin, smax;
-    __shared__ unsigned long long gbits;
-    const long long half = 1ll << (A.qb - 1);
-    const uint32_t wlo = (uint32_t)(half - kWin / 2);
-    uint32_t *ghist = A.hist + (uint64_t)pl * ((uint64_t)rsym + 1);
-    for (int k = tid; k < kWin / 4; k += kEncThreads) reinterpret_cast<uint4 *>(hist)[k] = make_uint4(0, 0, 0, 0);
-    if (tid == 0) { h0 = 0; hrun = 0; smin = 0xFFFFFFFFu; smax = 0; gbits = 0; ntouched = 0; }
-    uint64_t start[kPerThread], end[kPerThread];
-    const int32_t carries[4] = {prevb, nextb, 0, obase_i};
-    int32_t bases[2];
-    element_runs<ScanI>(A, sym, pl, t, t0, tl, tmp, s_next, start, end, sv, bases, carries); // (barriers inside)
-    auto count = [&](uint32_t s, uint32_t n) {
-        if (s == kOutlierSym) atomicAdd(&h0, n);
-        else if (s == rsym) atomicAdd(&hrun, n);
-        else if (s - wlo < (uint32_t)kWin) {
-            if (atomicAdd(&hist[s - wlo], n) == 0) touched[atomicAdd(&ntouched, 1u)] = (uint16_t)(s - wlo);
-        } else {
-            atomicAdd(&ghist[s], n);
-            atomicMin(&smin, s);
-            atomicMax(&smax, s);
-        }
-    };
-    int cnt[kPerThread], tpos[kPerThread], isout[kPerThread], opos[kPerThread];
-    for (int e = 0; e < kPerThread; ++e) {
-        const int k = tid * kPerThread + e;
-        cnt[e] = 0;
-        isout[e] = 0;
-        if (k >= tl) continue;
-        const uint64_t i = t0 + k;
-        const uint32_t s = sv[e + 1];
-        const uint64_t len = end[e] - start[e];
-        const bool longrun = s != kOutlierSym && len >= kMinRunLen;
-        cnt[e] = longrun ? (i == start[e] ? 2 : 0) : 1;
-        isout[e] = s == kOutlierSym;
-        if (cnt[e] == 2) {
-            count(s, 1);
-            count(rsym, 1);
-            atomicAdd(&gbits, (unsigned long long)(2 * bit_width64(len - 1) - 1));
-        } else if (cnt[e] == 1) {
-            count(s, 1);
-        }
-    }
-    __syncthreads();
-    int tile_tok, tile_out;
-    ScanI(tmp).ExclusiveSum(cnt, tpos, tile_tok);
-    __syncthreads();
-    ScanI(tmp).ExclusiveSum(isout, opos, tile_out);
-    // warp 0 looks back for the tile's token offset while the other warps
-    // flush the histogram window
-    if (tid < 32) {
-        const uint32_t b = lookback_exclusive(lbs, A.lb_epoch, t, (uint32_t)tile_tok);
-        if (tid == 0) {
-            s_tokbase = b;
-            if (h0) atomicAdd(&A.hspecial[2 * pl], h0);
-            if (hrun) atomicAdd(&A.hspecial[2 * pl + 1], hrun);
-            if (gbits) atomicAdd(&A.gamma_bits[pl], gbits);
-        }
-    } else {
-        for (uint32_t m = tid - 32; m < ntouched; m += kEncThreads - 32) {
-            const uint32_t k = touched[m];
-            const uint32_t v = hist[k];
-            const uint32_t sy = wlo + k;
-            if (sy != kOutlierSym && sy < rsym) {
-                atomicAdd(&ghist[sy], v);
-                atomicMin(&smin, sy);
-                atomicMax(&smax, sy);
-            }
-        }
-    }
-    __syncthreads();
-    if (tid == 0 && smin <= smax) {
-        atomicMin(&A.symrange[2 * pl], smin);
-        atomicMax(&A.symrange[2 * pl + 1], smax);
-    }
-    const uint32_t tokbase = s_tokbase, obase = (uint32_t)obase_i;
-    for (int e = 0; e < kPerThread; ++e) {
-        const int k = tid * kPerThread + e;
-        if (k >= tl) continue;
-        const uint64_t i = t0 + k;
-        const uint32_t s = sv[e + 1];
-        const uint32_t tk = tokbase + (uint32_t)tpos[e];
-        const uint64_t len = end[e] - start[e];
-        const bool longrun = s != kOutlierSym && len >= kMinRunLen;
-        if (cnt[e] == 2) {
-            tsym[tk] = s;
-            trep[tk] = 0;
-            tsym[tk + 1] = rsym;
-            trep[tk + 1] = (uint32_t)(len - 1);
-        } else if (cnt[e] == 1) {
-            tsym[tk] = s;
-            trep[tk] = 0;
-        }
-        if (isout[e]) {
-            A.opos[(uint64_t)pl * L + obase + opos[e]] = (uint32_t)i;
-            A.oval[(uint64_t)pl * L + obase + opos[e]] = x[i];
-        }
-        if ((i & (C - 1)) == 0) {
-            // decoder state at element i (codec.cpp:612-626), as tok_emit
-            IndexRec *r = idx + (i >> A.log2C);
-            const uint32_t ocur = obase + (uint32_t)opos[e];
-            r->tok = tk;
-            r->ocur = ocur;
-            if (i == start[e]) {
-                r->run_left = 0;
-                r->last_lit = i == 0 ? rsym : sym[i - 1];
-            } else {
-                r->last_lit = s;
-                r->run_left = longrun ? (uint32_t)(end[e] - i) : 0u;
-            }
-        }
-    }
-    if (t == A.ntiles - 1 && tid == 0) { // plane totals: the last tile's offsets + its own counts
-        A.ntok[pl] = tokbase + (uint32_t)tile_tok;
-        A.ocount[pl] = obase + (uint32_t)tile_out;
-    }
 }
 
 } // namespace qcb

@@ -836,24 +836,12 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     launch_plane_scan(st, S.t_lastb.p, S.t_prevb.p, ntiles, (int)planes, kScanMaxExcl);
     launch_plane_scan(st, S.t_firstb.p, S.t_nextb.p, ntiles, (int)planes, kScanMinExclRev);
     launch_plane_scan(st, S.t_nout.p, S.t_ooff.p, ntiles, (int)planes, kScanSumExcl);
-    // planes of many tiles: tokens counted, histogrammed and emitted in ONE
-    // grid (tok_fused, token offsets by look-back); QCSIM_FUSE_TOK=0: the
-    // counting grid + plane scan + emission grid
-    static const bool fuse_tok_off = std::getenv("QCSIM_FUSE_TOK") && std::getenv("QCSIM_FUSE_TOK")[0] == '0';
-    const bool fused_tok = !fuse_tok_off && ntiles > kInlineTiles && !flow;
-    T.lb = nullptr;
-    T.lb_epoch = 0;
-    if (fused_tok) {
-        T.lb = S.lb.p; // (the lattice's look-back slots are idle for planes of many tiles)
-        T.lb_epoch = ++S.lb_epoch;
-        PROF("tok_fused", st);
-        launch_k(tok_fused, tgrid_p, kEncThreads, 0, st, T, (int)planes);
-    } else {
+    {
         PROF("tok_count", st);
         launch_k(tok_count, tgrid_p, kEncThreads, 0, st, T, (int)planes,
                  (const uint32_t *)(flow ? S.ser_done.p : nullptr), flow_epoch);
     }
-    if (!fused_tok) launch_plane_scan(st, S.t_ntok.p, S.t_tokoff.p, ntiles, (int)planes, kScanSumExcl);
+    launch_plane_scan(st, S.t_ntok.p, S.t_tokoff.p, ntiles, (int)planes, kScanSumExcl);
     {
         // debug: QCSIM_ZT_STATS=1 prints how many tiles took the run-aware paths
         static const bool zt_stats = std::getenv("QCSIM_ZT_STATS") != nullptr;
@@ -920,8 +908,7 @@ void encode_launch(cudaStream_t st, EncScratch &S, const Src &src, int units, ui
     {
         // tokens and codebooks in one grid (both only consume tok_count)
         PROF("tok_emit_codebook", st);
-        // (after tok_fused only the codebook blocks remain)
-        launch_k(tok_emit_codebook, (unsigned)planes + (fused_tok ? 0u : tgrid_p), 256, 0, st, T, B, (int)planes);
+        launch_k(tok_emit_codebook, (unsigned)planes + tgrid_p, 256, 0, st, T, B, (int)planes);
     }
     if (cb_tracing) {
         std::vector<unsigned long long> h(16 * planes);

@@ -135,7 +135,7 @@ print(info["waves"], hashlib.sha256(blob).hexdigest(), hashlib.sha256(amps.tobyt
 def _run_script(script, args, env_extra):
     e = dict(os.environ)
     for k in ("QCSIM_WAVE_SLICES", "QCSIM_SYNC_GATES", "QCSIM_FOREIGN_SERIAL", "QCSIM_FUSE_GL", "QCSIM_ZERO_TILES",
-              "QCSIM_ENCX_VEC", "QCSIM_FUSE_TOK", "QCSIM_PACK_COUNT", "QCSIM_CHAIN_PIPE"):
+              "QCSIM_ENCX_VEC", "QCSIM_PACK_COUNT", "QCSIM_CHAIN_PIPE"):
         e.pop(k, None)
     e.update(env_extra)
     r = subprocess.run([sys.executable, "-c", script] + args, cwd=ROOT, env=e, capture_output=True, text=True,
@@ -435,10 +435,9 @@ def test_fused_gate_lattice_bit_identical(oracle):
     fused = _run_script(_FUSE_SCRIPT, [], {})
     split = _run_script(_FUSE_SCRIPT, [], {"QCSIM_FUSE_GL": "0"})
     plain = _run_script(_FUSE_SCRIPT, [], {"QCSIM_FUSE_GL": "0", "QCSIM_ZERO_TILES": "0", "QCSIM_ENCX_VEC": "0",
-                                           "QCSIM_FUSE_TOK": "0", "QCSIM_PACK_COUNT": "1", "QCSIM_CHAIN_PIPE": "0"})
-    tok = _run_script(_FUSE_SCRIPT, [], {"QCSIM_FUSE_TOK": "0"})
+                                           "QCSIM_PACK_COUNT": "1", "QCSIM_CHAIN_PIPE": "0"})
     pipe = _run_script(_FUSE_SCRIPT, [], {"QCSIM_CHAIN_PIPE": "0", "QCSIM_PACK_COUNT": "1"})
-    assert fused == split == plain == tok == pipe
+    assert fused == split == plain == pipe
     import paper_1811_05630_b200 as q
     n, s = 19, 17
     acts = q.lower(q.build_qft(n))[:60] + q.random_u3_circuit_actions(n, 1, seed=3)
