@@ -2770,32 +2770,30 @@ qcsim_status qcsim_engine_export_blocks(qcsim_engine *e, uint8_t *out, uint64_t 
         std::vector<uint64_t> off(P);
         CK(cudaMemcpyAsync(off.data(), e->blk_off[e->cur].p, P * 8, cudaMemcpyDeviceToHost, e->st));
         CK(cudaStreamSynchronize(e->st));
-        uint64_t hi = 0;
-        for (uint64_t k = 0; k < P; ++k) hi = std::max(hi, off[k] + e->blk_bytes_h[k]);
-        if (hi > 2 * tot + (1u << 20)) { // sparse arena (fixed slots): gather on the device, one copy
-            std::vector<uint64_t> meta(3 * P);
-            for (uint64_t k = 0; k < P; ++k) {
-                meta[k] = off[k];
-                meta[P + k] = (k ? meta[P + k - 1] + e->blk_bytes_h[k - 1] : 0);
-                meta[2 * P + k] = e->blk_bytes_h[k];
+        // gather on the device (slots carry padding and the decode index
+        // between the blocks), then one copy of exactly the blocks' bytes;
+        // in steps of <= 256 MB so a large state needs no large staging buffer
+        constexpr uint64_t kStep = 256ull << 20;
+        uint64_t done = 0;
+        for (uint64_t k0 = 0; k0 < P;) {
+            uint64_t k1 = k0, bytes = 0;
+            while (k1 < P && (k1 == k0 || bytes + e->blk_bytes_h[k1] <= kStep)) bytes += e->blk_bytes_h[k1++];
+            const uint64_t n = k1 - k0;
+            std::vector<uint64_t> meta(3 * n);
+            for (uint64_t k = 0; k < n; ++k) {
+                meta[k] = off[k0 + k];
+                meta[n + k] = (k ? meta[n + k - 1] + e->blk_bytes_h[k0 + k - 1] : 0);
+                meta[2 * n + k] = e->blk_bytes_h[k0 + k];
             }
-            e->exp_meta.ensure(3 * P);
-            e->exp_buf.ensure(tot + 16);
+            e->exp_meta.ensure(3 * n);
+            e->exp_buf.ensure(bytes + 16);
             CK(cudaMemcpyAsync(e->exp_meta.p, meta.data(), meta.size() * 8, cudaMemcpyHostToDevice, e->st));
-            launch_k(gather_blocks, (unsigned)P, 256, 0, e->st, (const uint8_t *)e->arena[e->cur].p,
-                     (const uint64_t *)e->exp_meta.p, (int)P, e->exp_buf.p);
-            CK(cudaMemcpyAsync(out, e->exp_buf.p, tot, cudaMemcpyDeviceToHost, e->st));
+            launch_k(gather_blocks, (unsigned)n, 256, 0, e->st, (const uint8_t *)e->arena[e->cur].p,
+                     (const uint64_t *)e->exp_meta.p, (int)n, e->exp_buf.p);
+            CK(cudaMemcpyAsync(out + done, e->exp_buf.p, bytes, cudaMemcpyDeviceToHost, e->st));
             CK(cudaStreamSynchronize(e->st));
-            return;
-        }
-        // one contiguous device->host copy of the arena, then gather on host
-        std::vector<uint8_t> host(hi);
-        CK(cudaMemcpyAsync(host.data(), e->arena[e->cur].p, hi, cudaMemcpyDeviceToHost, e->st));
-        CK(cudaStreamSynchronize(e->st));
-        uint64_t o = 0;
-        for (uint64_t k = 0; k < P; ++k) {
-            std::memcpy(out + o, host.data() + off[k], e->blk_bytes_h[k]);
-            o += e->blk_bytes_h[k];
+            done += bytes;
+            k0 = k1;
         }
     });
 }
