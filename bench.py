@@ -362,6 +362,19 @@ def roofline(res, wl, hbm, peak_kind, world):
                          "basis": "same bytes / whole gate-pass device time"}
     out["dense_equivalent"] = {"achieved": 32.0 * (1 << wl["n"]) / pass_s / 1e9,
                                "basis": "32 B per amplitude update (SURVEY.md 8(d), not judged)"}
+    # The fused in-slice gate kernel (north_star: ">= 50% of the HBM roofline
+    # for fused in-slice gates"): the one stage that streams the dense planes
+    # -- per amplitude it reads the old re/im (16 B; flagged zero tiles are
+    # not read, so this basis is an upper bound on its reads) and writes the
+    # new re/im (16 B), two symbols (8 B) and two flag bytes (2 B).
+    gk = next((k for k in kprof if k["kernel"] == "enc_gate_lattice"), None)
+    if gk and res["pgates"]:
+        t_g = gk["ms"] * 1e-3 / res["pgates"]
+        gbytes = 42.0 * (1 << wl["n"]) / max(1, world)
+        out["gate_kernel"] = {"kernel": "enc_gate_lattice", "s_per_pass": t_g, "achieved": gbytes / t_g / 1e9,
+                              "frac": gbytes / t_g / 1e9 / hbm,
+                              "basis": "42 B per amplitude (16 read + 16 + 8 + 2 written); ncu DRAM of the same "
+                                       "launch: profiles/r02_random30_pass_dram.json"}
     out["kernel_shares"] = kprof[:10]
     out["kernel_ms_total"] = sum(k["ms"] for k in kprof)
     out["chain"] = res.get("chain")

@@ -38,6 +38,15 @@ struct DecPlanes {
     const IndexRec *ext_index = nullptr; // [plane][ext_stride]
     const uint32_t *ext_nrec = nullptr;  // [plane]
     uint64_t ext_stride = 0;
+    // fine > 0: ext_index holds the ENCODER's fine checkpoints of the pass
+    // that wrote these blocks (one every 2^(fine) elements, still in the
+    // engine's scratch inside one run()): record k (1-based) is the decoder
+    // state at element k << fine, every plane has ext_fixed_nrec of them
+    // (ext_nrec unused).  Small planes carry only a few stored records
+    // (7.8% of a ~2.5 KB block); the scratch checkpoints give the deferred
+    // loop its chunk parallelism back without enlarging the stored state.
+    int fine = 0;
+    uint32_t ext_fixed_nrec = 0;
     const uint32_t *skip = nullptr;      // [plane] != 0: not decoded (a codec error was found)
     // Zero-tile flags (run-aware gate pass, SURVEY.md §7 H1 "run-aware
     // shortcut"): an encoder tile (kTile elements) that lies inside one long
@@ -240,7 +249,8 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
     const uint8_t *blk = D.arena + D.blk_off[pl];
     const uint64_t payload = load_le(blk + 32, 8);
     const uint64_t bbytes = kHeaderBytes + payload;
-    const uint64_t nchunks = (D.ext_index ? D.ext_nrec[pl] : index_records(D.L, bbytes, D.log2C)) + 1;
+    const uint64_t nchunks =
+        (D.ext_index ? (D.fine ? D.ext_fixed_nrec : D.ext_nrec[pl]) : index_records(D.L, bbytes, D.log2C)) + 1;
     const uint64_t j0 = (uint64_t)(blockIdx.x % groups) * kDecThreads;
     if (j0 >= nchunks) return;
     const uint64_t j = j0 + threadIdx.x;
@@ -301,8 +311,8 @@ __global__ void __launch_bounds__(kDecThreads, 5) dec_chunks(DecPlanes D, DecTab
     uint64_t ocur = r.ocur;
     double d1 = r.dprev, d2 = r.dprev2;
     // chunk j: from record j to record j + 1 (element indices in `tok`)
-    const uint64_t e0 = j == 0 ? 0 : (uint64_t)r.tok;
-    const uint64_t e1 = !active ? e0 : (j + 1 < nchunks ? (uint64_t)sidx[j].tok : D.L);
+    const uint64_t e0 = j == 0 ? 0 : (D.fine ? j << D.fine : (uint64_t)r.tok);
+    const uint64_t e1 = !active ? e0 : (j + 1 < nchunks ? (D.fine ? (j + 1) << D.fine : (uint64_t)sidx[j].tok) : D.L);
     double *out = D.out[pl];
     const int wbase_t = threadIdx.x & ~31; // first thread of this warp
 

@@ -1050,7 +1050,7 @@ struct DecScratch {
 void decode_batch(cudaStream_t st, DecScratch &S, const uint8_t *arena, const uint64_t *blk_off,
                   double *const *out, int planes, uint64_t L, int log2C, int qb,
                   bool prepare = true, const NormArgs *norm = nullptr, uint8_t *zflag = nullptr,
-                  uint64_t zflag_planes = 0) {
+                  uint64_t zflag_planes = 0, const IndexRec *fine_index = nullptr) {
     if (prepare) S.ensure(planes, L, qb);
     const DecTables T = S.tables();
     DecPlanes D;
@@ -1069,7 +1069,13 @@ void decode_batch(cudaStream_t st, DecScratch &S, const uint8_t *arena, const ui
         launch_k(dec_prepare, planes, 256, 0, st, D, T, planes);
     }
     const uint64_t nchunks = (L + (1ull << log2C) - 1) >> log2C;
-    const uint64_t groups = (nchunks + kDecThreads - 1) / kDecThreads;
+    if (fine_index) { // the previous pass's encoder checkpoints (scratch), [plane][nidx]
+        D.ext_index = fine_index + 1; // record k at fine[k]
+        D.ext_stride = (L >> log2C) + 1;
+        D.fine = log2C;
+        D.ext_fixed_nrec = (uint32_t)(nchunks - 1);
+    }
+    const uint64_t groups = ((fine_index ? D.ext_stride + 1 : nchunks) + kDecThreads - 1) / kDecThreads;
     {
         set_smem_once(dec_chunks, kDecSmem, g_smem_set, 2);
         PROF("dec_chunks", st);
@@ -1871,8 +1877,14 @@ template <class Src> void engine_dense(qcsim_engine *e, const Src &src) {
 void engine_deferred_pass(qcsim_engine *e, const GateSrc &g0) {
     const int nxt = e->cur ^ 1;
     ensure_outptrs(e, 2 * e->ns);
+    // from the second pass of a run on, the blocks being decoded were written
+    // by the previous pass, whose fine checkpoints are still in e->index:
+    // one decode chunk per checkpoint instead of per stored record
+    // (QCSIM_FINE_DECODE=0: the stored records only)
+    static const bool fine_off = std::getenv("QCSIM_FINE_DECODE") && std::getenv("QCSIM_FINE_DECODE")[0] == '0';
+    const IndexRec *fine = (!fine_off && !e->defer_fresh && e->index.p) ? e->index.p : nullptr;
     decode_batch(e->st, e->dec[e->cur], e->arena[e->cur].p, e->blk_off[e->cur].p, e->outptrs.p, (int)(2 * e->ns),
-                 e->L, e->log2C, e->cfg.codec.quant_code_bits, /*prepare=*/false, &e->norm);
+                 e->L, e->log2C, e->cfg.codec.quant_code_bits, /*prepare=*/false, &e->norm, nullptr, 0, fine);
     e->norm.enabled = 0;
     GateSrc g = g0;
     g.old = e->old.p;

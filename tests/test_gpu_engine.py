@@ -250,11 +250,12 @@ print(hashlib.sha256(bytes(blob)).hexdigest(), repr(m.mean_compression_ratio), r
 
 
 @pytest.mark.parametrize("env", [{"QCSIM_CHAIN": "2"}, {"QCSIM_SYNC_GATES": "1"}, {"QCSIM_PDL": "0"},
-                                 {"QCSIM_CHAIN_OVERLAP": "0"}, {"QCSIM_FIXED_SLOTS": "0"}])
+                                 {"QCSIM_CHAIN_OVERLAP": "0"}, {"QCSIM_FIXED_SLOTS": "0"}, {"QCSIM_FINE_DECODE": "0"}])
 def test_pipeline_variants_bit_identical(env):
     """The serial warp chain, the host-synchronous gate loop, plain launches,
     grid-wide waits instead of per-plane hand-offs and the packed (scanned)
-    slot layout produce the same blocks and metrics as the default pipeline
+    slot layout, and decoding from the stored slot records only (instead of
+    the previous pass's fine checkpoints) produce the same blocks and metrics as the default pipeline
     (block-parallel chain, deferred loop, programmatic dependent launch,
     per-plane hand-offs, fixed slots)."""
     import os
@@ -264,7 +265,8 @@ def test_pipeline_variants_bit_identical(env):
 
     def run(extra):
         e = dict(os.environ)
-        for k in ("QCSIM_CHAIN", "QCSIM_SYNC_GATES", "QCSIM_PDL", "QCSIM_CHAIN_OVERLAP", "QCSIM_FIXED_SLOTS"):
+        for k in ("QCSIM_CHAIN", "QCSIM_SYNC_GATES", "QCSIM_PDL", "QCSIM_CHAIN_OVERLAP", "QCSIM_FIXED_SLOTS",
+                  "QCSIM_FINE_DECODE"):
             e.pop(k, None)
         e.update(extra)
         r = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT], cwd=root, env=e, capture_output=True,
