@@ -218,18 +218,18 @@ constexpr size_t kDecSmem = sizeof(DecSmem);
 // are staged in shared memory.
 //
 // Decoding reproduces codec.cpp:591-626 in two alternating phases per warp:
-//  1. every lane decodes its own chunk (token by token, from its record)
-//     into up to kDecBatch *value runs* (end, value) in shared memory: a
-//     literal is a run of one element (d = p + (2eb)m, or the outlier), a
-//     RUN token of a zero code with the previous-value predictor is ONE run
-//     of the constant d (d + 0.0 == d, the first element canonicalises -0.0);
-//     other RUN tokens (nonzero code, linear predictor) emit one element per
-//     step, as the reference's serial loop does.  The FP64 work is per
-//     token, in the reference's order;
-//  2. the warp writes the runs of each of its 32 chunks in turn, 32
-//     consecutive elements per store (coalesced), each lane walking the run
-//     list with a cursor.  Runs of >= kDecBlockFill elements go to a block
-//     list written by all threads at the end.
+//  1. every lane decodes its own chunk, token by token, from its record.  A
+//     literal is one element (d = p + (2eb)m, or the outlier), written at
+//     once by the lane; a RUN token of a zero code with the previous-value
+//     predictor is ONE constant run of d (d + 0.0 == d, the first element
+//     canonicalises -0.0): shorter than kDecWarpRun elements it is written
+//     by the lane, longer it goes to the lane's run list, and from
+//     kDecBlockFill elements on to the block list; other RUN tokens (nonzero
+//     code, linear predictor) emit one element per step, as the reference's
+//     serial loop does.  The FP64 work is per token, in the reference's order;
+//  2. the warp writes the listed runs of its lanes in turn, 32 consecutive
+//     elements per store (coalesced).  The block list is written by all
+//     threads at the end (whole tiles of +0.0 are flagged instead, zflag).
 // N.enabled: the grid's last block runs the engine's normalization for this
 // gate pass instead (it needs only the previous pass's norms; the gate kernel
 // that applies the scale runs after this grid).

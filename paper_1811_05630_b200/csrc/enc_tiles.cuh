@@ -1525,7 +1525,8 @@ struct RunInfo {
     uint64_t start, end;
 };
 
-// Per element: run [start, end) from in-tile scans + the scanned carries.
+// Per element: run [start, end) from the tile's run starts (warp shuffles +
+// one shared-memory exchange) + the scanned carries.
 template <class ScanI>
 __device__ __forceinline__ void element_runs(const TokArgs &A, const uint32_t *sym, int pl, int t, uint64_t t0,
                                              int tl, typename ScanI::TempStorage &tmp, int *s_next,
@@ -1560,54 +1561,55 @@ __device__ __forceinline__ void element_runs(const TokArgs &A, const uint32_t *s
             carry_of2(A.t_tokoff, A.ntiles + 1, A.t_ntok, kScanSumExcl, A.t_ooff, A.ntiles + 1, A.t_nout,
                       kScanSumExcl, pl, t, A.ntiles, bases[0], bases[1]);
     }
+    // run starts (boundaries) of this thread's elements; st[e] = the last one
+    // at or before element e, nx[e] = the first one after it, both within
+    // this thread
+    int last_in = -1;
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
         const uint64_t i = t0 + k;
         isb[e] = (k < tl && (i == 0 || sv[e + 1] != sv[e])) ? (int)k : -1;
+        last_in = isb[e] >= 0 ? isb[e] : last_in;
+        st[e] = last_in;
     }
-    ScanI(tmp).InclusiveScan(isb, st, cub::Max());
-    // first run start after each element: next boundary in the tile, else
-    // the scanned carry from later tiles, else L
-    for (int e = 0; e < kPerThread; ++e) {
-        const int k = tid * kPerThread + e;
-        s_next[k] = isb[e];
+    int first_in = 0x7FFFFFFF;
+    int nx[kPerThread];
+    for (int e = kPerThread - 1; e >= 0; --e) {
+        nx[e] = first_in;
+        if (isb[e] >= 0) first_in = isb[e];
     }
-    __syncthreads();
-    // suffix min over boundaries: s_next[k] = first boundary > k
-    // (small serial-free pass: each thread scans forward within its items,
-    // then a block-wide reverse scan over thread minima)
-    __shared__ int tmin_s[kEncThreads];
-    __shared__ int wmin_s[kEncThreads / 32];
-    int m = 0x7FFFFFFF;
-    for (int e = 0; e < kPerThread; ++e) {
-        const int k = tid * kPerThread + e;
-        if (k < tl && isb[e] >= 0) m = min(m, k);
-    }
-    // reverse inclusive min-scan over threads: within the warp by shuffles,
-    // across warps through one shared-memory pass
+    // across threads: the last boundary of the lower threads (exclusive max
+    // scan) and the first boundary of the higher ones (exclusive reverse min
+    // scan) -- within the warp by shuffles, across warps through one
+    // shared-memory exchange and one barrier
+    (void)tmp;
+    (void)s_next;
+    __shared__ int s_wlast[kEncThreads / 32], s_wfirst[kEncThreads / 32];
     const int lane = tid & 31, wid = tid >> 5;
+    int incl_last = last_in, incl_first = first_in;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-        const int o = __shfl_down_sync(0xffffffffu, m, off);
-        if (lane + off < 32) m = min(m, o);
+        const int a = __shfl_up_sync(0xffffffffu, incl_last, off);
+        const int c = __shfl_down_sync(0xffffffffu, incl_first, off);
+        if (lane >= off) incl_last = max(incl_last, a);
+        if (lane + off < 32) incl_first = min(incl_first, c);
     }
-    if (lane == 0) wmin_s[wid] = m;
+    int prev_last = __shfl_up_sync(0xffffffffu, incl_last, 1);   // lower lanes of this warp
+    int next_first = __shfl_down_sync(0xffffffffu, incl_first, 1); // higher lanes of this warp
+    if (lane == 0) prev_last = -1;
+    if (lane == 31) next_first = 0x7FFFFFFF;
+    if (lane == 31) s_wlast[wid] = incl_last;
+    if (lane == 0) s_wfirst[wid] = incl_first;
     __syncthreads();
-    for (int w = wid + 1; w < kEncThreads / 32; ++w) m = min(m, wmin_s[w]);
-    tmin_s[tid] = m;
-    __syncthreads();
+    for (int w = 0; w < wid; ++w) prev_last = max(prev_last, s_wlast[w]);
+    for (int w = wid + 1; w < kEncThreads / 32; ++w) next_first = min(next_first, s_wfirst[w]);
+    __syncthreads(); // (the exchange arrays are reused by the caller's next tile)
     const uint64_t after = nextb_carry == 0x7FFFFFFF ? A.L : (uint64_t)nextb_carry;
     for (int e = 0; e < kPerThread; ++e) {
-        const int k = tid * kPerThread + e;
-        // start
-        start[e] = st[e] >= 0 ? t0 + st[e] : (uint64_t)prevb;
-        // end: first boundary > k
-        int nb = 0x7FFFFFFF;
-        for (int e2 = e + 1; e2 < kPerThread; ++e2)
-            if (tid * kPerThread + e2 < tl && isb[e2] >= 0) { nb = tid * kPerThread + e2; break; }
-        if (nb == 0x7FFFFFFF && tid + 1 < kEncThreads) nb = tmin_s[tid + 1];
+        const int sl = st[e] >= 0 ? st[e] : prev_last;
+        start[e] = sl >= 0 ? t0 + sl : (uint64_t)prevb;
+        const int nb = nx[e] != 0x7FFFFFFF ? nx[e] : next_first;
         end[e] = (nb != 0x7FFFFFFF && nb < tl) ? t0 + nb : after;
-        (void)k;
     }
 }
 
@@ -1702,7 +1704,6 @@ __global__ void __launch_bounds__(kEncThreads) tok_count(TokArgs A, int planes, 
     using RedI = cub::BlockReduce<int, kEncThreads>;
     __shared__ typename ScanI::TempStorage tmp;
     __shared__ typename RedI::TempStorage rtmp;
-    __shared__ int s_next[kTile];
     __shared__ __align__(16) uint32_t hist[kWin];
     __shared__ uint16_t touched[kTile + 1]; // window bins this tile hit (first-touch list)
     __shared__ uint32_t ntouched;
@@ -1715,7 +1716,7 @@ __global__ void __launch_bounds__(kEncThreads) tok_count(TokArgs A, int planes, 
     for (int k = tid; k < kWin / 4; k += kEncThreads) reinterpret_cast<uint4 *>(hist)[k] = make_uint4(0, 0, 0, 0);
     if (tid == 0) { h0 = 0; hrun = 0; smin = 0xFFFFFFFFu; smax = 0; gbits = 0; ntouched = 0; }
     uint64_t start[kPerThread], end[kPerThread];
-    element_runs<ScanI>(A, sym, pl, t, t0, tl, tmp, s_next, start, end, sv);
+    element_runs<ScanI>(A, sym, pl, t, t0, tl, tmp, nullptr, start, end, sv);
     auto count = [&](uint32_t s, uint32_t n) {
         if (s == kOutlierSym) atomicAdd(&h0, n);
         else if (s == rsym) atomicAdd(&hrun, n);
@@ -1785,7 +1786,6 @@ __device__ __forceinline__ void tok_emit_tile(const TokArgs &A, int planes, int 
     const double *x = A.x + (uint64_t)pl * L;
     using ScanI = cub::BlockScan<int, kEncThreads>;
     __shared__ typename ScanI::TempStorage tmp;
-    __shared__ int s_next[kTile];
     const uint32_t rsym = 1u << A.qb;
     const uint64_t C = 1ull << A.log2C;
     const uint64_t nidx = (L >> A.log2C) + 1;
@@ -1820,7 +1820,7 @@ __device__ __forceinline__ void tok_emit_tile(const TokArgs &A, int planes, int 
     }
     uint64_t start[kPerThread], end[kPerThread];
     int32_t bases[2];
-    element_runs<ScanI>(A, sym, pl, t, t0, tl, tmp, s_next, start, end, sv, bases, carries);
+    element_runs<ScanI>(A, sym, pl, t, t0, tl, tmp, nullptr, start, end, sv, bases, carries);
     int cnt[kPerThread], tpos[kPerThread], isout[kPerThread], opos[kPerThread];
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
@@ -1837,8 +1837,13 @@ __device__ __forceinline__ void tok_emit_tile(const TokArgs &A, int planes, int 
     __syncthreads();
     int tile_tok, tile_out;
     ScanI(tmp).ExclusiveSum(cnt, tpos, tile_tok);
-    __syncthreads();
-    ScanI(tmp).ExclusiveSum(isout, opos, tile_out);
+    if (A.t_nout[(uint64_t)pl * A.ntiles + t] != 0) { // (enc_verify's count: most tiles hold no outlier)
+        __syncthreads();
+        ScanI(tmp).ExclusiveSum(isout, opos, tile_out);
+    } else {
+        for (int e = 0; e < kPerThread; ++e) opos[e] = 0;
+        tile_out = 0;
+    }
     const uint32_t tokbase = (uint32_t)bases[0], obase = (uint32_t)bases[1];
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
