@@ -1527,11 +1527,9 @@ struct RunInfo {
 
 // Per element: run [start, end) from the tile's run starts (warp shuffles +
 // one shared-memory exchange) + the scanned carries.
-template <class ScanI>
-__device__ __forceinline__ void element_runs(const TokArgs &A, const uint32_t *sym, int pl, int t, uint64_t t0,
-                                             int tl, typename ScanI::TempStorage &tmp, int *s_next,
-                                             uint64_t *start, uint64_t *end, const uint32_t *sv,
-                                             int32_t *bases = nullptr, const int32_t *carries = nullptr) {
+__device__ __forceinline__ void element_runs(const TokArgs &A, int pl, int t, uint64_t t0, int tl, uint64_t *start,
+                                             uint64_t *end, const uint32_t *sv, int32_t *bases = nullptr,
+                                             const int32_t *carries = nullptr) {
     // sv: this thread's symbols as loaded by tile_load_syms; carries: the
     // tile_carries() result when the caller computed it already
     const int tid = threadIdx.x;
@@ -1582,8 +1580,6 @@ __device__ __forceinline__ void element_runs(const TokArgs &A, const uint32_t *s
     // scan) and the first boundary of the higher ones (exclusive reverse min
     // scan) -- within the warp by shuffles, across warps through one
     // shared-memory exchange and one barrier
-    (void)tmp;
-    (void)s_next;
     __shared__ int s_wlast[kEncThreads / 32], s_wfirst[kEncThreads / 32];
     const int lane = tid & 31, wid = tid >> 5;
     int incl_last = last_in, incl_first = first_in;
@@ -1700,9 +1696,7 @@ __global__ void __launch_bounds__(kEncThreads) tok_count(TokArgs A, int planes, 
             return;
         }
     }
-    using ScanI = cub::BlockScan<int, kEncThreads>;
     using RedI = cub::BlockReduce<int, kEncThreads>;
-    __shared__ typename ScanI::TempStorage tmp;
     __shared__ typename RedI::TempStorage rtmp;
     __shared__ __align__(16) uint32_t hist[kWin];
     __shared__ uint16_t touched[kTile + 1]; // window bins this tile hit (first-touch list)
@@ -1716,7 +1710,7 @@ __global__ void __launch_bounds__(kEncThreads) tok_count(TokArgs A, int planes, 
     for (int k = tid; k < kWin / 4; k += kEncThreads) reinterpret_cast<uint4 *>(hist)[k] = make_uint4(0, 0, 0, 0);
     if (tid == 0) { h0 = 0; hrun = 0; smin = 0xFFFFFFFFu; smax = 0; gbits = 0; ntouched = 0; }
     uint64_t start[kPerThread], end[kPerThread];
-    element_runs<ScanI>(A, sym, pl, t, t0, tl, tmp, nullptr, start, end, sv);
+    element_runs(A, pl, t, t0, tl, start, end, sv);
     auto count = [&](uint32_t s, uint32_t n) {
         if (s == kOutlierSym) atomicAdd(&h0, n);
         else if (s == rsym) atomicAdd(&hrun, n);
@@ -1820,7 +1814,7 @@ __device__ __forceinline__ void tok_emit_tile(const TokArgs &A, int planes, int 
     }
     uint64_t start[kPerThread], end[kPerThread];
     int32_t bases[2];
-    element_runs<ScanI>(A, sym, pl, t, t0, tl, tmp, nullptr, start, end, sv, bases, carries);
+    element_runs(A, pl, t, t0, tl, start, end, sv, bases, carries);
     int cnt[kPerThread], tpos[kPerThread], isout[kPerThread], opos[kPerThread];
     for (int e = 0; e < kPerThread; ++e) {
         const int k = tid * kPerThread + e;
