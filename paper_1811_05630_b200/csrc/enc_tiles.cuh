@@ -975,10 +975,9 @@ __device__ __forceinline__ void compact_tile(const TileArgs &A, int pl, int t) {
     __shared__ typename ScanI::TempStorage scan_tmp;
     const uint8_t *fl = A.fl + (uint64_t)pl * L;
     int f[kPerThread], pos[kPerThread];
-    for (int e = 0; e < kPerThread; ++e) {
-        const int k = tid * kPerThread + e;
-        f[e] = (k < tl && (fl[t0 + k] & 1)) ? 1 : 0;
-    }
+    uint32_t fv[kPerThread];
+    load4(fl + t0, tid * kPerThread, tl, fv); // (one 4-byte load; 0 past the end)
+    for (int e = 0; e < kPerThread; ++e) f[e] = (int)(fv[e] & 1u);
     ScanI(scan_tmp).ExclusiveSum(f, pos);
     const uint32_t base = (uint32_t)carry_of(reinterpret_cast<const int32_t *>(A.t_evoff), A.ntiles + 1,
                                              reinterpret_cast<const int32_t *>(A.t_nev), pl, t, A.ntiles, kScanSumExcl);
@@ -993,7 +992,7 @@ __device__ __forceinline__ void compact_tile(const TileArgs &A, int pl, int t) {
     for (int e = 0; e < kPerThread; ++e) {
         if (!f[e]) continue;
         const uint64_t i = t0 + tid * kPerThread + e;
-        const bool out = (fl[i] & 2) != 0;
+        const bool out = (fv[e] & 2u) != 0;
         // the event record the chain consumes: its addend (or outlier value)
         // and the element index with bit 31 = outlier
         ev[base + pos[e]] = (uint32_t)i | (out ? 0x80000000u : 0u);
@@ -1230,9 +1229,15 @@ __device__ __forceinline__ void verify_tile(const TileArgs &A, int planes, const
             no += sv[e] == kOutlierSym;
             prev = sv[e];
         }
-        if (fb != 0x7FFFFFFF) atomicMin(&s_fb, fb);
-        if (lb >= 0) atomicMax(&s_lb, lb);
-        if (no) atomicAdd(&s_no, no);
+        // (one shared-memory atomic per warp and statistic)
+        fb = __reduce_min_sync(0xffffffffu, fb);
+        lb = __reduce_max_sync(0xffffffffu, lb);
+        no = __reduce_add_sync(0xffffffffu, no);
+        if ((tid & 31) == 0) {
+            if (fb != 0x7FFFFFFF) atomicMin(&s_fb, fb);
+            if (lb >= 0) atomicMax(&s_lb, lb);
+            if (no) atomicAdd(&s_no, no);
+        }
         __syncthreads();
         if (tid == 0) {
             A.t_firstb[(uint64_t)pl * A.ntiles + t] = s_fb;
